@@ -1,0 +1,215 @@
+/*
+ * hetis.h -- C ABI of libhetis.so: the B200 (sm_100a) hot path of Hetis
+ * (arXiv 2509.08309), head-granular distributed decode Attention over a
+ * head-granular paged KV cache.
+ *
+ * Citations: "PAPER.md:N" = /root/reference/PAPER.md line N (section /
+ * equation given alongside); "reading N" = DESIGN.md §3 (the readings taken
+ * where the paper is silent or ambiguous).
+ *
+ * One decode step of one layer on device i:
+ *   hetis_plan_*      head -> device assignment x_i (Eq. 5)
+ *   hetis_scatter_q   primary -> attention workers: q of the device's heads and
+ *                     the new token's k, v (Eq. 4 traffic)
+ *   hetis_kv_append   head-granular store of the new K/V rows
+ *   hetis_attn_decode result_{i,j} = softmax(q K^T / sqrt(d)) V for the device's
+ *                     heads (Eq. 2b) = hetis_attn_partial (split-KV
+ *                     partial attention) + hetis_attn_combine (LSE merge)
+ *   hetis_gather      Attention_j = Concat_i result_{i,j} (Eq. 2a)
+ *
+ * Conventions
+ * -----------
+ * - Every call returns hetis_status; nothing throws, aborts or prints.  On a
+ *   validation error nothing is launched.  hetis_last_error() gives a
+ *   thread-local one-line detail of the last failure.
+ * - The caller owns every device buffer, stream and NCCL communicator.  The
+ *   library owns only plans (freed by hetis_plan_destroy); it never allocates
+ *   device memory (TMA descriptors are built per call on the host and passed
+ *   as kernel parameters).
+ *   Workspace is sized by the *_workspace queries.
+ * - All device work is asynchronous and ordered on the given stream
+ *   (cudaStream_t; NULL = legacy default stream).
+ * - "Local" indexing: on a device holding query heads [b, b + x) the q / o
+ *   shards are [num_seqs][x][head_dim] with local head h - b, and the block
+ *   table is [num_seqs][x / r][max_pages] with local kv head g - b / r.
+ *   Global head ids appear only in plans, scatter and gather.
+ * - Device-data contracts (not checked per call, as in vLLM): every page id a
+ *   kernel reads is in [0, num_pages); 1 <= seq_lens[j] <= min(max_seq_len,
+ *   max_pages * page_size).  Table entries past ceil(L_j / page_size) and
+ *   pool slots past L_j are never read into a result (they may hold NaN).
+ * - Builds: head_dim in {64, 128}; page_size 16; kv/q dtype in {bf16, f32}
+ *   with q_dtype == kv_dtype; o_dtype in {f32, bf16}; r = H / H_kv in
+ *   {1, 2, 4, 8}.  Anything else -> HETIS_E_UNSUPPORTED.  bf16 with r > 1
+ *   runs on tensor cores (mma.sync m16n8k16); everything else on CUDA cores.
+ */
+#ifndef HETIS_H_
+#define HETIS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HETIS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define HETIS_API __attribute__((visibility("default")))
+#else
+#define HETIS_API
+#endif
+
+typedef struct CUstream_st *hetis_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    HETIS_OK = 0,
+    HETIS_E_INVALID = 1,        /* null / misaligned pointer, bad size or shape              */
+    HETIS_E_HEAD_INTEGRITY = 2, /* Eq. 5: sum_i x_i^j != H                    */
+    HETIS_E_GROUP_ALIGN = 3,    /* x_i^j / r not integral, or a head range    */
+                                /* that does not start/end on a kv-group boundary            */
+    HETIS_E_CAPACITY = 4,       /* Eq. 6 in pages: sum_j ceil(L_j/P) x_i^j/r  */
+                                /*  > free_pages_i (reading 13)                              */
+    HETIS_E_UNSUPPORTED = 5,    /* dtype / head_dim / page_size / r / batch not built        */
+    HETIS_E_WORKSPACE = 6,      /* workspace too small or misaligned                         */
+    HETIS_E_CUDA = 7,           /* a CUDA runtime call or launch failed                      */
+    HETIS_E_NCCL = 8            /* NCCL missing or an NCCL call failed                       */
+} hetis_status;
+
+typedef enum { HETIS_F32 = 0, HETIS_BF16 = 1 } hetis_dtype;
+
+/* Model-side attention shape (D9).  H = num_q_heads (the "H" of Eq. 5),
+ * r = num_q_heads / num_kv_heads, head_dim = the d of Eq. 2b
+ * (reading 1), page_size = tokens per head-granular block. */
+typedef struct {
+    int32_t num_q_heads;
+    int32_t num_kv_heads;
+    int32_t head_dim;
+    int32_t page_size;
+    int32_t kv_dtype; /* hetis_dtype of K/V pools and of new K/V rows */
+    int32_t q_dtype;  /* hetis_dtype of q; must equal kv_dtype        */
+    int32_t o_dtype;  /* hetis_dtype of o: HETIS_F32 or HETIS_BF16    */
+} hetis_shape;
+
+/* Flags for hetis_attn_partial / hetis_attn_decode. */
+#define HETIS_ATTN_FORCE_SIMT 0x1u /* bf16 GQA on CUDA cores instead of tensor cores */
+
+/* ---- status ------------------------------------------------------------ */
+HETIS_API const char *hetis_status_str(hetis_status s);
+HETIS_API const char *hetis_last_error(void);
+HETIS_API int32_t hetis_abi_version(void);
+/* Tokens per split-KV chunk C (reading 12): a constant, so the chunking of a
+ * sequence depends on its length only -- partition invariance is bit-exact. */
+HETIS_API int32_t hetis_split_tokens(void);
+
+/* ---- plan: head -> device assignment (Eq. 5) --------- */
+typedef struct hetis_plan hetis_plan; /* opaque, immutable after create */
+
+/* x (host): per_request == 0: [num_devices] counts shared by every request;
+ *           per_request != 0: [num_seqs][num_devices] counts x_i^j.
+ * Validates x >= 0, x mod r == 0 (-> HETIS_E_GROUP_ALIGN) and sum_i x = H for
+ * every request (-> HETIS_E_HEAD_INTEGRITY; Eq. 7c uses "= H", reading 14).
+ * Device i gets the contiguous global head range [b_i, b_i + x_i), b_i =
+ * sum_{i' < i} x_i' (reading 3).  On success *out owns a new plan. */
+HETIS_API hetis_status hetis_plan_create(const hetis_shape *shape, int32_t num_devices, int32_t num_seqs,
+                               const int32_t *x, int32_t per_request, hetis_plan **out);
+HETIS_API void hetis_plan_destroy(hetis_plan *plan);
+/* Head range of request `seq` (ignored for global plans) on `device`. */
+HETIS_API hetis_status hetis_plan_heads(const hetis_plan *plan, int32_t device, int32_t seq, int32_t *q_begin,
+                              int32_t *q_count);
+HETIS_API int32_t hetis_plan_num_devices(const hetis_plan *plan);
+/* Eq. 6 in pages (reading 13): for every device i,
+ *   sum_j ceil(seq_lens[j] / P) * x_i^j / r <= free_pages[i].
+ * seq_lens_host: [num_seqs] lengths the requests will have (num_seqs must equal
+ * the plan's for per-request plans); free_pages: [N]. */
+HETIS_API hetis_status hetis_plan_check_capacity(const hetis_plan *plan, int32_t num_seqs,
+                                                 const int32_t *seq_lens_host, const int64_t *free_pages);
+
+/* ---- kv append: head-granular store --------------------- */
+/* For every request j and local kv head g: the new row goes to page
+ * block_table[j][g][(L_j - 1) / P], slot (L_j - 1) mod P, L_j = seq_lens[j]
+ * (length AFTER the append, reading 6).  A bit-exact copy.
+ *   k_new, v_new : device [num_seqs][kv_head_count][head_dim], kv_dtype
+ *   k_pool, v_pool: device [num_pages][page_size][head_dim], 16-B aligned
+ *   block_table  : device int32 [num_seqs][kv_head_count][max_pages]
+ *   seq_lens     : device int32 [num_seqs]
+ * The caller must have placed a valid page at (L_j - 1) / P beforehand (a new
+ * page is needed exactly when (L_j - 1) mod P == 0). */
+HETIS_API hetis_status hetis_kv_append(const hetis_shape *shape, int32_t num_seqs, int32_t kv_head_count,
+                             const void *k_new, const void *v_new, void *k_pool, void *v_pool, int64_t num_pages,
+                             const int32_t *block_table, int32_t max_pages, const int32_t *seq_lens,
+                             hetis_stream_t stream);
+
+/* ---- decode attention (Eq. 2b) --------------------------- */
+/* Workspace bytes for num_seqs requests of length <= max_seq_len and
+ * q_head_count local heads (partials of every split + the split offsets). */
+HETIS_API hetis_status hetis_attn_decode_workspace(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_count,
+                                         int32_t max_seq_len, size_t *bytes);
+
+/* Kernel 1 (a4): split-KV partial attention.  For every (request j, local kv
+ * head g, split s covering tokens [s C, min((s+1) C, L_j))) and each of the r
+ * query heads of g: o_s = softmax-weighted mean of V over the split and its
+ * log2-sum-exp, written to the workspace.  Arguments:
+ *   q_head_begin, q_head_count: this device's global head range (multiples
+ *       of r; only validated -- indexing is local)
+ *   q          : device [num_seqs][q_head_count][head_dim], q_dtype
+ *   k_pool, v_pool, num_pages, block_table, max_pages, seq_lens: as in
+ *       hetis_kv_append with kv_head_count = q_head_count / r
+ *   max_seq_len: upper bound of seq_lens (workspace sizing)
+ *   workspace  : device, >= hetis_attn_decode_workspace bytes, 256-B aligned
+ *   flags      : HETIS_ATTN_* */
+HETIS_API hetis_status hetis_attn_partial(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
+                                int32_t q_head_count, const void *q, const void *k_pool, const void *v_pool,
+                                int64_t num_pages, const int32_t *block_table, int32_t max_pages,
+                                const int32_t *seq_lens, int32_t max_seq_len, void *workspace,
+                                size_t workspace_bytes, uint32_t flags, hetis_stream_t stream);
+
+/* Kernel 2 (a5): o = sum_s 2^(lse_s - lse) o_s in ascending s (fixed order).
+ *   o : device [num_seqs][q_head_count][head_dim] (o_dtype), rows of request j
+ *       start at o + j * o_seq_stride elements (o_seq_stride >= q_head_count *
+ *       head_dim; pass q_head_count * head_dim for a dense shard). */
+HETIS_API hetis_status hetis_attn_combine(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_count,
+                                const int32_t *seq_lens, int32_t max_seq_len, void *o, int64_t o_seq_stride,
+                                const void *workspace, size_t workspace_bytes, hetis_stream_t stream);
+
+/* hetis_attn_partial followed by hetis_attn_combine with a dense o shard. */
+HETIS_API hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
+                               int32_t q_head_count, const void *q, const void *k_pool, const void *v_pool,
+                               int64_t num_pages, const int32_t *block_table, int32_t max_pages,
+                               const int32_t *seq_lens, int32_t max_seq_len, void *o, void *workspace,
+                               size_t workspace_bytes, uint32_t flags, hetis_stream_t stream);
+
+/* ---- scatter / gather over NCCL ------------------- */
+/* nccl_comm is an ncclComm_t (e.g. torch ProcessGroupNCCL._comm_ptr()) whose
+ * ranks are the plan's devices.  libnccl.so.2 is resolved at first use from
+ * the process (dlopen by soname); absent -> HETIS_E_NCCL.  Only global plans
+ * (per_request == 0) are supported here -> else HETIS_E_UNSUPPORTED.
+ *
+ * Staging bytes needed on `rank` by scatter and gather with this plan. */
+HETIS_API hetis_status hetis_comm_workspace(const hetis_plan *plan, int32_t rank, int32_t num_seqs, size_t *bytes);
+
+/* Root holds q_full [num_seqs][H][d] and k_new_full, v_new_full
+ * [num_seqs][H_kv][d] (q/kv dtypes); every rank receives its shards
+ * q_shard [num_seqs][x_rank][d] and k/v_new_shard [num_seqs][x_rank/r][d].
+ * Non-root ranks may pass NULL for the *_full pointers. */
+HETIS_API hetis_status hetis_scatter_q(const hetis_plan *plan, void *nccl_comm, int32_t rank, int32_t root,
+                             int32_t num_seqs, const void *q_full, const void *k_new_full,
+                             const void *v_new_full, void *q_shard, void *k_new_shard, void *v_new_shard,
+                             void *workspace, size_t workspace_bytes, hetis_stream_t stream);
+
+/* o_shard [num_seqs][x_rank][d] (o_dtype) from every rank -> o_full
+ * [num_seqs][H][d] with each head at its GLOBAL index (reading 4).
+ * root == -1: every rank receives o_full (all-gather, north star);
+ * root >= 0: only root does (gather to the Primary worker). */
+HETIS_API hetis_status hetis_gather(const hetis_plan *plan, void *nccl_comm, int32_t rank, int32_t root, int32_t num_seqs,
+                          const void *o_shard, void *o_full, void *workspace, size_t workspace_bytes,
+                          hetis_stream_t stream);
+
+/* Number of kernels this library has launched in the calling process (all
+ * threads) -- for the bench's gpu_launches accounting. */
+HETIS_API uint64_t hetis_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HETIS_H_ */

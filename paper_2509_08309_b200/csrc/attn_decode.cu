@@ -1,0 +1,782 @@
+// attn_decode.cu -- split-KV paged decode attention for sm_100a.
+//
+// result_{i,j} = softmax(q_{h} K_g^T / sqrt(d)) V_g for the heads h of this
+// device (Eq. 2b), K/V read from head-granular pages
+// (PAPER.md:539).  Each work item is (request j, local kv head g, split s)
+// covering tokens [s C, min((s+1) C, L_j)), C = kSplitTokens (reading 12), and
+// produces, for the r query heads of g, the normalised partial o_s and its
+// log2-sum-exp; attn_combine.cu merges the splits.
+//
+// Kernel structure (both variants), one persistent CTA per SM:
+//   warp 0      producer: decodes items, streams the item's q rows and every
+//               K/V page of the item into a ring of shared-memory stages with
+//               TMA (cp.async.bulk / cp.async.bulk.tensor) completing on
+//               mbarriers; the block-table entries of the next item are
+//               prefetched while the current item's pages are issued.
+//   warps 1..NW consumers: page p of an item goes to consumer warp p mod NW;
+//               each warp runs an fp32 online softmax over its pages; at the
+//               end of an item the NW partial states are merged in fixed warp
+//               order through shared memory (deterministic; depends on L_j only).
+// Variants:
+//   simt : CUDA cores.  q.k with fma.rn.f32.bf16 (exact bf16 products, fp32
+//          accumulate) or fp32 FFMA; p.v in fp32.  Any r, bf16 or fp32.
+//   tc   : bf16, r in {2,4,8}: the r query heads sharing a kv head form the
+//          M rows of mma.sync.m16n8k16 (rows r..7 zero).  S = Q K^T in bf16 with
+//          fp32 accumulate; P V with P split as P_hi + P_lo (two bf16 terms)
+//          carried in rows 8..15 of the same MMA, so P is effectively
+//          represented to ~2^-16 relative at no extra MMA cost.  K/V pages are
+//          loaded by 2-D TMA with the 128-byte swizzle so ldmatrix is
+//          bank-conflict free.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "device_utils.cuh"
+#include "hetis_internal.h"
+
+namespace hetis {
+
+namespace {
+
+constexpr int kP = kPageSize;
+constexpr int kC = kSplitTokens;
+constexpr int kPagesPerItem = kC / kP;  // 16
+constexpr int kQSlots = 2;
+constexpr int kMaxSmem = 227 * 1024;
+static_assert(kPagesPerItem <= 32, "one producer lane per page of an item");
+
+struct Params {
+    const uint8_t *q;
+    const uint8_t *k_pool;
+    const uint8_t *v_pool;
+    const int32_t *block_table;
+    const int32_t *seq_lens;
+    int32_t *split_off_out;  // global copy for the combine kernel
+    float *part_lse;
+    float *part_o;
+    int num_seqs;
+    int q_heads;   // local
+    int kv_heads;  // local
+    int max_pages;
+    int stages;    // ring depth
+    float scale_log2;  // log2(e) / sqrt(d)
+};
+
+struct ItemMeta {
+    int item;
+    int ntok;
+    int npages;
+    int pad;
+};
+
+__device__ __forceinline__ int upper_bound_smem(const int32_t *a, int n, int key) {
+    // first index i in [0, n) with a[i] > key
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] <= key)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// Block-wide: seq_lens -> smem copy and exclusive prefix of ceil(L/C).
+__device__ void build_split_offsets(const Params &p, int32_t *s_len, int32_t *s_off) {
+    const int B = p.num_seqs;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    __shared__ int32_t s_warp[32];
+    // each thread sums a contiguous chunk
+    const int per = (B + nt - 1) / nt;
+    const int b0 = tid * per, b1 = min(B, b0 + per);
+    int sum = 0;
+    for (int j = b0; j < b1; ++j) {
+        int L = p.seq_lens[j];
+        s_len[j] = L;
+        sum += (L + kC - 1) / kC;
+    }
+    // block exclusive scan of `sum`
+    const int lane = tid & 31, warp = tid >> 5;
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int nw = (nt + 31) / 32;
+        int v = lane < nw ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        if (lane < nw) s_warp[lane] = v;  // inclusive per-warp totals
+    }
+    __syncthreads();
+    int run = incl - sum + (warp > 0 ? s_warp[warp - 1] : 0);
+    for (int j = b0; j < b1; ++j) {
+        s_off[j] = run;
+        run += (s_len[j] + kC - 1) / kC;
+    }
+    __syncthreads();
+    if (tid == 0) s_off[B] = B > 0 ? s_off[B - 1] + (s_len[B - 1] + kC - 1) / kC : 0;
+    __syncthreads();
+    if (blockIdx.x == 0) {
+        for (int j = tid; j <= B; j += nt) p.split_off_out[j] = s_off[j];
+    }
+}
+
+// ---------------------------------------------------------------- producer
+// COPY = 0: two 1-D bulk copies per page (K, V).  COPY = 1: four 2-D tensor
+// copies per page (K, V halves of 64 elements, 128-B swizzle).
+template <int ROW_BYTES, int R, int COPY>
+__device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta *qmeta, uint64_t *full,
+                         uint64_t *empty, uint64_t *qfull, uint64_t *qempty, const int32_t *s_len,
+                         const int32_t *s_off, const void *tmap_k, const void *tmap_v) {
+    constexpr int kPageBytes = kP * ROW_BYTES;
+    constexpr int kStageBytes = 2 * kPageBytes;
+    constexpr int kQBytes = R * ROW_BYTES;
+    constexpr int kQStride = (kQBytes + 127) / 128 * 128;
+    const int lane = threadIdx.x & 31;
+    const int n_items = s_off[p.num_seqs] * p.kv_heads;
+    const uint64_t pol_stream = dev::policy_evict_first();
+    const uint64_t pol_q = dev::policy_evict_first();
+    if (COPY == 1 && lane == 0) {
+        dev::prefetch_tmap(tmap_k);
+        dev::prefetch_tmap(tmap_v);
+    }
+
+    // decode an item index into (seq, kv head, first token, token count)
+    auto decode = [&](int item, int &j, int &g, int &t0, int &ntok) {
+        const int k = item / p.kv_heads;
+        g = item - k * p.kv_heads;
+        j = upper_bound_smem(s_off, p.num_seqs + 1, k) - 1;
+        const int s = k - s_off[j];
+        t0 = s * kC;
+        ntok = min(kC, s_len[j] - t0);
+    };
+    auto issue_q = [&](int it, int item) {
+        int j, g, t0, ntok;
+        decode(item, j, g, t0, ntok);
+        const int slot = it % kQSlots;
+        if (lane == 0) {
+            if (it >= kQSlots) dev::mbar_wait(&qempty[slot], ((it / kQSlots) - 1) & 1);
+            qmeta[slot] = ItemMeta{item, ntok, (ntok + kP - 1) / kP, 0};
+            dev::mbar_arrive_expect_tx(&qfull[slot], kQBytes);
+            const uint8_t *src = p.q + ((size_t)j * p.q_heads + (size_t)g * R) * ROW_BYTES;
+            dev::bulk_g2s(qbuf + (size_t)slot * kQStride, src, kQBytes, &qfull[slot], pol_q);
+        }
+        __syncwarp();
+    };
+    auto load_pids = [&](int item) -> int32_t {
+        int j, g, t0, ntok;
+        decode(item, j, g, t0, ntok);
+        const int np = (ntok + kP - 1) / kP;
+        int32_t pid = 0;
+        if (lane < np) pid = __ldg(p.block_table + ((size_t)j * p.kv_heads + g) * p.max_pages + t0 / kP + lane);
+        return pid;
+    };
+
+    int it = 0;
+    int item = blockIdx.x;
+    if (item >= n_items) return;
+    issue_q(0, item);
+    int32_t pid = load_pids(item);
+    uint32_t n = 0;  // pages issued by this CTA
+    int stage = 0;
+    for (; item < n_items; item += gridDim.x, ++it) {
+        const int next = item + gridDim.x;
+        int32_t pid_next = 0;
+        if (next < n_items) {
+            issue_q(it + 1, next);
+            pid_next = load_pids(next);
+        }
+        int j, g, t0, ntok;
+        decode(item, j, g, t0, ntok);
+        const int np = (ntok + kP - 1) / kP;
+        for (int pg = 0; pg < np; ++pg) {
+            const int32_t page = __shfl_sync(0xffffffffu, pid, pg);
+            if (lane == 0) {
+                if (n >= (uint32_t)p.stages) dev::mbar_wait(&empty[stage], ((n / p.stages) - 1) & 1);
+                uint8_t *dst = ring + (size_t)stage * kStageBytes;
+                dev::mbar_arrive_expect_tx(&full[stage], kStageBytes);
+                if (COPY == 0) {
+                    const size_t off = (size_t)page * kPageBytes;
+                    dev::bulk_g2s(dst, p.k_pool + off, kPageBytes, &full[stage], pol_stream);
+                    dev::bulk_g2s(dst + kPageBytes, p.v_pool + off, kPageBytes, &full[stage], pol_stream);
+                } else {
+                    // one 64-column block (16 rows x 128 B, swizzled) per TMA
+                    const int row = page * kP;
+#pragma unroll
+                    for (int cb = 0; cb < ROW_BYTES / 128; ++cb) {
+                        dev::tma_load_2d(dst + cb * 2048, tmap_k, 64 * cb, row, &full[stage], pol_stream);
+                        dev::tma_load_2d(dst + kPageBytes + cb * 2048, tmap_v, 64 * cb, row, &full[stage], pol_stream);
+                    }
+                }
+            }
+            __syncwarp();
+            ++n;
+            if (++stage == p.stages) stage = 0;
+        }
+        pid = pid_next;
+    }
+}
+
+// ---------------------------------------------------------------- merge of NW warp states
+// mbuf layout: [NW][R][D + 2] floats: acc[D], m (log2 domain), l.
+template <int D, int R, int NW>
+__device__ __forceinline__ void merge_and_store(const Params &p, const float *mbuf, int item, int ctid) {
+    constexpr int kRow = D + 2;
+    for (int e = ctid; e < R * D; e += NW * 32) {
+        const int rr = e / D, d = e - rr * D;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) M = fmaxf(M, mbuf[(w * R + rr) * kRow + D]);
+        float lsum = 0.f, a = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const float mw = mbuf[(w * R + rr) * kRow + D];
+            const float f = (mw == -INFINITY) ? 0.f : dev::ex2(mw - M);
+            lsum = fmaf(f, mbuf[(w * R + rr) * kRow + D + 1], lsum);
+            a = fmaf(f, mbuf[(w * R + rr) * kRow + d], a);
+        }
+        const size_t row = (size_t)item * R + rr;
+        p.part_o[row * D + d] = __fdiv_rn(a, lsum);
+        if (d == 0) p.part_lse[row] = M + __log2f(lsum);
+    }
+}
+
+// ---------------------------------------------------------------- simt consumer
+template <int DT, int D, int R, int NW>
+__device__ void consumer_simt(const Params &p, const uint8_t *ring, const uint8_t *qbuf, const ItemMeta *qmeta,
+                              uint64_t *full, uint64_t *empty, uint64_t *qfull, uint64_t *qempty, float *mbuf,
+                              int n_items) {
+    constexpr int EB = DT == HETIS_BF16 ? 2 : 4;
+    constexpr int ROW_BYTES = D * EB;
+    constexpr int kPageBytes = kP * ROW_BYTES;
+    constexpr int kStageBytes = 2 * kPageBytes;
+    constexpr int kQBytes = R * ROW_BYTES;
+    constexpr int kQStride = (kQBytes + 127) / 128 * 128;
+    constexpr int LPT = ROW_BYTES / 16;  // lanes per token row
+    constexpr int TPS = 32 / LPT;        // tokens per step
+    constexpr int STEPS = kP / TPS;      // steps per page
+    constexpr int EPL = 16 / EB;         // elements per lane chunk
+    static_assert(LPT >= 1 && LPT <= 32 && TPS * LPT == 32, "row must be 16..512 bytes");
+
+    const int lane = threadIdx.x & 31;
+    const int cw = (threadIdx.x >> 5) - 1;  // consumer warp index
+    const int ctid = threadIdx.x - 32;
+    const int ltok = lane / LPT, lchk = lane % LPT;
+
+    uint32_t n_base = 0;
+    int it = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        const int slot = it % kQSlots;
+        dev::mbar_wait(&qfull[slot], (it / kQSlots) & 1);
+        const ItemMeta meta = qmeta[slot];
+        // q chunk of every head: EPL elements at lchk
+        uint4 qv[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr)
+            qv[rr] = *reinterpret_cast<const uint4 *>(qbuf + (size_t)slot * kQStride + rr * ROW_BYTES + lchk * 16);
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&qempty[slot]);
+
+        float m[R], l[R], acc[R][EPL];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+            m[rr] = -INFINITY;
+            l[rr] = 0.f;
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) acc[rr][e] = 0.f;
+        }
+
+        int stage = (int)((n_base + cw) % (uint32_t)p.stages);
+        for (int pg = cw; pg < meta.npages; pg += NW) {
+            const uint32_t n = n_base + pg;
+            dev::mbar_wait(&full[stage], (n / p.stages) & 1);
+            const uint8_t *kb = ring + (size_t)stage * kStageBytes;
+            const uint8_t *vb = kb + kPageBytes;
+            const int valid = min(kP, meta.ntok - pg * kP);
+
+            uint4 kr[STEPS];
+#pragma unroll
+            for (int i = 0; i < STEPS; ++i)
+                kr[i] = *reinterpret_cast<const uint4 *>(kb + (i * TPS + ltok) * ROW_BYTES + lchk * 16);
+            float pr[R][STEPS];
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+                float s[STEPS];
+#pragma unroll
+                for (int i = 0; i < STEPS; ++i) {
+                    float acc_s = 0.f;
+                    if constexpr (DT == HETIS_BF16) {
+                        acc_s = dev::fma_bf16x2(qv[rr].x, kr[i].x, acc_s);
+                        acc_s = dev::fma_bf16x2(qv[rr].y, kr[i].y, acc_s);
+                        acc_s = dev::fma_bf16x2(qv[rr].z, kr[i].z, acc_s);
+                        acc_s = dev::fma_bf16x2(qv[rr].w, kr[i].w, acc_s);
+                    } else {
+                        acc_s = fmaf(__uint_as_float(qv[rr].x), __uint_as_float(kr[i].x), acc_s);
+                        acc_s = fmaf(__uint_as_float(qv[rr].y), __uint_as_float(kr[i].y), acc_s);
+                        acc_s = fmaf(__uint_as_float(qv[rr].z), __uint_as_float(kr[i].z), acc_s);
+                        acc_s = fmaf(__uint_as_float(qv[rr].w), __uint_as_float(kr[i].w), acc_s);
+                    }
+                    s[i] = acc_s;
+                }
+#pragma unroll
+                for (int i = 0; i < STEPS; ++i) {
+#pragma unroll
+                    for (int o = LPT / 2; o >= 1; o >>= 1) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
+                    const int t = i * TPS + ltok;
+                    s[i] = (t < valid) ? s[i] * p.scale_log2 : -INFINITY;
+                }
+                float mx = s[0];
+#pragma unroll
+                for (int i = 1; i < STEPS; ++i) mx = fmaxf(mx, s[i]);
+#pragma unroll
+                for (int o = 16; o >= LPT; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                const float m_new = fmaxf(m[rr], mx);
+                const float alpha = dev::ex2(m[rr] - m_new);  // m = -inf -> 0
+                float ls = 0.f;
+#pragma unroll
+                for (int i = 0; i < STEPS; ++i) {
+                    pr[rr][i] = dev::ex2(s[i] - m_new);
+                    ls += pr[rr][i];
+                }
+                l[rr] = fmaf(l[rr], alpha, ls);
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) acc[rr][e] *= alpha;
+                m[rr] = m_new;
+            }
+            // p . v
+#pragma unroll
+            for (int i = 0; i < STEPS; ++i) {
+                const int t = i * TPS + ltok;
+                if (t < valid) {
+                    const uint4 vr = *reinterpret_cast<const uint4 *>(vb + t * ROW_BYTES + lchk * 16);
+                    float v[EPL];
+                    if constexpr (DT == HETIS_BF16) {
+                        v[0] = dev::bf16lo(vr.x); v[1] = dev::bf16hi(vr.x);
+                        v[2] = dev::bf16lo(vr.y); v[3] = dev::bf16hi(vr.y);
+                        v[4] = dev::bf16lo(vr.z); v[5] = dev::bf16hi(vr.z);
+                        v[6] = dev::bf16lo(vr.w); v[7] = dev::bf16hi(vr.w);
+                    } else {
+                        v[0] = __uint_as_float(vr.x); v[1] = __uint_as_float(vr.y);
+                        v[2] = __uint_as_float(vr.z); v[3] = __uint_as_float(vr.w);
+                    }
+#pragma unroll
+                    for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+                        for (int e = 0; e < EPL; ++e) acc[rr][e] = fmaf(pr[rr][i], v[e], acc[rr][e]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) dev::mbar_arrive(&empty[stage]);
+            stage += NW;
+            while (stage >= p.stages) stage -= p.stages;
+        }
+        n_base += meta.npages;
+
+        // fold token groups of this warp
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+#pragma unroll
+            for (int o = 16; o >= LPT; o >>= 1) {
+                l[rr] += __shfl_xor_sync(0xffffffffu, l[rr], o);
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) acc[rr][e] += __shfl_xor_sync(0xffffffffu, acc[rr][e], o);
+            }
+        }
+        constexpr int kRow = D + 2;
+        if (ltok == 0) {
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+                float *row = mbuf + (cw * R + rr) * kRow;
+#pragma unroll
+                for (int e = 0; e < EPL; ++e) row[lchk * EPL + e] = acc[rr][e];
+                if (lchk == 0) {
+                    row[D] = m[rr];
+                    row[D + 1] = l[rr];
+                }
+            }
+        }
+        dev::named_bar_sync(1, NW * 32);
+        merge_and_store<D, R, NW>(p, mbuf, meta.item, ctid);
+        dev::named_bar_sync(1, NW * 32);
+    }
+}
+
+// ---------------------------------------------------------------- tensor-core consumer (bf16, r <= 8, D = 64/128)
+template <int D, int R, int NW>
+__device__ void consumer_tc(const Params &p, const uint8_t *ring, const uint8_t *qbuf, const ItemMeta *qmeta,
+                            uint64_t *full, uint64_t *empty, uint64_t *qfull, uint64_t *qempty, float *mbuf,
+                            int n_items) {
+    constexpr int ROW_BYTES = D * 2;
+    constexpr int kPageBytes = kP * ROW_BYTES;
+    constexpr int kHalfBytes = kPageBytes / (D / 64);  // one 64-element column block: 16 rows x 128 B
+    constexpr int kStageBytes = 2 * kPageBytes;
+    constexpr int kQBytes = R * ROW_BYTES;
+    constexpr int kQStride = (kQBytes + 127) / 128 * 128;
+    constexpr int KSTEPS = D / 16;
+    constexpr int NT_O = D / 8;  // output n-tiles
+    static_assert(R <= 8, "r query heads must fit the 8 M rows");
+
+    const int lane = threadIdx.x & 31;
+    const int cw = (threadIdx.x >> 5) - 1;
+    const int ctid = threadIdx.x - 32;
+    const int grp = lane >> 2;  // head row 0..7
+    const int tq = lane & 3;
+
+    // smem byte offset (within a K or V page) of 16-B chunk c of token row t, 128-B swizzle
+    auto swz = [](int t, int c) -> uint32_t {
+        const int half = c >> 3, cc = c & 7;
+        return (uint32_t)(half * kHalfBytes + t * 128 + ((cc ^ (t & 7)) << 4));
+    };
+    // per-lane ldmatrix addresses (relative to a page base)
+    uint32_t k_off[2][KSTEPS / 2];  // [n-tile][pair of k-steps]
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int q4 = 0; q4 < KSTEPS / 2; ++q4) k_off[nt][q4] = swz(8 * nt + (lane & 7), 4 * q4 + (lane >> 3));
+    uint32_t v_off[NT_O / 2];
+#pragma unroll
+    for (int c2 = 0; c2 < NT_O / 2; ++c2) {
+        const int mi = lane >> 3;
+        v_off[c2] = swz((mi & 1) * 8 + (lane & 7), 2 * c2 + (mi >> 1));
+    }
+
+    uint32_t n_base = 0;
+    int it = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        const int slot = it % kQSlots;
+        dev::mbar_wait(&qfull[slot], (it / kQSlots) & 1);
+        const ItemMeta meta = qmeta[slot];
+        // A fragments of Q: row grp (zero if grp >= R), k-step ks: reg0 cols 16ks+2tq, reg2 cols +8
+        uint32_t qa[KSTEPS][2];
+        {
+            const uint8_t *qs = qbuf + (size_t)slot * kQStride;
+#pragma unroll
+            for (int ks = 0; ks < KSTEPS; ++ks) {
+                if (grp < R) {
+                    qa[ks][0] = *reinterpret_cast<const uint32_t *>(qs + grp * ROW_BYTES + (16 * ks + 2 * tq) * 2);
+                    qa[ks][1] = *reinterpret_cast<const uint32_t *>(qs + grp * ROW_BYTES + (16 * ks + 8 + 2 * tq) * 2);
+                } else {
+                    qa[ks][0] = 0u;
+                    qa[ks][1] = 0u;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&qempty[slot]);
+
+        float m = -INFINITY, l = 0.f;
+        float o[NT_O][4];
+#pragma unroll
+        for (int nt = 0; nt < NT_O; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
+
+        int stage = (int)((n_base + cw) % (uint32_t)p.stages);
+        for (int pg = cw; pg < meta.npages; pg += NW) {
+            const uint32_t n = n_base + pg;
+            dev::mbar_wait(&full[stage], (n / p.stages) & 1);
+            const uint32_t kb = dev::smem_u32(ring + (size_t)stage * kStageBytes);
+            const uint32_t vb = kb + kPageBytes;
+            const int valid = min(kP, meta.ntok - pg * kP);
+
+            // S = Q K^T : 2 n-tiles of 8 tokens
+            float s[2][4];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+                for (int q4 = 0; q4 < KSTEPS / 2; ++q4) {
+                    uint32_t b[4];
+                    dev::ldmatrix_x4(b, kb + k_off[nt][q4]);
+                    dev::mma_bf16_16816(s[nt], qa[2 * q4][0], 0u, qa[2 * q4][1], 0u, b[0], b[1]);
+                    dev::mma_bf16_16816(s[nt], qa[2 * q4 + 1][0], 0u, qa[2 * q4 + 1][1], 0u, b[2], b[3]);
+                }
+            }
+            // scores of row grp: tokens 8nt + 2tq + e
+            float sc[4];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int t = 8 * nt + 2 * tq + e;
+                    sc[2 * nt + e] = (t < valid) ? s[nt][e] * p.scale_log2 : -INFINITY;
+                }
+            float mx = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            const float m_new = fmaxf(m, mx);
+            if (__any_sync(0xffffffffu, m_new != m)) {
+                const float alpha = dev::ex2(m - m_new);
+                l *= alpha;
+#pragma unroll
+                for (int nt = 0; nt < NT_O; ++nt) {
+                    o[nt][0] *= alpha; o[nt][1] *= alpha; o[nt][2] *= alpha; o[nt][3] *= alpha;
+                }
+                m = m_new;
+            }
+            float pp[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                pp[e] = dev::ex2(sc[e] - m);
+                l += pp[e];
+            }
+            // P = P_hi + P_lo (bf16 each): rows grp carry P_hi, rows grp + 8 carry P_lo
+            uint32_t pa[4];
+            {
+                __nv_bfloat162 h0 = __floats2bfloat162_rn(pp[0], pp[1]);
+                __nv_bfloat162 h1 = __floats2bfloat162_rn(pp[2], pp[3]);
+                const float2 f0 = __bfloat1622float2(h0), f1 = __bfloat1622float2(h1);
+                __nv_bfloat162 l0 = __floats2bfloat162_rn(pp[0] - f0.x, pp[1] - f0.y);
+                __nv_bfloat162 l1 = __floats2bfloat162_rn(pp[2] - f1.x, pp[3] - f1.y);
+                pa[0] = *reinterpret_cast<uint32_t *>(&h0);
+                pa[1] = *reinterpret_cast<uint32_t *>(&l0);
+                pa[2] = *reinterpret_cast<uint32_t *>(&h1);
+                pa[3] = *reinterpret_cast<uint32_t *>(&l1);
+            }
+            // tail: V rows past `valid` may hold anything (NaN) -- 0 * NaN = NaN inside the MMA
+            uint32_t mk0 = 0xffffffffu, mk1 = 0xffffffffu;
+            if (valid < kP) {
+                const int t0 = 2 * tq, t1 = 8 + 2 * tq;
+                mk0 = (t0 < valid ? 0x0000ffffu : 0u) | (t0 + 1 < valid ? 0xffff0000u : 0u);
+                mk1 = (t1 < valid ? 0x0000ffffu : 0u) | (t1 + 1 < valid ? 0xffff0000u : 0u);
+            }
+#pragma unroll
+            for (int c2 = 0; c2 < NT_O / 2; ++c2) {
+                uint32_t b[4];
+                dev::ldmatrix_x4_trans(b, vb + v_off[c2]);
+                dev::mma_bf16_16816(o[2 * c2], pa[0], pa[1], pa[2], pa[3], b[0] & mk0, b[1] & mk1);
+                dev::mma_bf16_16816(o[2 * c2 + 1], pa[0], pa[1], pa[2], pa[3], b[2] & mk0, b[3] & mk1);
+            }
+            __syncwarp();
+            if (lane == 0) dev::mbar_arrive(&empty[stage]);
+            stage += NW;
+            while (stage >= p.stages) stage -= p.stages;
+        }
+        n_base += meta.npages;
+
+        l += __shfl_xor_sync(0xffffffffu, l, 1);
+        l += __shfl_xor_sync(0xffffffffu, l, 2);
+        constexpr int kRow = D + 2;
+        if (grp < R) {
+            float *row = mbuf + (cw * R + grp) * kRow;
+#pragma unroll
+            for (int nt = 0; nt < NT_O; ++nt) {
+                row[8 * nt + 2 * tq] = o[nt][0] + o[nt][2];
+                row[8 * nt + 2 * tq + 1] = o[nt][1] + o[nt][3];
+            }
+            if (tq == 0) {
+                row[D] = m;
+                row[D + 1] = l;
+            }
+        }
+        dev::named_bar_sync(1, NW * 32);
+        merge_and_store<D, R, NW>(p, mbuf, meta.item, ctid);
+        dev::named_bar_sync(1, NW * 32);
+    }
+}
+
+// ---------------------------------------------------------------- kernels
+template <int DT, int D, int R, int NW, bool TC>
+__global__ void __launch_bounds__(32 * (NW + 1), 1)
+    attn_decode_kernel(const Params p, const __grid_constant__ CUtensorMap tmap_k,
+                       const __grid_constant__ CUtensorMap tmap_v) {
+    constexpr int EB = DT == HETIS_BF16 ? 2 : 4;
+    constexpr int ROW_BYTES = D * EB;
+    constexpr int kQBytes = R * ROW_BYTES;
+    constexpr int kQStride = (kQBytes + 127) / 128 * 128;
+    constexpr int kStageBytes = 2 * kP * ROW_BYTES;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // TMA with the 128-B swizzle wants 1024-B aligned destinations
+    uint8_t *smem = smem_raw + ((1024u - (dev::smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t *ring = smem;
+    uint8_t *qbuf = ring + (size_t)p.stages * kStageBytes;
+    float *mbuf = reinterpret_cast<float *>(qbuf + kQSlots * kQStride);
+    const size_t mbuf_bytes = (size_t)NW * R * (D + 2) * sizeof(float);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(mbuf) + ((mbuf_bytes + 15) / 16 * 16));
+    uint64_t *full = bars;
+    uint64_t *empty = full + p.stages;
+    uint64_t *qfull = empty + p.stages;
+    uint64_t *qempty = qfull + kQSlots;
+    ItemMeta *qmeta = reinterpret_cast<ItemMeta *>(qempty + kQSlots);
+    int32_t *s_len = reinterpret_cast<int32_t *>(qmeta + kQSlots);
+    int32_t *s_off = s_len + p.num_seqs;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < p.stages; ++i) {
+            dev::mbar_init(&full[i], 1);
+            dev::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < kQSlots; ++i) {
+            dev::mbar_init(&qfull[i], 1);
+            dev::mbar_init(&qempty[i], NW);
+        }
+        dev::fence_barrier_init();
+    }
+    build_split_offsets(p, s_len, s_off);  // contains __syncthreads
+    const int n_items = s_off[p.num_seqs] * p.kv_heads;
+
+    if (threadIdx.x < 32) {
+        producer<ROW_BYTES, R, TC ? 1 : 0>(p, ring, qbuf, qmeta, full, empty, qfull, qempty, s_len, s_off, &tmap_k,
+                                           &tmap_v);
+    } else {
+        if constexpr (TC) {
+            consumer_tc<D, R, NW>(p, ring, qbuf, qmeta, full, empty, qfull, qempty, mbuf, n_items);
+        } else {
+            consumer_simt<DT, D, R, NW>(p, ring, qbuf, qmeta, full, empty, qfull, qempty, mbuf, n_items);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- host side
+template <int DT, int D, int R, bool TC>
+struct Launch {
+    static constexpr int NW = 8;
+    static constexpr int EB = DT == HETIS_BF16 ? 2 : 4;
+    static constexpr int ROW_BYTES = D * EB;
+    static constexpr int kStageBytes = 2 * kP * ROW_BYTES;
+    static constexpr int kQStride = (R * ROW_BYTES + 127) / 128 * 128;
+
+    static size_t fixed_bytes(int num_seqs, int stages) {
+        size_t mb = (size_t)NW * R * (D + 2) * sizeof(float);
+        mb = (mb + 15) / 16 * 16;
+        return (size_t)kQSlots * kQStride + mb + (size_t)(2 * stages + 2 * kQSlots) * 8 +
+               (size_t)kQSlots * sizeof(ItemMeta) + (size_t)(2 * num_seqs + 1) * 4;
+    }
+
+    static cudaError_t run(const Params &p0, int num_seqs, cudaStream_t s, const CUtensorMap &tk,
+                           const CUtensorMap &tv, std::string *err) {
+        Params p = p0;
+        // ring depth: as deep as shared memory allows, at most 24 stages
+        int stages = 24;
+        while (stages > 4 && (size_t)stages * kStageBytes + fixed_bytes(num_seqs, stages) + 1024 > (size_t)kMaxSmem)
+            --stages;
+        const size_t smem = (size_t)stages * kStageBytes + fixed_bytes(num_seqs, stages) + 1024;
+        if (smem > (size_t)kMaxSmem) {
+            if (err) *err = "batch too large for the shared-memory split table";
+            return cudaErrorInvalidValue;
+        }
+        p.stages = stages;
+        auto kern = attn_decode_kernel<DT, D, R, NW, TC>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        const int grid = num_sms();
+        kern<<<grid, 32 * (NW + 1), smem, s>>>(p, tk, tv);
+        note_launch();
+        return cudaGetLastError();
+    }
+};
+
+Params make_params(const AttnArgs &a) {
+    Params p{};
+    p.q = static_cast<const uint8_t *>(a.q);
+    p.k_pool = static_cast<const uint8_t *>(a.k_pool);
+    p.v_pool = static_cast<const uint8_t *>(a.v_pool);
+    p.block_table = a.block_table;
+    p.seq_lens = a.seq_lens;
+    p.split_off_out = a.split_off;
+    p.part_lse = a.part_lse;
+    p.part_o = a.part_o;
+    p.num_seqs = a.num_seqs;
+    p.q_heads = a.q_heads;
+    p.kv_heads = a.kv_heads;
+    p.max_pages = a.max_pages;
+    p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)a.head_dim));
+    return p;
+}
+
+template <int DT, int D, bool TC>
+cudaError_t dispatch_r(const AttnArgs &a, const Params &p, cudaStream_t s, const CUtensorMap &tk,
+                       const CUtensorMap &tv, std::string *err) {
+    switch (a.r) {
+        case 1:
+            if constexpr (!TC) return Launch<DT, D, 1, false>::run(p, a.num_seqs, s, tk, tv, err);
+            break;
+        case 2: return Launch<DT, D, 2, TC>::run(p, a.num_seqs, s, tk, tv, err);
+        case 4: return Launch<DT, D, 4, TC>::run(p, a.num_seqs, s, tk, tv, err);
+        case 8: return Launch<DT, D, 8, TC>::run(p, a.num_seqs, s, tk, tv, err);
+        default: break;
+    }
+    if (err) *err = "unsupported r";
+    return cudaErrorInvalidValue;
+}
+
+// ---- TMA descriptors (driver entry point resolved through the runtime; no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+    static std::once_flag once;
+    static EncodeTiledFn fn = nullptr;
+    std::call_once(once, [] {
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    });
+    return fn;
+}
+
+// 2-D map over a pool [num_pages * P rows][D] bf16 with box {64, 16} and 128-B swizzle.
+bool make_pool_map(CUtensorMap *m, const void *pool, int64_t num_pages, int D, std::string *err) {
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) {
+        if (err) *err = "cuTensorMapEncodeTiled unavailable";
+        return false;
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)(num_pages * kP)};
+    cuuint64_t strides[1] = {(cuuint64_t)D * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)kP};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(pool), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        if (err) *err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+        return false;
+    }
+    return true;
+}
+
+}  // namespace
+
+cudaError_t launch_attn_simt(const AttnArgs &a, cudaStream_t s) {
+    Params p = make_params(a);
+    CUtensorMap dummy;
+    std::memset(&dummy, 0, sizeof dummy);
+    std::string err;
+    if (a.dtype == HETIS_BF16) {
+        if (a.head_dim == 128) return dispatch_r<HETIS_BF16, 128, false>(a, p, s, dummy, dummy, &err);
+        if (a.head_dim == 64) return dispatch_r<HETIS_BF16, 64, false>(a, p, s, dummy, dummy, &err);
+    } else {
+        if (a.head_dim == 128) return dispatch_r<HETIS_F32, 128, false>(a, p, s, dummy, dummy, &err);
+        if (a.head_dim == 64) return dispatch_r<HETIS_F32, 64, false>(a, p, s, dummy, dummy, &err);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_attn_tc(const AttnArgs &a, cudaStream_t s, std::string *err) {
+    Params p = make_params(a);
+    CUtensorMap tk, tv;
+    if (!make_pool_map(&tk, a.k_pool, a.num_pages, a.head_dim, err)) return cudaErrorInvalidValue;
+    if (!make_pool_map(&tv, a.v_pool, a.num_pages, a.head_dim, err)) return cudaErrorInvalidValue;
+    if (a.head_dim == 128) return dispatch_r<HETIS_BF16, 128, true>(a, p, s, tk, tv, err);
+    if (a.head_dim == 64) return dispatch_r<HETIS_BF16, 64, true>(a, p, s, tk, tv, err);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace hetis

@@ -1,0 +1,67 @@
+// hetis_internal.h -- host-side declarations shared by the library's .cu/.cpp
+// files (never installed, never seen by the oracle).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "hetis.h"
+
+namespace hetis {
+
+// split-KV chunk C in tokens (reading 12): fixed, a multiple of the page size.
+constexpr int kSplitTokens = 256;
+constexpr int kPageSize = 16;
+
+// Everything a decode-attention launch needs, validated by the API layer.
+struct AttnArgs {
+    int num_seqs;
+    int q_heads;       // local query heads x
+    int kv_heads;      // local kv heads x / r
+    int r;
+    int head_dim;
+    int dtype;         // hetis_dtype of q / kv
+    const void *q;
+    const void *k_pool;
+    const void *v_pool;
+    int64_t num_pages;
+    const int32_t *block_table;
+    int max_pages;
+    const int32_t *seq_lens;
+    int max_seq_len;
+    // workspace carve-up
+    int32_t *split_off;   // [num_seqs + 1]
+    float *part_lse;      // [max_items][r]
+    float *part_o;        // [max_items][r][head_dim]
+    int64_t max_items;
+};
+
+struct WorkspaceLayout {
+    size_t split_off_offset, lse_offset, o_offset, total;
+    int64_t max_items;
+};
+
+WorkspaceLayout workspace_layout(int num_seqs, int kv_heads, int r, int head_dim, int max_seq_len);
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_attn_simt(const AttnArgs &a, cudaStream_t s);
+cudaError_t launch_attn_tc(const AttnArgs &a, cudaStream_t s, std::string *err);
+cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const int32_t *seq_lens,
+                           const int32_t *split_off, const float *part_lse, const float *part_o, void *o,
+                           int o_dtype, int64_t o_seq_stride, cudaStream_t s);
+cudaError_t launch_kv_append(int num_seqs, int kv_heads, int head_dim, int page_size, int elem_bytes,
+                             const void *k_new, const void *v_new, void *k_pool, void *v_pool,
+                             const int32_t *block_table, int max_pages, const int32_t *seq_lens, cudaStream_t s);
+// copy rows [num_seqs][src_heads][d] head slice [h0, h0 + n) -> dense [num_seqs][n][d]
+cudaError_t launch_head_slice(const void *src, void *dst, int num_seqs, int src_heads, int h0, int n,
+                              int row_bytes, cudaStream_t s);
+// dense [num_seqs][n][d] -> rows [num_seqs][dst_heads][d] at head offset h0
+cudaError_t launch_head_place(const void *src, void *dst, int num_seqs, int dst_heads, int h0, int n,
+                              int row_bytes, cudaStream_t s);
+
+void note_launch();
+int num_sms();
+
+}  // namespace hetis

@@ -1,0 +1,182 @@
+// small_kernels.cu -- the non-attention kernels of the step:
+//   kv_append    head-granular store of the new token's K/V rows (a3)
+//   combine      LSE merge of the split-KV partials in ascending split order (a5)
+//   head slice / place: strided [B][H][d] <-> dense [B][x][d] shard copies around
+//                the NCCL scatter / gather (a2, a6; Eq. 2a Concat)
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+
+#include "device_utils.cuh"
+#include "hetis_internal.h"
+
+namespace hetis {
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+
+// ---------------------------------------------------------------- kv append
+// One warp per (request j, kv head g); lanes move 16-byte chunks of the K and V rows.
+__global__ void kv_append_kernel(int num_seqs, int kv_heads, int row_bytes, int page_size, const uint8_t *k_new,
+                                 const uint8_t *v_new, uint8_t *k_pool, uint8_t *v_pool, const int32_t *block_table,
+                                 int max_pages, const int32_t *seq_lens) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= num_seqs * kv_heads) return;
+    const int j = warp / kv_heads, g = warp - j * kv_heads;
+    const int pos = seq_lens[j] - 1;
+    const int32_t page = block_table[((size_t)j * kv_heads + g) * max_pages + pos / page_size];
+    const size_t dst = ((size_t)page * page_size + (size_t)(pos % page_size)) * row_bytes;
+    const size_t src = (size_t)warp * row_bytes;
+    for (int c = lane * 16; c < row_bytes; c += 32 * 16) {
+        *reinterpret_cast<uint4 *>(k_pool + dst + c) = *reinterpret_cast<const uint4 *>(k_new + src + c);
+        *reinterpret_cast<uint4 *>(v_pool + dst + c) = *reinterpret_cast<const uint4 *>(v_new + src + c);
+    }
+}
+
+// ---------------------------------------------------------------- combine
+// o = sum_s 2^(lse_s - M) o_s / sum_s 2^(lse_s - M), M = max_s lse_s, s ascending.
+// One group of D/4 threads per (request, local query head); each thread owns 4 dims.
+template <int D, int OUT_BF16>
+__global__ void combine_kernel(int num_seqs, int q_heads, int r, const int32_t *seq_lens, const int32_t *split_off,
+                               const float *part_lse, const float *part_o, void *o, int64_t o_seq_stride) {
+    constexpr int TPH = D / 4;  // threads per head
+    const int heads_per_block = blockDim.x / TPH;
+    const int hl = threadIdx.x / TPH, d4 = threadIdx.x % TPH;
+    const int64_t flat = (int64_t)blockIdx.x * heads_per_block + hl;
+    if (flat >= (int64_t)num_seqs * q_heads) return;
+    const int j = (int)(flat / q_heads), h = (int)(flat - (int64_t)j * q_heads);
+    const int kv_heads = q_heads / r;
+    const int g = h / r, rr = h - g * r;
+    const int s0 = split_off[j];
+    const int ns = split_off[j + 1] - s0;
+    float M = -INFINITY;
+    for (int s = 0; s < ns; ++s) M = fmaxf(M, part_lse[((size_t)(s0 + s) * kv_heads + g) * r + rr]);
+    float wsum = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < ns; ++s) {
+        const size_t row = ((size_t)(s0 + s) * kv_heads + g) * r + rr;
+        const float w = dev::ex2(part_lse[row] - M);
+        const float4 v = reinterpret_cast<const float4 *>(part_o + row * D)[d4];
+        wsum += w;
+        acc.x = fmaf(w, v.x, acc.x);
+        acc.y = fmaf(w, v.y, acc.y);
+        acc.z = fmaf(w, v.z, acc.z);
+        acc.w = fmaf(w, v.w, acc.w);
+    }
+    // single split: w = 2^0 = 1 exactly, so o = o_0 bit for bit
+    acc.x = __fdiv_rn(acc.x, wsum);
+    acc.y = __fdiv_rn(acc.y, wsum);
+    acc.z = __fdiv_rn(acc.z, wsum);
+    acc.w = __fdiv_rn(acc.w, wsum);
+    const size_t base = (size_t)j * o_seq_stride + (size_t)h * D + 4 * d4;
+    if (OUT_BF16) {
+        uint2 pk;
+        pk.x = dev::pack_bf16x2(acc.x, acc.y);
+        pk.y = dev::pack_bf16x2(acc.z, acc.w);
+        *reinterpret_cast<uint2 *>(static_cast<__nv_bfloat16 *>(o) + base) = pk;
+    } else {
+        *reinterpret_cast<float4 *>(static_cast<float *>(o) + base) = acc;
+    }
+}
+
+// ---------------------------------------------------------------- shard copies
+// src rows [B][src_heads] of row_bytes -> dst rows [B][dst_heads]; copies n heads
+// from src head offset hs to dst head offset hd.  16-byte chunks.
+__global__ void head_copy_kernel(const uint8_t *src, uint8_t *dst, int num_seqs, int src_heads, int hs,
+                                 int dst_heads, int hd, int n, int row_bytes) {
+    const int chunks = row_bytes / 16;
+    const int64_t total = (int64_t)num_seqs * n * chunks;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % chunks);
+        const int64_t rowi = i / chunks;
+        const int hh = (int)(rowi % n);
+        const int j = (int)(rowi / n);
+        const uint4 v =
+            *reinterpret_cast<const uint4 *>(src + (((size_t)j * src_heads + hs + hh) * row_bytes) + 16 * c);
+        *reinterpret_cast<uint4 *>(dst + (((size_t)j * dst_heads + hd + hh) * row_bytes) + 16 * c) = v;
+    }
+}
+
+}  // namespace
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+int num_sms() {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) return 148;
+    return n;
+}
+
+cudaError_t launch_kv_append(int num_seqs, int kv_heads, int head_dim, int page_size, int elem_bytes,
+                             const void *k_new, const void *v_new, void *k_pool, void *v_pool,
+                             const int32_t *block_table, int max_pages, const int32_t *seq_lens, cudaStream_t s) {
+    const int rows = num_seqs * kv_heads;
+    if (rows == 0) return cudaSuccess;
+    const int threads = 256;
+    const int blocks = (rows * 32 + threads - 1) / threads;
+    kv_append_kernel<<<blocks, threads, 0, s>>>(num_seqs, kv_heads, head_dim * elem_bytes, page_size,
+                                                 static_cast<const uint8_t *>(k_new),
+                                                 static_cast<const uint8_t *>(v_new), static_cast<uint8_t *>(k_pool),
+                                                 static_cast<uint8_t *>(v_pool), block_table, max_pages, seq_lens);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const int32_t *seq_lens,
+                           const int32_t *split_off, const float *part_lse, const float *part_o, void *o,
+                           int o_dtype, int64_t o_seq_stride, cudaStream_t s) {
+    const int64_t heads = (int64_t)num_seqs * q_heads;
+    if (heads == 0) return cudaSuccess;
+    const int tph = head_dim / 4;
+    const int threads = 128;
+    const int hpb = threads / tph;
+    const int64_t blocks = (heads + hpb - 1) / hpb;
+    if (head_dim == 128) {
+        if (o_dtype == HETIS_BF16)
+            combine_kernel<128, 1><<<(unsigned)blocks, threads, 0, s>>>(num_seqs, q_heads, r, seq_lens, split_off,
+                                                                        part_lse, part_o, o, o_seq_stride);
+        else
+            combine_kernel<128, 0><<<(unsigned)blocks, threads, 0, s>>>(num_seqs, q_heads, r, seq_lens, split_off,
+                                                                        part_lse, part_o, o, o_seq_stride);
+    } else {
+        if (o_dtype == HETIS_BF16)
+            combine_kernel<64, 1><<<(unsigned)blocks, threads, 0, s>>>(num_seqs, q_heads, r, seq_lens, split_off,
+                                                                       part_lse, part_o, o, o_seq_stride);
+        else
+            combine_kernel<64, 0><<<(unsigned)blocks, threads, 0, s>>>(num_seqs, q_heads, r, seq_lens, split_off,
+                                                                       part_lse, part_o, o, o_seq_stride);
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+static cudaError_t head_copy(const void *src, void *dst, int num_seqs, int src_heads, int hs, int dst_heads, int hd,
+                             int n, int row_bytes, cudaStream_t s) {
+    const int64_t total = (int64_t)num_seqs * n * (row_bytes / 16);
+    if (total == 0) return cudaSuccess;
+    const int threads = 256;
+    int64_t blocks = (total + threads - 1) / threads;
+    if (blocks > 4 * 148) blocks = 4 * 148;
+    head_copy_kernel<<<(unsigned)blocks, threads, 0, s>>>(static_cast<const uint8_t *>(src),
+                                                          static_cast<uint8_t *>(dst), num_seqs, src_heads, hs,
+                                                          dst_heads, hd, n, row_bytes);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_head_slice(const void *src, void *dst, int num_seqs, int src_heads, int h0, int n, int row_bytes,
+                              cudaStream_t s) {
+    return head_copy(src, dst, num_seqs, src_heads, h0, n, 0, n, row_bytes, s);
+}
+
+cudaError_t launch_head_place(const void *src, void *dst, int num_seqs, int dst_heads, int h0, int n, int row_bytes,
+                              cudaStream_t s) {
+    return head_copy(src, dst, num_seqs, n, 0, dst_heads, h0, n, row_bytes, s);
+}
+
+}  // namespace hetis

@@ -1,0 +1,260 @@
+"""Thin Python binding of libhetis.so (include/hetis.h), same names as the C ABI.
+
+Argument marshalling only: torch tensors -> raw pointers, sizes and the current
+CUDA stream.  Every step of the decode path runs in the library's kernels; if
+the library is missing this module raises at import-time use -- there is no
+CPU or eager fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+from . import workload
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libhetis.so")
+
+HETIS_OK = 0
+STATUS = {0: "HETIS_OK", 1: "HETIS_E_INVALID", 2: "HETIS_E_HEAD_INTEGRITY", 3: "HETIS_E_GROUP_ALIGN",
+          4: "HETIS_E_CAPACITY", 5: "HETIS_E_UNSUPPORTED", 6: "HETIS_E_WORKSPACE", 7: "HETIS_E_CUDA",
+          8: "HETIS_E_NCCL"}
+F32, BF16 = 0, 1
+ATTN_FORCE_SIMT = 0x1
+
+EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_split_tokens",
+            "hetis_plan_create", "hetis_plan_destroy", "hetis_plan_heads", "hetis_plan_num_devices",
+            "hetis_plan_check_capacity", "hetis_kv_append", "hetis_attn_decode_workspace", "hetis_attn_partial",
+            "hetis_attn_combine", "hetis_attn_decode", "hetis_comm_workspace", "hetis_scatter_q", "hetis_gather",
+            "hetis_launch_count")
+
+
+class HetisError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        self.status = status
+        self.name = STATUS.get(status, f"status {status}")
+        super().__init__(f"{where}: {self.name}: {detail}")
+
+
+class CShape(ctypes.Structure):
+    _fields_ = [("num_q_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("page_size", ctypes.c_int32), ("kv_dtype", ctypes.c_int32), ("q_dtype", ctypes.c_int32),
+                ("o_dtype", ctypes.c_int32)]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load the in-tree libhetis.so (built by paper_2509_08309_b200.build)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2509_08309_b200.build` "
+                                  "(there is no fallback path)")
+            L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+            vp, i32, i64, u32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_size_t
+            P = ctypes.POINTER
+            sp = P(CShape)
+            sig = {
+                "hetis_status_str": (ctypes.c_char_p, [ctypes.c_int]),
+                "hetis_last_error": (ctypes.c_char_p, []),
+                "hetis_abi_version": (i32, []),
+                "hetis_split_tokens": (i32, []),
+                "hetis_launch_count": (ctypes.c_uint64, []),
+                "hetis_plan_create": (ctypes.c_int, [sp, i32, i32, P(i32), i32, P(vp)]),
+                "hetis_plan_destroy": (None, [vp]),
+                "hetis_plan_heads": (ctypes.c_int, [vp, i32, i32, P(i32), P(i32)]),
+                "hetis_plan_num_devices": (i32, [vp]),
+                "hetis_plan_check_capacity": (ctypes.c_int, [vp, i32, P(i32), P(i64)]),
+                "hetis_kv_append": (ctypes.c_int, [sp, i32, i32, vp, vp, vp, vp, i64, vp, i32, vp, vp]),
+                "hetis_attn_decode_workspace": (ctypes.c_int, [sp, i32, i32, i32, P(sz)]),
+                "hetis_attn_partial": (ctypes.c_int, [sp, i32, i32, i32, vp, vp, vp, i64, vp, i32, vp, i32, vp, sz,
+                                                      u32, vp]),
+                "hetis_attn_combine": (ctypes.c_int, [sp, i32, i32, vp, i32, vp, i64, vp, sz, vp]),
+                "hetis_attn_decode": (ctypes.c_int, [sp, i32, i32, i32, vp, vp, vp, i64, vp, i32, vp, i32, vp, vp,
+                                                     sz, u32, vp]),
+                "hetis_comm_workspace": (ctypes.c_int, [vp, i32, i32, P(sz)]),
+                "hetis_scatter_q": (ctypes.c_int, [vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+                "hetis_gather": (ctypes.c_int, [vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]),
+            }
+            for name, (res, args) in sig.items():
+                f = getattr(L, name)
+                f.restype = res
+                f.argtypes = args
+            _lib = L
+    return _lib
+
+
+def _check(rc: int, where: str):
+    if rc != HETIS_OK:
+        raise HetisError(rc, where, lib().hetis_last_error().decode())
+
+
+def dtype_code(dt: torch.dtype | str) -> int:
+    if dt in (torch.bfloat16, "bf16"):
+        return BF16
+    if dt in (torch.float32, "f32"):
+        return F32
+    raise ValueError(f"unsupported dtype {dt}")
+
+
+def make_shape(shape: workload.Shape, o_dtype: str = "f32") -> CShape:
+    c = dtype_code(shape.dtype)
+    return CShape(shape.num_q_heads, shape.num_kv_heads, shape.head_dim, shape.page_size, c, c, dtype_code(o_dtype))
+
+
+def _dev(t: torch.Tensor | None, name: str):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (the library has no host path)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def status_str(s: int) -> str:
+    return lib().hetis_status_str(s).decode()
+
+
+def abi_version() -> int:
+    return lib().hetis_abi_version()
+
+
+def split_tokens() -> int:
+    return lib().hetis_split_tokens()
+
+
+def launch_count() -> int:
+    return int(lib().hetis_launch_count())
+
+
+# ---------------------------------------------------------------- plans
+class Plan:
+    """Owned hetis_plan (Eq. 5 validated head -> device assignment)."""
+
+    def __init__(self, shape: CShape, num_devices: int, x, per_request: bool = False, num_seqs: int = 0):
+        arr = (ctypes.c_int32 * len(x))(*[int(v) for v in x])
+        h = ctypes.c_void_p()
+        _check(lib().hetis_plan_create(ctypes.byref(shape), num_devices, num_seqs, arr, int(per_request),
+                                       ctypes.byref(h)), "hetis_plan_create")
+        self._h = h
+        self.shape = shape
+        self.num_devices = num_devices
+        self.num_seqs = num_seqs
+
+    @property
+    def handle(self):
+        return self._h
+
+    def heads(self, device: int, seq: int = 0) -> tuple[int, int]:
+        b, c = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().hetis_plan_heads(self._h, device, seq, ctypes.byref(b), ctypes.byref(c)), "hetis_plan_heads")
+        return b.value, c.value
+
+    def check_capacity(self, seq_lens, free_pages) -> None:
+        sl = (ctypes.c_int32 * max(len(seq_lens), 1))(*[int(v) for v in seq_lens])
+        fp = (ctypes.c_int64 * len(free_pages))(*[int(v) for v in free_pages])
+        _check(lib().hetis_plan_check_capacity(self._h, len(seq_lens), sl, fp), "hetis_plan_check_capacity")
+
+    def comm_workspace(self, rank: int, num_seqs: int) -> int:
+        b = ctypes.c_size_t()
+        _check(lib().hetis_comm_workspace(self._h, rank, num_seqs, ctypes.byref(b)), "hetis_comm_workspace")
+        return b.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.hetis_plan_destroy(h)
+            self._h = None
+
+
+def plan_create(shape: CShape, num_devices: int, x, per_request: bool = False, num_seqs: int = 0) -> Plan:
+    return Plan(shape, num_devices, x, per_request, num_seqs)
+
+
+# ---------------------------------------------------------------- kernels
+def kv_append(shape: CShape, k_new, v_new, k_pool, v_pool, block_table, seq_lens, stream=None) -> None:
+    B, G, _ = k_new.shape
+    _check(lib().hetis_kv_append(ctypes.byref(shape), B, G, _dev(k_new, "k_new"), _dev(v_new, "v_new"),
+                                 _dev(k_pool, "k_pool"), _dev(v_pool, "v_pool"), k_pool.shape[0],
+                                 _dev(block_table, "block_table"), block_table.shape[2], _dev(seq_lens, "seq_lens"),
+                                 _stream(stream)), "hetis_kv_append")
+
+
+def attn_decode_workspace(shape: CShape, num_seqs: int, q_head_count: int, max_seq_len: int) -> int:
+    b = ctypes.c_size_t()
+    _check(lib().hetis_attn_decode_workspace(ctypes.byref(shape), num_seqs, q_head_count, max_seq_len,
+                                             ctypes.byref(b)), "hetis_attn_decode_workspace")
+    return b.value
+
+
+def alloc_workspace(nbytes: int, device) -> torch.Tensor:
+    """A 256-byte aligned uint8 device buffer (torch's caching allocator aligns to 512)."""
+    return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+
+
+def attn_partial(shape: CShape, q, k_pool, v_pool, block_table, seq_lens, max_seq_len: int, workspace,
+                 q_head_begin: int = 0, flags: int = 0, stream=None) -> None:
+    B, x, _ = q.shape
+    _check(lib().hetis_attn_partial(ctypes.byref(shape), B, q_head_begin, x, _dev(q, "q"), _dev(k_pool, "k_pool"),
+                                    _dev(v_pool, "v_pool"), k_pool.shape[0], _dev(block_table, "block_table"),
+                                    block_table.shape[2], _dev(seq_lens, "seq_lens"), max_seq_len,
+                                    _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(),
+                                    flags, _stream(stream)), "hetis_attn_partial")
+
+
+def attn_combine(shape: CShape, seq_lens, max_seq_len: int, o, workspace, q_head_count: int | None = None,
+                 o_seq_stride: int | None = None, stream=None) -> None:
+    B = seq_lens.shape[0]
+    if q_head_count is None:
+        q_head_count = o.shape[1]
+    if o_seq_stride is None:
+        o_seq_stride = o.stride(0)
+    if not o.is_cuda:
+        raise ValueError("o must be a CUDA tensor")
+    _check(lib().hetis_attn_combine(ctypes.byref(shape), B, q_head_count, _dev(seq_lens, "seq_lens"), max_seq_len,
+                                    ctypes.c_void_p(o.data_ptr()), o_seq_stride, _dev(workspace, "workspace"),
+                                    workspace.numel() * workspace.element_size(), _stream(stream)),
+           "hetis_attn_combine")
+
+
+def attn_decode(shape: CShape, q, k_pool, v_pool, block_table, seq_lens, max_seq_len: int, o, workspace,
+                q_head_begin: int = 0, flags: int = 0, stream=None) -> None:
+    B, x, _ = q.shape
+    _check(lib().hetis_attn_decode(ctypes.byref(shape), B, q_head_begin, x, _dev(q, "q"), _dev(k_pool, "k_pool"),
+                                   _dev(v_pool, "v_pool"), k_pool.shape[0], _dev(block_table, "block_table"),
+                                   block_table.shape[2], _dev(seq_lens, "seq_lens"), max_seq_len, _dev(o, "o"),
+                                   _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(), flags,
+                                   _stream(stream)), "hetis_attn_decode")
+
+
+# ---------------------------------------------------------------- NCCL scatter / gather
+def scatter_q(plan: Plan, comm_ptr: int, rank: int, root: int, num_seqs: int, q_full, k_new_full, v_new_full,
+              q_shard, k_new_shard, v_new_shard, workspace, stream=None) -> None:
+    _check(lib().hetis_scatter_q(plan.handle, ctypes.c_void_p(comm_ptr), rank, root, num_seqs,
+                                 _dev(q_full, "q_full"), _dev(k_new_full, "k_new_full"), _dev(v_new_full, "v_new_full"),
+                                 _dev(q_shard, "q_shard"), _dev(k_new_shard, "k_new_shard"),
+                                 _dev(v_new_shard, "v_new_shard"), _dev(workspace, "workspace"),
+                                 0 if workspace is None else workspace.numel() * workspace.element_size(),
+                                 _stream(stream)), "hetis_scatter_q")
+
+
+def gather(plan: Plan, comm_ptr: int, rank: int, root: int, num_seqs: int, o_shard, o_full, workspace,
+           stream=None) -> None:
+    _check(lib().hetis_gather(plan.handle, ctypes.c_void_p(comm_ptr), rank, root, num_seqs, _dev(o_shard, "o_shard"),
+                              _dev(o_full, "o_full"), _dev(workspace, "workspace"),
+                              0 if workspace is None else workspace.numel() * workspace.element_size(),
+                              _stream(stream)), "hetis_gather")

@@ -1,0 +1,95 @@
+"""One rank's decode step of one layer: the composition of
+the C-ABI calls -- scatter (N > 1), kv_append, attention partial + combine,
+gather (N > 1).  Buffers are torch tensors (device memory only); every step
+runs in libhetis.so kernels or NCCL.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import hetis, workload
+
+
+@dataclass
+class RankBuffers:
+    """Device buffers one rank owns for one layer."""
+    q_shard: torch.Tensor       # [B][x][D]
+    k_new: torch.Tensor         # [B][x/r][D]
+    v_new: torch.Tensor
+    o_shard: torch.Tensor       # [B][x][D] (o dtype)
+    workspace: torch.Tensor     # attention workspace
+    comm_ws: torch.Tensor | None
+
+
+class DecodeStep:
+    """Runs the hot path for one rank.
+
+    shape      : global model shape (H, H_kv, d, P, dtype)
+    plan       : hetis.Plan with the head split (global, per_request = 0)
+    rank, comm : position in the plan and the raw ncclComm_t (None at N = 1)
+    """
+
+    def __init__(self, shape: workload.Shape, plan: hetis.Plan, rank: int, num_seqs: int, max_seq_len: int,
+                 device, o_dtype: str = "f32", comm_ptr: int | None = None, root: int = 0):
+        self.shape = shape
+        self.cshape = hetis.make_shape(shape, o_dtype)
+        self.plan = plan
+        self.rank = rank
+        self.world = plan.num_devices
+        self.root = root
+        self.comm_ptr = comm_ptr
+        self.num_seqs = num_seqs
+        self.max_seq_len = max_seq_len
+        self.q_begin, self.q_count = plan.heads(rank)
+        self.device = device
+        D, r = shape.head_dim, shape.r
+        dt = shape.torch_dtype
+        odt = torch.bfloat16 if o_dtype == "bf16" else torch.float32
+        ws = hetis.attn_decode_workspace(self.cshape, num_seqs, self.q_count, max_seq_len)
+        comm_ws = None
+        if self.world > 1:
+            comm_ws = hetis.alloc_workspace(plan.comm_workspace(rank, num_seqs), device)
+        self.buf = RankBuffers(
+            q_shard=torch.empty((num_seqs, self.q_count, D), dtype=dt, device=device),
+            k_new=torch.empty((num_seqs, self.q_count // r, D), dtype=dt, device=device),
+            v_new=torch.empty((num_seqs, self.q_count // r, D), dtype=dt, device=device),
+            o_shard=torch.empty((num_seqs, self.q_count, D), dtype=odt, device=device),
+            workspace=hetis.alloc_workspace(ws, device),
+            comm_ws=comm_ws,
+        )
+        self.o_dtype = odt
+
+    # kernels launched per step by this rank (for gpu_launches accounting)
+    def launches_per_step(self) -> int:
+        n = 3  # kv_append, attention partial, combine
+        if self.world > 1:
+            x = [self.plan.heads(i)[1] for i in range(self.world)]
+            if self.rank == self.root:
+                n += 3 * sum(1 for v in x if v > 0)       # scatter packs (incl. own shard)
+            n += sum(1 for v in x if v > 0)               # gather places
+        return n
+
+    def scatter(self, q_full, k_new_full, v_new_full, stream=None):
+        if self.world == 1:
+            raise RuntimeError("scatter needs N > 1")
+        hetis.scatter_q(self.plan, self.comm_ptr, self.rank, self.root, self.num_seqs, q_full, k_new_full,
+                        v_new_full, self.buf.q_shard, self.buf.k_new, self.buf.v_new, self.buf.comm_ws, stream)
+
+    def append(self, k_pool, v_pool, block_table, seq_lens, k_new=None, v_new=None, stream=None):
+        hetis.kv_append(self.cshape, self.buf.k_new if k_new is None else k_new,
+                        self.buf.v_new if v_new is None else v_new, k_pool, v_pool, block_table, seq_lens, stream)
+
+    def attention(self, k_pool, v_pool, block_table, seq_lens, q=None, o=None, stream=None, flags: int = 0):
+        q = self.buf.q_shard if q is None else q
+        o = self.buf.o_shard if o is None else o
+        hetis.attn_partial(self.cshape, q, k_pool, v_pool, block_table, seq_lens, self.max_seq_len,
+                           self.buf.workspace, q_head_begin=self.q_begin, flags=flags, stream=stream)
+        hetis.attn_combine(self.cshape, seq_lens, self.max_seq_len, o, self.buf.workspace, q_head_count=self.q_count,
+                           stream=stream)
+        return o
+
+    def gather(self, o_full, root: int = -1, stream=None):
+        hetis.gather(self.plan, self.comm_ptr, self.rank, root, self.num_seqs, self.buf.o_shard, o_full,
+                     self.buf.comm_ws, stream)

@@ -1,0 +1,285 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Tolerance (north star / DESIGN.md §5): max |O - O_ref| <= 2e-3 and
+||O - O_ref||_F / ||O_ref||_F <= 1e-2 over the whole fp32 O, no NaN/Inf.
+Index and byte work is bit-exact: kv_append (memcmp against the oracle's host
+placement), page-permutation and head-partition invariance of the GPU output,
+L = 1 returning the V row, bf16 O == RNE(fp32 O).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2509_08309_b200 import hetis, workload
+from tests.helpers import dtype_code, err_stats, host_batch, oracle_full, to_f64
+
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL = 2e-3, 1e-2
+C = 256
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    hetis.lib()
+
+
+def run_gpu(b: workload.DecodeBatch, o_dtype="f32", flags=0, append=True, o_stride_heads=None):
+    s = hetis.make_shape(b.shape, o_dtype)
+    B, x, D = b.q.shape
+    if append:
+        hetis.kv_append(s, b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens)
+    L = b.max_seq_len
+    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), b.q.device)
+    odt = torch.bfloat16 if o_dtype == "bf16" else torch.float32
+    if o_stride_heads is None:
+        o = torch.full((B, x, D), float("nan"), dtype=odt, device=b.q.device)
+        hetis.attn_decode(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, o, ws, q_head_begin=b.q_begin,
+                          flags=flags)
+    else:
+        big = torch.full((B, o_stride_heads, D), float("nan"), dtype=odt, device=b.q.device)
+        hetis.attn_partial(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, ws, q_head_begin=b.q_begin,
+                           flags=flags)
+        view = big[:, b.q_begin:b.q_begin + x]
+        hetis.attn_combine(s, b.seq_lens, L, view, ws, q_head_count=x, o_seq_stride=big.stride(0))
+        o = big
+    torch.cuda.synchronize()
+    return o
+
+
+def assert_close(got, ref, what=""):
+    st = err_stats(got.float().cpu().numpy() if isinstance(got, torch.Tensor) else got, ref)
+    assert st["nonfinite"] == 0, (what, st)
+    assert st["max_abs"] <= ATOL and st["rel_fro"] <= RTOL, (what, st)
+    return st
+
+
+def gpu_batch(H, Hkv, D, dtype, lens, seed, q_begin=0, q_count=None, rank_salt=0):
+    shape = workload.Shape(H, Hkv, D, 16, dtype)
+    return workload.make_decode_batch(shape, torch.tensor(lens, dtype=torch.int32), seed, "cuda", q_begin=q_begin,
+                                      q_count=q_count, rank_salt=rank_salt)
+
+
+EDGE_LENS = (1, 2, 15, 16, 17, 31, 33, C - 1, C, C + 1, 2 * C + 5, 1000)
+
+
+# ------------------------------------------------------------------ c1: the parity config
+def test_c1_two_virtual_devices_match_oracle_and_unsplit():
+    cfg = workload.CONFIGS["c1"]
+    full = workload.make_decode_batch(cfg.shape, cfg.seq_lens(), cfg.seed, "cuda")
+    ref = oracle_full(full)
+    o_full = run_gpu(full)
+    assert_close(o_full, ref, "c1 unsplit")
+    parts = []
+    begin = 0
+    for i, x in enumerate(cfg.split):
+        part = workload.make_decode_batch(cfg.shape, cfg.seq_lens(), cfg.seed, "cuda", q_begin=begin, q_count=x,
+                                          rank_salt=i + 1)
+        parts.append(run_gpu(part))
+        begin += x
+    o_split = torch.cat(parts, dim=1)
+    st = assert_close(o_split, ref, "c1 split")
+    assert st["max_abs"] < 1e-5            # fp32 path: far inside the budget
+    assert torch.equal(o_split, o_full)    # head partition invariance, bit-exact
+
+
+# ------------------------------------------------------------------ edge lengths, all kernels
+@pytest.mark.parametrize("H,Hkv,D,dtype", [(8, 8, 128, "bf16"), (16, 2, 128, "bf16"), (8, 8, 64, "f32"),
+                                           (16, 4, 64, "bf16"), (8, 1, 128, "bf16"), (4, 2, 128, "f32"),
+                                           (8, 4, 128, "bf16")])
+def test_edge_lengths_ragged(H, Hkv, D, dtype):
+    b = gpu_batch(H, Hkv, D, dtype, EDGE_LENS, seed=H * 7 + D + Hkv)
+    o = run_gpu(b)
+    assert_close(o, oracle_full(b), f"{H}/{Hkv}/{D}/{dtype}")
+    # L = 1: the output is the new token's V row, bit for bit
+    j1 = EDGE_LENS.index(1)
+    v = b.v_new[j1].float()
+    for h in range(H):
+        assert torch.equal(o[j1, h], v[h // (H // Hkv)])
+
+
+def test_single_sequence_and_all_length_one():
+    for lens in [(4096,), (1,) * 37]:
+        b = gpu_batch(64, 8, 128, "bf16", lens, seed=len(lens))
+        assert_close(run_gpu(b), oracle_full(b), str(lens[:2]))
+
+
+# ------------------------------------------------------------------ closed-form cases on the GPU
+def test_q_zero_and_identical_keys_give_mean():
+    b = gpu_batch(16, 2, 128, "bf16", (300, 17, 1), seed=5)
+    b.q.zero_()
+    o = run_gpu(b)
+    ref = oracle_full(b)
+    assert_close(o, ref, "q=0")
+    b2 = gpu_batch(8, 8, 128, "bf16", (700, 33), seed=6)
+    key = b2.k_pool[b2.block_table[0, 0, 0].long(), 0].clone()      # history token 0 of request 0
+    b2.k_pool.copy_(key.expand_as(b2.k_pool))
+    b2.k_new.copy_(key.expand_as(b2.k_new))
+    assert_close(run_gpu(b2), oracle_full(b2), "identical keys")
+
+
+@pytest.mark.parametrize("H,Hkv", [(8, 8), (64, 8)])
+def test_peaked_attention_catches_low_precision_p(H, Hkv):
+    """K x 4 and one key = 8 q: a few tokens dominate; bf16-rounded P would miss 2e-3."""
+    b = gpu_batch(H, Hkv, 128, "bf16", (2048, 513, 64), seed=77)
+    b.k_pool.mul_(4)          # exact in bf16 (power of two)
+    b.k_new.mul_(4)
+    r = H // Hkv
+    for j in range(3):
+        for g in range(Hkv):
+            page = b.block_table[j, g, 3].long()
+            b.k_pool[page, 5] = (b.q[j, g * r] * 8)
+    st = assert_close(run_gpu(b), oracle_full(b), "peaked")
+    assert st["max_abs"] < 1e-3
+
+
+# ------------------------------------------------------------------ bit-exact invariances
+@pytest.mark.parametrize("H,Hkv", [(40, 40), (64, 8)])
+def test_page_permutation_bit_identical(H, Hkv):
+    b = gpu_batch(H, Hkv, 128, "bf16", (777, 2048, 16), seed=12)
+    hetis.kv_append(hetis.make_shape(b.shape), b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens)
+    o1 = run_gpu(b, append=False)
+    n = b.k_pool.shape[0]
+    perm = torch.randperm(n, generator=torch.Generator().manual_seed(3)).cuda()
+    kp = torch.empty_like(b.k_pool)
+    vp = torch.empty_like(b.v_pool)
+    kp[perm] = b.k_pool
+    vp[perm] = b.v_pool
+    bt = b.block_table.clone()
+    m = bt >= 0
+    bt[m] = perm[bt[m].long()].int()
+    b2 = workload.DecodeBatch(b.shape, 0, H, b.q, b.k_new, b.v_new, kp, vp, bt, b.seq_lens)
+    o2 = run_gpu(b2, append=False)
+    assert torch.equal(o1, o2)
+
+
+@pytest.mark.parametrize("H,Hkv,splits", [(40, 40, [(16, 8, 8, 4, 4), (20, 20), (5,) * 8]),
+                                          (64, 8, [(32, 32), (16,) * 4, (8,) * 8, (48, 16)])])
+def test_head_partition_bit_identical(H, Hkv, splits):
+    shape = workload.Shape(H, Hkv, 128, 16, "bf16")
+    lens = torch.tensor([600, 5, 1300, 256], dtype=torch.int32)
+    full = workload.make_decode_batch(shape, lens, 21, "cuda")
+    o_full = run_gpu(full)
+    for split in splits:
+        begin, outs = 0, []
+        for i, x in enumerate(split):
+            part = workload.make_decode_batch(shape, lens, 21, "cuda", q_begin=begin, q_count=x, rank_salt=i + 1)
+            outs.append(run_gpu(part))
+            begin += x
+        assert torch.equal(torch.cat(outs, 1), o_full), split
+
+
+def test_deterministic_repeat():
+    b = gpu_batch(64, 8, 128, "bf16", (2048, 999, 1), seed=31)
+    o1 = run_gpu(b)
+    o2 = run_gpu(b, append=False)
+    assert torch.equal(o1, o2)
+
+
+def test_tensor_core_vs_cuda_core_gqa():
+    b = gpu_batch(64, 8, 128, "bf16", (1500, 40, 257), seed=41)
+    o_tc = run_gpu(b)
+    o_simt = run_gpu(b, flags=hetis.ATTN_FORCE_SIMT, append=False)
+    ref = oracle_full(b)
+    assert_close(o_tc, ref, "tc")
+    assert_close(o_simt, ref, "simt")
+    assert (o_tc - o_simt).abs().max().item() < 1e-4
+
+
+def test_gqa_equals_expanded_mha_on_gpu():
+    b = gpu_batch(16, 2, 128, "bf16", (900, 31), seed=44)
+    o_gqa = run_gpu(b)
+    r = 8
+    bt = b.block_table.repeat_interleave(r, dim=1).contiguous()
+    shape = workload.Shape(16, 16, 128, 16, "bf16")
+    b2 = workload.DecodeBatch(shape, 0, 16, b.q, b.k_new.repeat_interleave(r, 1).contiguous(),
+                              b.v_new.repeat_interleave(r, 1).contiguous(), b.k_pool, b.v_pool, bt, b.seq_lens)
+    o_mha = run_gpu(b2, append=False)
+    assert (o_gqa - o_mha).abs().max().item() < 1e-4
+
+
+def test_bf16_output_is_rne_of_fp32():
+    b = gpu_batch(64, 8, 128, "bf16", (1024, 77), seed=51)
+    o32 = run_gpu(b)
+    o16 = run_gpu(b, o_dtype="bf16", append=False)
+    assert torch.equal(o16, o32.to(torch.bfloat16))
+
+
+def test_strided_output_places_heads_in_full_tensor():
+    b = gpu_batch(40, 40, 128, "bf16", (300, 1), seed=52, q_begin=16, q_count=8)
+    o = run_gpu(b, o_stride_heads=40)
+    dense = run_gpu(b, append=False)
+    assert torch.equal(o[:, 16:24], dense)
+    assert torch.isnan(o[:, :16]).all() and torch.isnan(o[:, 24:]).all()
+
+
+# ------------------------------------------------------------------ kv append bit-exactness
+@pytest.mark.parametrize("dtype,D,Hkv", [("bf16", 128, 8), ("f32", 64, 4), ("bf16", 64, 2)])
+def test_kv_append_memcmp_against_oracle_placement(dtype, D, Hkv):
+    b = gpu_batch(Hkv, Hkv, D, dtype, (1, 16, 17, 33, 4096, 255), seed=61)
+    before = workload.to_numpy_bits(b.k_pool).copy()
+    hb = host_batch(b)                         # oracle placement on host copies
+    hetis.kv_append(hetis.make_shape(b.shape), b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens)
+    torch.cuda.synchronize()
+    gk = workload.to_numpy_bits(b.k_pool)
+    gv = workload.to_numpy_bits(b.v_pool)
+    assert np.array_equal(gk.view(np.uint8), hb["k_pool"].view(np.uint8))
+    assert np.array_equal(gv.view(np.uint8), hb["v_pool"].view(np.uint8))
+    changed = np.any(gk.view(np.uint8).reshape(gk.shape[0], 16, -1) != before.view(np.uint8).reshape(
+        gk.shape[0], 16, -1), axis=2)
+    assert changed.sum() == 6 * Hkv
+
+
+# ------------------------------------------------------------------ full-size configs, sampled outputs
+def _compact_for_pairs(b: workload.DecodeBatch, pairs):
+    """Host copy of only the pages the sampled (seq, head) pairs read, with a remapped table."""
+    r = b.shape.r
+    jg = sorted({(j, h // r) for j, h in pairs})
+    bt = b.block_table.cpu()
+    lens = b.seq_lens.cpu()
+    P = b.shape.page_size
+    pages, new_bt = [], {}
+    for (j, g) in jg:
+        n = (int(lens[j]) + P - 1) // P
+        ids = bt[j, g, :n]
+        new_bt[(j, g)] = list(range(len(pages), len(pages) + n))
+        pages.extend(ids.tolist())
+    idx = torch.tensor(pages, dtype=torch.long, device=b.k_pool.device)
+    kp = workload.to_numpy_bits(b.k_pool.index_select(0, idx))
+    vp = workload.to_numpy_bits(b.v_pool.index_select(0, idx))
+    B, G = bt.shape[0], bt.shape[1]
+    table = np.full((B, G, bt.shape[2]), -1, np.int32)
+    for (j, g), ids in new_bt.items():
+        table[j, g, :len(ids)] = ids
+    return kp, vp, table
+
+
+@pytest.mark.parametrize("name,rank", [("c2", 0), ("c3", 0), ("c4", 0), ("c4", 4), ("c5", 3)])
+def test_full_size_config_sampled(name, rank):
+    cfg = workload.CONFIGS[name]
+    n_dev = len(cfg.split) if cfg.split else 1
+    split = cfg.head_split(n_dev)
+    begin = sum(split[:rank])
+    b = workload.make_decode_batch(cfg.shape, cfg.seq_lens(), cfg.seed, "cuda", q_begin=begin,
+                                   q_count=split[rank], rank_salt=rank)
+    B, x = b.q.shape[0], b.q.shape[1]
+    g = torch.Generator().manual_seed(5)
+    pairs = sorted({(int(torch.randint(B, (1,), generator=g)), int(torch.randint(x, (1,), generator=g)))
+                    for _ in range(24)} | {(0, 0), (B - 1, x - 1)})
+    # oracle inputs: the pages the pairs read, copied BEFORE the GPU append; the new
+    # token is placed on the host by the oracle's own kv_append
+    kp, vp, table = _compact_for_pairs(b, pairs)
+    oracle.kv_append(workload.to_numpy_bits(b.k_new), workload.to_numpy_bits(b.v_new), kp, vp, table,
+                     b.seq_lens.cpu().numpy())
+    q = workload.to_numpy_bits(b.q)
+    ref = oracle.decode_pairs(q, kp, vp, table, b.seq_lens.cpu().numpy(), pairs, num_kv_heads=b.kv_count,
+                              dtype=dtype_code(b.shape))
+    o = run_gpu(b)                                # appends the new token, then attends
+    assert torch.isfinite(o).all()
+    got = np.stack([o[j, h].cpu().numpy() for j, h in pairs])
+    assert_close(got, ref, name)
