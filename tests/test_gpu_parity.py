@@ -274,8 +274,11 @@ def test_full_size_config_sampled(name, rank):
     # oracle inputs: the pages the pairs read, copied BEFORE the GPU append; the new
     # token is placed on the host by the oracle's own kv_append
     kp, vp, table = _compact_for_pairs(b, pairs)
-    oracle.kv_append(workload.to_numpy_bits(b.k_new), workload.to_numpy_bits(b.v_new), kp, vp, table,
-                     b.seq_lens.cpu().numpy())
+    kn, vn, sl = workload.to_numpy_bits(b.k_new), workload.to_numpy_bits(b.v_new), b.seq_lens.cpu().numpy()
+    for (j, gg) in sorted({(j, h // b.shape.r) for j, h in pairs}):
+        # one (request, kv head) at a time: only the sampled pairs' pages are in the compact pool
+        oracle.kv_append(kn[j:j + 1, gg:gg + 1], vn[j:j + 1, gg:gg + 1], kp, vp, table[j:j + 1, gg:gg + 1],
+                         sl[j:j + 1])
     q = workload.to_numpy_bits(b.q)
     ref = oracle.decode_pairs(q, kp, vp, table, b.seq_lens.cpu().numpy(), pairs, num_kv_heads=b.kv_count,
                               dtype=dtype_code(b.shape))
