@@ -136,9 +136,27 @@ __device__ void build_split_offsets(const Params &p, int32_t *s_len, int32_t *s_
     }
 }
 
-// ---------------------------------------------------------------- producer
-// COPY = 0: two 1-D bulk copies per page (K, V).  COPY = 1: four 2-D tensor
-// copies per page (K, V halves of 64 elements, 128-B swizzle).
+// ---------------------------------------------------------------- ring position
+// Stage index and mbarrier phase of the n-th page a CTA streams, advanced
+// incrementally (no runtime division on the issue path).
+struct RingPos {
+    int stage;
+    uint32_t phase;
+    __device__ __forceinline__ void advance(int by, int stages) {
+        stage += by;
+        while (stage >= stages) {
+            stage -= stages;
+            phase ^= 1u;
+        }
+    }
+};
+
+// ---------------------------------------------------------------- producer (one thread)
+// COPY = 0: two 1-D bulk copies per page (K, V).  COPY = 1: 2-D tensor copies
+// of 64-column blocks (16 rows x 128 B, 128-B swizzle) for K and V.
+// Runs on lane 0 of warp 0 only; the item's block-table entries are loaded one
+// item ahead (16 independent loads) so their latency hides behind the current
+// item's page issue.
 template <int ROW_BYTES, int R, int COPY>
 __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta *qmeta, uint64_t *full,
                          uint64_t *empty, uint64_t *qfull, uint64_t *qempty, const int32_t *s_len,
@@ -147,88 +165,83 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
     constexpr int kStageBytes = 2 * kPageBytes;
     constexpr int kQBytes = R * ROW_BYTES;
     constexpr int kQStride = (kQBytes + 127) / 128 * 128;
-    const int lane = threadIdx.x & 31;
     const int n_items = s_off[p.num_seqs] * p.kv_heads;
     const uint64_t pol_stream = dev::policy_evict_first();
-    const uint64_t pol_q = dev::policy_evict_first();
-    if (COPY == 1 && lane == 0) {
+    if (COPY == 1) {
         dev::prefetch_tmap(tmap_k);
         dev::prefetch_tmap(tmap_v);
     }
-
-    // decode an item index into (seq, kv head, first token, token count)
-    auto decode = [&](int item, int &j, int &g, int &t0, int &ntok) {
+    struct Dec {
+        int j, g, t0, ntok;
+    };
+    auto decode = [&](int item) -> Dec {
+        Dec d;
         const int k = item / p.kv_heads;
-        g = item - k * p.kv_heads;
-        j = upper_bound_smem(s_off, p.num_seqs + 1, k) - 1;
-        const int s = k - s_off[j];
-        t0 = s * kC;
-        ntok = min(kC, s_len[j] - t0);
+        d.g = item - k * p.kv_heads;
+        d.j = upper_bound_smem(s_off, p.num_seqs + 1, k) - 1;
+        d.t0 = (k - s_off[d.j]) * kC;
+        d.ntok = min(kC, s_len[d.j] - d.t0);
+        return d;
     };
-    auto issue_q = [&](int it, int item) {
-        int j, g, t0, ntok;
-        decode(item, j, g, t0, ntok);
-        const int slot = it % kQSlots;
-        if (lane == 0) {
-            if (it >= kQSlots) dev::mbar_wait(&qempty[slot], ((it / kQSlots) - 1) & 1);
-            qmeta[slot] = ItemMeta{item, ntok, (ntok + kP - 1) / kP, 0};
-            dev::mbar_arrive_expect_tx(&qfull[slot], kQBytes);
-            const uint8_t *src = p.q + ((size_t)j * p.q_heads + (size_t)g * R) * ROW_BYTES;
-            dev::bulk_g2s(qbuf + (size_t)slot * kQStride, src, kQBytes, &qfull[slot], pol_q);
-        }
-        __syncwarp();
+    auto issue_q = [&](int it, int item, const Dec &d) {
+        const int slot = it & (kQSlots - 1);
+        dev::mbar_wait(&qempty[slot], ((it / kQSlots) & 1) ^ 1);
+        qmeta[slot] = ItemMeta{item, d.ntok, (d.ntok + kP - 1) / kP, 0};
+        dev::mbar_arrive_expect_tx(&qfull[slot], kQBytes);
+        const uint8_t *src = p.q + ((size_t)d.j * p.q_heads + (size_t)d.g * R) * ROW_BYTES;
+        dev::bulk_g2s(qbuf + (size_t)slot * kQStride, src, kQBytes, &qfull[slot], pol_stream);
     };
-    auto load_pids = [&](int item) -> int32_t {
-        int j, g, t0, ntok;
-        decode(item, j, g, t0, ntok);
-        const int np = (ntok + kP - 1) / kP;
-        int32_t pid = 0;
-        if (lane < np) pid = __ldg(p.block_table + ((size_t)j * p.kv_heads + g) * p.max_pages + t0 / kP + lane);
-        return pid;
+    auto load_pids = [&](const Dec &d, int32_t (&pid)[kPagesPerItem]) {
+        const int np = (d.ntok + kP - 1) / kP;
+        const int32_t *row = p.block_table + ((size_t)d.j * p.kv_heads + d.g) * p.max_pages + d.t0 / kP;
+#pragma unroll
+        for (int i = 0; i < kPagesPerItem; ++i) pid[i] = i < np ? __ldg(row + i) : 0;
     };
 
-    int it = 0;
     int item = blockIdx.x;
     if (item >= n_items) return;
-    issue_q(0, item);
-    int32_t pid = load_pids(item);
-    uint32_t n = 0;  // pages issued by this CTA
-    int stage = 0;
-    for (; item < n_items; item += gridDim.x, ++it) {
+    static_assert((kQSlots & (kQSlots - 1)) == 0, "q slots: power of two");
+    Dec cur = decode(item);
+    issue_q(0, item, cur);
+    int32_t pid[kPagesPerItem];
+    load_pids(cur, pid);
+    RingPos pos{0, 0u};
+    for (int it = 0; item < n_items; item += gridDim.x, ++it) {
         const int next = item + gridDim.x;
-        int32_t pid_next = 0;
+        int32_t pid_next[kPagesPerItem];
+        Dec nd{0, 0, 0, 0};
         if (next < n_items) {
-            issue_q(it + 1, next);
-            pid_next = load_pids(next);
+            nd = decode(next);
+            issue_q(it + 1, next, nd);
+            load_pids(nd, pid_next);
         }
-        int j, g, t0, ntok;
-        decode(item, j, g, t0, ntok);
-        const int np = (ntok + kP - 1) / kP;
-        for (int pg = 0; pg < np; ++pg) {
-            const int32_t page = __shfl_sync(0xffffffffu, pid, pg);
-            if (lane == 0) {
-                if (n >= (uint32_t)p.stages) dev::mbar_wait(&empty[stage], ((n / p.stages) - 1) & 1);
-                uint8_t *dst = ring + (size_t)stage * kStageBytes;
-                dev::mbar_arrive_expect_tx(&full[stage], kStageBytes);
+        const int np = (cur.ntok + kP - 1) / kP;
+#pragma unroll
+        for (int pg = 0; pg < kPagesPerItem; ++pg) {
+            if (pg < np) {
+                const int32_t page = pid[pg];
+                dev::mbar_wait(&empty[pos.stage], pos.phase ^ 1u);
+                uint8_t *dst = ring + (size_t)pos.stage * kStageBytes;
+                dev::mbar_arrive_expect_tx(&full[pos.stage], kStageBytes);
                 if (COPY == 0) {
                     const size_t off = (size_t)page * kPageBytes;
-                    dev::bulk_g2s(dst, p.k_pool + off, kPageBytes, &full[stage], pol_stream);
-                    dev::bulk_g2s(dst + kPageBytes, p.v_pool + off, kPageBytes, &full[stage], pol_stream);
+                    dev::bulk_g2s(dst, p.k_pool + off, kPageBytes, &full[pos.stage], pol_stream);
+                    dev::bulk_g2s(dst + kPageBytes, p.v_pool + off, kPageBytes, &full[pos.stage], pol_stream);
                 } else {
-                    // one 64-column block (16 rows x 128 B, swizzled) per TMA
                     const int row = page * kP;
 #pragma unroll
                     for (int cb = 0; cb < ROW_BYTES / 128; ++cb) {
-                        dev::tma_load_2d(dst + cb * 2048, tmap_k, 64 * cb, row, &full[stage], pol_stream);
-                        dev::tma_load_2d(dst + kPageBytes + cb * 2048, tmap_v, 64 * cb, row, &full[stage], pol_stream);
+                        dev::tma_load_2d(dst + cb * 2048, tmap_k, 64 * cb, row, &full[pos.stage], pol_stream);
+                        dev::tma_load_2d(dst + kPageBytes + cb * 2048, tmap_v, 64 * cb, row, &full[pos.stage],
+                                         pol_stream);
                     }
                 }
+                pos.advance(1, p.stages);
             }
-            __syncwarp();
-            ++n;
-            if (++stage == p.stages) stage = 0;
         }
-        pid = pid_next;
+        cur = nd;
+#pragma unroll
+        for (int i = 0; i < kPagesPerItem; ++i) pid[i] = pid_next[i];
     }
 }
 
@@ -257,6 +270,47 @@ __device__ __forceinline__ void merge_and_store(const Params &p, const float *mb
 }
 
 // ---------------------------------------------------------------- simt consumer
+// Lane layout for one page (16 token rows of ROW_BYTES): LPT lanes share a
+// token row, each owning one 16-byte chunk (EPL elements); a warp covers TPS
+// tokens per step and STEPS = 16 / TPS steps per page (STEPS == LPT / 2).
+// q.k: per-lane partial dots for the STEPS tokens it touches, reduced over
+// the LPT lanes by a transposing butterfly (log2(STEPS) exchange rounds +
+// one add round) that leaves lane (ltok, lchk) with the score of token
+// (lchk >> 1) * TPS + ltok.  p is broadcast back for p.v with one shuffle per
+// step.  Full pages take an unmasked path; only a sequence's last page masks.
+template <int STEPS>
+__device__ __forceinline__ float butterfly_reduce(float (&s)[STEPS], int lane, int lpt) {
+    // exchange rounds: halve the value set, keep the half selected by the lane bit
+    float v[STEPS];
+#pragma unroll
+    for (int i = 0; i < STEPS; ++i) v[i] = s[i];
+    int mask = lpt >> 1;
+#pragma unroll
+    for (int n = STEPS; n > 1; n >>= 1) {
+        const bool up = (lane & mask) != 0;
+#pragma unroll
+        for (int k = 0; k < n / 2; ++k) {
+            const float send = up ? v[k] : v[k + n / 2];
+            const float keep = up ? v[k + n / 2] : v[k];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+        }
+        mask >>= 1;
+    }
+    // the remaining lane bit (mask == 1) holds the other half of the sum
+    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+__device__ __forceinline__ void ffma2(float &a0, float &a1, float b0, float b1, float c) {
+    asm("{\n\t.reg .b64 a, b, c;\n\t"
+        "mov.b64 a, {%0, %1};\n\t"
+        "mov.b64 b, {%2, %3};\n\t"
+        "mov.b64 c, {%4, %4};\n\t"
+        "fma.rn.f32x2 a, b, c, a;\n\t"
+        "mov.b64 {%0, %1}, a;\n\t}"
+        : "+f"(a0), "+f"(a1)
+        : "f"(b0), "f"(b1), "f"(c));
+}
+
 template <int DT, int D, int R, int NW>
 __device__ void consumer_simt(const Params &p, const uint8_t *ring, const uint8_t *qbuf, const ItemMeta *qmeta,
                               uint64_t *full, uint64_t *empty, uint64_t *qfull, uint64_t *qempty, float *mbuf,
@@ -271,20 +325,21 @@ __device__ void consumer_simt(const Params &p, const uint8_t *ring, const uint8_
     constexpr int TPS = 32 / LPT;        // tokens per step
     constexpr int STEPS = kP / TPS;      // steps per page
     constexpr int EPL = 16 / EB;         // elements per lane chunk
-    static_assert(LPT >= 1 && LPT <= 32 && TPS * LPT == 32, "row must be 16..512 bytes");
+    static_assert(LPT >= 2 && LPT <= 32 && TPS * LPT == 32 && STEPS * 2 == LPT, "row must be 64..512 bytes");
 
     const int lane = threadIdx.x & 31;
     const int cw = (threadIdx.x >> 5) - 1;  // consumer warp index
     const int ctid = threadIdx.x - 32;
     const int ltok = lane / LPT, lchk = lane % LPT;
+    const int my_step = lchk >> 1;          // after the butterfly: this lane's token is my_step * TPS + ltok
+    const bool l_owner = (lchk & 1) == 0;   // counts its token once in l
 
-    uint32_t n_base = 0;
+    RingPos base{0, 0u};  // ring position of this CTA's first page of the current item
     int it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        const int slot = it % kQSlots;
+        const int slot = it & (kQSlots - 1);
         dev::mbar_wait(&qfull[slot], (it / kQSlots) & 1);
         const ItemMeta meta = qmeta[slot];
-        // q chunk of every head: EPL elements at lchk
         uint4 qv[R];
 #pragma unroll
         for (int rr = 0; rr < R; ++rr)
@@ -301,11 +356,11 @@ __device__ void consumer_simt(const Params &p, const uint8_t *ring, const uint8_
             for (int e = 0; e < EPL; ++e) acc[rr][e] = 0.f;
         }
 
-        int stage = (int)((n_base + cw) % (uint32_t)p.stages);
+        RingPos pos = base;
+        pos.advance(cw, p.stages);
         for (int pg = cw; pg < meta.npages; pg += NW) {
-            const uint32_t n = n_base + pg;
-            dev::mbar_wait(&full[stage], (n / p.stages) & 1);
-            const uint8_t *kb = ring + (size_t)stage * kStageBytes;
+            dev::mbar_wait(&full[pos.stage], pos.phase);
+            const uint8_t *kb = ring + (size_t)pos.stage * kStageBytes;
             const uint8_t *vb = kb + kPageBytes;
             const int valid = min(kP, meta.ntok - pg * kP);
 
@@ -313,86 +368,78 @@ __device__ void consumer_simt(const Params &p, const uint8_t *ring, const uint8_
 #pragma unroll
             for (int i = 0; i < STEPS; ++i)
                 kr[i] = *reinterpret_cast<const uint4 *>(kb + (i * TPS + ltok) * ROW_BYTES + lchk * 16);
-            float pr[R][STEPS];
+            float pr[R];
 #pragma unroll
             for (int rr = 0; rr < R; ++rr) {
                 float s[STEPS];
 #pragma unroll
                 for (int i = 0; i < STEPS; ++i) {
-                    float acc_s = 0.f;
+                    float a = 0.f;
                     if constexpr (DT == HETIS_BF16) {
-                        acc_s = dev::fma_bf16x2(qv[rr].x, kr[i].x, acc_s);
-                        acc_s = dev::fma_bf16x2(qv[rr].y, kr[i].y, acc_s);
-                        acc_s = dev::fma_bf16x2(qv[rr].z, kr[i].z, acc_s);
-                        acc_s = dev::fma_bf16x2(qv[rr].w, kr[i].w, acc_s);
+                        a = dev::fma_bf16x2(qv[rr].x, kr[i].x, a);
+                        a = dev::fma_bf16x2(qv[rr].y, kr[i].y, a);
+                        a = dev::fma_bf16x2(qv[rr].z, kr[i].z, a);
+                        a = dev::fma_bf16x2(qv[rr].w, kr[i].w, a);
                     } else {
-                        acc_s = fmaf(__uint_as_float(qv[rr].x), __uint_as_float(kr[i].x), acc_s);
-                        acc_s = fmaf(__uint_as_float(qv[rr].y), __uint_as_float(kr[i].y), acc_s);
-                        acc_s = fmaf(__uint_as_float(qv[rr].z), __uint_as_float(kr[i].z), acc_s);
-                        acc_s = fmaf(__uint_as_float(qv[rr].w), __uint_as_float(kr[i].w), acc_s);
+                        a = fmaf(__uint_as_float(qv[rr].x), __uint_as_float(kr[i].x), a);
+                        a = fmaf(__uint_as_float(qv[rr].y), __uint_as_float(kr[i].y), a);
+                        a = fmaf(__uint_as_float(qv[rr].z), __uint_as_float(kr[i].z), a);
+                        a = fmaf(__uint_as_float(qv[rr].w), __uint_as_float(kr[i].w), a);
                     }
-                    s[i] = acc_s;
+                    s[i] = a;
                 }
+                float sc = butterfly_reduce<STEPS>(s, lane, LPT) * p.scale_log2;
+                if (valid < kP && my_step * TPS + ltok >= valid) sc = -INFINITY;
+                float mx = sc;
 #pragma unroll
-                for (int i = 0; i < STEPS; ++i) {
-#pragma unroll
-                    for (int o = LPT / 2; o >= 1; o >>= 1) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
-                    const int t = i * TPS + ltok;
-                    s[i] = (t < valid) ? s[i] * p.scale_log2 : -INFINITY;
-                }
-                float mx = s[0];
-#pragma unroll
-                for (int i = 1; i < STEPS; ++i) mx = fmaxf(mx, s[i]);
-#pragma unroll
-                for (int o = 16; o >= LPT; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                for (int o = 16; o >= 2; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
                 const float m_new = fmaxf(m[rr], mx);
-                const float alpha = dev::ex2(m[rr] - m_new);  // m = -inf -> 0
-                float ls = 0.f;
+                if (m_new != m[rr]) {  // warp-uniform
+                    const float alpha = dev::ex2(m[rr] - m_new);  // m = -inf -> 0
+                    l[rr] *= alpha;
 #pragma unroll
-                for (int i = 0; i < STEPS; ++i) {
-                    pr[rr][i] = dev::ex2(s[i] - m_new);
-                    ls += pr[rr][i];
+                    for (int e = 0; e < EPL; ++e) acc[rr][e] *= alpha;
+                    m[rr] = m_new;
                 }
-                l[rr] = fmaf(l[rr], alpha, ls);
-#pragma unroll
-                for (int e = 0; e < EPL; ++e) acc[rr][e] *= alpha;
-                m[rr] = m_new;
+                pr[rr] = dev::ex2(sc - m_new);
+                if (l_owner) l[rr] += pr[rr];
             }
-            // p . v
+            // p . v : lane (ltok, lchk) accumulates the tokens i * TPS + ltok on its chunk
 #pragma unroll
             for (int i = 0; i < STEPS; ++i) {
                 const int t = i * TPS + ltok;
-                if (t < valid) {
+                float pt[R];
+#pragma unroll
+                for (int rr = 0; rr < R; ++rr) pt[rr] = __shfl_sync(0xffffffffu, pr[rr], ltok * LPT + 2 * i);
+                if (valid == kP || t < valid) {  // rows past the sequence end may hold anything (NaN)
                     const uint4 vr = *reinterpret_cast<const uint4 *>(vb + t * ROW_BYTES + lchk * 16);
-                    float v[EPL];
-                    if constexpr (DT == HETIS_BF16) {
-                        v[0] = dev::bf16lo(vr.x); v[1] = dev::bf16hi(vr.x);
-                        v[2] = dev::bf16lo(vr.y); v[3] = dev::bf16hi(vr.y);
-                        v[4] = dev::bf16lo(vr.z); v[5] = dev::bf16hi(vr.z);
-                        v[6] = dev::bf16lo(vr.w); v[7] = dev::bf16hi(vr.w);
-                    } else {
-                        v[0] = __uint_as_float(vr.x); v[1] = __uint_as_float(vr.y);
-                        v[2] = __uint_as_float(vr.z); v[3] = __uint_as_float(vr.w);
+#pragma unroll
+                    for (int rr = 0; rr < R; ++rr) {
+                        if constexpr (DT == HETIS_BF16) {
+                            ffma2(acc[rr][0], acc[rr][1], dev::bf16lo(vr.x), dev::bf16hi(vr.x), pt[rr]);
+                            ffma2(acc[rr][2], acc[rr][3], dev::bf16lo(vr.y), dev::bf16hi(vr.y), pt[rr]);
+                            ffma2(acc[rr][4], acc[rr][5], dev::bf16lo(vr.z), dev::bf16hi(vr.z), pt[rr]);
+                            ffma2(acc[rr][6], acc[rr][7], dev::bf16lo(vr.w), dev::bf16hi(vr.w), pt[rr]);
+                        } else {
+                            ffma2(acc[rr][0], acc[rr][1], __uint_as_float(vr.x), __uint_as_float(vr.y), pt[rr]);
+                            ffma2(acc[rr][2], acc[rr][3], __uint_as_float(vr.z), __uint_as_float(vr.w), pt[rr]);
+                        }
                     }
-#pragma unroll
-                    for (int rr = 0; rr < R; ++rr)
-#pragma unroll
-                        for (int e = 0; e < EPL; ++e) acc[rr][e] = fmaf(pr[rr][i], v[e], acc[rr][e]);
                 }
             }
             __syncwarp();
-            if (lane == 0) dev::mbar_arrive(&empty[stage]);
-            stage += NW;
-            while (stage >= p.stages) stage -= p.stages;
+            if (lane == 0) dev::mbar_arrive(&empty[pos.stage]);
+            pos.advance(NW, p.stages);
         }
-        n_base += meta.npages;
+        base.advance(meta.npages, p.stages);
 
-        // fold token groups of this warp
+        // fold: l over the whole warp, acc over the token groups
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) {
 #pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) l[rr] += __shfl_xor_sync(0xffffffffu, l[rr], o);
+#pragma unroll
             for (int o = 16; o >= LPT; o >>= 1) {
-                l[rr] += __shfl_xor_sync(0xffffffffu, l[rr], o);
 #pragma unroll
                 for (int e = 0; e < EPL; ++e) acc[rr][e] += __shfl_xor_sync(0xffffffffu, acc[rr][e], o);
             }
@@ -455,10 +502,10 @@ __device__ void consumer_tc(const Params &p, const uint8_t *ring, const uint8_t 
         v_off[c2] = swz((mi & 1) * 8 + (lane & 7), 2 * c2 + (mi >> 1));
     }
 
-    uint32_t n_base = 0;
+    RingPos base{0, 0u};
     int it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        const int slot = it % kQSlots;
+        const int slot = it & (kQSlots - 1);
         dev::mbar_wait(&qfull[slot], (it / kQSlots) & 1);
         const ItemMeta meta = qmeta[slot];
         // A fragments of Q: row grp (zero if grp >= R), k-step ks: reg0 cols 16ks+2tq, reg2 cols +8
@@ -484,11 +531,11 @@ __device__ void consumer_tc(const Params &p, const uint8_t *ring, const uint8_t 
 #pragma unroll
         for (int nt = 0; nt < NT_O; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
 
-        int stage = (int)((n_base + cw) % (uint32_t)p.stages);
+        RingPos pos = base;
+        pos.advance(cw, p.stages);
         for (int pg = cw; pg < meta.npages; pg += NW) {
-            const uint32_t n = n_base + pg;
-            dev::mbar_wait(&full[stage], (n / p.stages) & 1);
-            const uint32_t kb = dev::smem_u32(ring + (size_t)stage * kStageBytes);
+            dev::mbar_wait(&full[pos.stage], pos.phase);
+            const uint32_t kb = dev::smem_u32(ring + (size_t)pos.stage * kStageBytes);
             const uint32_t vb = kb + kPageBytes;
             const int valid = min(kP, meta.ntok - pg * kP);
 
@@ -561,11 +608,10 @@ __device__ void consumer_tc(const Params &p, const uint8_t *ring, const uint8_t 
                 dev::mma_bf16_16816(o[2 * c2 + 1], pa[0], pa[1], pa[2], pa[3], b[2] & mk0, b[3] & mk1);
             }
             __syncwarp();
-            if (lane == 0) dev::mbar_arrive(&empty[stage]);
-            stage += NW;
-            while (stage >= p.stages) stage -= p.stages;
+            if (lane == 0) dev::mbar_arrive(&empty[pos.stage]);
+            pos.advance(NW, p.stages);
         }
-        n_base += meta.npages;
+        base.advance(meta.npages, p.stages);
 
         l += __shfl_xor_sync(0xffffffffu, l, 1);
         l += __shfl_xor_sync(0xffffffffu, l, 2);
@@ -628,10 +674,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     build_split_offsets(p, s_len, s_off);  // contains __syncthreads
     const int n_items = s_off[p.num_seqs] * p.kv_heads;
 
-    if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
         producer<ROW_BYTES, R, TC ? 1 : 0>(p, ring, qbuf, qmeta, full, empty, qfull, qempty, s_len, s_off, &tmap_k,
                                            &tmap_v);
-    } else {
+    } else if (threadIdx.x >= 32) {
         if constexpr (TC) {
             consumer_tc<D, R, NW>(p, ring, qbuf, qmeta, full, empty, qfull, qempty, mbuf, n_items);
         } else {
