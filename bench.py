@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--cpu-sample-seqs", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--o-dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--attn-flags", type=int, default=0, help="HETIS_ATTN_* flags (diagnostics)")
     return ap.parse_args()
 
 
@@ -267,7 +268,8 @@ def run_ours(args, world, rank, local):
         if ev_a is not None:
             ev_a.record(stream)
         hetis.attn_partial(step.cshape, step.buf.q_shard, k_pools[li], v_pools[li], batch.block_table,
-                           batch.seq_lens, max_len, step.buf.workspace, q_head_begin=q_begin)
+                           batch.seq_lens, max_len, step.buf.workspace, q_head_begin=q_begin,
+                           flags=args.attn_flags)
         if ev_b is not None:
             ev_b.record(stream)
         hetis.attn_combine(step.cshape, batch.seq_lens, max_len, step.buf.o_shard, step.buf.workspace,

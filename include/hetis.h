@@ -93,6 +93,10 @@ typedef struct {
 
 /* Flags for hetis_attn_partial / hetis_attn_decode. */
 #define HETIS_ATTN_FORCE_SIMT 0x1u /* bf16 GQA on CUDA cores instead of tensor cores */
+/* Diagnostic only: stream every K/V page through the shared-memory ring but
+ * skip the math (partials are left unwritten).  Measures the memory-system
+ * ceiling of the pipeline; the CUDA-core kernel honours it. */
+#define HETIS_ATTN_DIAG_STREAM_ONLY 0x100u
 
 /* ---- status ------------------------------------------------------------ */
 HETIS_API const char *hetis_status_str(hetis_status s);

@@ -17,7 +17,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-LIB = os.path.join(PKG, "libhetis.so")
+LIB = os.environ.get("HETIS_LIB") or os.path.join(PKG, "libhetis.so")
+EXTRA = os.environ.get("HETIS_NVCC_FLAGS", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -56,10 +57,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     objs = []
-    build_dir = os.path.join(PKG, "build")
+    build_dir = os.path.join(PKG, "build", os.path.basename(LIB))
     os.makedirs(build_dir, exist_ok=True)
     common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
-              "-I", INCLUDE, "-I", CSRC, "-I", _nccl_include(), "--expt-relaxed-constexpr"]
+              "-I", INCLUDE, "-I", CSRC, "-I", _nccl_include(), "--expt-relaxed-constexpr", *EXTRA]
     if verbose:
         common += ["-Xptxas", "-v"]
     procs = []

@@ -352,6 +352,7 @@ hetis_status hetis_attn_partial(const hetis_shape *shape, int32_t num_seqs, int3
                                 block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes, &a);
     if (st != HETIS_OK) return st;
     if (num_seqs == 0) return HETIS_OK;
+    a.flags = flags;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const bool tc = a.dtype == HETIS_BF16 && a.r > 1 && !(flags & HETIS_ATTN_FORCE_SIMT);
     cudaError_t e;

@@ -48,6 +48,16 @@ constexpr int kP = kPageSize;
 constexpr int kC = kSplitTokens;
 constexpr int kPagesPerItem = kC / kP;  // 16
 constexpr int kQSlots = 2;
+// tunables (compile-time; scripts/ sweeps override them with -D)
+#ifndef HETIS_SIMT_NW
+#define HETIS_SIMT_NW 8
+#endif
+#ifndef HETIS_TC_NW
+#define HETIS_TC_NW 8
+#endif
+#ifndef HETIS_MAX_STAGES
+#define HETIS_MAX_STAGES 24
+#endif
 constexpr int kMaxSmem = 227 * 1024;
 static_assert(kPagesPerItem <= 32, "one producer lane per page of an item");
 
@@ -66,6 +76,7 @@ struct Params {
     int max_pages;
     int stages;    // ring depth
     float scale_log2;  // log2(e) / sqrt(d)
+    uint32_t flags;    // HETIS_ATTN_*
 };
 
 struct ItemMeta {
@@ -360,6 +371,12 @@ __device__ void consumer_simt(const Params &p, const uint8_t *ring, const uint8_
         pos.advance(cw, p.stages);
         for (int pg = cw; pg < meta.npages; pg += NW) {
             dev::mbar_wait(&full[pos.stage], pos.phase);
+            if (p.flags & HETIS_ATTN_DIAG_STREAM_ONLY) {  // diagnostic: memory-system ceiling of this pipeline
+                __syncwarp();
+                if (lane == 0) dev::mbar_arrive(&empty[pos.stage]);
+                pos.advance(NW, p.stages);
+                continue;
+            }
             const uint8_t *kb = ring + (size_t)pos.stage * kStageBytes;
             const uint8_t *vb = kb + kPageBytes;
             const int valid = min(kP, meta.ntok - pg * kP);
@@ -689,7 +706,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
 // ---------------------------------------------------------------- host side
 template <int DT, int D, int R, bool TC>
 struct Launch {
-    static constexpr int NW = 8;
+    static constexpr int NW = TC ? HETIS_TC_NW : HETIS_SIMT_NW;
     static constexpr int EB = DT == HETIS_BF16 ? 2 : 4;
     static constexpr int ROW_BYTES = D * EB;
     static constexpr int kStageBytes = 2 * kP * ROW_BYTES;
@@ -706,7 +723,7 @@ struct Launch {
                            const CUtensorMap &tv, std::string *err) {
         Params p = p0;
         // ring depth: as deep as shared memory allows, at most 24 stages
-        int stages = 24;
+        int stages = HETIS_MAX_STAGES;
         while (stages > 4 && (size_t)stages * kStageBytes + fixed_bytes(num_seqs, stages) + 1024 > (size_t)kMaxSmem)
             --stages;
         const size_t smem = (size_t)stages * kStageBytes + fixed_bytes(num_seqs, stages) + 1024;
@@ -740,6 +757,7 @@ Params make_params(const AttnArgs &a) {
     p.kv_heads = a.kv_heads;
     p.max_pages = a.max_pages;
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)a.head_dim));
+    p.flags = a.flags;
     return p;
 }
 

@@ -36,6 +36,7 @@ struct AttnArgs {
     float *part_lse;      // [max_items][r]
     float *part_o;        // [max_items][r][head_dim]
     int64_t max_items;
+    uint32_t flags;       // HETIS_ATTN_*
 };
 
 struct WorkspaceLayout {

@@ -16,7 +16,7 @@ import torch
 from . import workload
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libhetis.so")
+LIB_PATH = os.environ.get("HETIS_LIB") or os.path.join(_PKG, "libhetis.so")
 
 HETIS_OK = 0
 STATUS = {0: "HETIS_OK", 1: "HETIS_E_INVALID", 2: "HETIS_E_HEAD_INTEGRITY", 3: "HETIS_E_GROUP_ALIGN",
