@@ -58,6 +58,11 @@ constexpr int kQSlots = 2;
 #ifndef HETIS_MAX_STAGES
 #define HETIS_MAX_STAGES 24
 #endif
+#ifndef HETIS_PRODUCER_LANES
+#define HETIS_PRODUCER_LANES 4
+#endif
+constexpr int kProducerLanes = HETIS_PRODUCER_LANES;
+static_assert(kPagesPerItem % kProducerLanes == 0, "producer lanes must divide the pages of an item");
 constexpr int kMaxSmem = 227 * 1024;
 static_assert(kPagesPerItem <= 32, "one producer lane per page of an item");
 
@@ -162,12 +167,13 @@ struct RingPos {
     }
 };
 
-// ---------------------------------------------------------------- producer (one thread)
+// ---------------------------------------------------------------- producer (kProducerLanes threads)
 // COPY = 0: two 1-D bulk copies per page (K, V).  COPY = 1: 2-D tensor copies
 // of 64-column blocks (16 rows x 128 B, 128-B swizzle) for K and V.
-// Runs on lane 0 of warp 0 only; the item's block-table entries are loaded one
-// item ahead (16 independent loads) so their latency hides behind the current
-// item's page issue.
+// Runs on lanes 0 .. kProducerLanes-1 of warp 0: lane 0 alone streams the q
+// rows; each lane issues every kProducerLanes-th page, so ring waits and
+// expect_tx arrivals of consecutive pages overlap.  Block-table entries are
+// loaded one item ahead so their latency hides behind the current item.
 template <int ROW_BYTES, int R, int COPY>
 __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta *qmeta, uint64_t *full,
                          uint64_t *empty, uint64_t *qfull, uint64_t *qempty, const int32_t *s_len,
@@ -177,8 +183,9 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
     constexpr int kQBytes = R * ROW_BYTES;
     constexpr int kQStride = (kQBytes + 127) / 128 * 128;
     const int n_items = s_off[p.num_seqs] * p.kv_heads;
+    const int lane = threadIdx.x & 31;
     const uint64_t pol_stream = dev::policy_evict_first();
-    if (COPY == 1) {
+    if (COPY == 1 && lane == 0) {
         dev::prefetch_tmap(tmap_k);
         dev::prefetch_tmap(tmap_v);
     }
@@ -202,57 +209,73 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
         const uint8_t *src = p.q + ((size_t)d.j * p.q_heads + (size_t)d.g * R) * ROW_BYTES;
         dev::bulk_g2s(qbuf + (size_t)slot * kQStride, src, kQBytes, &qfull[slot], pol_stream);
     };
-    auto load_pids = [&](const Dec &d, int32_t (&pid)[kPagesPerItem]) {
+    // lane k of the G producer lanes owns pages k, k + G, k + 2G, ... of every item
+    constexpr int PPL = kPagesPerItem / kProducerLanes;
+    auto load_pids = [&](const Dec &d, int32_t (&pid)[PPL]) {
         const int np = (d.ntok + kP - 1) / kP;
         const int32_t *row = p.block_table + ((size_t)d.j * p.kv_heads + d.g) * p.max_pages + d.t0 / kP;
 #pragma unroll
-        for (int i = 0; i < kPagesPerItem; ++i) pid[i] = i < np ? __ldg(row + i) : 0;
+        for (int i = 0; i < PPL; ++i) {
+            const int pg = i * kProducerLanes + lane;
+            pid[i] = pg < np ? __ldg(row + pg) : 0;
+        }
     };
+    constexpr unsigned kMask = (1u << kProducerLanes) - 1u;
 
     int item = blockIdx.x;
     if (item >= n_items) return;
     static_assert((kQSlots & (kQSlots - 1)) == 0, "q slots: power of two");
     Dec cur = decode(item);
-    issue_q(0, item, cur);
-    int32_t pid[kPagesPerItem];
+    if (lane == 0) issue_q(0, item, cur);
+    int32_t pid[PPL];
     load_pids(cur, pid);
     RingPos pos{0, 0u};
     for (int it = 0; item < n_items; item += gridDim.x, ++it) {
         const int next = item + gridDim.x;
-        int32_t pid_next[kPagesPerItem];
+        int32_t pid_next[PPL];
         Dec nd{0, 0, 0, 0};
         if (next < n_items) {
             nd = decode(next);
-            issue_q(it + 1, next, nd);
+            if (lane == 0) issue_q(it + 1, next, nd);
             load_pids(nd, pid_next);
         }
+        __syncwarp(kMask);
         const int np = (cur.ntok + kP - 1) / kP;
+        // G lanes issue G consecutive pages at once: their ring waits and
+        // expect_tx arrivals overlap instead of serialising on one thread
 #pragma unroll
-        for (int pg = 0; pg < kPagesPerItem; ++pg) {
-            if (pg < np) {
-                const int32_t page = pid[pg];
-                dev::mbar_wait(&empty[pos.stage], pos.phase ^ 1u);
-                uint8_t *dst = ring + (size_t)pos.stage * kStageBytes;
-                dev::mbar_arrive_expect_tx(&full[pos.stage], kStageBytes);
-                if (COPY == 0) {
-                    const size_t off = (size_t)page * kPageBytes;
-                    dev::bulk_g2s(dst, p.k_pool + off, kPageBytes, &full[pos.stage], pol_stream);
-                    dev::bulk_g2s(dst + kPageBytes, p.v_pool + off, kPageBytes, &full[pos.stage], pol_stream);
-                } else {
-                    const int row = page * kP;
+        for (int i = 0; i < PPL; ++i) {
+            const int pg0 = i * kProducerLanes;
+            if (pg0 < np) {
+                const int pg = pg0 + lane;
+                if (pg < np) {
+                    RingPos my = pos;
+                    my.advance(lane, p.stages);
+                    const int32_t page = pid[i];
+                    dev::mbar_wait(&empty[my.stage], my.phase ^ 1u);
+                    uint8_t *dst = ring + (size_t)my.stage * kStageBytes;
+                    dev::mbar_arrive_expect_tx(&full[my.stage], kStageBytes);
+                    if (COPY == 0) {
+                        const size_t off = (size_t)page * kPageBytes;
+                        dev::bulk_g2s(dst, p.k_pool + off, kPageBytes, &full[my.stage], pol_stream);
+                        dev::bulk_g2s(dst + kPageBytes, p.v_pool + off, kPageBytes, &full[my.stage], pol_stream);
+                    } else {
+                        const int row = page * kP;
 #pragma unroll
-                    for (int cb = 0; cb < ROW_BYTES / 128; ++cb) {
-                        dev::tma_load_2d(dst + cb * 2048, tmap_k, 64 * cb, row, &full[pos.stage], pol_stream);
-                        dev::tma_load_2d(dst + kPageBytes + cb * 2048, tmap_v, 64 * cb, row, &full[pos.stage],
-                                         pol_stream);
+                        for (int cb = 0; cb < ROW_BYTES / 128; ++cb) {
+                            dev::tma_load_2d(dst + cb * 2048, tmap_k, 64 * cb, row, &full[my.stage], pol_stream);
+                            dev::tma_load_2d(dst + kPageBytes + cb * 2048, tmap_v, 64 * cb, row, &full[my.stage],
+                                             pol_stream);
+                        }
                     }
                 }
-                pos.advance(1, p.stages);
+                __syncwarp(kMask);
+                pos.advance(min(kProducerLanes, np - pg0), p.stages);
             }
         }
         cur = nd;
 #pragma unroll
-        for (int i = 0; i < kPagesPerItem; ++i) pid[i] = pid_next[i];
+        for (int i = 0; i < PPL; ++i) pid[i] = pid_next[i];
     }
 }
 
@@ -691,7 +714,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     build_split_offsets(p, s_len, s_off);  // contains __syncthreads
     const int n_items = s_off[p.num_seqs] * p.kv_heads;
 
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < kProducerLanes) {
         producer<ROW_BYTES, R, TC ? 1 : 0>(p, ring, qbuf, qmeta, full, empty, qfull, qempty, s_len, s_off, &tmap_k,
                                            &tmap_v);
     } else if (threadIdx.x >= 32) {
