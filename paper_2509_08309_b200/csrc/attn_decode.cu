@@ -280,26 +280,41 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
 }
 
 // ---------------------------------------------------------------- merge of NW warp states
-// mbuf layout: [NW][R][D + 2] floats: acc[D], m (log2 domain), l.
+// mbuf layout (one of two alternating buffers): [NW][R][D + 4] floats:
+// acc[D], m (log2 domain), l.  Head rr of item number `it` is merged by consumer
+// warp (rr + it) mod NW: lanes < NW fetch the NW (m, l) pairs, the max and the
+// weighted sum of l are warp reductions, then every lane combines D / 32
+// dimensions over the NW warps in ascending warp order (deterministic).
 template <int D, int R, int NW>
-__device__ __forceinline__ void merge_and_store(const Params &p, const float *mbuf, int item, int ctid) {
-    constexpr int kRow = D + 2;
-    for (int e = ctid; e < R * D; e += NW * 32) {
-        const int rr = e / D, d = e - rr * D;
-        float M = -INFINITY;
+__device__ __forceinline__ void merge_warp(const Params &p, const float *mbuf, int item, int it, int cw, int lane) {
+    constexpr int kRow = D + 4;  // 16-B aligned rows
+    constexpr int DPL = D / 32;
+    static_assert(NW <= 32 && D % 32 == 0, "merge layout");
+    for (int rr = (cw + NW - (it % NW)) % NW; rr < R; rr += NW) {
+        const float mw = lane < NW ? mbuf[(lane * R + rr) * kRow + D] : -INFINITY;
+        const float lw = lane < NW ? mbuf[(lane * R + rr) * kRow + D + 1] : 0.f;
+        float M = mw;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) M = fmaxf(M, mbuf[(w * R + rr) * kRow + D]);
-        float lsum = 0.f, a = 0.f;
+        for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const float f = (mw == -INFINITY) ? 0.f : dev::ex2(mw - M);
+        float lsum = f * lw;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+        float a[DPL];
+#pragma unroll
+        for (int k = 0; k < DPL; ++k) a[k] = 0.f;
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
-            const float mw = mbuf[(w * R + rr) * kRow + D];
-            const float f = (mw == -INFINITY) ? 0.f : dev::ex2(mw - M);
-            lsum = fmaf(f, mbuf[(w * R + rr) * kRow + D + 1], lsum);
-            a = fmaf(f, mbuf[(w * R + rr) * kRow + d], a);
+            const float fw = __shfl_sync(0xffffffffu, f, w);
+            const float *src = mbuf + (w * R + rr) * kRow + lane * DPL;
+#pragma unroll
+            for (int k = 0; k < DPL; ++k) a[k] = fmaf(fw, src[k], a[k]);
         }
         const size_t row = (size_t)item * R + rr;
-        p.part_o[row * D + d] = __fdiv_rn(a, lsum);
-        if (d == 0) p.part_lse[row] = M + __log2f(lsum);
+        float *dst = p.part_o + row * D + lane * DPL;
+#pragma unroll
+        for (int k = 0; k < DPL; ++k) dst[k] = __fdiv_rn(a[k], lsum);
+        if (lane == 0) p.part_lse[row] = M + __log2f(lsum);
     }
 }
 
@@ -484,11 +499,12 @@ __device__ void consumer_simt(const Params &p, const uint8_t *ring, const uint8_
                 for (int e = 0; e < EPL; ++e) acc[rr][e] += __shfl_xor_sync(0xffffffffu, acc[rr][e], o);
             }
         }
-        constexpr int kRow = D + 2;
+        constexpr int kRow = D + 4;  // 16-B aligned rows
+        float *mb = mbuf + (it & 1) * (NW * R * kRow);  // double-buffered: one barrier per item
         if (ltok == 0) {
 #pragma unroll
             for (int rr = 0; rr < R; ++rr) {
-                float *row = mbuf + (cw * R + rr) * kRow;
+                float *row = mb + (cw * R + rr) * kRow;
 #pragma unroll
                 for (int e = 0; e < EPL; ++e) row[lchk * EPL + e] = acc[rr][e];
                 if (lchk == 0) {
@@ -498,8 +514,7 @@ __device__ void consumer_simt(const Params &p, const uint8_t *ring, const uint8_
             }
         }
         dev::named_bar_sync(1, NW * 32);
-        merge_and_store<D, R, NW>(p, mbuf, meta.item, ctid);
-        dev::named_bar_sync(1, NW * 32);
+        merge_warp<D, R, NW>(p, mb, meta.item, it, cw, lane);
     }
 }
 
@@ -655,22 +670,20 @@ __device__ void consumer_tc(const Params &p, const uint8_t *ring, const uint8_t 
 
         l += __shfl_xor_sync(0xffffffffu, l, 1);
         l += __shfl_xor_sync(0xffffffffu, l, 2);
-        constexpr int kRow = D + 2;
+        constexpr int kRow = D + 4;  // 16-B aligned rows
+        float *mb = mbuf + (it & 1) * (NW * R * kRow);  // double-buffered: one barrier per item
         if (grp < R) {
-            float *row = mbuf + (cw * R + grp) * kRow;
+            float *row = mb + (cw * R + grp) * kRow;
 #pragma unroll
-            for (int nt = 0; nt < NT_O; ++nt) {
-                row[8 * nt + 2 * tq] = o[nt][0] + o[nt][2];
-                row[8 * nt + 2 * tq + 1] = o[nt][1] + o[nt][3];
-            }
+            for (int nt = 0; nt < NT_O; ++nt)
+                *reinterpret_cast<float2 *>(row + 8 * nt + 2 * tq) = make_float2(o[nt][0] + o[nt][2], o[nt][1] + o[nt][3]);
             if (tq == 0) {
                 row[D] = m;
                 row[D + 1] = l;
             }
         }
         dev::named_bar_sync(1, NW * 32);
-        merge_and_store<D, R, NW>(p, mbuf, meta.item, ctid);
-        dev::named_bar_sync(1, NW * 32);
+        merge_warp<D, R, NW>(p, mb, meta.item, it, cw, lane);
     }
 }
 
@@ -690,7 +703,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     uint8_t *ring = smem;
     uint8_t *qbuf = ring + (size_t)p.stages * kStageBytes;
     float *mbuf = reinterpret_cast<float *>(qbuf + kQSlots * kQStride);
-    const size_t mbuf_bytes = (size_t)NW * R * (D + 2) * sizeof(float);
+    const size_t mbuf_bytes = 2 * (size_t)NW * R * (D + 4) * sizeof(float);
     uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(mbuf) + ((mbuf_bytes + 15) / 16 * 16));
     uint64_t *full = bars;
     uint64_t *empty = full + p.stages;
@@ -736,7 +749,7 @@ struct Launch {
     static constexpr int kQStride = (R * ROW_BYTES + 127) / 128 * 128;
 
     static size_t fixed_bytes(int num_seqs, int stages) {
-        size_t mb = (size_t)NW * R * (D + 2) * sizeof(float);
+        size_t mb = 2 * (size_t)NW * R * (D + 4) * sizeof(float);
         mb = (mb + 15) / 16 * 16;
         return (size_t)kQSlots * kQStride + mb + (size_t)(2 * stages + 2 * kQSlots) * 8 +
                (size_t)kQSlots * sizeof(ItemMeta) + (size_t)(2 * num_seqs + 1) * 4;
