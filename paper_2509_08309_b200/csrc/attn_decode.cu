@@ -260,13 +260,11 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
                         dev::bulk_g2s(dst, p.k_pool + off, kPageBytes, &full[my.stage], pol_stream);
                         dev::bulk_g2s(dst + kPageBytes, p.v_pool + off, kPageBytes, &full[my.stage], pol_stream);
                     } else {
+                        // one 3-D box {64 cols, 16 rows, ROW_BYTES/128 column blocks} per page:
+                        // smem [block][16 rows][128 B], 128-B swizzled
                         const int row = page * kP;
-#pragma unroll
-                        for (int cb = 0; cb < ROW_BYTES / 128; ++cb) {
-                            dev::tma_load_2d(dst + cb * 2048, tmap_k, 64 * cb, row, &full[my.stage], pol_stream);
-                            dev::tma_load_2d(dst + kPageBytes + cb * 2048, tmap_v, 64 * cb, row, &full[my.stage],
-                                             pol_stream);
-                        }
+                        dev::tma_load_3d(dst, tmap_k, 0, row, 0, &full[my.stage], pol_stream);
+                        dev::tma_load_3d(dst + kPageBytes, tmap_v, 0, row, 0, &full[my.stage], pol_stream);
                     }
                 }
                 __syncwarp(kMask);
@@ -590,6 +588,12 @@ __device__ void consumer_tc(const Params &p, const uint8_t *ring, const uint8_t 
         pos.advance(cw, p.stages);
         for (int pg = cw; pg < meta.npages; pg += NW) {
             dev::mbar_wait(&full[pos.stage], pos.phase);
+            if (p.flags & HETIS_ATTN_DIAG_STREAM_ONLY) {  // diagnostic: memory-system ceiling of this pipeline
+                __syncwarp();
+                if (lane == 0) dev::mbar_arrive(&empty[pos.stage]);
+                pos.advance(NW, p.stages);
+                continue;
+            }
             const uint32_t kb = dev::smem_u32(ring + (size_t)pos.stage * kStageBytes);
             const uint32_t vb = kb + kPageBytes;
             const int valid = min(kP, meta.ntok - pg * kP);
@@ -838,11 +842,13 @@ bool make_pool_map(CUtensorMap *m, const void *pool, int64_t num_pages, int D, s
         if (err) *err = "cuTensorMapEncodeTiled unavailable";
         return false;
     }
-    cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)(num_pages * kP)};
-    cuuint64_t strides[1] = {(cuuint64_t)D * 2};
-    cuuint32_t box[2] = {64, (cuuint32_t)kP};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(pool), dims, strides, box, es,
+    // view the pool [rows][D] as {64 cols, rows, D/64 column blocks}: dim 1 strides one
+    // row (D*2 bytes), dim 2 one 64-column block (128 bytes)
+    cuuint64_t dims[3] = {64, (cuuint64_t)(num_pages * kP), (cuuint64_t)(D / 64)};
+    cuuint64_t strides[2] = {(cuuint64_t)D * 2, 128};
+    cuuint32_t box[3] = {64, (cuuint32_t)kP, (cuuint32_t)(D / 64)};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(pool), dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
