@@ -59,7 +59,7 @@ constexpr int kQSlots = 2;
 #define HETIS_MAX_STAGES 24
 #endif
 #ifndef HETIS_PRODUCER_LANES
-#define HETIS_PRODUCER_LANES 4
+#define HETIS_PRODUCER_LANES 8
 #endif
 constexpr int kProducerLanes = HETIS_PRODUCER_LANES;
 static_assert(kPagesPerItem % kProducerLanes == 0, "producer lanes must divide the pages of an item");
