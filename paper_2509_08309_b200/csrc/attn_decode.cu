@@ -34,6 +34,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -773,8 +774,17 @@ struct Launch {
         }
         p.stages = stages;
         auto kern = attn_decode_kernel<DT, D, R, NW, TC>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        // opt in to the full 227 KB once per device (kept off the per-step host path)
+        static std::atomic<uint64_t> configured{0};
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
         if (e != cudaSuccess) return e;
+        const uint64_t bit = 1ull << (dev & 63);
+        if (!(configured.load(std::memory_order_acquire) & bit)) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+            if (e != cudaSuccess) return e;
+            configured.fetch_or(bit, std::memory_order_release);
+        }
         const int grid = num_sms();
         kern<<<grid, 32 * (NW + 1), smem, s>>>(p, tk, tv);
         note_launch();

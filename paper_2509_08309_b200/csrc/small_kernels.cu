@@ -106,9 +106,12 @@ void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 int num_sms() {
+    static std::atomic<int> cache[64];  // per device; 0 = not queried yet
     int dev = 0, n = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if ((n = cache[dev & 63].load(std::memory_order_relaxed)) > 0) return n;
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) return 148;
+    cache[dev & 63].store(n, std::memory_order_relaxed);
     return n;
 }
 
