@@ -774,16 +774,16 @@ struct Launch {
         }
         p.stages = stages;
         auto kern = attn_decode_kernel<DT, D, R, NW, TC>;
-        // opt in to the full 227 KB once per device (kept off the per-step host path)
-        static std::atomic<uint64_t> configured{0};
+        // raise the dynamic shared-memory opt-in only when a launch needs more than
+        // this device has been configured for (kept off the per-step host path)
+        static std::atomic<int> configured[64];
         int dev = 0;
         cudaError_t e = cudaGetDevice(&dev);
         if (e != cudaSuccess) return e;
-        const uint64_t bit = 1ull << (dev & 63);
-        if (!(configured.load(std::memory_order_acquire) & bit)) {
-            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+        if ((int)smem > configured[dev & 63].load(std::memory_order_acquire)) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
-            configured.fetch_or(bit, std::memory_order_release);
+            configured[dev & 63].store((int)smem, std::memory_order_release);
         }
         const int grid = num_sms();
         kern<<<grid, 32 * (NW + 1), smem, s>>>(p, tk, tv);

@@ -49,7 +49,7 @@ class DecodeStep:
         odt = torch.bfloat16 if o_dtype == "bf16" else torch.float32
         ws = hetis.attn_decode_workspace(self.cshape, num_seqs, self.q_count, max_seq_len)
         comm_ws = None
-        if self.world > 1:
+        if comm_ptr is not None:
             comm_ws = hetis.alloc_workspace(plan.comm_workspace(rank, num_seqs), device)
         self.buf = RankBuffers(
             q_shard=torch.empty((num_seqs, self.q_count, D), dtype=dt, device=device),
@@ -72,8 +72,6 @@ class DecodeStep:
         return n
 
     def scatter(self, q_full, k_new_full, v_new_full, stream=None):
-        if self.world == 1:
-            raise RuntimeError("scatter needs N > 1")
         hetis.scatter_q(self.plan, self.comm_ptr, self.rank, self.root, self.num_seqs, q_full, k_new_full,
                         v_new_full, self.buf.q_shard, self.buf.k_new, self.buf.v_new, self.buf.comm_ws, stream)
 
