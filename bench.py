@@ -301,8 +301,10 @@ def run_ours(args, world, rank, local):
     # are captured once into a CUDA graph (the same kernels, no host launch gaps) and
     # the graph is replayed once inside the timed region; per-step events are graph nodes.
     sampler = ClockSampler(local)
-    evs_a = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    evs_b = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    # external=True: inside a capture the records become event-record graph nodes
+    use_graph = bool(args.graph) and world == 1
+    evs_a = [torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(args.steps)]
+    evs_b = [torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     graph = None
     launch_mode = "eager"
