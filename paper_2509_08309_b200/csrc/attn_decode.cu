@@ -344,8 +344,6 @@ __device__ __forceinline__ void merge_warp(const Params &p, const float *mbuf, i
 // combiner warp (done ring of kDoneSlots).  The arrive has release semantics at
 // CTA scope; the combiner's gpu-scope fence before its counter atomic then
 // publishes these writes device-wide (cumulativity, as in a grid barrier).
-// The warp reconverges before returning: the next item ends in an aligned
-// bar.sync, which a lane still spinning here would otherwise miss.
 __device__ __forceinline__ void signal_item_done(const FusedBars &fb, int it, int lane) {
     __syncwarp();
     if (lane == 0) {
@@ -353,7 +351,6 @@ __device__ __forceinline__ void signal_item_done(const FusedBars &fb, int it, in
         dev::mbar_wait(&fb.done_empty[slot], ((it / kDoneSlots) & 1) ^ 1);
         dev::mbar_arrive(&fb.done_full[slot]);
     }
-    __syncwarp();
 }
 
 // ---------------------------------------------------------------- simt consumer
