@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--o-dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--attn-flags", type=int, default=0, help="HETIS_ATTN_* flags (diagnostics)")
     ap.add_argument("--graph", type=int, default=1, help="N = 1: replay the K timed steps as one CUDA graph")
-    ap.add_argument("--fused", type=int, default=0,
+    ap.add_argument("--fused", type=int, default=1,
                     help="1: hetis_decode_step (append + attention + combine in one launch); 0: three calls")
     return ap.parse_args()
 
