@@ -93,8 +93,7 @@ struct Params {
     int32_t *counters;     // [B][kv_heads] split-completion counters, zero between calls
 };
 
-constexpr int kDoneSlots = 32;    // items in flight between consumers and the combiner warp
-constexpr int kCombineGroup = 16; // items the combiner retires per round trip
+constexpr int kDoneSlots = 4;  // items in flight between consumers and the combiner warp
 
 struct FusedBars {
     uint64_t *done_full;   // [kDoneSlots] consumers -> combiner: item partials written
@@ -777,125 +776,82 @@ __device__ void append_prologue(const Params &p, const int32_t *s_len, const int
 }
 
 // ---------------------------------------------------------------- fused step: split combine
-// Merge all ns splits of (request j, kv head g) and write O: identical
-// arithmetic and order to combine_kernel (M = max_s lse_s; w_s = 2^(lse_s - M);
-// acc and wsum accumulated in ascending s; o = acc / wsum), so fused and
-// unfused results are bit-identical.  Lanes are split into R groups of 32 / R
-// lanes, one head each, so every load of a batch is independent: the merge
-// costs a few memory round trips instead of one per (head, split).
-template <int D, int R>
-__device__ void merge_pair(const Params &p, int j, int g, int s0, int ns, int lane) {
-    constexpr int LPH = 32 / R;             // lanes per head
-    constexpr int DPL = D / LPH;            // dims per lane
-    constexpr int VEC = DPL >= 4 ? 4 : 2;   // float4 / float2 loads
-    constexpr int NV = DPL / VEC;
-    constexpr int KB = (64 / DPL) < 1 ? 1 : ((64 / DPL) > LPH ? LPH : (64 / DPL));  // splits per load batch
-    const int rr = lane / LPH, lc = lane % LPH, hb = rr * LPH;
-    const size_t sstride = (size_t)p.kv_heads * R;  // rows between consecutive splits
-    const size_t row0 = ((size_t)s0 * p.kv_heads + g) * R + rr;
-    float M = -INFINITY;
-    for (int s = lc; s < ns; s += LPH) M = fmaxf(M, __ldcg(p.part_lse + row0 + s * sstride));
-#pragma unroll
-    for (int o = LPH / 2; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    float acc[DPL];
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
-    float wsum = 0.f;
-    for (int sb = 0; sb < ns; sb += LPH) {
-        const int nb = min(LPH, ns - sb);
-        const float w_own = lc < nb ? dev::ex2(__ldcg(p.part_lse + row0 + (sb + lc) * sstride) - M) : 0.f;
-        for (int k0 = 0; k0 < nb; k0 += KB) {
-            float v[KB][DPL];
-#pragma unroll
-            for (int k = 0; k < KB; ++k) {
-                if (k0 + k < nb) {
-                    const float *src = p.part_o + (row0 + (sb + k0 + k) * sstride) * D + lc * DPL;
-#pragma unroll
-                    for (int q = 0; q < NV; ++q) {
-                        if constexpr (VEC == 4) {
-                            const float4 t = __ldcg(reinterpret_cast<const float4 *>(src) + q);
-                            v[k][4 * q] = t.x; v[k][4 * q + 1] = t.y; v[k][4 * q + 2] = t.z; v[k][4 * q + 3] = t.w;
-                        } else {
-                            const float2 t = __ldcg(reinterpret_cast<const float2 *>(src) + q);
-                            v[k][2 * q] = t.x; v[k][2 * q + 1] = t.y;
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < KB; ++k) {
-                if (k0 + k < nb) {  // warp-uniform: every head has the same ns
-                    const float ws = __shfl_sync(0xffffffffu, w_own, hb + k0 + k);
-                    wsum += ws;
-#pragma unroll
-                    for (int e = 0; e < DPL; ++e) acc[e] = fmaf(ws, v[k][e], acc[e]);
-                }
-            }
-        }
-    }
-    const size_t obase = (size_t)j * p.o_seq_stride + (size_t)(g * R + rr) * D + lc * DPL;
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) acc[e] = __fdiv_rn(acc[e], wsum);
-    if (p.o_bf16) {
-        __nv_bfloat16 *o = static_cast<__nv_bfloat16 *>(p.o) + obase;
-#pragma unroll
-        for (int e = 0; e < DPL; e += 2) *reinterpret_cast<uint32_t *>(o + e) = dev::pack_bf16x2(acc[e], acc[e + 1]);
-    } else {
-        float *o = static_cast<float *>(p.o) + obase;
-#pragma unroll
-        for (int e = 0; e < DPL; e += VEC) {
-            if constexpr (VEC == 4)
-                *reinterpret_cast<float4 *>(o + e) = make_float4(acc[e], acc[e + 1], acc[e + 2], acc[e + 3]);
-            else
-                *reinterpret_cast<float2 *>(o + e) = make_float2(acc[e], acc[e + 1]);
-        }
-    }
-}
-
-// Warp NW + 1.  Items of this CTA are retired in groups of up to kCombineGroup:
-// after the consumer warps signal a group's partials written (done_full),
-// one lane per item bumps the (j, g) split counter (fence + atomic, all lanes
-// in parallel, so one round trip per group); the CTA that completes the last
-// split of (j, g) merges it (merge_pair) and resets the counter to 0.
+// Warp NW + 1.  For every item of this CTA, after the consumer warps have
+// written its partials (done_full), bump the (j, g) counter; the CTA that
+// completes the last split merges all splits of (j, g) in ascending split
+// order -- the same arithmetic as combine_kernel, so fused and unfused results
+// are bit-identical -- and writes O.  The counter is reset to 0 for the next call.
 template <int D, int R>
 __device__ void combiner(const Params &p, const int32_t *s_len, const int32_t *s_off, const FusedBars &fb,
                          int n_items) {
+    constexpr int DPL = D / 32;
+    static_assert(DPL == 2 || DPL == 4, "head_dim 64 or 128");
     const int lane = threadIdx.x & 31;
     int it = 0;
-    int item = blockIdx.x;
-    while (item < n_items) {
-        const int left = (n_items - 1 - item) / (int)gridDim.x + 1;
-        const int gn = min(kCombineGroup, left);
-        for (int k = 0; k < gn; ++k) dev::mbar_wait(&fb.done_full[(it + k) & (kDoneSlots - 1)], ((it + k) / kDoneSlots) & 1);
-        int j = 0, g = 0, s0 = 0, ns = 1;
-        bool last = false;
-        if (lane < gn) {
-            const int my = item + lane * (int)gridDim.x;
-            const int k = my / p.kv_heads;
-            g = my - k * p.kv_heads;
-            j = upper_bound_smem(s_off, p.num_seqs + 1, k) - 1;
-            s0 = s_off[j];
-            ns = s_off[j + 1] - s0;
-            last = true;
-            if (ns > 1) {
-                __threadfence();  // publish the partials this CTA's consumers wrote (cumulative)
-                const int old = atomicAdd(p.counters + (size_t)j * p.kv_heads + g, 1);
-                last = old == ns - 1;
-                if (last) p.counters[(size_t)j * p.kv_heads + g] = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+        const int slot = it & (kDoneSlots - 1);
+        dev::mbar_wait(&fb.done_full[slot], (it / kDoneSlots) & 1);
+        const int k = item / p.kv_heads;
+        const int g = item - k * p.kv_heads;
+        const int j = upper_bound_smem(s_off, p.num_seqs + 1, k) - 1;
+        const int s0 = s_off[j], ns = s_off[j + 1] - s0;
+        bool last = true;
+        if (ns > 1) {
+            int old = 0;
+            if (lane == 0) {
+                __threadfence();
+                old = atomicAdd(p.counters + (size_t)j * p.kv_heads + g, 1);
+            }
+            old = __shfl_sync(0xffffffffu, old, 0);
+            last = old == ns - 1;
+            if (last && lane == 0) p.counters[(size_t)j * p.kv_heads + g] = 0;
+            __threadfence();
+        }
+        if (last) {
+            for (int rr = 0; rr < R; ++rr) {
+                float M = -INFINITY;
+#pragma unroll 8
+                for (int s = 0; s < ns; ++s)
+                    M = fmaxf(M, __ldcg(p.part_lse + ((size_t)(s0 + s) * p.kv_heads + g) * R + rr));
+                float wsum = 0.f;
+                float acc[DPL];
+#pragma unroll
+                for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
+#pragma unroll 4
+                for (int s = 0; s < ns; ++s) {
+                    const size_t row = ((size_t)(s0 + s) * p.kv_heads + g) * R + rr;
+                    const float w = dev::ex2(__ldcg(p.part_lse + row) - M);
+                    const float *src = p.part_o + row * D + lane * DPL;
+                    wsum += w;
+                    if constexpr (DPL == 4) {
+                        const float4 v = __ldcg(reinterpret_cast<const float4 *>(src));
+                        acc[0] = fmaf(w, v.x, acc[0]);
+                        acc[1] = fmaf(w, v.y, acc[1]);
+                        acc[2] = fmaf(w, v.z, acc[2]);
+                        acc[3] = fmaf(w, v.w, acc[3]);
+                    } else {
+                        const float2 v = __ldcg(reinterpret_cast<const float2 *>(src));
+                        acc[0] = fmaf(w, v.x, acc[0]);
+                        acc[1] = fmaf(w, v.y, acc[1]);
+                    }
+                }
+                const size_t obase = (size_t)j * p.o_seq_stride + (size_t)(g * R + rr) * D + lane * DPL;
+#pragma unroll
+                for (int e = 0; e < DPL; ++e) acc[e] = __fdiv_rn(acc[e], wsum);
+                if (p.o_bf16) {
+                    __nv_bfloat16 *o = static_cast<__nv_bfloat16 *>(p.o) + obase;
+#pragma unroll
+                    for (int e = 0; e < DPL; e += 2)
+                        *reinterpret_cast<uint32_t *>(o + e) = dev::pack_bf16x2(acc[e], acc[e + 1]);
+                } else {
+                    float *o = static_cast<float *>(p.o) + obase;
+#pragma unroll
+                    for (int e = 0; e < DPL; ++e) o[e] = acc[e];
+                }
             }
         }
-        __threadfence();  // acquire side: the other CTAs' partials of a completed pair
-        unsigned todo = __ballot_sync(0xffffffffu, last);
-        while (todo) {
-            const int src = __ffs(todo) - 1;
-            todo &= todo - 1;
-            merge_pair<D, R>(p, __shfl_sync(0xffffffffu, j, src), __shfl_sync(0xffffffffu, g, src),
-                             __shfl_sync(0xffffffffu, s0, src), __shfl_sync(0xffffffffu, ns, src), lane);
-        }
         __syncwarp();
-        if (lane < gn) dev::mbar_arrive(&fb.done_empty[(it + lane) & (kDoneSlots - 1)]);
-        it += gn;
-        item += gn * (int)gridDim.x;
+        if (lane == 0) dev::mbar_arrive(&fb.done_empty[slot]);
     }
 }
 
