@@ -339,11 +339,10 @@ __device__ __forceinline__ void merge_warp(const Params &p, const float *mbuf, i
     }
 }
 
-// Fused step: this warp's partial rows of item `it` are written -> tell the
-// combiner warp (done ring of kDoneSlots).  The arrive has release semantics at
-// CTA scope; the combiner's gpu-scope fence before its counter atomic then
-// publishes these writes device-wide (cumulativity, as in a grid barrier).
+// Fused step: this warp's partial rows of item `it` are written -> make them
+// visible device-wide and tell the combiner warp (done ring of kDoneSlots).
 __device__ __forceinline__ void signal_item_done(const FusedBars &fb, int it, int lane) {
+    __threadfence();
     __syncwarp();
     if (lane == 0) {
         const int slot = it & (kDoneSlots - 1);
@@ -810,14 +809,12 @@ __device__ void combiner(const Params &p, const int32_t *s_len, const int32_t *s
         if (last) {
             for (int rr = 0; rr < R; ++rr) {
                 float M = -INFINITY;
-#pragma unroll 8
                 for (int s = 0; s < ns; ++s)
                     M = fmaxf(M, __ldcg(p.part_lse + ((size_t)(s0 + s) * p.kv_heads + g) * R + rr));
                 float wsum = 0.f;
                 float acc[DPL];
 #pragma unroll
                 for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
-#pragma unroll 4
                 for (int s = 0; s < ns; ++s) {
                     const size_t row = ((size_t)(s0 + s) * p.kv_heads + g) * R + rr;
                     const float w = dev::ex2(__ldcg(p.part_lse + row) - M);
@@ -883,7 +880,7 @@ __global__ void __launch_bounds__(32 * (NW + 2), 1)
     int32_t *s_off = s_len + p.num_seqs;
 
     FusedBars fb;
-    fb.done_full = reinterpret_cast<uint64_t *>(s_len + 2 * p.num_seqs + 2);  // 2B + 1 ints, padded to 8 B
+    fb.done_full = reinterpret_cast<uint64_t *>(s_off + p.num_seqs + 1 + ((p.num_seqs + 1) & 1));  // 8-B aligned
     fb.done_empty = fb.done_full + kDoneSlots;
     fb.appended = fb.done_empty + kDoneSlots;
 
