@@ -51,8 +51,6 @@ def parse():
     ap.add_argument("--o-dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--attn-flags", type=int, default=0, help="HETIS_ATTN_* flags (diagnostics)")
     ap.add_argument("--graph", type=int, default=1, help="N = 1: replay the K timed steps as one CUDA graph")
-    ap.add_argument("--fused", type=int, default=1,
-                    help="1: hetis_decode_step (append + attention + combine in one launch); 0: three calls")
     return ap.parse_args()
 
 
@@ -267,26 +265,16 @@ def run_ours(args, world, rank, local):
         li = i % n_layers
         if world > 1:
             step.scatter(q_full, kn_full, vn_full)
-        if args.fused:
-            # one launch: append + split-KV attention + combine (hetis_decode_step)
-            if ev_a is not None:
-                ev_a.record(torch.cuda.current_stream(device))
-            hetis.decode_step(step.cshape, step.buf.q_shard, step.buf.k_new, step.buf.v_new, k_pools[li],
-                              v_pools[li], batch.block_table, batch.seq_lens, max_len, step.buf.o_shard,
-                              step.buf.workspace, q_head_begin=q_begin, flags=args.attn_flags)
-            if ev_b is not None:
-                ev_b.record(torch.cuda.current_stream(device))
-        else:
-            step.append(k_pools[li], v_pools[li], batch.block_table, batch.seq_lens)
-            if ev_a is not None:
-                ev_a.record(torch.cuda.current_stream(device))
-            hetis.attn_partial(step.cshape, step.buf.q_shard, k_pools[li], v_pools[li], batch.block_table,
-                               batch.seq_lens, max_len, step.buf.workspace, q_head_begin=q_begin,
-                               flags=args.attn_flags)
-            if ev_b is not None:
-                ev_b.record(torch.cuda.current_stream(device))
-            hetis.attn_combine(step.cshape, batch.seq_lens, max_len, step.buf.o_shard, step.buf.workspace,
-                               q_head_count=q_count)
+        step.append(k_pools[li], v_pools[li], batch.block_table, batch.seq_lens)
+        if ev_a is not None:
+            ev_a.record(torch.cuda.current_stream(device))
+        hetis.attn_partial(step.cshape, step.buf.q_shard, k_pools[li], v_pools[li], batch.block_table,
+                           batch.seq_lens, max_len, step.buf.workspace, q_head_begin=q_begin,
+                           flags=args.attn_flags)
+        if ev_b is not None:
+            ev_b.record(torch.cuda.current_stream(device))
+        hetis.attn_combine(step.cshape, batch.seq_lens, max_len, step.buf.o_shard, step.buf.workspace,
+                           q_head_count=q_count)
         if world > 1:
             step.gather(o_full, root=-1)
 
@@ -406,15 +394,10 @@ def run_ours(args, world, rank, local):
     sb = accounting.step_bytes(seq_lens.tolist(), q_count, shape.r, shape.head_dim, shape.page_size,
                                shape.elem_bytes, shape.elem_bytes, 4)
     alg_bytes = sb.kv + sb.q + sb.table + sb.seq_lens
-    kernel_name = "hetis_attn_partial (split-KV partial attention)"
-    if args.fused:
-        # the fused kernel also reads the new K/V rows, writes them into the pool and writes O
-        alg_bytes += 2 * sb.new_kv + (sb.o if args.o_dtype == "f32" else sb.o // 2)
-        kernel_name = "hetis_decode_step (append + split-KV attention + combine, one launch)"
     achieved = alg_bytes / (attn_ms / 1e3) / 1e9
     peak, peak_src = peaks()
     clocks = sampler.summary()
-    traffic = traffic_from_profiles(f"{cfg.name}/N{world}/{'fused' if args.fused else 'partial'}")
+    traffic = traffic_from_profiles(f"{cfg.name}/N{world}")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -435,7 +418,7 @@ def run_ours(args, world, rank, local):
                       f"rotated per step (L2 = 126 MB)",
                 "tokens": "one token = one request's decode step of one layer, all heads"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name,
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "hetis_attn_partial (split-KV)",
                          "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": attn_ms,
                          "avg_launch_ms_max_rank": attn_ms_max, "peak_source": peak_src,
                          "frac_of_8TBps_nominal": achieved / 8000.0},

@@ -183,26 +183,6 @@ HETIS_API hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_s
                                const int32_t *seq_lens, int32_t max_seq_len, void *o, void *workspace,
                                size_t workspace_bytes, uint32_t flags, hetis_stream_t stream);
 
-/* The whole per-device step in ONE kernel launch: head-granular append of the
- * new token (as hetis_kv_append) + split-KV partial attention +
- * split combine (Eq. 2b).  The CTA streaming a request's last
- * split stores the new K/V row first; the CTA finishing a (request, kv head)'s
- * last split merges its splits (same arithmetic and order as
- * hetis_attn_combine, so results are bit-identical to the three-call path).
- *   q, k_pool, v_pool, block_table, seq_lens, max_seq_len: as hetis_attn_partial
- *   k_new, v_new: device [num_seqs][q_head_count / r][head_dim], kv_dtype, 16-B aligned
- *   o, o_seq_stride: as hetis_attn_combine
- *   workspace: >= hetis_attn_decode_workspace bytes; its split-completion
- *       counters must be ZERO before the first call (e.g. cudaMemset once after
- *       allocation); every completed call leaves them zero again.
- *   flags: HETIS_ATTN_FORCE_SIMT only. */
-HETIS_API hetis_status hetis_decode_step(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
-                                         int32_t q_head_count, const void *q, const void *k_new, const void *v_new,
-                                         void *k_pool, void *v_pool, int64_t num_pages, const int32_t *block_table,
-                                         int32_t max_pages, const int32_t *seq_lens, int32_t max_seq_len, void *o,
-                                         int64_t o_seq_stride, void *workspace, size_t workspace_bytes,
-                                         uint32_t flags, hetis_stream_t stream);
-
 /* ---- scatter / gather over NCCL ------------------- */
 /* nccl_comm is an ncclComm_t (e.g. torch ProcessGroupNCCL._comm_ptr()) whose
  * ranks are the plan's devices.  libnccl.so.2 is resolved at first use from

@@ -145,8 +145,7 @@ WorkspaceLayout workspace_layout(int num_seqs, int kv_heads, int r, int head_dim
     w.split_off_offset = 0;
     w.lse_offset = round256((size_t)(num_seqs + 1) * 4);
     w.o_offset = w.lse_offset + round256((size_t)w.max_items * r * 4);
-    w.counter_offset = w.o_offset + round256((size_t)w.max_items * r * head_dim * 4);
-    w.total = w.counter_offset + round256((size_t)num_seqs * kv_heads * 4);
+    w.total = w.o_offset + round256((size_t)w.max_items * r * head_dim * 4);
     return w;
 }
 }  // namespace hetis
@@ -405,40 +404,6 @@ hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_seqs, int32
     if (st != HETIS_OK) return st;
     return hetis_attn_combine(shape, num_seqs, q_head_count, seq_lens, max_seq_len, o,
                               (int64_t)q_head_count * shape->head_dim, workspace, workspace_bytes, stream);
-}
-
-hetis_status hetis_decode_step(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin, int32_t q_head_count,
-                               const void *q, const void *k_new, const void *v_new, void *k_pool, void *v_pool,
-                               int64_t num_pages, const int32_t *block_table, int32_t max_pages,
-                               const int32_t *seq_lens, int32_t max_seq_len, void *o, int64_t o_seq_stride,
-                               void *workspace, size_t workspace_bytes, uint32_t flags, hetis_stream_t stream) {
-    hetis::AttnArgs a{};
-    hetis_status st = attn_args(shape, num_seqs, q_head_begin, q_head_count, q, k_pool, v_pool, num_pages,
-                                block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes, &a);
-    if (st != HETIS_OK) return st;
-    if (num_seqs == 0) return HETIS_OK;
-    if (!k_new || !v_new || !o) return fail(HETIS_E_INVALID, "NULL pointer");
-    if (!aligned(k_new, 16) || !aligned(v_new, 16)) return fail(HETIS_E_INVALID, "k_new/v_new must be 16-byte aligned");
-    const int oe = esize(shape->o_dtype);
-    if (o_seq_stride < (int64_t)q_head_count * shape->head_dim) return fail(HETIS_E_INVALID, "o_seq_stride too small");
-    if (!aligned(o, 8) || (o_seq_stride * oe) % 8) return fail(HETIS_E_INVALID, "o rows must be 8-byte aligned");
-    if (flags & HETIS_ATTN_DIAG_STREAM_ONLY) return fail(HETIS_E_INVALID, "diagnostic flags are for hetis_attn_partial");
-    hetis::WorkspaceLayout w = hetis::workspace_layout(num_seqs, a.kv_heads, a.r, shape->head_dim, max_seq_len);
-    a.flags = flags;
-    a.fused = 1;
-    a.k_new = k_new;
-    a.v_new = v_new;
-    a.o = o;
-    a.o_seq_stride = o_seq_stride;
-    a.o_dtype = shape->o_dtype;
-    a.counters = reinterpret_cast<int32_t *>(static_cast<uint8_t *>(workspace) + w.counter_offset);
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const bool tc = a.dtype == HETIS_BF16 && a.r > 1 && !(flags & HETIS_ATTN_FORCE_SIMT);
-    std::string err;
-    cudaError_t e = tc ? hetis::launch_attn_tc(a, s, &err) : hetis::launch_attn_simt(a, s);
-    if (e != cudaSuccess)
-        return err.empty() ? cuda_fail(e, "decode_step launch") : fail(HETIS_E_CUDA, "decode_step: " + err);
-    return HETIS_OK;
 }
 
 // ---------------------------------------------------------------- scatter / gather

@@ -83,22 +83,6 @@ struct Params {
     int stages;    // ring depth
     float scale_log2;  // log2(e) / sqrt(d)
     uint32_t flags;    // HETIS_ATTN_*
-    // fused step (hetis_decode_step): append + partial + combine in one launch
-    int fused;
-    const uint8_t *k_new;  // [B][kv_heads][D]
-    const uint8_t *v_new;
-    void *o;               // [B] rows of o_seq_stride elements, local heads
-    int64_t o_seq_stride;
-    int o_bf16;
-    int32_t *counters;     // [B][kv_heads] split-completion counters, zero between calls
-};
-
-constexpr int kDoneSlots = 4;  // items in flight between consumers and the combiner warp
-
-struct FusedBars {
-    uint64_t *done_full;   // [kDoneSlots] consumers -> combiner: item partials written
-    uint64_t *done_empty;  // [kDoneSlots] combiner -> consumers: slot reusable
-    uint64_t *appended;    // consumers -> producer: new K/V rows stored (fused append)
 };
 
 struct ItemMeta {
@@ -194,7 +178,7 @@ struct RingPos {
 template <int ROW_BYTES, int R, int COPY>
 __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta *qmeta, uint64_t *full,
                          uint64_t *empty, uint64_t *qfull, uint64_t *qempty, const int32_t *s_len,
-                         const int32_t *s_off, const void *tmap_k, const void *tmap_v, const FusedBars &fb) {
+                         const int32_t *s_off, const void *tmap_k, const void *tmap_v) {
     constexpr int kPageBytes = kP * ROW_BYTES;
     constexpr int kStageBytes = 2 * kPageBytes;
     constexpr int kQBytes = R * ROW_BYTES;
@@ -247,7 +231,6 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
     int32_t pid[PPL];
     load_pids(cur, pid);
     RingPos pos{0, 0u};
-    bool wait_append = p.fused != 0;
     for (int it = 0; item < n_items; item += gridDim.x, ++it) {
         const int next = item + gridDim.x;
         int32_t pid_next[PPL];
@@ -259,11 +242,6 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
         }
         __syncwarp(kMask);
         const int np = (cur.ntok + kP - 1) / kP;
-        if (wait_append && cur.t0 + cur.ntok == s_len[cur.j]) {
-            // this item's last page holds the new token: its row must be stored first
-            dev::mbar_wait(fb.appended, 0);
-            wait_append = false;
-        }
         // G lanes issue G consecutive pages at once: their ring waits and
         // expect_tx arrivals overlap instead of serialising on one thread
 #pragma unroll
@@ -339,18 +317,6 @@ __device__ __forceinline__ void merge_warp(const Params &p, const float *mbuf, i
     }
 }
 
-// Fused step: this warp's partial rows of item `it` are written -> make them
-// visible device-wide and tell the combiner warp (done ring of kDoneSlots).
-__device__ __forceinline__ void signal_item_done(const FusedBars &fb, int it, int lane) {
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) {
-        const int slot = it & (kDoneSlots - 1);
-        dev::mbar_wait(&fb.done_empty[slot], ((it / kDoneSlots) & 1) ^ 1);
-        dev::mbar_arrive(&fb.done_full[slot]);
-    }
-}
-
 // ---------------------------------------------------------------- simt consumer
 // Lane layout for one page (16 token rows of ROW_BYTES): LPT lanes share a
 // token row, each owning one 16-byte chunk (EPL elements); a warp covers TPS
@@ -396,7 +362,7 @@ __device__ __forceinline__ void ffma2(float &a0, float &a1, float b0, float b1, 
 template <int DT, int D, int R, int NW>
 __device__ void consumer_simt(const Params &p, const uint8_t *ring, const uint8_t *qbuf, const ItemMeta *qmeta,
                               uint64_t *full, uint64_t *empty, uint64_t *qfull, uint64_t *qempty, float *mbuf,
-                              int n_items, const FusedBars &fb) {
+                              int n_items) {
     constexpr int EB = DT == HETIS_BF16 ? 2 : 4;
     constexpr int ROW_BYTES = D * EB;
     constexpr int kPageBytes = kP * ROW_BYTES;
@@ -548,7 +514,6 @@ __device__ void consumer_simt(const Params &p, const uint8_t *ring, const uint8_
         }
         dev::named_bar_sync(1, NW * 32);
         merge_warp<D, R, NW>(p, mb, meta.item, it, cw, lane);
-        if (p.fused) signal_item_done(fb, it, lane);
     }
 }
 
@@ -556,7 +521,7 @@ __device__ void consumer_simt(const Params &p, const uint8_t *ring, const uint8_
 template <int D, int R, int NW>
 __device__ void consumer_tc(const Params &p, const uint8_t *ring, const uint8_t *qbuf, const ItemMeta *qmeta,
                             uint64_t *full, uint64_t *empty, uint64_t *qfull, uint64_t *qempty, float *mbuf,
-                            int n_items, const FusedBars &fb) {
+                            int n_items) {
     constexpr int ROW_BYTES = D * 2;
     constexpr int kPageBytes = kP * ROW_BYTES;
     constexpr int kHalfBytes = kPageBytes / (D / 64);  // one 64-element column block: 16 rows x 128 B
@@ -724,138 +689,12 @@ __device__ void consumer_tc(const Params &p, const uint8_t *ring, const uint8_t 
         }
         dev::named_bar_sync(1, NW * 32);
         merge_warp<D, R, NW>(p, mb, meta.item, it, cw, lane);
-        if (p.fused) signal_item_done(fb, it, lane);
-    }
-}
-
-// ---------------------------------------------------------------- fused step: kv append prologue
-// The CTA that will stream the LAST split of (request j, kv head g) -- the split
-// holding position L_j - 1 -- first stores the new token's K and V rows into
-// their page slot (head-granular store).  Lanes of the consumer
-// warps test the (j, g) pairs in parallel; a warp copies each matching row
-// with 16-byte stores, then fences the generic-proxy writes against the
-// async proxy (the TMA loads that read the page) and arrives on `appended`.
-template <int ROW_BYTES, int NW>
-__device__ void append_prologue(const Params &p, const int32_t *s_len, const int32_t *s_off, const FusedBars &fb) {
-    constexpr int CH = ROW_BYTES / 16;  // 16-byte chunks per row
-    const int lane = threadIdx.x & 31;
-    const int cw = (threadIdx.x >> 5) - 1;
-    const int pairs = p.num_seqs * p.kv_heads;
-    for (int base = cw * 32; base < pairs; base += NW * 32) {
-        const int pr = base + lane;
-        bool mine = false;
-        int j = 0, g = 0;
-        if (pr < pairs) {
-            j = pr / p.kv_heads;
-            g = pr - j * p.kv_heads;
-            const int last_item = (s_off[j + 1] - 1) * p.kv_heads + g;
-            mine = (last_item % (int)gridDim.x) == (int)blockIdx.x;
-        }
-        unsigned todo = __ballot_sync(0xffffffffu, mine);
-        while (todo) {
-            const int src = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const int jj = __shfl_sync(0xffffffffu, j, src);
-            const int gg = __shfl_sync(0xffffffffu, g, src);
-            const int pos = s_len[jj] - 1;
-            const int32_t page = __ldg(p.block_table + ((size_t)jj * p.kv_heads + gg) * p.max_pages + pos / kP);
-            const size_t dst = ((size_t)page * kP + (size_t)(pos % kP)) * ROW_BYTES;
-            const size_t srow = ((size_t)jj * p.kv_heads + gg) * ROW_BYTES;
-            for (int c = lane; c < 2 * CH; c += 32) {
-                const bool is_v = c >= CH;
-                const int cc = is_v ? c - CH : c;
-                const uint4 v = __ldg(reinterpret_cast<const uint4 *>((is_v ? p.v_new : p.k_new) + srow) + cc);
-                *reinterpret_cast<uint4 *>(const_cast<uint8_t *>(is_v ? p.v_pool : p.k_pool) + dst + 16 * cc) = v;
-            }
-        }
-    }
-    dev::fence_proxy_async_global();
-    __syncwarp();
-    if (lane == 0) dev::mbar_arrive(fb.appended);
-}
-
-// ---------------------------------------------------------------- fused step: split combine
-// Warp NW + 1.  For every item of this CTA, after the consumer warps have
-// written its partials (done_full), bump the (j, g) counter; the CTA that
-// completes the last split merges all splits of (j, g) in ascending split
-// order -- the same arithmetic as combine_kernel, so fused and unfused results
-// are bit-identical -- and writes O.  The counter is reset to 0 for the next call.
-template <int D, int R>
-__device__ void combiner(const Params &p, const int32_t *s_len, const int32_t *s_off, const FusedBars &fb,
-                         int n_items) {
-    constexpr int DPL = D / 32;
-    static_assert(DPL == 2 || DPL == 4, "head_dim 64 or 128");
-    const int lane = threadIdx.x & 31;
-    int it = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-        const int slot = it & (kDoneSlots - 1);
-        dev::mbar_wait(&fb.done_full[slot], (it / kDoneSlots) & 1);
-        const int k = item / p.kv_heads;
-        const int g = item - k * p.kv_heads;
-        const int j = upper_bound_smem(s_off, p.num_seqs + 1, k) - 1;
-        const int s0 = s_off[j], ns = s_off[j + 1] - s0;
-        bool last = true;
-        if (ns > 1) {
-            int old = 0;
-            if (lane == 0) {
-                __threadfence();
-                old = atomicAdd(p.counters + (size_t)j * p.kv_heads + g, 1);
-            }
-            old = __shfl_sync(0xffffffffu, old, 0);
-            last = old == ns - 1;
-            if (last && lane == 0) p.counters[(size_t)j * p.kv_heads + g] = 0;
-            __threadfence();
-        }
-        if (last) {
-            for (int rr = 0; rr < R; ++rr) {
-                float M = -INFINITY;
-                for (int s = 0; s < ns; ++s)
-                    M = fmaxf(M, __ldcg(p.part_lse + ((size_t)(s0 + s) * p.kv_heads + g) * R + rr));
-                float wsum = 0.f;
-                float acc[DPL];
-#pragma unroll
-                for (int e = 0; e < DPL; ++e) acc[e] = 0.f;
-                for (int s = 0; s < ns; ++s) {
-                    const size_t row = ((size_t)(s0 + s) * p.kv_heads + g) * R + rr;
-                    const float w = dev::ex2(__ldcg(p.part_lse + row) - M);
-                    const float *src = p.part_o + row * D + lane * DPL;
-                    wsum += w;
-                    if constexpr (DPL == 4) {
-                        const float4 v = __ldcg(reinterpret_cast<const float4 *>(src));
-                        acc[0] = fmaf(w, v.x, acc[0]);
-                        acc[1] = fmaf(w, v.y, acc[1]);
-                        acc[2] = fmaf(w, v.z, acc[2]);
-                        acc[3] = fmaf(w, v.w, acc[3]);
-                    } else {
-                        const float2 v = __ldcg(reinterpret_cast<const float2 *>(src));
-                        acc[0] = fmaf(w, v.x, acc[0]);
-                        acc[1] = fmaf(w, v.y, acc[1]);
-                    }
-                }
-                const size_t obase = (size_t)j * p.o_seq_stride + (size_t)(g * R + rr) * D + lane * DPL;
-#pragma unroll
-                for (int e = 0; e < DPL; ++e) acc[e] = __fdiv_rn(acc[e], wsum);
-                if (p.o_bf16) {
-                    __nv_bfloat16 *o = static_cast<__nv_bfloat16 *>(p.o) + obase;
-#pragma unroll
-                    for (int e = 0; e < DPL; e += 2)
-                        *reinterpret_cast<uint32_t *>(o + e) = dev::pack_bf16x2(acc[e], acc[e + 1]);
-                } else {
-                    float *o = static_cast<float *>(p.o) + obase;
-#pragma unroll
-                    for (int e = 0; e < DPL; ++e) o[e] = acc[e];
-                }
-            }
-        }
-        __syncwarp();
-        if (lane == 0) dev::mbar_arrive(&fb.done_empty[slot]);
     }
 }
 
 // ---------------------------------------------------------------- kernels
-// Block = producer warp + NW consumer warps + combiner warp (active when fused).
 template <int DT, int D, int R, int NW, bool TC>
-__global__ void __launch_bounds__(32 * (NW + 2), 1)
+__global__ void __launch_bounds__(32 * (NW + 1), 1)
     attn_decode_kernel(const Params p, const __grid_constant__ CUtensorMap tmap_k,
                        const __grid_constant__ CUtensorMap tmap_v) {
     constexpr int EB = DT == HETIS_BF16 ? 2 : 4;
@@ -879,11 +718,6 @@ __global__ void __launch_bounds__(32 * (NW + 2), 1)
     int32_t *s_len = reinterpret_cast<int32_t *>(qmeta + kQSlots);
     int32_t *s_off = s_len + p.num_seqs;
 
-    FusedBars fb;
-    fb.done_full = reinterpret_cast<uint64_t *>(s_off + p.num_seqs + 1 + ((p.num_seqs + 1) & 1));  // 8-B aligned
-    fb.done_empty = fb.done_full + kDoneSlots;
-    fb.appended = fb.done_empty + kDoneSlots;
-
     if (threadIdx.x == 0) {
         for (int i = 0; i < p.stages; ++i) {
             dev::mbar_init(&full[i], 1);
@@ -893,29 +727,20 @@ __global__ void __launch_bounds__(32 * (NW + 2), 1)
             dev::mbar_init(&qfull[i], 1);
             dev::mbar_init(&qempty[i], NW);
         }
-        for (int i = 0; i < kDoneSlots; ++i) {
-            dev::mbar_init(&fb.done_full[i], NW);
-            dev::mbar_init(&fb.done_empty[i], 1);
-        }
-        dev::mbar_init(fb.appended, NW);
         dev::fence_barrier_init();
     }
     build_split_offsets(p, s_len, s_off);  // contains __syncthreads
     const int n_items = s_off[p.num_seqs] * p.kv_heads;
 
-    if (threadIdx.x < 32) {
-        if (threadIdx.x < kProducerLanes)
-            producer<ROW_BYTES, R, TC ? 1 : 0>(p, ring, qbuf, qmeta, full, empty, qfull, qempty, s_len, s_off,
-                                               &tmap_k, &tmap_v, fb);
-    } else if (threadIdx.x < 32 * (NW + 1)) {
-        if (p.fused) append_prologue<ROW_BYTES, NW>(p, s_len, s_off, fb);
+    if (threadIdx.x < kProducerLanes) {
+        producer<ROW_BYTES, R, TC ? 1 : 0>(p, ring, qbuf, qmeta, full, empty, qfull, qempty, s_len, s_off, &tmap_k,
+                                           &tmap_v);
+    } else if (threadIdx.x >= 32) {
         if constexpr (TC) {
-            consumer_tc<D, R, NW>(p, ring, qbuf, qmeta, full, empty, qfull, qempty, mbuf, n_items, fb);
+            consumer_tc<D, R, NW>(p, ring, qbuf, qmeta, full, empty, qfull, qempty, mbuf, n_items);
         } else {
-            consumer_simt<DT, D, R, NW>(p, ring, qbuf, qmeta, full, empty, qfull, qempty, mbuf, n_items, fb);
+            consumer_simt<DT, D, R, NW>(p, ring, qbuf, qmeta, full, empty, qfull, qempty, mbuf, n_items);
         }
-    } else if (p.fused) {
-        combiner<D, R>(p, s_len, s_off, fb, n_items);
     }
 }
 
@@ -932,7 +757,7 @@ struct Launch {
         size_t mb = 2 * (size_t)NW * R * (D + 4) * sizeof(float);
         mb = (mb + 15) / 16 * 16;
         return (size_t)kQSlots * kQStride + mb + (size_t)(2 * stages + 2 * kQSlots) * 8 +
-               (size_t)kQSlots * sizeof(ItemMeta) + (size_t)(2 * num_seqs + 2) * 4 + (2 * kDoneSlots + 1) * 8;
+               (size_t)kQSlots * sizeof(ItemMeta) + (size_t)(2 * num_seqs + 1) * 4;
     }
 
     static cudaError_t run(const Params &p0, int num_seqs, cudaStream_t s, const CUtensorMap &tk,
@@ -961,7 +786,7 @@ struct Launch {
             configured[dev & 63].store((int)smem, std::memory_order_release);
         }
         const int grid = num_sms();
-        kern<<<grid, 32 * (NW + 2), smem, s>>>(p, tk, tv);
+        kern<<<grid, 32 * (NW + 1), smem, s>>>(p, tk, tv);
         note_launch();
         return cudaGetLastError();
     }
@@ -983,13 +808,6 @@ Params make_params(const AttnArgs &a) {
     p.max_pages = a.max_pages;
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)a.head_dim));
     p.flags = a.flags;
-    p.fused = a.fused;
-    p.k_new = static_cast<const uint8_t *>(a.k_new);
-    p.v_new = static_cast<const uint8_t *>(a.v_new);
-    p.o = a.o;
-    p.o_seq_stride = a.o_seq_stride;
-    p.o_bf16 = a.o_dtype == HETIS_BF16;
-    p.counters = a.counters;
     return p;
 }
 

@@ -37,18 +37,10 @@ struct AttnArgs {
     float *part_o;        // [max_items][r][head_dim]
     int64_t max_items;
     uint32_t flags;       // HETIS_ATTN_*
-    // fused step only (hetis_decode_step)
-    int fused;
-    const void *k_new;    // [num_seqs][kv_heads][head_dim]
-    const void *v_new;
-    void *o;              // rows of o_seq_stride elements
-    int64_t o_seq_stride;
-    int o_dtype;
-    int32_t *counters;    // [num_seqs][kv_heads], zero between calls
 };
 
 struct WorkspaceLayout {
-    size_t split_off_offset, lse_offset, o_offset, counter_offset, total;
+    size_t split_off_offset, lse_offset, o_offset, total;
     int64_t max_items;
 };
 

@@ -28,8 +28,8 @@ ATTN_FORCE_SIMT = 0x1
 EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_split_tokens",
             "hetis_plan_create", "hetis_plan_destroy", "hetis_plan_heads", "hetis_plan_num_devices",
             "hetis_plan_check_capacity", "hetis_kv_append", "hetis_attn_decode_workspace", "hetis_attn_partial",
-            "hetis_attn_combine", "hetis_attn_decode", "hetis_decode_step", "hetis_comm_workspace", "hetis_scatter_q",
-            "hetis_gather", "hetis_launch_count")
+            "hetis_attn_combine", "hetis_attn_decode", "hetis_comm_workspace", "hetis_scatter_q", "hetis_gather",
+            "hetis_launch_count")
 
 
 class HetisError(RuntimeError):
@@ -79,8 +79,6 @@ def lib() -> ctypes.CDLL:
                 "hetis_attn_combine": (ctypes.c_int, [sp, i32, i32, vp, i32, vp, i64, vp, sz, vp]),
                 "hetis_attn_decode": (ctypes.c_int, [sp, i32, i32, i32, vp, vp, vp, i64, vp, i32, vp, i32, vp, vp,
                                                      sz, u32, vp]),
-                "hetis_decode_step": (ctypes.c_int, [sp, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32, vp, i32,
-                                                     vp, i64, vp, sz, u32, vp]),
                 "hetis_comm_workspace": (ctypes.c_int, [vp, i32, i32, P(sz)]),
                 "hetis_scatter_q": (ctypes.c_int, [vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
                 "hetis_gather": (ctypes.c_int, [vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]),
@@ -204,10 +202,8 @@ def attn_decode_workspace(shape: CShape, num_seqs: int, q_head_count: int, max_s
 
 
 def alloc_workspace(nbytes: int, device) -> torch.Tensor:
-    """A zero-filled, 256-byte aligned uint8 device buffer (torch's caching allocator
-    aligns to 512).  Zero-filled because hetis_decode_step's split counters must
-    start at zero; the library leaves them zero after every call."""
-    return torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
+    """A 256-byte aligned uint8 device buffer (torch's caching allocator aligns to 512)."""
+    return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
 
 
 def attn_partial(shape: CShape, q, k_pool, v_pool, block_table, seq_lens, max_seq_len: int, workspace,
@@ -243,24 +239,6 @@ def attn_decode(shape: CShape, q, k_pool, v_pool, block_table, seq_lens, max_seq
                                    block_table.shape[2], _dev(seq_lens, "seq_lens"), max_seq_len, _dev(o, "o"),
                                    _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(), flags,
                                    _stream(stream)), "hetis_attn_decode")
-
-
-def decode_step(shape: CShape, q, k_new, v_new, k_pool, v_pool, block_table, seq_lens, max_seq_len: int, o,
-                workspace, q_head_begin: int = 0, o_seq_stride: int | None = None, flags: int = 0,
-                stream=None) -> None:
-    """kv append + split-KV attention + combine in one kernel launch (hetis_decode_step)."""
-    B, x, _ = q.shape
-    if o_seq_stride is None:
-        o_seq_stride = o.stride(0)
-    if not o.is_cuda:
-        raise ValueError("o must be a CUDA tensor")
-    _check(lib().hetis_decode_step(ctypes.byref(shape), B, q_head_begin, x, _dev(q, "q"), _dev(k_new, "k_new"),
-                                   _dev(v_new, "v_new"), _dev(k_pool, "k_pool"), _dev(v_pool, "v_pool"),
-                                   k_pool.shape[0], _dev(block_table, "block_table"), block_table.shape[2],
-                                   _dev(seq_lens, "seq_lens"), max_seq_len, ctypes.c_void_p(o.data_ptr()),
-                                   o_seq_stride, _dev(workspace, "workspace"),
-                                   workspace.numel() * workspace.element_size(), flags, _stream(stream)),
-           "hetis_decode_step")
 
 
 # ---------------------------------------------------------------- NCCL scatter / gather

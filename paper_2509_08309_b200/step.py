@@ -63,7 +63,7 @@ class DecodeStep:
 
     # kernels launched per step by this rank (for gpu_launches accounting)
     def launches_per_step(self) -> int:
-        n = 1  # hetis_decode_step (append + attention + combine); 3 with the separate calls
+        n = 3  # kv_append, attention partial, combine
         if self.world > 1:
             x = [self.plan.heads(i)[1] for i in range(self.world)]
             if self.rank == self.root:

@@ -104,7 +104,7 @@ def main():
             if "dram__bytes_read.sum" in raw:
                 rb = to_bytes(*raw["dram__bytes_read.sum"])
                 wb = to_bytes(*raw["dram__bytes_write.sum"])
-                traffic[f"{c}/N1/{os.environ.get('HETIS_KERNEL_TAG', 'fused')}"] = rb + wb
+                traffic[f"{c}/N1"] = rb + wb
                 lines.append(f"DRAM traffic per launch: {rb / 1e9:.4f} GB read + {wb / 1e6:.2f} MB written\n")
         with open(os.path.join(PROF, f"{tag}_{c}.md"), "w") as f:
             f.write("\n".join(lines) + "\n")

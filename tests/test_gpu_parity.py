@@ -286,63 +286,3 @@ def test_full_size_config_sampled(name, rank):
     assert torch.isfinite(o).all()
     got = np.stack([o[j, h].cpu().numpy() for j, h in pairs])
     assert_close(got, ref, name)
-
-
-# ------------------------------------------------------------------ fused step (one launch)
-def run_fused(b: workload.DecodeBatch, o_dtype="f32", flags=0, ws=None, o_stride_heads=None):
-    s = hetis.make_shape(b.shape, o_dtype)
-    B, x, D = b.q.shape
-    L = b.max_seq_len
-    if ws is None:
-        ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), b.q.device)
-    odt = torch.bfloat16 if o_dtype == "bf16" else torch.float32
-    heads = x if o_stride_heads is None else o_stride_heads
-    big = torch.full((B, heads, D), float("nan"), dtype=odt, device=b.q.device)
-    view = big if o_stride_heads is None else big[:, b.q_begin:b.q_begin + x]
-    hetis.decode_step(s, b.q, b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, view, ws,
-                      q_head_begin=b.q_begin, o_seq_stride=big.stride(0), flags=flags)
-    torch.cuda.synchronize()
-    return big, ws
-
-
-@pytest.mark.parametrize("H,Hkv,D,dtype,lens", [
-    (40, 40, 128, "bf16", (1, 17, 300, 4096, 256, 257)),
-    (64, 8, 128, "bf16", (2048, 5, 1, 777, 512)),
-    (8, 8, 64, "f32", (128, 128, 128, 128)),
-    (16, 4, 64, "bf16", EDGE_LENS),
-    (8, 2, 128, "f32", (33, 1000, 1)),
-])
-def test_fused_step_bit_identical_to_three_calls(H, Hkv, D, dtype, lens):
-    b1 = gpu_batch(H, Hkv, D, dtype, lens, seed=H + D)
-    b2 = gpu_batch(H, Hkv, D, dtype, lens, seed=H + D)
-    o_ref = run_gpu(b1)                                   # kv_append + partial + combine
-    o_fused, ws = run_fused(b2)                           # one launch
-    assert torch.equal(o_fused, o_ref)
-    assert torch.equal(b1.k_pool.view(torch.uint8), b2.k_pool.view(torch.uint8))   # same append
-    assert torch.equal(b1.v_pool.view(torch.uint8), b2.v_pool.view(torch.uint8))
-    assert_close(o_fused, oracle_full(b1), "fused")
-    # repeated calls reuse the workspace: the split counters must have been left at zero
-    for _ in range(3):
-        o_again, _ = run_fused(b2, ws=ws)
-        assert torch.equal(o_again, o_ref)
-
-
-def test_fused_step_strided_bf16_output_and_force_simt():
-    b = gpu_batch(64, 8, 128, "bf16", (900, 31, 2048), seed=71, q_begin=16, q_count=16)
-    o_ref = run_gpu(b, o_dtype="bf16", o_stride_heads=64)
-    o_f, _ = run_fused(b, o_dtype="bf16", o_stride_heads=64)
-    assert torch.equal(o_f[:, 16:32], o_ref[:, 16:32])
-    assert torch.isnan(o_f[:, :16].float()).all() and torch.isnan(o_f[:, 32:].float()).all()
-    o_s, _ = run_fused(b, flags=hetis.ATTN_FORCE_SIMT)
-    assert_close(o_s, oracle_full(b), "fused simt gqa")
-
-
-@pytest.mark.parametrize("name", ["c2", "c3"])
-def test_fused_step_full_size_equals_three_calls(name):
-    cfg = workload.CONFIGS[name]
-    b1 = workload.make_decode_batch(cfg.shape, cfg.seq_lens(), cfg.seed, "cuda")
-    o_ref = run_gpu(b1)
-    del b1
-    b2 = workload.make_decode_batch(cfg.shape, cfg.seq_lens(), cfg.seed, "cuda")
-    o_f, _ = run_fused(b2)
-    assert torch.equal(o_f, o_ref)
