@@ -1,0 +1,92 @@
+#!/usr/bin/env python
+"""Per-rank compute of the head-parallel step at N = 1, 2, 4, 8, measured on ONE GPU.
+
+For each N, rank 0's share of the workload (its x = H/N query heads, its own
+kv pages) runs kv_append + attention partial + combine, replayed as a CUDA
+graph; the per-step device time is what that rank would spend on compute at N
+GPUs.  NVLink scatter/gather is NOT included (only one GPU is reachable), so
+`compute_scaling` = t(1) / t(N) is an upper bound for the full-step scaling.
+
+    python scripts/scaling_probe.py [--config c3] [--steps 200]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2509_08309_b200 import accounting, hetis, workload  # noqa: E402
+
+
+def share_time(cfg, n: int, steps: int, warmup: int, device):
+    split = cfg.head_split(n)
+    shape = cfg.shape
+    x = split[0]
+    lens = cfg.seq_lens()
+    b = workload.make_decode_batch(shape, lens, cfg.seed, device, q_begin=0, q_count=x)
+    s = hetis.make_shape(shape)
+    B, L = len(lens), int(lens.max())
+    kv_bytes = accounting.step_bytes(lens.tolist(), x, shape.r, shape.head_dim, shape.page_size, shape.elem_bytes,
+                                     shape.elem_bytes, 4).kv
+    n_layers = max(1, math.ceil(4 * 126 * 2 ** 20 / kv_bytes))
+    kp = [b.k_pool] + [b.k_pool.clone() for _ in range(n_layers - 1)]
+    vp = [b.v_pool] + [b.v_pool.clone() for _ in range(n_layers - 1)]
+    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), device)
+    o = torch.empty((B, x, shape.head_dim), device=device)
+
+    def step(i, ea=None, eb=None):
+        li = i % n_layers
+        hetis.kv_append(s, b.k_new, b.v_new, kp[li], vp[li], b.block_table, b.seq_lens)
+        if ea is not None:
+            ea.record()
+        hetis.attn_partial(s, b.q, kp[li], vp[li], b.block_table, b.seq_lens, L, ws)
+        if eb is not None:
+            eb.record()
+        hetis.attn_combine(s, b.seq_lens, L, o, ws)
+
+    for i in range(warmup):
+        step(i)
+    ea = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(steps)]
+    eb = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(steps)]
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(steps):
+            step(i, ea[i], eb[i])
+    g.replay()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    g.replay()
+    t1.record()
+    torch.cuda.synchronize()
+    step_ms = t0.elapsed_time(t1) / steps
+    attn_ms = sum(a.elapsed_time(c) for a, c in zip(ea, eb)) / steps
+    return {"n": n, "heads_per_rank": x, "kv_bytes_per_rank": kv_bytes, "layers_rotated": n_layers,
+            "step_us": step_ms * 1e3, "attn_us": attn_ms * 1e3, "attn_gbs": kv_bytes / (attn_ms / 1e3) / 1e9}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--ns", default="1,2,4,8")
+    a = ap.parse_args()
+    cfg = workload.CONFIGS[a.config]
+    dev = torch.device("cuda", 0)
+    rows = [share_time(cfg, int(n), a.steps, a.warmup, dev) for n in a.ns.split(",")]
+    t1 = rows[0]["step_us"]
+    for r in rows:
+        r["compute_scaling_vs_n1"] = t1 / r["step_us"]
+        r["config"] = cfg.name
+        print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    main()
