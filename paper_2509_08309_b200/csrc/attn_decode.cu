@@ -729,6 +729,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         }
         dev::fence_barrier_init();
     }
+    dev::pdl_wait_then_release();          // first global access below (PDL, see launch_pdl)
     build_split_offsets(p, s_len, s_off);  // contains __syncthreads
     const int n_items = s_off[p.num_seqs] * p.kv_heads;
 
@@ -786,9 +787,7 @@ struct Launch {
             configured[dev & 63].store((int)smem, std::memory_order_release);
         }
         const int grid = num_sms();
-        kern<<<grid, 32 * (NW + 1), smem, s>>>(p, tk, tv);
-        note_launch();
-        return cudaGetLastError();
+        return launch_pdl(kern, dim3(grid), dim3(32 * (NW + 1)), smem, s, p, tk, tv);
     }
 };
 

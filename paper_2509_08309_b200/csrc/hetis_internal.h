@@ -65,4 +65,26 @@ cudaError_t launch_head_place(const void *src, void *dst, int num_seqs, int dst_
 void note_launch();
 int num_sms();
 
+// Launch with programmatic dependent launch (PDL): the kernel may be scheduled
+// while the previous kernel in the stream is still running; every kernel of
+// this library executes griddepcontrol.wait before its first global-memory
+// access (so stream order is preserved) and then griddepcontrol.launch_dependents,
+// which hides launch latency and CTA scheduling between the step's kernels.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    note_launch();
+    return e;
+}
+
 }  // namespace hetis

@@ -22,6 +22,7 @@ std::atomic<uint64_t> g_launches{0};
 __global__ void kv_append_kernel(int num_seqs, int kv_heads, int row_bytes, int page_size, const uint8_t *k_new,
                                  const uint8_t *v_new, uint8_t *k_pool, uint8_t *v_pool, const int32_t *block_table,
                                  int max_pages, const int32_t *seq_lens) {
+    dev::pdl_wait_then_release();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= num_seqs * kv_heads) return;
@@ -42,6 +43,7 @@ __global__ void kv_append_kernel(int num_seqs, int kv_heads, int row_bytes, int 
 template <int D, int OUT_BF16>
 __global__ void combine_kernel(int num_seqs, int q_heads, int r, const int32_t *seq_lens, const int32_t *split_off,
                                const float *part_lse, const float *part_o, void *o, int64_t o_seq_stride) {
+    dev::pdl_wait_then_release();
     constexpr int TPH = D / 4;  // threads per head
     const int heads_per_block = blockDim.x / TPH;
     const int hl = threadIdx.x / TPH, d4 = threadIdx.x % TPH;
@@ -53,9 +55,11 @@ __global__ void combine_kernel(int num_seqs, int q_heads, int r, const int32_t *
     const int s0 = split_off[j];
     const int ns = split_off[j + 1] - s0;
     float M = -INFINITY;
+#pragma unroll 8
     for (int s = 0; s < ns; ++s) M = fmaxf(M, part_lse[((size_t)(s0 + s) * kv_heads + g) * r + rr]);
     float wsum = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
     for (int s = 0; s < ns; ++s) {
         const size_t row = ((size_t)(s0 + s) * kv_heads + g) * r + rr;
         const float w = dev::ex2(part_lse[row] - M);
@@ -122,12 +126,10 @@ cudaError_t launch_kv_append(int num_seqs, int kv_heads, int head_dim, int page_
     if (rows == 0) return cudaSuccess;
     const int threads = 256;
     const int blocks = (rows * 32 + threads - 1) / threads;
-    kv_append_kernel<<<blocks, threads, 0, s>>>(num_seqs, kv_heads, head_dim * elem_bytes, page_size,
-                                                 static_cast<const uint8_t *>(k_new),
-                                                 static_cast<const uint8_t *>(v_new), static_cast<uint8_t *>(k_pool),
-                                                 static_cast<uint8_t *>(v_pool), block_table, max_pages, seq_lens);
-    note_launch();
-    return cudaGetLastError();
+    return launch_pdl(kv_append_kernel, dim3(blocks), dim3(threads), 0, s, num_seqs, kv_heads, head_dim * elem_bytes,
+                      page_size, static_cast<const uint8_t *>(k_new), static_cast<const uint8_t *>(v_new),
+                      static_cast<uint8_t *>(k_pool), static_cast<uint8_t *>(v_pool), block_table, max_pages,
+                      seq_lens);
 }
 
 cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const int32_t *seq_lens,
@@ -139,23 +141,10 @@ cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const
     const int threads = 128;
     const int hpb = threads / tph;
     const int64_t blocks = (heads + hpb - 1) / hpb;
-    if (head_dim == 128) {
-        if (o_dtype == HETIS_BF16)
-            combine_kernel<128, 1><<<(unsigned)blocks, threads, 0, s>>>(num_seqs, q_heads, r, seq_lens, split_off,
-                                                                        part_lse, part_o, o, o_seq_stride);
-        else
-            combine_kernel<128, 0><<<(unsigned)blocks, threads, 0, s>>>(num_seqs, q_heads, r, seq_lens, split_off,
-                                                                        part_lse, part_o, o, o_seq_stride);
-    } else {
-        if (o_dtype == HETIS_BF16)
-            combine_kernel<64, 1><<<(unsigned)blocks, threads, 0, s>>>(num_seqs, q_heads, r, seq_lens, split_off,
-                                                                       part_lse, part_o, o, o_seq_stride);
-        else
-            combine_kernel<64, 0><<<(unsigned)blocks, threads, 0, s>>>(num_seqs, q_heads, r, seq_lens, split_off,
-                                                                       part_lse, part_o, o, o_seq_stride);
-    }
-    note_launch();
-    return cudaGetLastError();
+    auto kern = head_dim == 128 ? (o_dtype == HETIS_BF16 ? combine_kernel<128, 1> : combine_kernel<128, 0>)
+                                : (o_dtype == HETIS_BF16 ? combine_kernel<64, 1> : combine_kernel<64, 0>);
+    return launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), 0, s, num_seqs, q_heads, r, seq_lens, split_off,
+                      part_lse, part_o, o, o_seq_stride);
 }
 
 static cudaError_t head_copy(const void *src, void *dst, int num_seqs, int src_heads, int hs, int dst_heads, int hd,
