@@ -231,6 +231,7 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
     int32_t pid[PPL];
     load_pids(cur, pid);
     RingPos pos{0, 0u};
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // pools may hold rows the previous kernel (kv_append) wrote
     for (int it = 0; item < n_items; item += gridDim.x, ++it) {
         const int next = item + gridDim.x;
         int32_t pid_next[PPL];
@@ -729,7 +730,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         }
         dev::fence_barrier_init();
     }
-    dev::pdl_wait_then_release();          // first global access below (PDL, see launch_pdl)
+    // PDL: seq_lens, block tables and q are never written by this library's
+    // kernels, so the prologue reads them before griddepcontrol.wait; only the
+    // K/V pools (new-token rows from kv_append) must wait -- the producer lanes
+    // execute griddepcontrol.wait before their first page copy.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     build_split_offsets(p, s_len, s_off);  // contains __syncthreads
     const int n_items = s_off[p.num_seqs] * p.kv_heads;
 
