@@ -58,6 +58,11 @@ def share_time(cfg, n: int, steps: int, warmup: int, device):
     with torch.cuda.graph(g):
         for i in range(steps):
             step(i, ea[i], eb[i])
+    # the same steps without event nodes between the kernels (lets PDL overlap them)
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g2):
+        for i in range(steps):
+            step(i)
     g.replay()
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -67,8 +72,15 @@ def share_time(cfg, n: int, steps: int, warmup: int, device):
     torch.cuda.synchronize()
     step_ms = t0.elapsed_time(t1) / steps
     attn_ms = sum(a.elapsed_time(c) for a, c in zip(ea, eb)) / steps
+    g2.replay()
+    torch.cuda.synchronize()
+    t0.record()
+    g2.replay()
+    t1.record()
+    torch.cuda.synchronize()
+    step_noev_ms = t0.elapsed_time(t1) / steps
     return {"n": n, "heads_per_rank": x, "kv_bytes_per_rank": kv_bytes, "layers_rotated": n_layers,
-            "step_us": step_ms * 1e3, "attn_us": attn_ms * 1e3, "attn_gbs": kv_bytes / (attn_ms / 1e3) / 1e9}
+            "step_us": step_ms * 1e3, "step_no_events_us": step_noev_ms * 1e3, "attn_us": attn_ms * 1e3, "attn_gbs": kv_bytes / (attn_ms / 1e3) / 1e9}
 
 
 def main():
