@@ -1,0 +1,296 @@
+"""Hetis' head-wise dispatching on top of the measured B200 kernel.
+
+* Cost models (§5.1): attention time tau_i = a_i h_i + b_i g_i + c_i (Eq. 3,
+  PAPER.md:419-423) and transfer time rho_i = gamma_i d_i + beta_i with
+  d_i = (2 + 2/r) h_i head-vectors (Eq. 4), fitted by ordinary
+  least squares (the paper fits on an 8 x 8 grid).
+* Dispatch (§5.2.2): the min-max program of Eq. 7 solved as a
+  linear program ("reformulated as a linear programming
+  problem"; the paper used cvxpy + MOSEK, PAPER.md:549 -- here scipy's HiGHS),
+  then rounded to whole kv groups (x / r in N) by largest-remainder
+  apportionment so every request keeps exactly H heads (Eq. 7c), with a repair
+  pass for the cache budget.
+* State update (Eq. 8): h_i += sum_j x_i^j,
+  g_i += (2/r) sum_j x_i^j l_j.
+
+Units (reading 13 in DESIGN.md): g and the capacity M are counted in cached
+K/V head-vectors (one token of one kv head = 2 vectors, K and V), which is the
+unit Eq. 8 accumulates in; the budget is then g_i + (2/r) sum_j x_i^j l_j <= M_i
+(Eq. 6 / 7b rewritten in Eq. 8's units).  The plan a dispatch returns feeds
+`hetis_plan_create(per_request=1)` or, for a uniform split, a global plan.
+"""
+from __future__ import annotations
+
+import itertools
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+
+# ---------------------------------------------------------------- cost models (Eq. 3, Eq. 4)
+class FitError(ValueError):
+    pass
+
+
+def fit_linear(X: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """Ordinary least squares y ~ X @ beta with an explicit rank check (no silent pseudo-inverse)."""
+    X = np.asarray(X, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    if X.ndim != 2 or y.shape != (X.shape[0],):
+        raise FitError("shape mismatch")
+    if X.shape[0] < X.shape[1]:
+        raise FitError(f"need at least {X.shape[1]} samples, got {X.shape[0]}")
+    if np.linalg.matrix_rank(X) < X.shape[1]:
+        raise FitError("design matrix is rank deficient: vary every regressor independently")
+    beta, *_ = np.linalg.lstsq(X, y, rcond=None)
+    return beta
+
+
+@dataclass(frozen=True)
+class AttentionCost:
+    """tau = a h + b g + c (Eq. 3); for an Attention worker also gamma, beta of Eq. 4."""
+    a: float
+    b: float
+    c: float
+    gamma: float = 0.0
+    beta: float = 0.0
+
+    def attention_time(self, h: float, g: float) -> float:
+        return self.a * h + self.b * g + self.c
+
+    def transfer_time(self, h: float, r: int) -> float:
+        return self.gamma * (2.0 + 2.0 / r) * h + self.beta
+
+
+def fit_attention_cost(h, g, tau) -> AttentionCost:
+    """Fit Eq. 3 on measured (heads, cache, seconds) samples."""
+    h = np.asarray(h, dtype=np.float64)
+    X = np.stack([h, np.asarray(g, dtype=np.float64), np.ones_like(h)], axis=1)
+    a, b, c = fit_linear(X, tau)
+    return AttentionCost(float(a), float(b), float(c))
+
+
+def fit_transfer_cost(d, rho) -> tuple[float, float]:
+    """Fit Eq. 4 rho = gamma d + beta on (head-vectors moved, seconds) samples."""
+    d = np.asarray(d, dtype=np.float64)
+    gamma, beta = fit_linear(np.stack([d, np.ones_like(d)], axis=1), rho)
+    return float(gamma), float(beta)
+
+
+def model_accuracy(pred, meas) -> np.ndarray:
+    """Per-sample accuracy 1 - |pred - meas| / meas (the paper reports 'up to 93.8%')."""
+    pred = np.asarray(pred, dtype=np.float64)
+    meas = np.asarray(meas, dtype=np.float64)
+    return 1.0 - np.abs(pred - meas) / meas
+
+
+# ---------------------------------------------------------------- device state and f_i (Eq. 7)
+@dataclass(frozen=True)
+class DeviceState:
+    """h: resident query heads; g: resident cache (K/V head-vectors); mem: capacity M_i in the same unit."""
+    h: float
+    g: float
+    mem: float
+    primary: bool
+    cost: AttentionCost
+
+
+def eval_f(dev: DeviceState, x_row, lens, r: int) -> float:
+    """f_i of Eq. 7 for adding x_row[j] heads of new request j (length lens[j]) to device `dev`.
+
+    Primary:   a (h + sum x) + b (g + (2/r) sum l x) + c
+    Attention: (a + (2 + 2/r) gamma) (h + sum x) + b (g + (2/r) sum l x) + c + beta
+    """
+    x = np.asarray(x_row, dtype=np.float64)
+    l = np.asarray(lens, dtype=np.float64)
+    heads = dev.h + x.sum()
+    cache = dev.g + (2.0 / r) * float((l * x).sum())
+    k = dev.cost
+    if dev.primary:
+        return k.a * heads + k.b * cache + k.c
+    return (k.a + (2.0 + 2.0 / r) * k.gamma) * heads + k.b * cache + k.c + k.beta
+
+
+def _coeffs(dev: DeviceState, r: int):
+    """f_i(x) = sum_j (alpha + b (2/r) l_j) x_j + const."""
+    k = dev.cost
+    alpha = k.a if dev.primary else k.a + (2.0 + 2.0 / r) * k.gamma
+    const = alpha * dev.h + k.b * dev.g + k.c + (0.0 if dev.primary else k.beta)
+    return alpha, const
+
+
+class InfeasibleError(RuntimeError):
+    pass
+
+
+@dataclass
+class Dispatch:
+    x: np.ndarray               # [N][J] integer heads, multiples of r, columns sum to H
+    objective: float            # max_i f_i of the rounded allocation
+    lp_objective: float         # optimum of the continuous relaxation
+    per_device_f: list = field(default_factory=list)
+
+
+def dispatch(devices: list[DeviceState], lens, H: int, r: int) -> Dispatch:
+    """Solve Eq. 7 for the new requests `lens` (tokens each) over `devices`."""
+    from scipy.optimize import linprog
+
+    lens = np.asarray(lens, dtype=np.float64)
+    N, J = len(devices), len(lens)
+    if H % r:
+        raise ValueError("H must be a multiple of r")
+    if J == 0:
+        f = [eval_f(d, np.zeros(0), lens, r) for d in devices]
+        return Dispatch(np.zeros((N, 0), dtype=np.int64), max(f), max(f), f)
+    # variables: x[i, j] (row major) then T
+    nv = N * J + 1
+    cvec = np.zeros(nv)
+    cvec[-1] = 1.0
+    A_ub, b_ub = [], []
+    for i, d in enumerate(devices):
+        alpha, const = _coeffs(d, r)
+        row = np.zeros(nv)
+        row[i * J:(i + 1) * J] = alpha + d.cost.b * (2.0 / r) * lens
+        row[-1] = -1.0
+        A_ub.append(row)                      # f_i(x) - T <= 0   (Eq. 7a)
+        b_ub.append(-const)
+        cap = np.zeros(nv)
+        cap[i * J:(i + 1) * J] = (2.0 / r) * lens
+        A_ub.append(cap)                      # cache budget      (Eq. 7b, Eq. 8 units)
+        b_ub.append(d.mem - d.g)
+    A_eq, b_eq = [], []
+    for j in range(J):
+        row = np.zeros(nv)
+        row[[i * J + j for i in range(N)]] = 1.0
+        A_eq.append(row)                      # sum_i x_i^j = H   (Eq. 7c)
+        b_eq.append(float(H))
+    bounds = [(0.0, float(H))] * (N * J) + [(None, None)]
+    res = linprog(cvec, A_ub=np.array(A_ub), b_ub=np.array(b_ub), A_eq=np.array(A_eq), b_eq=np.array(b_eq),
+                  bounds=bounds, method="highs")
+    if res.status != 0:
+        need = (2.0 / r) * H * float(lens.sum())
+        free = sum(d.mem - d.g for d in devices)
+        raise InfeasibleError(f"no feasible dispatch (cache needed {need:.0f} head-vectors, free {free:.0f}): "
+                              f"{res.message}")
+    xr = res.x[:-1].reshape(N, J)
+    x = _round_groups(xr, H, r)
+    x = _repair_budget(devices, x, lens, r)
+    x = _improve(devices, x, lens, r)
+    f = [eval_f(d, x[i], lens, r) for i, d in enumerate(devices)]
+    return Dispatch(x, max(f), float(res.x[-1]), f)
+
+
+def _round_groups(xr: np.ndarray, H: int, r: int) -> np.ndarray:
+    """Largest-remainder apportionment of each request's H / r kv groups (sum preserved exactly)."""
+    N, J = xr.shape
+    groups = H // r
+    x = np.zeros((N, J), dtype=np.int64)
+    for j in range(J):
+        q = np.clip(xr[:, j], 0.0, None) / r
+        base = np.floor(q + 1e-9).astype(np.int64)
+        rem = groups - int(base.sum())
+        frac = q - base
+        for i in np.argsort(-frac, kind="stable")[:max(rem, 0)]:
+            base[i] += 1
+        while base.sum() > groups:             # numerical overshoot guard
+            base[int(np.argmax(base))] -= 1
+        x[:, j] = base * r
+    return x
+
+
+def _repair_budget(devices, x, lens, r):
+    """Move r-head chunks off devices over their cache budget to the feasible device with the smallest f."""
+    x = x.copy()
+    N, J = x.shape
+
+    def used(i):
+        return devices[i].g + (2.0 / r) * float((lens * x[i]).sum())
+
+    for _ in range(N * int(x.sum() // max(r, 1)) + 1):
+        over = [i for i in range(N) if used(i) > devices[i].mem + 1e-9]
+        if not over:
+            return x
+        i = over[0]
+        js = [j for j in range(J) if x[i, j] > 0]
+        j = max(js, key=lambda jj: lens[jj])   # the largest request frees the most cache per move
+        best, best_f = None, None
+        for k in range(N):
+            if k == i or used(k) + (2.0 / r) * lens[j] * r > devices[k].mem + 1e-9:
+                continue
+            trial = x[k].copy()
+            trial[j] += r
+            fk = eval_f(devices[k], trial, lens, r)
+            if best_f is None or fk < best_f:
+                best, best_f = k, fk
+        if best is None:
+            raise InfeasibleError("rounded allocation cannot be repaired within the cache budgets")
+        x[i, j] -= r
+        x[best, j] += r
+    raise InfeasibleError("budget repair did not converge")
+
+
+def _improve(devices, x, lens, r, max_moves: int = 256):
+    """Greedy post-rounding descent: move one r-head chunk off the bottleneck device whenever that lowers
+    max_i f_i while keeping every cache budget (the LP relaxation is the lower bound it approaches)."""
+    x = x.copy()
+    N, J = x.shape
+
+    def f_all(xx):
+        return [eval_f(d, xx[i], lens, r) for i, d in enumerate(devices)]
+
+    def fits(xx, i):
+        return devices[i].g + (2.0 / r) * float((lens * xx[i]).sum()) <= devices[i].mem + 1e-9
+
+    for _ in range(max_moves):
+        f = f_all(x)
+        worst = int(np.argmax(f))
+        best_x, best_max = None, max(f)
+        for j in range(J):
+            if x[worst, j] < r:
+                continue
+            for k in range(N):
+                if k == worst:
+                    continue
+                trial = x.copy()
+                trial[worst, j] -= r
+                trial[k, j] += r
+                if not fits(trial, k):
+                    continue
+                m = max(f_all(trial))
+                if m < best_max * (1 - 1e-12):
+                    best_x, best_max = trial, m
+        if best_x is None:
+            return x
+        x = best_x
+    return x
+
+
+def commit(devices: list[DeviceState], x: np.ndarray, lens, r: int) -> list[DeviceState]:
+    """Eq. 8: h_i += sum_j x_i^j; g_i += (2/r) sum_j x_i^j l_j."""
+    lens = np.asarray(lens, dtype=np.float64)
+    out = []
+    for i, d in enumerate(devices):
+        out.append(replace(d, h=d.h + float(x[i].sum()), g=d.g + (2.0 / r) * float((lens * x[i]).sum())))
+    return out
+
+
+def brute_force_optimum(devices: list[DeviceState], lens, H: int, r: int) -> float:
+    """Exhaustive optimum over all integral allocations (multiples of r) within the budgets -- test oracle
+    for small instances (<= 3 devices, <= 3 requests)."""
+    lens = np.asarray(lens, dtype=np.float64)
+    N, J = len(devices), len(lens)
+    groups = H // r
+    per_req = [c for c in itertools.product(range(groups + 1), repeat=N) if sum(c) == groups]
+    best = np.inf
+    for combo in itertools.product(per_req, repeat=J):
+        x = np.array(combo, dtype=np.int64).T * r          # [N][J]
+        ok = all(d.g + (2.0 / r) * float((lens * x[i]).sum()) <= d.mem + 1e-9 for i, d in enumerate(devices))
+        if not ok:
+            continue
+        best = min(best, max(eval_f(d, x[i], lens, r) for i, d in enumerate(devices)))
+    return best
+
+
+def plan_rows(x: np.ndarray) -> list[int]:
+    """Flatten a [N][J] allocation into hetis_plan_create(per_request=1)'s [J][N] row-major x."""
+    return [int(v) for v in np.asarray(x).T.reshape(-1)]

@@ -1,0 +1,141 @@
+"""Cost models (Eq. 3, Eq. 4) and the Eq. 7 dispatcher (CPU only).
+
+Worked examples follow SPEC.md's dispatcher interface with the
+paper's formulas; optimality is pinned by exhaustive
+enumeration on small instances.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_2509_08309_b200 import dispatch as dp
+from paper_2509_08309_b200 import hetis
+
+
+def test_fit_recovers_known_coefficients():
+    rng = np.random.default_rng(0)
+    h = np.repeat(np.arange(1, 9) * 40.0, 8)
+    g = np.tile(np.arange(1, 9) * 1e6, 8)
+    tau = 2e-8 * h + 1.5e-12 * g + 4e-6
+    noisy = tau * (1 + 1e-3 * rng.standard_normal(tau.shape))
+    m = dp.fit_attention_cost(h, g, noisy)
+    assert abs(m.a - 2e-8) / 2e-8 < 0.05 and abs(m.b - 1.5e-12) / 1.5e-12 < 0.01 and abs(m.c - 4e-6) / 4e-6 < 0.05
+    acc = dp.model_accuracy([m.attention_time(a, b) for a, b in zip(h, g)], tau)
+    assert acc.min() > 0.99
+    gamma, beta = dp.fit_transfer_cost([1, 2, 3, 4], [3.0, 5.0, 7.0, 9.0])
+    assert abs(gamma - 2.0) < 1e-12 and abs(beta - 1.0) < 1e-12
+
+
+def test_fit_rejects_rank_deficient_or_short_designs():
+    with pytest.raises(dp.FitError):
+        dp.fit_attention_cost([1, 2], [1, 2], [1, 2])                      # fewer samples than coefficients
+    with pytest.raises(dp.FitError):
+        dp.fit_attention_cost([1, 2, 3, 4], [2, 4, 6, 8], [1, 2, 3, 4])    # g proportional to h
+    with pytest.raises(dp.FitError):
+        dp.fit_attention_cost([5, 5, 5], [1, 2, 3], [1, 2, 3])             # h never varies
+
+
+def test_eval_f_worked_examples():
+    # primary, nothing added -> pure Eq. 3
+    k = dp.AttentionCost(a=1e-4, b=1e-7, c=2e-5)
+    d = dp.DeviceState(h=8, g=1000, mem=1e9, primary=True, cost=k)
+    assert dp.eval_f(d, [0], [100], 1) == pytest.approx(1e-4 * 8 + 1e-7 * 1000 + 2e-5)
+    # attention worker, h = 0, one request x = r = 1, l = 100:
+    # (a + (2 + 2/r) gamma) * 1 + b * (2/r) * 100 + c + beta
+    kw = dp.AttentionCost(a=1e-4, b=1e-7, c=0.0, gamma=1e-6, beta=1e-4)
+    w = dp.DeviceState(h=0, g=0, mem=1e9, primary=False, cost=kw)
+    assert dp.eval_f(w, [1], [100], 1) == pytest.approx(2.24e-4)
+
+
+def _devs(n, mem=1e12, primary=True, a=1e-6, b=1e-9, c=0.0):
+    return [dp.DeviceState(0, 0, mem, primary, dp.AttentionCost(a, b, c)) for _ in range(n)]
+
+
+def test_dispatch_single_device_and_even_split():
+    one = dp.dispatch(_devs(1), [500], H=8, r=1)
+    assert one.x.tolist() == [[8]]
+    two = dp.dispatch(_devs(2), [500], H=8, r=1)
+    assert sorted(two.x[:, 0].tolist()) == [4, 4]
+    assert two.objective == pytest.approx(1e-6 * 4 + 1e-9 * 2 * 4 * 500)
+
+
+def test_dispatch_budget_binding():
+    # device A can hold only 2 heads' cache: 2 heads x 100 tokens x 2 (K, V) = 400 head-vectors (r = 1)
+    devs = [dp.DeviceState(0, 0, 400, True, dp.AttentionCost(1e-6, 1e-9, 0.0)),
+            dp.DeviceState(0, 0, 1e9, True, dp.AttentionCost(1e-6, 1e-9, 0.0))]
+    out = dp.dispatch(devs, [100], H=8, r=1)
+    assert out.x[:, 0].tolist() == [2, 6]
+
+
+def test_dispatch_heterogeneous_speed_and_groups():
+    # device 1 twice as slow per head and per byte -> about 2:1 split, in whole kv groups (r = 8)
+    fast = dp.DeviceState(0, 0, 1e12, True, dp.AttentionCost(1e-7, 1e-10, 0.0))
+    slow = dp.DeviceState(0, 0, 1e12, True, dp.AttentionCost(2e-7, 2e-10, 0.0))
+    out = dp.dispatch([fast, slow], [2048] * 4, H=64, r=8)
+    assert (out.x % 8 == 0).all() and (out.x.sum(axis=0) == 64).all()
+    share_fast = out.x[0].sum() / out.x.sum()
+    assert 0.6 <= share_fast <= 0.72
+    plan = hetis.plan_create(hetis.make_shape(__import__("paper_2509_08309_b200.workload", fromlist=["x"]).LLAMA2_70B),
+                             2, dp.plan_rows(out.x), per_request=True, num_seqs=4)
+    assert plan.heads(1, seq=0) == (int(out.x[0, 0]), int(out.x[1, 0]))
+
+
+def test_transfer_cost_moves_load_to_primary():
+    prim = dp.DeviceState(0, 0, 1e12, True, dp.AttentionCost(1e-7, 1e-10, 0.0))
+    att = dp.DeviceState(0, 0, 1e12, False, dp.AttentionCost(1e-7, 1e-10, 0.0, gamma=5e-8, beta=1e-5))
+    out = dp.dispatch([prim, att], [1000], H=40, r=1)
+    assert out.x[0, 0] > out.x[1, 0]                    # network cost makes the attention worker pricier
+
+
+def test_commit_eq8_and_conservation():
+    devs = _devs(2)
+    x = np.array([[8, 0], [0, 8]])
+    new = dp.commit(devs, x, [50, 10], r=2)
+    assert new[0].h == 8 and new[0].g == pytest.approx((2 / 2) * 8 * 50)       # SPEC.md:322 example
+    assert new[1].h == 8 and new[1].g == pytest.approx((2 / 2) * 8 * 10)
+    rng = np.random.default_rng(3)
+    states = _devs(3)
+    total = 0.0
+    for _ in range(20):
+        lens = rng.integers(1, 500, size=2)
+        out = dp.dispatch(states, lens, H=8, r=2)
+        states = dp.commit(states, out.x, lens, r=2)
+        total += (2 / 2) * 8 * float(lens.sum())
+        assert (out.x.sum(axis=0) == 8).all()
+    assert sum(s.g for s in states) == pytest.approx(total)
+
+
+def test_infeasible_reports_shortfall():
+    devs = _devs(2, mem=100)
+    with pytest.raises(dp.InfeasibleError):
+        dp.dispatch(devs, [1000], H=8, r=1)
+
+
+def test_small_instance_optimality_against_exhaustive_enumeration():
+    """<= 3 devices, <= 3 requests, H <= 8, r in {1, 2}: the rounded LP solution is within the rounding
+    slack of the exhaustive optimum, and equal to it in most instances."""
+    rng = np.random.default_rng(7)
+    exact = 0
+    trials = 120
+    for _ in range(trials):
+        N = int(rng.integers(1, 4))
+        J = int(rng.integers(1, 4))
+        r = int(rng.choice([1, 2]))
+        H = int(rng.choice([4, 8]))
+        devs = []
+        for _i in range(N):
+            k = dp.AttentionCost(a=float(rng.uniform(1e-7, 1e-6)), b=float(rng.uniform(1e-10, 1e-9)),
+                                 c=float(rng.uniform(0, 1e-6)), gamma=float(rng.uniform(0, 1e-7)),
+                                 beta=float(rng.uniform(0, 1e-6)))
+            devs.append(dp.DeviceState(float(rng.integers(0, 64)), float(rng.integers(0, 10000)), 1e12,
+                                       bool(rng.integers(0, 2)), k))
+        lens = rng.integers(16, 2048, size=J)
+        out = dp.dispatch(devs, lens, H, r)
+        opt = dp.brute_force_optimum(devs, lens, H, r)
+        slack = max(d.cost.a + (2 + 2 / r) * d.cost.gamma + d.cost.b * (2 / r) * float(lens.max()) for d in devs) \
+            * r * J
+        assert out.lp_objective <= opt + 1e-12
+        assert out.objective <= opt + slack + 1e-12
+        exact += out.objective <= opt * (1 + 1e-9)
+    assert exact / trials >= 0.85, exact / trials      # measured 0.91 over 300 instances
