@@ -1,0 +1,114 @@
+#!/usr/bin/env python
+"""fit Hetis' attention-time model (Eq. 3)
+tau = a h + b g + c on this repo's B200 kernel over an 8 x 8 (heads, cache) grid
+(the paper's profiling grid), report the model accuracy the way
+the paper does (1 - |pred - meas| / meas, "up to 93.8%"), and check the
+paper's observation that attention time does not depend on the number of
+requests at fixed heads and cache (fig:execution_time_modeling (a)).
+
+h = query heads resident on the device (sum over requests), g = cached K/V
+head-vectors (2 * tokens * kv heads, Eq. 8's unit).  tau = one decode step's
+hetis_attn_partial + hetis_attn_combine, CUDA-graph replayed, KV larger than L2.
+
+    python scripts/cost_model_fit.py [--shape 13b|70b] > gpurun_out/cost_model.json
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2509_08309_b200 import dispatch, hetis, workload  # noqa: E402
+
+L2 = 126 * 2 ** 20
+
+
+def time_attention(shape, B: int, x: int, L: int, steps: int = 30) -> float:
+    dev = torch.device("cuda", 0)
+    lens = torch.full((B,), L, dtype=torch.int32)
+    b = workload.make_decode_batch(shape, lens, 1234 + B + x + L, dev, q_begin=0, q_count=x)
+    s = hetis.make_shape(shape)
+    hetis.kv_append(s, b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens)
+    kv = B * L * (x // shape.r) * shape.head_dim * 2 * shape.elem_bytes
+    n_layers = max(1, math.ceil(4 * L2 / kv))
+    kp = [b.k_pool] + [b.k_pool.clone() for _ in range(n_layers - 1)]
+    vp = [b.v_pool] + [b.v_pool.clone() for _ in range(n_layers - 1)]
+    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), dev)
+    o = torch.empty((B, x, shape.head_dim), device=dev)
+
+    def step(i):
+        hetis.attn_partial(s, b.q, kp[i % n_layers], vp[i % n_layers], b.block_table, b.seq_lens, L, ws)
+        hetis.attn_combine(s, b.seq_lens, L, o, ws)
+
+    for i in range(3):
+        step(i)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(steps):
+            step(i)
+    g.replay()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    g.replay()
+    t1.record()
+    torch.cuda.synchronize()
+    del kp, vp, b
+    return t0.elapsed_time(t1) / steps / 1e3          # seconds
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--shape", default="13b", choices=["13b", "70b"])
+    ap.add_argument("--batch", type=int, default=32)
+    a = ap.parse_args()
+    shape = workload.LLAMA2_13B if a.shape == "13b" else workload.LLAMA2_70B
+    r = shape.r
+    xs = [shape.num_q_heads * k // 8 for k in range(1, 9)]            # 8 head counts (multiples of r)
+    xs = [max(r, (v // r) * r) for v in xs]
+    Ls = [512 * k for k in range(1, 9)]                               # 8 context lengths
+    rows = []
+    for x in xs:
+        for L in Ls:
+            t = time_attention(shape, a.batch, x, L)
+            h = a.batch * x
+            gvec = 2 * a.batch * (x // r) * L
+            rows.append({"B": a.batch, "x": x, "L": L, "h": h, "g": gvec, "tau_s": t})
+            torch.cuda.empty_cache()
+    h = np.array([q["h"] for q in rows], dtype=np.float64)
+    g = np.array([q["g"] for q in rows], dtype=np.float64)
+    tau = np.array([q["tau_s"] for q in rows])
+    m = dispatch.fit_attention_cost(h, g, tau)
+    pred = np.array([m.attention_time(hh, gg) for hh, gg in zip(h, g)])
+    acc = dispatch.model_accuracy(pred, tau)
+    # batch independence at fixed h and g (fig:execution_time_modeling (a))
+    hx = shape.num_q_heads * 16
+    batch_rows = []
+    for B in (16, 32, 64, 128):
+        x = hx // B
+        if x % r or x < r or x > shape.num_q_heads:
+            continue
+        t = time_attention(shape, B, x, 2048)
+        batch_rows.append({"B": B, "x": x, "L": 2048, "h": B * x, "g": 2 * B * (x // r) * 2048, "tau_s": t})
+        torch.cuda.empty_cache()
+    bt = np.array([q["tau_s"] for q in batch_rows])
+    out = {
+        "shape": a.shape, "r": r, "grid": rows,
+        "fit": {"a_s_per_head": m.a, "b_s_per_headvector": m.b, "c_s": m.c,
+                "implied_GBps_from_b": shape.head_dim * shape.elem_bytes / m.b / 1e9},
+        "accuracy": {"mean": float(acc.mean()), "min": float(acc.min()), "max": float(acc.max())},
+        "batch_independence": {"rows": batch_rows,
+                               "spread_pct": float(100 * (bt.max() - bt.min()) / bt.mean()) if len(bt) else None},
+    }
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
