@@ -122,6 +122,18 @@ HETIS_API void hetis_plan_destroy(hetis_plan *plan);
 HETIS_API hetis_status hetis_plan_heads(const hetis_plan *plan, int32_t device, int32_t seq, int32_t *q_begin,
                               int32_t *q_count);
 HETIS_API int32_t hetis_plan_num_devices(const hetis_plan *plan);
+/* Work units of `device`: one unit = one (request j, kv head g) pair the device
+ * owns, i.e. r query heads of one request.  A per-request plan (x_i^j varying
+ * with j, the dispatcher's output, Eq. 7) is executed by the unchanged kernels
+ * by treating each unit as a request with ONE kv head: q, o as [U][r][head_dim],
+ * block table [U][1][max_pages], seq_lens[u] = L_j of the unit's request, and
+ * the shape's head range = (0, r).  The chunking of a unit depends on L_j only,
+ * so results are bit-identical to the uniform-plan path.
+ *   units: host int32 [2 * U] receiving (request, GLOBAL kv head) pairs in the
+ *          device's order (requests ascending, kv heads ascending), or NULL to
+ *          query the count; *num_units: in = capacity in units (ignored when
+ *          units is NULL), out = U.  Too small a capacity -> HETIS_E_INVALID. */
+HETIS_API hetis_status hetis_plan_units(const hetis_plan *plan, int32_t device, int32_t *units, int32_t *num_units);
 /* Eq. 6 in pages (reading 13): for every device i,
  *   sum_j ceil(seq_lens[j] / P) * x_i^j / r <= free_pages[i].
  * seq_lens_host: [num_seqs] lengths the requests will have (num_seqs must equal

@@ -223,6 +223,34 @@ void hetis_plan_destroy(hetis_plan *plan) { delete plan; }
 
 int32_t hetis_plan_num_devices(const hetis_plan *plan) { return plan ? plan->num_devices : 0; }
 
+hetis_status hetis_plan_units(const hetis_plan *plan, int32_t device, int32_t *units, int32_t *num_units) {
+    if (!plan || !num_units) return fail(HETIS_E_INVALID, "NULL argument");
+    if (device < 0 || device >= plan->num_devices) return fail(HETIS_E_INVALID, "device outside the plan");
+    const int r = plan->shape.num_q_heads / plan->shape.num_kv_heads;
+    const int rows = plan->per_request ? plan->num_seqs : 1;
+    const int B = plan->per_request ? plan->num_seqs : 0;
+    // a global plan has no request count; it describes every request identically
+    if (!plan->per_request) return fail(HETIS_E_UNSUPPORTED, "units are defined for per-request plans");
+    int64_t U = 0;
+    for (int j = 0; j < rows; ++j) U += plan->x[(size_t)j * plan->num_devices + device] / r;
+    if (!units) {
+        *num_units = (int32_t)U;
+        return HETIS_OK;
+    }
+    if (*num_units < U) return fail(HETIS_E_INVALID, "units capacity too small: need " + std::to_string(U));
+    int64_t u = 0;
+    for (int j = 0; j < B; ++j) {
+        const size_t k = (size_t)j * plan->num_devices + device;
+        for (int g = 0; g < plan->x[k] / r; ++g) {
+            units[2 * u] = j;
+            units[2 * u + 1] = plan->begin[k] / r + g;
+            ++u;
+        }
+    }
+    *num_units = (int32_t)U;
+    return HETIS_OK;
+}
+
 hetis_status hetis_plan_heads(const hetis_plan *plan, int32_t device, int32_t seq, int32_t *q_begin,
                               int32_t *q_count) {
     if (!plan || !q_begin || !q_count) return fail(HETIS_E_INVALID, "NULL argument");

