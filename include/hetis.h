@@ -93,6 +93,9 @@ typedef struct {
 
 /* Flags for hetis_attn_partial / hetis_attn_decode. */
 #define HETIS_ATTN_FORCE_SIMT 0x1u /* bf16 GQA on CUDA cores instead of tensor cores */
+/* bf16 GQA tensor-core kernel with the shared page ring and per-item CTA merge
+ * (the default gives every consumer warp whole items and its own sub-ring). */
+#define HETIS_ATTN_TC_SHARED_RING 0x2u
 /* Diagnostic only: stream every K/V page through the shared-memory ring but
  * skip the math (partials are left unwritten).  Measures the memory-system
  * ceiling of the pipeline; the CUDA-core kernel honours it. */

@@ -59,6 +59,9 @@ constexpr int kQSlots = 2;
 #ifndef HETIS_MAX_STAGES
 #define HETIS_MAX_STAGES 24
 #endif
+#ifndef HETIS_WARP_STAGES
+#define HETIS_WARP_STAGES 4
+#endif
 #ifndef HETIS_PRODUCER_LANES
 #define HETIS_PRODUCER_LANES 8
 #endif
@@ -693,6 +696,341 @@ __device__ void consumer_tc(const Params &p, const uint8_t *ring, const uint8_t 
     }
 }
 
+// ---------------------------------------------------------------- GQA tensor-core kernel, one work item per warp
+// Same math as consumer_tc, different work decomposition: every consumer warp
+// is an independent worker (v = blockIdx.x * NW + w) that streams WHOLE items
+// through its own sub-ring of SW stages, so no warp ever waits for another and
+// there is no cross-warp merge (the per-item named barrier and the shared-memory
+// merge were the largest overhead of the shared-ring kernel for r = 8).  Items
+// are round-robin over the gridDim.x * NW workers.  Lane w of warp 0 feeds
+// worker w: a non-blocking (test_wait) state machine issues q and pages into
+// the worker's sub-ring whenever a slot is free, so a slow worker never stalls
+// the others' producers.
+struct WarpSmem {
+    uint8_t *ring;      // [NW][SW] stages of (K page, V page)
+    uint8_t *qbuf;      // [NW] q rows of the worker's next item
+    ItemMeta *meta;     // [NW]
+    int32_t *pids;      // [NW][2][kPagesPerItem] page ids (double-buffered by item parity)
+    uint64_t *full;     // [NW][SW]
+    uint64_t *empty;    // [NW][SW]
+    uint64_t *qfull;    // [NW]
+    uint64_t *qempty;   // [NW]
+};
+
+template <int ROW_BYTES, int R, int NW>
+__device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW, const int32_t *s_len,
+                                    const int32_t *s_off, const void *tmap_k, const void *tmap_v) {
+    constexpr int kPageBytes = kP * ROW_BYTES;
+    constexpr int kStageBytes = 2 * kPageBytes;
+    constexpr int kQBytes = R * ROW_BYTES;
+    constexpr int kQStride = (kQBytes + 127) / 128 * 128;
+    const int w = threadIdx.x & 31;  // worker served by this lane
+    const unsigned mask = (1u << NW) - 1u;
+    const int n_items = s_off[p.num_seqs] * p.kv_heads;
+    const int V = gridDim.x * NW;
+    const uint64_t pol = dev::policy_evict_first();
+    if (w == 0) {
+        dev::prefetch_tmap(tmap_k);
+        dev::prefetch_tmap(tmap_v);
+    }
+    auto decode = [&](int item, int &j, int &g, int &t0, int &ntok) {
+        const int k = item / p.kv_heads;
+        g = item - k * p.kv_heads;
+        j = upper_bound_smem(s_off, p.num_seqs + 1, k) - 1;
+        t0 = (k - s_off[j]) * kC;
+        ntok = min(kC, s_len[j] - t0);
+    };
+    int32_t nxt[kPagesPerItem];  // page ids of the NEXT item, in flight in registers
+    auto load_next = [&](int item) {
+        int j, g, t0, ntok;
+        if (item < n_items) {
+            decode(item, j, g, t0, ntok);
+            const int np = (ntok + kP - 1) / kP;
+            const int32_t *row = p.block_table + ((size_t)j * p.kv_heads + g) * p.max_pages + t0 / kP;
+#pragma unroll
+            for (int i = 0; i < kPagesPerItem; ++i) nxt[i] = i < np ? __ldg(row + i) : 0;
+        }
+    };
+    int item = blockIdx.x * NW + w;
+    int it = 0;
+    int j = 0, g = 0, t0 = 0, ntok = 0, np = 0;
+    int pg = 0;
+    bool q_done = false;
+    RingPos pos{0, 0u};
+    if (item < n_items) {
+        decode(item, j, g, t0, ntok);
+        np = (ntok + kP - 1) / kP;
+        load_next(item);
+#pragma unroll
+        for (int i = 0; i < kPagesPerItem; ++i) sm.pids[(w * 2 + 0) * kPagesPerItem + i] = nxt[i];
+        load_next(item + V);
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // pools may hold rows the previous kernel wrote
+    while (__any_sync(mask, item < n_items)) {
+        if (item < n_items) {
+            if (!q_done && dev::mbar_test(&sm.qempty[w], (it & 1) ^ 1)) {
+                sm.meta[w] = ItemMeta{item, ntok, np, 0};
+                dev::mbar_arrive_expect_tx(&sm.qfull[w], kQBytes);
+                const uint8_t *src = p.q + ((size_t)j * p.q_heads + (size_t)g * R) * ROW_BYTES;
+                dev::bulk_g2s(sm.qbuf + (size_t)w * kQStride, src, kQBytes, &sm.qfull[w], pol);
+                q_done = true;
+            }
+            // issue as many pages as the worker's sub-ring has free stages
+            while (q_done && pg < np && dev::mbar_test(&sm.empty[w * SW + pos.stage], pos.phase ^ 1u)) {
+                const int32_t page = sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + pg];
+                uint64_t *bar = &sm.full[w * SW + pos.stage];
+                uint8_t *dst = sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes;
+                dev::mbar_arrive_expect_tx(bar, kStageBytes);
+                const int row = page * kP;
+                dev::tma_load_3d(dst, tmap_k, 0, row, 0, bar, pol);
+                dev::tma_load_3d(dst + kPageBytes, tmap_v, 0, row, 0, bar, pol);
+                ++pg;
+                pos.advance(1, SW);
+            }
+            if (q_done && pg == np) {  // item fully issued: move to this worker's next item
+                item += V;
+                ++it;
+                pg = 0;
+                q_done = false;
+                if (item < n_items) {
+                    decode(item, j, g, t0, ntok);
+                    np = (ntok + kP - 1) / kP;
+#pragma unroll
+                    for (int i = 0; i < kPagesPerItem; ++i) sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + i] = nxt[i];
+                    load_next(item + V);
+                }
+            }
+        }
+    }
+}
+
+template <int D, int R, int NW>
+__device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW, int n_items) {
+    constexpr int ROW_BYTES = D * 2;
+    constexpr int kPageBytes = kP * ROW_BYTES;
+    constexpr int kHalfBytes = kPageBytes / (D / 64);
+    constexpr int kStageBytes = 2 * kPageBytes;
+    constexpr int kQBytes = R * ROW_BYTES;
+    constexpr int kQStride = (kQBytes + 127) / 128 * 128;
+    constexpr int KSTEPS = D / 16;
+    constexpr int NT_O = D / 8;
+    static_assert(R <= 8, "r query heads must fit the 8 M rows");
+    const int lane = threadIdx.x & 31;
+    const int w = (threadIdx.x >> 5) - 1;
+    const int grp = lane >> 2;
+    const int tq = lane & 3;
+    auto swz = [](int t, int c) -> uint32_t {
+        const int half = c >> 3, cc = c & 7;
+        return (uint32_t)(half * kHalfBytes + t * 128 + ((cc ^ (t & 7)) << 4));
+    };
+    uint32_t k_off[2][KSTEPS / 2];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int q4 = 0; q4 < KSTEPS / 2; ++q4) k_off[nt][q4] = swz(8 * nt + (lane & 7), 4 * q4 + (lane >> 3));
+    uint32_t v_off[NT_O / 2];
+#pragma unroll
+    for (int c2 = 0; c2 < NT_O / 2; ++c2) {
+        const int mi = lane >> 3;
+        v_off[c2] = swz((mi & 1) * 8 + (lane & 7), 2 * c2 + (mi >> 1));
+    }
+    const int V = gridDim.x * NW;
+    RingPos pos{0, 0u};
+    int it = 0;
+    for (int item = blockIdx.x * NW + w; item < n_items; item += V, ++it) {
+        dev::mbar_wait(&sm.qfull[w], it & 1);
+        const ItemMeta meta = sm.meta[w];
+        uint32_t qa[KSTEPS][2];
+        {
+            const uint8_t *qs = sm.qbuf + (size_t)w * kQStride;
+#pragma unroll
+            for (int ks = 0; ks < KSTEPS; ++ks) {
+                if (grp < R) {
+                    qa[ks][0] = *reinterpret_cast<const uint32_t *>(qs + grp * ROW_BYTES + (16 * ks + 2 * tq) * 2);
+                    qa[ks][1] = *reinterpret_cast<const uint32_t *>(qs + grp * ROW_BYTES + (16 * ks + 8 + 2 * tq) * 2);
+                } else {
+                    qa[ks][0] = 0u;
+                    qa[ks][1] = 0u;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&sm.qempty[w]);
+
+        float m = -INFINITY, l = 0.f;
+        float o[NT_O][4];
+#pragma unroll
+        for (int nt = 0; nt < NT_O; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
+        for (int pg = 0; pg < meta.npages; ++pg) {
+            dev::mbar_wait(&sm.full[w * SW + pos.stage], pos.phase);
+            if (p.flags & HETIS_ATTN_DIAG_STREAM_ONLY) {
+                __syncwarp();
+                if (lane == 0) dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
+                pos.advance(1, SW);
+                continue;
+            }
+            const uint32_t kb = dev::smem_u32(sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes);
+            const uint32_t vb = kb + kPageBytes;
+            const int valid = min(kP, meta.ntok - pg * kP);
+            float s[2][4];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+                for (int q4 = 0; q4 < KSTEPS / 2; ++q4) {
+                    uint32_t b[4];
+                    dev::ldmatrix_x4(b, kb + k_off[nt][q4]);
+                    dev::mma_bf16_16816(s[nt], qa[2 * q4][0], 0u, qa[2 * q4][1], 0u, b[0], b[1]);
+                    dev::mma_bf16_16816(s[nt], qa[2 * q4 + 1][0], 0u, qa[2 * q4 + 1][1], 0u, b[2], b[3]);
+                }
+            }
+            float sc[4];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int t = 8 * nt + 2 * tq + e;
+                    sc[2 * nt + e] = (t < valid) ? s[nt][e] * p.scale_log2 : -INFINITY;
+                }
+            float mx = fmaxf(fmaxf(sc[0], sc[1]), fmaxf(sc[2], sc[3]));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            const float m_new = fmaxf(m, mx);
+            // o and l are still zero before the first page: nothing to rescale
+            if (__any_sync(0xffffffffu, m_new != m && m != -INFINITY)) {
+                const float alpha = dev::ex2(m - m_new);
+                l *= alpha;
+#pragma unroll
+                for (int nt = 0; nt < NT_O; ++nt) {
+                    o[nt][0] *= alpha; o[nt][1] *= alpha; o[nt][2] *= alpha; o[nt][3] *= alpha;
+                }
+            }
+            m = m_new;
+            float pp[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                pp[e] = dev::ex2(sc[e] - m);
+                l += pp[e];
+            }
+            uint32_t pa[4];
+            {
+                __nv_bfloat162 h0 = __floats2bfloat162_rn(pp[0], pp[1]);
+                __nv_bfloat162 h1 = __floats2bfloat162_rn(pp[2], pp[3]);
+                const float2 f0 = __bfloat1622float2(h0), f1 = __bfloat1622float2(h1);
+                __nv_bfloat162 l0 = __floats2bfloat162_rn(pp[0] - f0.x, pp[1] - f0.y);
+                __nv_bfloat162 l1 = __floats2bfloat162_rn(pp[2] - f1.x, pp[3] - f1.y);
+                pa[0] = *reinterpret_cast<uint32_t *>(&h0);
+                pa[1] = *reinterpret_cast<uint32_t *>(&l0);
+                pa[2] = *reinterpret_cast<uint32_t *>(&h1);
+                pa[3] = *reinterpret_cast<uint32_t *>(&l1);
+            }
+            uint32_t mk0 = 0xffffffffu, mk1 = 0xffffffffu;
+            if (valid < kP) {
+                const int t0 = 2 * tq, t1 = 8 + 2 * tq;
+                mk0 = (t0 < valid ? 0x0000ffffu : 0u) | (t0 + 1 < valid ? 0xffff0000u : 0u);
+                mk1 = (t1 < valid ? 0x0000ffffu : 0u) | (t1 + 1 < valid ? 0xffff0000u : 0u);
+            }
+#pragma unroll
+            for (int c2 = 0; c2 < NT_O / 2; ++c2) {
+                uint32_t b[4];
+                dev::ldmatrix_x4_trans(b, vb + v_off[c2]);
+                dev::mma_bf16_16816(o[2 * c2], pa[0], pa[1], pa[2], pa[3], b[0] & mk0, b[1] & mk1);
+                dev::mma_bf16_16816(o[2 * c2 + 1], pa[0], pa[1], pa[2], pa[3], b[2] & mk0, b[3] & mk1);
+            }
+            __syncwarp();
+            if (lane == 0) dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
+            pos.advance(1, SW);
+        }
+        // the item's partial: o_s = acc / l and lse_s = m + log2(l) for each of the r heads
+        l += __shfl_xor_sync(0xffffffffu, l, 1);
+        l += __shfl_xor_sync(0xffffffffu, l, 2);
+        if (grp < R && !(p.flags & HETIS_ATTN_DIAG_STREAM_ONLY)) {
+            const size_t row = (size_t)meta.item * R + grp;
+            float *dst = p.part_o + row * D;
+#pragma unroll
+            for (int nt = 0; nt < NT_O; ++nt)
+                *reinterpret_cast<float2 *>(dst + 8 * nt + 2 * tq) =
+                    make_float2(__fdiv_rn(o[nt][0] + o[nt][2], l), __fdiv_rn(o[nt][1] + o[nt][3], l));
+            if (tq == 0) p.part_lse[row] = m + __log2f(l);
+        }
+    }
+}
+
+template <int D, int R, int NW>
+__global__ void __launch_bounds__(32 * (NW + 1), 1)
+    attn_gqa_warp_kernel(const Params p, const __grid_constant__ CUtensorMap tmap_k,
+                         const __grid_constant__ CUtensorMap tmap_v) {
+    constexpr int ROW_BYTES = D * 2;
+    constexpr int kStageBytes = 2 * kP * ROW_BYTES;
+    constexpr int kQStride = (R * ROW_BYTES + 127) / 128 * 128;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024u - (dev::smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int SW = p.stages;  // stages per worker
+    WarpSmem sm;
+    sm.ring = smem;
+    sm.qbuf = sm.ring + (size_t)NW * SW * kStageBytes;
+    sm.meta = reinterpret_cast<ItemMeta *>(sm.qbuf + (size_t)NW * kQStride);
+    sm.pids = reinterpret_cast<int32_t *>(sm.meta + NW);
+    sm.full = reinterpret_cast<uint64_t *>(sm.pids + NW * 2 * kPagesPerItem);
+    sm.empty = sm.full + NW * SW;
+    sm.qfull = sm.empty + NW * SW;
+    sm.qempty = sm.qfull + NW;
+    int32_t *s_len = reinterpret_cast<int32_t *>(sm.qempty + NW);
+    int32_t *s_off = s_len + p.num_seqs;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NW * SW; ++i) {
+            dev::mbar_init(&sm.full[i], 1);
+            dev::mbar_init(&sm.empty[i], 1);
+        }
+        for (int i = 0; i < NW; ++i) {
+            dev::mbar_init(&sm.qfull[i], 1);
+            dev::mbar_init(&sm.qempty[i], 1);
+        }
+        dev::fence_barrier_init();
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    build_split_offsets(p, s_len, s_off);  // contains __syncthreads
+    const int n_items = s_off[p.num_seqs] * p.kv_heads;
+    if (threadIdx.x < 32) {
+        if (threadIdx.x < NW) producer_warp_items<ROW_BYTES, R, NW>(p, sm, SW, s_len, s_off, &tmap_k, &tmap_v);
+    } else {
+        consumer_warp_items<D, R, NW>(p, sm, SW, n_items);
+    }
+}
+
+template <int D, int R>
+cudaError_t launch_gqa_warp(const Params &p0, int num_seqs, cudaStream_t s, const CUtensorMap &tk,
+                            const CUtensorMap &tv, std::string *err) {
+    constexpr int NW = HETIS_TC_NW;
+    constexpr int ROW_BYTES = D * 2;
+    constexpr int kStageBytes = 2 * kP * ROW_BYTES;
+    constexpr int kQStride = (R * ROW_BYTES + 127) / 128 * 128;
+    Params p = p0;
+    auto fixed = [&](int sw) {
+        return (size_t)NW * kQStride + (size_t)NW * sizeof(ItemMeta) + (size_t)NW * 2 * kPagesPerItem * 4 +
+               (size_t)(2 * NW * sw + 2 * NW) * 8 + (size_t)(2 * num_seqs + 1) * 4 + 1024;
+    };
+    int sw = HETIS_WARP_STAGES;
+    while (sw > 2 && (size_t)NW * sw * kStageBytes + fixed(sw) > (size_t)kMaxSmem) --sw;
+    const size_t smem = (size_t)NW * sw * kStageBytes + fixed(sw);
+    if (smem > (size_t)kMaxSmem) {
+        if (err) *err = "batch too large for the shared-memory split table";
+        return cudaErrorInvalidValue;
+    }
+    p.stages = sw;
+    auto kern = attn_gqa_warp_kernel<D, R, NW>;
+    static std::atomic<int> configured[64];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if ((int)smem > configured[dev & 63].load(std::memory_order_acquire)) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured[dev & 63].store((int)smem, std::memory_order_release);
+    }
+    return launch_pdl(kern, dim3(num_sms()), dim3(32 * (NW + 1)), smem, s, p, tk, tv);
+}
+
 // ---------------------------------------------------------------- kernels
 template <int DT, int D, int R, int NW, bool TC>
 __global__ void __launch_bounds__(32 * (NW + 1), 1)
@@ -894,8 +1232,20 @@ cudaError_t launch_attn_tc(const AttnArgs &a, cudaStream_t s, std::string *err) 
     CUtensorMap tk, tv;
     if (!make_pool_map(&tk, a.k_pool, a.num_pages, a.head_dim, err)) return cudaErrorInvalidValue;
     if (!make_pool_map(&tv, a.v_pool, a.num_pages, a.head_dim, err)) return cudaErrorInvalidValue;
-    if (a.head_dim == 128) return dispatch_r<HETIS_BF16, 128, true>(a, p, s, tk, tv, err);
-    if (a.head_dim == 64) return dispatch_r<HETIS_BF16, 64, true>(a, p, s, tk, tv, err);
+    if (a.flags & HETIS_ATTN_TC_SHARED_RING) {
+        if (a.head_dim == 128) return dispatch_r<HETIS_BF16, 128, true>(a, p, s, tk, tv, err);
+        if (a.head_dim == 64) return dispatch_r<HETIS_BF16, 64, true>(a, p, s, tk, tv, err);
+        return cudaErrorInvalidValue;
+    }
+    switch (a.head_dim * 16 + a.r) {
+        case 128 * 16 + 2: return launch_gqa_warp<128, 2>(p, a.num_seqs, s, tk, tv, err);
+        case 128 * 16 + 4: return launch_gqa_warp<128, 4>(p, a.num_seqs, s, tk, tv, err);
+        case 128 * 16 + 8: return launch_gqa_warp<128, 8>(p, a.num_seqs, s, tk, tv, err);
+        case 64 * 16 + 2: return launch_gqa_warp<64, 2>(p, a.num_seqs, s, tk, tv, err);
+        case 64 * 16 + 4: return launch_gqa_warp<64, 4>(p, a.num_seqs, s, tk, tv, err);
+        case 64 * 16 + 8: return launch_gqa_warp<64, 8>(p, a.num_seqs, s, tk, tv, err);
+        default: break;
+    }
     return cudaErrorInvalidValue;
 }
 
