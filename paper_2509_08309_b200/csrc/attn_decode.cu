@@ -1232,7 +1232,16 @@ cudaError_t launch_attn_tc(const AttnArgs &a, cudaStream_t s, std::string *err) 
     CUtensorMap tk, tv;
     if (!make_pool_map(&tk, a.k_pool, a.num_pages, a.head_dim, err)) return cudaErrorInvalidValue;
     if (!make_pool_map(&tv, a.v_pool, a.num_pages, a.head_dim, err)) return cudaErrorInvalidValue;
-    if (a.flags & HETIS_ATTN_TC_SHARED_RING) {
+    // Work decomposition: whole items per warp avoids the per-item CTA merge but
+    // balances at item granularity over num_sms * NW workers; when the (upper
+    // bound on the) number of items per worker is between 1 and 5 the
+    // quantisation tail costs more than the merge (measured on c3 at N = 2, 4),
+    // so the shared-ring kernel, which splits every item over the CTA's warps,
+    // is used instead.
+    const double per_worker = (double)a.num_seqs * a.kv_heads * ((a.max_seq_len + kSplitTokens - 1) / kSplitTokens) /
+                              ((double)num_sms() * HETIS_TC_NW);
+    const bool shared_ring = (a.flags & HETIS_ATTN_TC_SHARED_RING) || (per_worker > 1.0 && per_worker < 5.0);
+    if (shared_ring) {
         if (a.head_dim == 128) return dispatch_r<HETIS_BF16, 128, true>(a, p, s, tk, tv, err);
         if (a.head_dim == 64) return dispatch_r<HETIS_BF16, 64, true>(a, p, s, tk, tv, err);
         return cudaErrorInvalidValue;
