@@ -715,6 +715,7 @@ struct WarpSmem {
     uint64_t *empty;    // [NW][SW]
     uint64_t *qfull;    // [NW]
     uint64_t *qempty;   // [NW]
+    int *claim;         // next CTA-local item index to hand out
 };
 
 template <int ROW_BYTES, int R, int NW>
@@ -751,11 +752,19 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             for (int i = 0; i < kPagesPerItem; ++i) nxt[i] = i < np ? __ldg(row + i) : 0;
         }
     };
-    int item = blockIdx.x * NW + w;
+    // Items are dealt to CTAs round-robin (item = blockIdx.x + k * gridDim.x, the
+    // same per-SM balance as the shared-ring kernel); inside the CTA each lane
+    // claims the CTA's next k from a shared counter when its worker needs
+    // work, so the CTA's items spread over its warps dynamically and a warp
+    // that finishes early takes more.  One item is claimed ahead (its page ids
+    // are loaded in the background); a claim past the end posts a sentinel.
+    auto claim = [&]() -> int { return (int)blockIdx.x + atomicAdd(sm.claim, 1) * (int)gridDim.x; };
+    int item = claim();
+    int next = item < n_items ? claim() : n_items;
     int it = 0;
     int j = 0, g = 0, t0 = 0, ntok = 0, np = 0;
     int pg = 0;
-    bool q_done = false;
+    bool q_done = false, finished = false;
     RingPos pos{0, 0u};
     if (item < n_items) {
         decode(item, j, g, t0, ntok);
@@ -763,42 +772,50 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         load_next(item);
 #pragma unroll
         for (int i = 0; i < kPagesPerItem; ++i) sm.pids[(w * 2 + 0) * kPagesPerItem + i] = nxt[i];
-        load_next(item + V);
+        load_next(next);
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");  // pools may hold rows the previous kernel wrote
-    while (__any_sync(mask, item < n_items)) {
-        if (item < n_items) {
-            if (!q_done && dev::mbar_test(&sm.qempty[w], (it & 1) ^ 1)) {
-                sm.meta[w] = ItemMeta{item, ntok, np, 0};
-                dev::mbar_arrive_expect_tx(&sm.qfull[w], kQBytes);
-                const uint8_t *src = p.q + ((size_t)j * p.q_heads + (size_t)g * R) * ROW_BYTES;
-                dev::bulk_g2s(sm.qbuf + (size_t)w * kQStride, src, kQBytes, &sm.qfull[w], pol);
-                q_done = true;
+    while (__any_sync(mask, !finished)) {
+        if (finished) continue;
+        if (item >= n_items) {  // no more work for this worker: post the sentinel when the q slot is free
+            if (dev::mbar_test(&sm.qempty[w], (it & 1) ^ 1)) {
+                sm.meta[w] = ItemMeta{-1, 0, 0, 0};
+                dev::mbar_arrive(&sm.qfull[w]);
+                finished = true;
             }
-            // issue as many pages as the worker's sub-ring has free stages
-            while (q_done && pg < np && dev::mbar_test(&sm.empty[w * SW + pos.stage], pos.phase ^ 1u)) {
-                const int32_t page = sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + pg];
-                uint64_t *bar = &sm.full[w * SW + pos.stage];
-                uint8_t *dst = sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes;
-                dev::mbar_arrive_expect_tx(bar, kStageBytes);
-                const int row = page * kP;
-                dev::tma_load_3d(dst, tmap_k, 0, row, 0, bar, pol);
-                dev::tma_load_3d(dst + kPageBytes, tmap_v, 0, row, 0, bar, pol);
-                ++pg;
-                pos.advance(1, SW);
-            }
-            if (q_done && pg == np) {  // item fully issued: move to this worker's next item
-                item += V;
-                ++it;
-                pg = 0;
-                q_done = false;
-                if (item < n_items) {
-                    decode(item, j, g, t0, ntok);
-                    np = (ntok + kP - 1) / kP;
+            continue;
+        }
+        if (!q_done && dev::mbar_test(&sm.qempty[w], (it & 1) ^ 1)) {
+            sm.meta[w] = ItemMeta{item, ntok, np, 0};
+            dev::mbar_arrive_expect_tx(&sm.qfull[w], kQBytes);
+            const uint8_t *src = p.q + ((size_t)j * p.q_heads + (size_t)g * R) * ROW_BYTES;
+            dev::bulk_g2s(sm.qbuf + (size_t)w * kQStride, src, kQBytes, &sm.qfull[w], pol);
+            q_done = true;
+        }
+        // issue as many pages as the worker's sub-ring has free stages
+        while (q_done && pg < np && dev::mbar_test(&sm.empty[w * SW + pos.stage], pos.phase ^ 1u)) {
+            const int32_t page = sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + pg];
+            uint64_t *bar = &sm.full[w * SW + pos.stage];
+            uint8_t *dst = sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes;
+            dev::mbar_arrive_expect_tx(bar, kStageBytes);
+            const int row = page * kP;
+            dev::tma_load_3d(dst, tmap_k, 0, row, 0, bar, pol);
+            dev::tma_load_3d(dst + kPageBytes, tmap_v, 0, row, 0, bar, pol);
+            ++pg;
+            pos.advance(1, SW);
+        }
+        if (q_done && pg == np) {  // item fully issued: move to the claimed next item
+            item = next;
+            ++it;
+            pg = 0;
+            q_done = false;
+            if (item < n_items) {
+                next = claim();
+                decode(item, j, g, t0, ntok);
+                np = (ntok + kP - 1) / kP;
 #pragma unroll
-                    for (int i = 0; i < kPagesPerItem; ++i) sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + i] = nxt[i];
-                    load_next(item + V);
-                }
+                for (int i = 0; i < kPagesPerItem; ++i) sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + i] = nxt[i];
+                load_next(next);
             }
         }
     }
@@ -834,12 +851,11 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         const int mi = lane >> 3;
         v_off[c2] = swz((mi & 1) * 8 + (lane & 7), 2 * c2 + (mi >> 1));
     }
-    const int V = gridDim.x * NW;
     RingPos pos{0, 0u};
-    int it = 0;
-    for (int item = blockIdx.x * NW + w; item < n_items; item += V, ++it) {
+    for (int it = 0;; ++it) {
         dev::mbar_wait(&sm.qfull[w], it & 1);
         const ItemMeta meta = sm.meta[w];
+        if (meta.item < 0) break;  // sentinel: the CTA's items are exhausted
         uint32_t qa[KSTEPS][2];
         {
             const uint8_t *qs = sm.qbuf + (size_t)w * kQStride;
@@ -975,7 +991,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     sm.empty = sm.full + NW * SW;
     sm.qfull = sm.empty + NW * SW;
     sm.qempty = sm.qfull + NW;
-    int32_t *s_len = reinterpret_cast<int32_t *>(sm.qempty + NW);
+    sm.claim = reinterpret_cast<int *>(sm.qempty + NW);
+    int32_t *s_len = sm.claim + 2;
     int32_t *s_off = s_len + p.num_seqs;
     if (threadIdx.x == 0) {
         for (int i = 0; i < NW * SW; ++i) {
@@ -986,6 +1003,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
             dev::mbar_init(&sm.qfull[i], 1);
             dev::mbar_init(&sm.qempty[i], 1);
         }
+        *sm.claim = 0;
         dev::fence_barrier_init();
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -1008,7 +1026,7 @@ cudaError_t launch_gqa_warp(const Params &p0, int num_seqs, cudaStream_t s, cons
     Params p = p0;
     auto fixed = [&](int sw) {
         return (size_t)NW * kQStride + (size_t)NW * sizeof(ItemMeta) + (size_t)NW * 2 * kPagesPerItem * 4 +
-               (size_t)(2 * NW * sw + 2 * NW) * 8 + (size_t)(2 * num_seqs + 1) * 4 + 1024;
+               (size_t)(2 * NW * sw + 2 * NW) * 8 + 8 + (size_t)(2 * num_seqs + 1) * 4 + 1024;
     };
     int sw = HETIS_WARP_STAGES;
     while (sw > 2 && (size_t)NW * sw * kStageBytes + fixed(sw) > (size_t)kMaxSmem) --sw;
@@ -1232,15 +1250,9 @@ cudaError_t launch_attn_tc(const AttnArgs &a, cudaStream_t s, std::string *err) 
     CUtensorMap tk, tv;
     if (!make_pool_map(&tk, a.k_pool, a.num_pages, a.head_dim, err)) return cudaErrorInvalidValue;
     if (!make_pool_map(&tv, a.v_pool, a.num_pages, a.head_dim, err)) return cudaErrorInvalidValue;
-    // Work decomposition: whole items per warp avoids the per-item CTA merge but
-    // balances at item granularity over num_sms * NW workers; when the (upper
-    // bound on the) number of items per worker is between 1 and 5 the
-    // quantisation tail costs more than the merge (measured on c3 at N = 2, 4),
-    // so the shared-ring kernel, which splits every item over the CTA's warps,
-    // is used instead.
-    const double per_worker = (double)a.num_seqs * a.kv_heads * ((a.max_seq_len + kSplitTokens - 1) / kSplitTokens) /
-                              ((double)num_sms() * HETIS_TC_NW);
-    const bool shared_ring = (a.flags & HETIS_ATTN_TC_SHARED_RING) || (per_worker > 1.0 && per_worker < 5.0);
+    // Default: whole items per warp (no per-item CTA merge); the shared-ring
+    // kernel that splits every item over the CTA's warps stays selectable.
+    const bool shared_ring = (a.flags & HETIS_ATTN_TC_SHARED_RING) != 0;
     if (shared_ring) {
         if (a.head_dim == 128) return dispatch_r<HETIS_BF16, 128, true>(a, p, s, tk, tv, err);
         if (a.head_dim == 64) return dispatch_r<HETIS_BF16, 64, true>(a, p, s, tk, tv, err);
