@@ -336,3 +336,24 @@ def test_per_request_plan_units_bit_identical_to_unsplit():
     assert seen == len(lens) * 8
     assert torch.equal(assembled, o_full)
     assert_close(assembled, oracle_full(full), "per-request plan")
+
+
+@pytest.mark.parametrize("name", ["c3", "c2"])
+def test_head_partition_bit_identical_at_config_size(name):
+    """The c3 / c2 batch split over 2, 4 and 8 ranks (each rank's share generated on its own) reassembles
+    bit for bit to the single-device result: the per-warp work claiming and the CTA item dealing never
+    change an item's arithmetic."""
+    cfg = workload.CONFIGS[name]
+    full = workload.make_decode_batch(cfg.shape, cfg.seq_lens(), cfg.seed, "cuda")
+    o_full = run_gpu(full)
+    del full
+    for n in (2, 4, 8):
+        split = cfg.head_split(n)
+        begin, outs = 0, []
+        for i, x in enumerate(split):
+            part = workload.make_decode_batch(cfg.shape, cfg.seq_lens(), cfg.seed, "cuda", q_begin=begin, q_count=x,
+                                              rank_salt=i + 1)
+            outs.append(run_gpu(part))
+            del part
+            begin += x
+        assert torch.equal(torch.cat(outs, 1), o_full), n
