@@ -171,6 +171,23 @@ struct RingPos {
     }
 };
 
+// ---------------------------------------------------------------- optional timeline trace
+// Built only with -DHETIS_TRACE (scripts/trace_kernel.py): per-CTA %globaltimer
+// stamps of the per-warp GQA kernel's phases, read back by hetis_trace_read.
+#ifdef HETIS_TRACE
+__device__ unsigned long long g_trace[1024][8];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define HETIS_TS(slot) (g_trace[blockIdx.x & 1023][(slot)] = gtimer())
+#define HETIS_TS_MAX(slot) atomicMax(&g_trace[blockIdx.x & 1023][(slot)], gtimer())
+#else
+#define HETIS_TS(slot) ((void)0)
+#define HETIS_TS_MAX(slot) ((void)0)
+#endif
+
 // ---------------------------------------------------------------- producer (kProducerLanes threads)
 // COPY = 0: two 1-D bulk copies per page (K, V).  COPY = 1: 2-D tensor copies
 // of 64-column blocks (16 rows x 128 B, 128-B swizzle) for K and V.
@@ -775,6 +792,9 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         load_next(next);
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");  // pools may hold rows the previous kernel wrote
+    if (w == 0) {
+        HETIS_TS(2);
+    }
     while (__any_sync(mask, !finished)) {
         if (finished) continue;
         if (item >= n_items) {  // no more work for this worker: post the sentinel when the q slot is free
@@ -803,6 +823,9 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             dev::tma_load_3d(dst + kPageBytes, tmap_v, 0, row, 0, bar, pol);
             ++pg;
             pos.advance(1, SW);
+            if (w == 0 && it == 0 && pg == 1) {
+                HETIS_TS(3);
+            }
         }
         if (q_done && pg == np) {  // item fully issued: move to the claimed next item
             item = next;
@@ -855,7 +878,12 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     for (int it = 0;; ++it) {
         dev::mbar_wait(&sm.qfull[w], it & 1);
         const ItemMeta meta = sm.meta[w];
-        if (meta.item < 0) break;  // sentinel: the CTA's items are exhausted
+        if (meta.item < 0) {  // sentinel: the CTA's items are exhausted
+            if (lane == 0) {
+                HETIS_TS_MAX(5);
+            }
+            break;
+        }
         uint32_t qa[KSTEPS][2];
         {
             const uint8_t *qs = sm.qbuf + (size_t)w * kQStride;
@@ -879,6 +907,9 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         for (int nt = 0; nt < NT_O; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
         for (int pg = 0; pg < meta.npages; ++pg) {
             dev::mbar_wait(&sm.full[w * SW + pos.stage], pos.phase);
+            if (w == 0 && lane == 0 && it == 0 && pg == 0) {
+                HETIS_TS(4);
+            }
             if (p.flags & HETIS_ATTN_DIAG_STREAM_ONLY) {
                 __syncwarp();
                 if (lane == 0) dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
@@ -1006,8 +1037,14 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         *sm.claim = 0;
         dev::fence_barrier_init();
     }
+    if (threadIdx.x == 0) {
+        HETIS_TS(0);
+    }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     build_split_offsets(p, s_len, s_off);  // contains __syncthreads
+    if (threadIdx.x == 0) {
+        HETIS_TS(1);
+    }
     const int n_items = s_off[p.num_seqs] * p.kv_heads;
     if (threadIdx.x < 32) {
         if (threadIdx.x < NW) producer_warp_items<ROW_BYTES, R, NW>(p, sm, SW, s_len, s_off, &tmap_k, &tmap_v);
@@ -1270,4 +1307,15 @@ cudaError_t launch_attn_tc(const AttnArgs &a, cudaStream_t s, std::string *err) 
     return cudaErrorInvalidValue;
 }
 
+#ifdef HETIS_TRACE
+extern "C" __attribute__((visibility("default"))) int hetis_trace_read(void *dst, size_t bytes, int clear) {
+    if (bytes > sizeof(g_trace)) bytes = sizeof(g_trace);
+    if (cudaMemcpyFromSymbol(dst, g_trace, bytes) != cudaSuccess) return 1;
+    if (clear) {
+        static unsigned long long zeros[1024][8];
+        if (cudaMemcpyToSymbol(g_trace, zeros, sizeof(zeros)) != cudaSuccess) return 1;
+    }
+    return 0;
+}
+#endif
 }  // namespace hetis
