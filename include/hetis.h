@@ -175,7 +175,9 @@ HETIS_API hetis_status hetis_attn_decode_workspace(const hetis_shape *shape, int
  *   k_pool, v_pool, num_pages, block_table, max_pages, seq_lens: as in
  *       hetis_kv_append with kv_head_count = q_head_count / r
  *   max_seq_len: upper bound of seq_lens (workspace sizing)
- *   workspace  : device, >= hetis_attn_decode_workspace bytes, 256-B aligned
+ *   workspace  : device, >= hetis_attn_decode_workspace bytes, 256-B aligned,
+ *                ZERO-filled before its first use (it ends in two work-claim
+ *                counters that every completed launch returns to zero)
  *   flags      : HETIS_ATTN_* */
 HETIS_API hetis_status hetis_attn_partial(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
                                 int32_t q_head_count, const void *q, const void *k_pool, const void *v_pool,

@@ -145,7 +145,8 @@ WorkspaceLayout workspace_layout(int num_seqs, int kv_heads, int r, int head_dim
     w.split_off_offset = 0;
     w.lse_offset = round256((size_t)(num_seqs + 1) * 4);
     w.o_offset = w.lse_offset + round256((size_t)w.max_items * r * 4);
-    w.total = w.o_offset + round256((size_t)w.max_items * r * head_dim * 4);
+    w.counter_offset = w.o_offset + round256((size_t)w.max_items * r * head_dim * 4);
+    w.total = w.counter_offset + 256;
     return w;
 }
 }  // namespace hetis
@@ -367,6 +368,7 @@ static hetis_status attn_args(const hetis_shape *shape, int32_t num_seqs, int32_
     a->part_lse = reinterpret_cast<float *>(ws + w.lse_offset);
     a->part_o = reinterpret_cast<float *>(ws + w.o_offset);
     a->max_items = w.max_items;
+    a->counters = reinterpret_cast<int32_t *>(ws + w.counter_offset);
     return HETIS_OK;
 }
 

@@ -59,6 +59,9 @@ constexpr int kQSlots = 2;
 #ifndef HETIS_MAX_STAGES
 #define HETIS_MAX_STAGES 24
 #endif
+#ifndef HETIS_GLOBAL_CLAIM
+#define HETIS_GLOBAL_CLAIM 1
+#endif
 #ifndef HETIS_WARP_STAGES
 #define HETIS_WARP_STAGES 4
 #endif
@@ -86,6 +89,7 @@ struct Params {
     int stages;    // ring depth
     float scale_log2;  // log2(e) / sqrt(d)
     uint32_t flags;    // HETIS_ATTN_*
+    int32_t *counters; // [0] global work-claim counter, [1] CTA-finish counter (zero between launches)
 };
 
 struct ItemMeta {
@@ -769,13 +773,18 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             for (int i = 0; i < kPagesPerItem; ++i) nxt[i] = i < np ? __ldg(row + i) : 0;
         }
     };
-    // Items are dealt to CTAs round-robin (item = blockIdx.x + k * gridDim.x, the
-    // same per-SM balance as the shared-ring kernel); inside the CTA each lane
-    // claims the CTA's next k from a shared counter when its worker needs
-    // work, so the CTA's items spread over its warps dynamically and a warp
-    // that finishes early takes more.  One item is claimed ahead (its page ids
-    // are loaded in the background); a claim past the end posts a sentinel.
+    // Work is claimed dynamically: every lane takes the next item from a
+    // device-wide counter when its worker needs work (HETIS_GLOBAL_CLAIM, the
+    // default), so faster SMs and warps take more items and the kernel ends
+    // within about one item of perfect balance; the alternative deals items to
+    // CTAs round-robin and claims only within the CTA.  One item is claimed
+    // ahead (its page ids load in the background); a claim past the end posts
+    // a sentinel.  The claim order never changes an item's arithmetic.
+#if HETIS_GLOBAL_CLAIM
+    auto claim = [&]() -> int { return atomicAdd(p.counters, 1); };
+#else
     auto claim = [&]() -> int { return (int)blockIdx.x + atomicAdd(sm.claim, 1) * (int)gridDim.x; };
+#endif
     int item = claim();
     int next = item < n_items ? claim() : n_items;
     int it = 0;
@@ -1051,6 +1060,18 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     } else {
         consumer_warp_items<D, R, NW>(p, sm, SW, n_items);
     }
+#if HETIS_GLOBAL_CLAIM
+    // the last CTA to finish returns the device-wide counters to zero for the next launch
+    __syncwarp();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(p.counters + 1, 1) == (int)gridDim.x - 1) {
+            p.counters[0] = 0;
+            p.counters[1] = 0;
+        }
+    }
+#endif
 }
 
 template <int D, int R>
@@ -1205,6 +1226,7 @@ Params make_params(const AttnArgs &a) {
     p.max_pages = a.max_pages;
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)a.head_dim));
     p.flags = a.flags;
+    p.counters = a.counters;
     return p;
 }
 

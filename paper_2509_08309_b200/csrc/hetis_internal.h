@@ -37,10 +37,11 @@ struct AttnArgs {
     float *part_o;        // [max_items][r][head_dim]
     int64_t max_items;
     uint32_t flags;       // HETIS_ATTN_*
+    int32_t *counters;    // [2] work-claim and CTA-finish counters; zero between launches
 };
 
 struct WorkspaceLayout {
-    size_t split_off_offset, lse_offset, o_offset, total;
+    size_t split_off_offset, lse_offset, o_offset, counter_offset, total;
     int64_t max_items;
 };
 

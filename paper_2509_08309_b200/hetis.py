@@ -213,8 +213,10 @@ def attn_decode_workspace(shape: CShape, num_seqs: int, q_head_count: int, max_s
 
 
 def alloc_workspace(nbytes: int, device) -> torch.Tensor:
-    """A 256-byte aligned uint8 device buffer (torch's caching allocator aligns to 512)."""
-    return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+    """A zero-filled, 256-byte aligned uint8 device buffer (torch's caching allocator aligns to
+    512).  Zero-filled because the attention workspace ends in work-claim counters that must start
+    at zero; every completed launch leaves them zero again."""
+    return torch.zeros(max(nbytes, 256), dtype=torch.uint8, device=device)
 
 
 def attn_partial(shape: CShape, q, k_pool, v_pool, block_table, seq_lens, max_seq_len: int, workspace,
