@@ -780,12 +780,16 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     // CTAs round-robin and claims only within the CTA.  One item is claimed
     // ahead (its page ids load in the background); a claim past the end posts
     // a sentinel.  The claim order never changes an item's arithmetic.
+    // The first round is static and interleaved over the CTAs (worker (cta, w)
+    // takes item w * gridDim.x + cta), so a problem smaller than one round is
+    // spread evenly over the SMs; claims after that come from the counter.
 #if HETIS_GLOBAL_CLAIM
-    auto claim = [&]() -> int { return atomicAdd(p.counters, 1); };
+    auto claim = [&]() -> int { return (int)gridDim.x * NW + atomicAdd(p.counters, 1); };
+    int item = w * (int)gridDim.x + (int)blockIdx.x;
 #else
     auto claim = [&]() -> int { return (int)blockIdx.x + atomicAdd(sm.claim, 1) * (int)gridDim.x; };
-#endif
     int item = claim();
+#endif
     int next = item < n_items ? claim() : n_items;
     int it = 0;
     int j = 0, g = 0, t0 = 0, ntok = 0, np = 0;
