@@ -790,7 +790,11 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     auto claim = [&]() -> int { return (int)blockIdx.x + atomicAdd(sm.claim, 1) * (int)gridDim.x; };
     int item = claim();
 #endif
-    int next = item < n_items ? claim() : n_items;
+    // The next item is claimed lazily, once half of the current item's pages
+    // are issued: a worker on a faster SM gets there sooner, which is what
+    // balances the device (claiming at the start would hand out every item
+    // before any work is done).  Its page ids then load in the background.
+    int next = -1;  // -1: not claimed yet
     int it = 0;
     int j = 0, g = 0, t0 = 0, ntok = 0, np = 0;
     int pg = 0;
@@ -802,7 +806,6 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         load_next(item);
 #pragma unroll
         for (int i = 0; i < kPagesPerItem; ++i) sm.pids[(w * 2 + 0) * kPagesPerItem + i] = nxt[i];
-        load_next(next);
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");  // pools may hold rows the previous kernel wrote
     if (w == 0) {
@@ -840,18 +843,21 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
                 HETIS_TS(3);
             }
         }
+        if (next < 0 && 2 * pg >= np) {
+            next = claim();
+            load_next(next);
+        }
         if (q_done && pg == np) {  // item fully issued: move to the claimed next item
             item = next;
+            next = -1;
             ++it;
             pg = 0;
             q_done = false;
             if (item < n_items) {
-                next = claim();
                 decode(item, j, g, t0, ntok);
                 np = (ntok + kP - 1) / kP;
 #pragma unroll
                 for (int i = 0; i < kPagesPerItem; ++i) sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + i] = nxt[i];
-                load_next(next);
             }
         }
     }
