@@ -200,6 +200,34 @@ HETIS_API hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_s
                                const int32_t *seq_lens, int32_t max_seq_len, void *o, void *workspace,
                                size_t workspace_bytes, uint32_t flags, hetis_stream_t stream);
 
+/* ---- combine fused with the O all-gather over peer memory -------------- */
+/* Kernel 2 (a5) and the gather (a6, Eq. 2a Concat) in ONE kernel:
+ * every merged row o[j][h] is stored straight into every rank's o_full at its
+ * GLOBAL head index q_head_begin + h (NVLink 5 / NVSwitch peer stores), then the
+ * last block publishes `epoch` into signal_peers[p][rank] of every rank p with a
+ * system-scope release store.  Same arithmetic as hetis_attn_combine.
+ *   o_full_peers : host array [num_ranks] of device pointers, rank p's o_full
+ *                  [num_seqs][H][head_dim] (o_dtype) as mapped in THIS process
+ *                  (own buffer at [rank]; peers via cudaIpcOpenMemHandle or any
+ *                  other peer mapping); rows o_seq_stride elements apart
+ *   signal_peers : host array [num_ranks] of device pointers to each rank's
+ *                  int64 signal array [num_ranks] (zero-initialised once)
+ *   epoch        : > every epoch previously published into these signals
+ *   workspace    : the hetis_attn_partial workspace of this step
+ * num_ranks <= 8.  The consumer of o_full must hetis_peer_wait first. */
+HETIS_API hetis_status hetis_attn_combine_peers(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
+                                                int32_t q_head_count, const int32_t *seq_lens, int32_t max_seq_len,
+                                                void *const *o_full_peers, int64_t o_seq_stride,
+                                                int64_t *const *signal_peers, int32_t num_ranks, int32_t rank,
+                                                int64_t epoch, void *workspace, size_t workspace_bytes,
+                                                hetis_stream_t stream);
+/* Stream-ordered wait (acquire) until signal_local[p] >= epoch for every rank p:
+ * after it, o_full holds every rank's rows of that epoch.  A rank that never
+ * signals makes the wait kernel trap after ~10 s (HETIS_E_CUDA on the stream)
+ * instead of hanging the device.  signal_local: device int64 [num_ranks]. */
+HETIS_API hetis_status hetis_peer_wait(const int64_t *signal_local, int32_t num_ranks, int64_t epoch,
+                                       hetis_stream_t stream);
+
 /* ---- scatter / gather over NCCL ------------------- */
 /* nccl_comm is an ncclComm_t (e.g. torch ProcessGroupNCCL._comm_ptr()) whose
  * ranks are the plan's devices.  libnccl.so.2 is resolved at first use from

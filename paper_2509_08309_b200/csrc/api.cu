@@ -422,6 +422,59 @@ hetis_status hetis_attn_combine(const hetis_shape *shape, int32_t num_seqs, int3
     return HETIS_OK;
 }
 
+hetis_status hetis_attn_combine_peers(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
+                                      int32_t q_head_count, const int32_t *seq_lens, int32_t max_seq_len,
+                                      void *const *o_full_peers, int64_t o_seq_stride, int64_t *const *signal_peers,
+                                      int32_t num_ranks, int32_t rank, int64_t epoch, void *workspace,
+                                      size_t workspace_bytes, hetis_stream_t stream) {
+    hetis_status st = check_shape(shape);
+    if (st != HETIS_OK) return st;
+    const int H = shape->num_q_heads, r = H / shape->num_kv_heads;
+    if (num_seqs < 0 || q_head_count < 1 || max_seq_len < 1) return fail(HETIS_E_INVALID, "bad sizes");
+    if (q_head_begin < 0 || q_head_begin + q_head_count > H) return fail(HETIS_E_INVALID, "head range outside [0, H)");
+    if (q_head_begin % r || q_head_count % r) return fail(HETIS_E_GROUP_ALIGN, "head range must cover whole kv groups");
+    if (num_ranks < 1 || num_ranks > hetis::kMaxPeers || rank < 0 || rank >= num_ranks)
+        return fail(HETIS_E_INVALID, "num_ranks must be 1..8 and rank inside it");
+    if (epoch < 1) return fail(HETIS_E_INVALID, "epoch must be >= 1");
+    if (!o_full_peers || !signal_peers || !workspace || (num_seqs > 0 && !seq_lens))
+        return fail(HETIS_E_INVALID, "NULL argument");
+    if (o_seq_stride < (int64_t)H * shape->head_dim) return fail(HETIS_E_INVALID, "o_seq_stride below H * head_dim");
+    const int oe = esize(shape->o_dtype);
+    hetis::PeerTargets t{};
+    for (int p = 0; p < num_ranks; ++p) {
+        if (!o_full_peers[p] || !signal_peers[p]) return fail(HETIS_E_INVALID, "NULL peer pointer");
+        if (!aligned(o_full_peers[p], 8) || (o_seq_stride * oe) % 8 || !aligned(signal_peers[p], 8))
+            return fail(HETIS_E_INVALID, "peer buffers must be 8-byte aligned");
+        t.o[p] = o_full_peers[p];
+        t.sig[p] = signal_peers[p];
+    }
+    if (!aligned(workspace, 256)) return fail(HETIS_E_WORKSPACE, "workspace must be 256-byte aligned");
+    hetis::WorkspaceLayout w = hetis::workspace_layout(num_seqs, q_head_count / r, r, shape->head_dim, max_seq_len);
+    if (workspace_bytes < w.total) return fail(HETIS_E_WORKSPACE, "workspace too small");
+    if (num_seqs == 0) return HETIS_OK;
+    uint8_t *ws = static_cast<uint8_t *>(workspace);
+    t.n = num_ranks;
+    t.rank = rank;
+    t.head0 = q_head_begin;
+    t.epoch = epoch;
+    t.o_seq_stride = o_seq_stride;
+    t.done = reinterpret_cast<int32_t *>(ws + w.counter_offset) + 2;
+    cudaError_t e = hetis::launch_combine_peers(
+        num_seqs, q_head_count, r, shape->head_dim, reinterpret_cast<const int32_t *>(ws + w.split_off_offset),
+        reinterpret_cast<const float *>(ws + w.lse_offset), reinterpret_cast<const float *>(ws + w.o_offset),
+        shape->o_dtype, t, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "combine_peers launch");
+    return HETIS_OK;
+}
+
+hetis_status hetis_peer_wait(const int64_t *signal_local, int32_t num_ranks, int64_t epoch, hetis_stream_t stream) {
+    if (!signal_local || num_ranks < 1 || num_ranks > 32 || epoch < 1) return fail(HETIS_E_INVALID, "bad arguments");
+    if (!aligned(signal_local, 8)) return fail(HETIS_E_INVALID, "signal array must be 8-byte aligned");
+    cudaError_t e = hetis::launch_peer_wait(signal_local, num_ranks, epoch, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "peer_wait launch");
+    return HETIS_OK;
+}
+
 hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin, int32_t q_head_count,
                                const void *q, const void *k_pool, const void *v_pool, int64_t num_pages,
                                const int32_t *block_table, int32_t max_pages, const int32_t *seq_lens,

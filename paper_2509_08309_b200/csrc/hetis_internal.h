@@ -63,6 +63,21 @@ cudaError_t launch_head_slice(const void *src, void *dst, int num_seqs, int src_
 cudaError_t launch_head_place(const void *src, void *dst, int num_seqs, int dst_heads, int h0, int n,
                               int row_bytes, cudaStream_t s);
 
+// Peer-memory targets of the fused combine + all-gather (at most kMaxPeers ranks).
+constexpr int kMaxPeers = 8;
+struct PeerTargets {
+    void *o[kMaxPeers];        // every rank's o_full [num_seqs][H][d], mapped in this process
+    int64_t *sig[kMaxPeers];   // every rank's signal array [n] (int64), mapped in this process
+    int n, rank, head0;
+    int64_t epoch;
+    int64_t o_seq_stride;      // elements between requests in o_full (>= H * d)
+    int32_t *done;             // block-completion counter (zero between calls)
+};
+cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim, const int32_t *split_off,
+                                 const float *part_lse, const float *part_o, int o_dtype, const PeerTargets &t,
+                                 cudaStream_t s);
+cudaError_t launch_peer_wait(const int64_t *sig, int n, int64_t epoch, cudaStream_t s);
+
 void note_launch();
 int num_sms();
 

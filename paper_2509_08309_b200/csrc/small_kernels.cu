@@ -40,16 +40,9 @@ __global__ void kv_append_kernel(int num_seqs, int kv_heads, int row_bytes, int 
 // ---------------------------------------------------------------- combine
 // o = sum_s 2^(lse_s - M) o_s / sum_s 2^(lse_s - M), M = max_s lse_s, s ascending.
 // One group of D/4 threads per (request, local query head); each thread owns 4 dims.
-template <int D, int OUT_BF16>
-__global__ void combine_kernel(int num_seqs, int q_heads, int r, const int32_t *seq_lens, const int32_t *split_off,
-                               const float *part_lse, const float *part_o, void *o, int64_t o_seq_stride) {
-    dev::pdl_wait_then_release();
-    constexpr int TPH = D / 4;  // threads per head
-    const int heads_per_block = blockDim.x / TPH;
-    const int hl = threadIdx.x / TPH, d4 = threadIdx.x % TPH;
-    const int64_t flat = (int64_t)blockIdx.x * heads_per_block + hl;
-    if (flat >= (int64_t)num_seqs * q_heads) return;
-    const int j = (int)(flat / q_heads), h = (int)(flat - (int64_t)j * q_heads);
+template <int D>
+__device__ __forceinline__ float4 combine_row(int j, int h, int q_heads, int r, const int32_t *split_off,
+                                              const float *part_lse, const float *part_o, int d4) {
     const int kv_heads = q_heads / r;
     const int g = h / r, rr = h - g * r;
     const int s0 = split_off[j];
@@ -75,14 +68,80 @@ __global__ void combine_kernel(int num_seqs, int q_heads, int r, const int32_t *
     acc.y = __fdiv_rn(acc.y, wsum);
     acc.z = __fdiv_rn(acc.z, wsum);
     acc.w = __fdiv_rn(acc.w, wsum);
-    const size_t base = (size_t)j * o_seq_stride + (size_t)h * D + 4 * d4;
+    return acc;
+}
+
+template <int OUT_BF16>
+__device__ __forceinline__ void store_row4(void *o, size_t idx, float4 acc) {
     if (OUT_BF16) {
         uint2 pk;
         pk.x = dev::pack_bf16x2(acc.x, acc.y);
         pk.y = dev::pack_bf16x2(acc.z, acc.w);
-        *reinterpret_cast<uint2 *>(static_cast<__nv_bfloat16 *>(o) + base) = pk;
+        *reinterpret_cast<uint2 *>(static_cast<__nv_bfloat16 *>(o) + idx) = pk;
     } else {
-        *reinterpret_cast<float4 *>(static_cast<float *>(o) + base) = acc;
+        *reinterpret_cast<float4 *>(static_cast<float *>(o) + idx) = acc;
+    }
+}
+
+template <int D, int OUT_BF16>
+__global__ void combine_kernel(int num_seqs, int q_heads, int r, const int32_t *seq_lens, const int32_t *split_off,
+                               const float *part_lse, const float *part_o, void *o, int64_t o_seq_stride) {
+    dev::pdl_wait_then_release();
+    constexpr int TPH = D / 4;  // threads per head
+    const int heads_per_block = blockDim.x / TPH;
+    const int hl = threadIdx.x / TPH, d4 = threadIdx.x % TPH;
+    const int64_t flat = (int64_t)blockIdx.x * heads_per_block + hl;
+    if (flat >= (int64_t)num_seqs * q_heads) return;
+    const int j = (int)(flat / q_heads), h = (int)(flat - (int64_t)j * q_heads);
+    const float4 acc = combine_row<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4);
+    store_row4<OUT_BF16>(o, (size_t)j * o_seq_stride + (size_t)h * D + 4 * d4, acc);
+}
+
+// Combine fused with the all-gather over peer memory (NVLink / NVSwitch): each
+// merged O row is stored straight into every rank's o_full at its GLOBAL head
+// index (Eq. 2a Concat), then the last block publishes `epoch` into every
+// rank's signal slot [rank] with a system-scope release store.
+template <int D, int OUT_BF16>
+__global__ void combine_peers_kernel(int num_seqs, int q_heads, int r, const int32_t *split_off, const float *part_lse,
+                                     const float *part_o, PeerTargets t) {
+    dev::pdl_wait_then_release();
+    constexpr int TPH = D / 4;
+    const int heads_per_block = blockDim.x / TPH;
+    const int hl = threadIdx.x / TPH, d4 = threadIdx.x % TPH;
+    const int64_t flat = (int64_t)blockIdx.x * heads_per_block + hl;
+    if (flat < (int64_t)num_seqs * q_heads) {
+        const int j = (int)(flat / q_heads), h = (int)(flat - (int64_t)j * q_heads);
+        const float4 acc = combine_row<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4);
+        const size_t idx = (size_t)j * t.o_seq_stride + (size_t)(t.head0 + h) * D + 4 * d4;
+        for (int p = 0; p < t.n; ++p) store_row4<OUT_BF16>(t.o[p], idx, acc);
+    }
+    __threadfence_system();  // this thread's peer stores are visible system-wide ...
+    __syncthreads();
+    if (threadIdx.x == 0) {  // ... before the block is counted
+        if (atomicAdd(t.done, 1) == (int)gridDim.x - 1) {
+            __threadfence_system();
+            for (int p = 0; p < t.n; ++p)
+                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(t.sig[p] + t.rank), "l"(t.epoch) : "memory");
+            *t.done = 0;  // self-cleaning for the next call
+        }
+    }
+}
+
+// Stream-ordered wait until every rank published `epoch` (acquire), bounded:
+// a peer that never signals traps after ~10 s instead of hanging the device.
+__global__ void peer_wait_kernel(const int64_t *sig, int n, int64_t epoch) {
+    if ((int)threadIdx.x < n) {
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+        for (;;) {
+            int64_t v;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(sig + threadIdx.x) : "memory");
+            if (v >= epoch) break;
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 10000000000ull) __trap();
+            __nanosleep(200);
+        }
     }
 }
 
@@ -145,6 +204,25 @@ cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const
                                 : (o_dtype == HETIS_BF16 ? combine_kernel<64, 1> : combine_kernel<64, 0>);
     return launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), 0, s, num_seqs, q_heads, r, seq_lens, split_off,
                       part_lse, part_o, o, o_seq_stride);
+}
+
+cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim, const int32_t *split_off,
+                                 const float *part_lse, const float *part_o, int o_dtype, const PeerTargets &t,
+                                 cudaStream_t s) {
+    const int64_t heads = (int64_t)num_seqs * q_heads;
+    if (heads == 0) return cudaSuccess;
+    const int threads = 128;
+    const int64_t blocks = (heads + threads / (head_dim / 4) - 1) / (threads / (head_dim / 4));
+    auto kern = head_dim == 128 ? (o_dtype == HETIS_BF16 ? combine_peers_kernel<128, 1> : combine_peers_kernel<128, 0>)
+                                : (o_dtype == HETIS_BF16 ? combine_peers_kernel<64, 1> : combine_peers_kernel<64, 0>);
+    return launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), 0, s, num_seqs, q_heads, r, split_off, part_lse,
+                      part_o, t);
+}
+
+cudaError_t launch_peer_wait(const int64_t *sig, int n, int64_t epoch, cudaStream_t s) {
+    peer_wait_kernel<<<1, 32, 0, s>>>(sig, n, epoch);
+    note_launch();
+    return cudaGetLastError();
 }
 
 static cudaError_t head_copy(const void *src, void *dst, int num_seqs, int src_heads, int hs, int dst_heads, int hd,

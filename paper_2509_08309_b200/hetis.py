@@ -30,7 +30,8 @@ ATTN_DIAG_STREAM_ONLY = 0x100
 EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_split_tokens",
             "hetis_plan_create", "hetis_plan_destroy", "hetis_plan_heads", "hetis_plan_num_devices", "hetis_plan_units",
             "hetis_plan_check_capacity", "hetis_kv_append", "hetis_attn_decode_workspace", "hetis_attn_partial",
-            "hetis_attn_combine", "hetis_attn_decode", "hetis_comm_workspace", "hetis_scatter_q", "hetis_gather",
+            "hetis_attn_combine", "hetis_attn_decode", "hetis_attn_combine_peers", "hetis_peer_wait",
+            "hetis_comm_workspace", "hetis_scatter_q", "hetis_gather",
             "hetis_launch_count")
 
 
@@ -82,6 +83,9 @@ def lib() -> ctypes.CDLL:
                 "hetis_attn_combine": (ctypes.c_int, [sp, i32, i32, vp, i32, vp, i64, vp, sz, vp]),
                 "hetis_attn_decode": (ctypes.c_int, [sp, i32, i32, i32, vp, vp, vp, i64, vp, i32, vp, i32, vp, vp,
                                                      sz, u32, vp]),
+                "hetis_attn_combine_peers": (ctypes.c_int, [sp, i32, i32, i32, vp, i32, P(vp), i64, P(vp), i32, i32,
+                                                            i64, vp, sz, vp]),
+                "hetis_peer_wait": (ctypes.c_int, [vp, i32, i64, vp]),
                 "hetis_comm_workspace": (ctypes.c_int, [vp, i32, i32, P(sz)]),
                 "hetis_scatter_q": (ctypes.c_int, [vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
                 "hetis_gather": (ctypes.c_int, [vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]),
@@ -252,6 +256,31 @@ def attn_decode(shape: CShape, q, k_pool, v_pool, block_table, seq_lens, max_seq
                                    block_table.shape[2], _dev(seq_lens, "seq_lens"), max_seq_len, _dev(o, "o"),
                                    _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(), flags,
                                    _stream(stream)), "hetis_attn_decode")
+
+
+# ---------------------------------------------------------------- combine fused with the peer all-gather
+def attn_combine_peers(shape: CShape, seq_lens, max_seq_len: int, o_full_peers, signal_peers, rank: int, epoch: int,
+                       workspace, q_head_begin: int, q_head_count: int, stream=None) -> None:
+    """Merge this rank's splits and store every row into every rank's o_full (peer memory), then publish `epoch`.
+
+    o_full_peers / signal_peers: per rank, tensors (or raw device pointers) mapped in this process."""
+    n = len(o_full_peers)
+    ptr = lambda t: t.data_ptr() if hasattr(t, "data_ptr") else int(t)
+    o_arr = (ctypes.c_void_p * n)(*[ptr(t) for t in o_full_peers])
+    s_arr = (ctypes.c_void_p * n)(*[ptr(t) for t in signal_peers])
+    o0 = o_full_peers[rank]
+    stride = o0.stride(0) if hasattr(o0, "stride") else shape.num_q_heads * shape.head_dim
+    B = seq_lens.shape[0]
+    _check(lib().hetis_attn_combine_peers(ctypes.byref(shape), B, q_head_begin, q_head_count,
+                                          _dev(seq_lens, "seq_lens"), max_seq_len, o_arr, stride, s_arr, n, rank,
+                                          epoch, _dev(workspace, "workspace"),
+                                          workspace.numel() * workspace.element_size(), _stream(stream)),
+           "hetis_attn_combine_peers")
+
+
+def peer_wait(signal_local, epoch: int, stream=None) -> None:
+    _check(lib().hetis_peer_wait(_dev(signal_local, "signal_local"), signal_local.numel(), epoch, _stream(stream)),
+           "hetis_peer_wait")
 
 
 # ---------------------------------------------------------------- NCCL scatter / gather

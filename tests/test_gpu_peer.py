@@ -1,0 +1,85 @@
+"""Fused combine + all-gather over peer memory (hetis_attn_combine_peers), two ranks.
+
+Only one GPU is reachable, so the two ranks are two processes on cuda:0 that map
+each other's o_full and signal arrays through CUDA IPC (torch.multiprocessing
+shares CUDA tensors that way) -- the same peer-pointer code path an 8-GPU box
+uses over NVLink, with the data staying on one device.  Each rank runs its own
+heads' attention and stores every merged row into BOTH ranks' o_full at the
+global head index (Eq. 2a Concat), then publishes the epoch.
+Host barriers order the two processes (kernels of two processes time-slice on
+one GPU, so no kernel spin-waits on the other process); hetis_peer_wait runs
+after the barrier and must see both signals.  Both ranks must end with the
+single-device result, bit for bit.
+"""
+from __future__ import annotations
+
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+LENS = (300, 17, 1029, 2048, 5, 256)
+
+
+def _rank(rank, split, shape_args, q_in, q_out, barrier, res):
+    import torch
+    from paper_2509_08309_b200 import hetis, workload
+    torch.cuda.set_device(0)
+    shape = workload.Shape(*shape_args)
+    lens = torch.tensor(LENS, dtype=torch.int32)
+    B, H, D = len(LENS), shape.num_q_heads, shape.head_dim
+    begin, count = sum(split[:rank]), split[rank]
+    o_full = torch.full((B, H, D), float("nan"), device="cuda")
+    sig = torch.zeros(2, dtype=torch.int64, device="cuda")
+    q_out.put((o_full, sig))                 # share my buffers with the peer (CUDA IPC)
+    peer_o, peer_sig = q_in.get(timeout=120)
+    o_peers = [o_full, peer_o] if rank == 0 else [peer_o, o_full]
+    s_peers = [sig, peer_sig] if rank == 0 else [peer_sig, sig]
+    b = workload.make_decode_batch(shape, lens, 13, "cuda", q_begin=begin, q_count=count, rank_salt=rank + 1)
+    s = hetis.make_shape(shape)
+    hetis.kv_append(s, b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens)
+    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, count, b.max_seq_len), "cuda")
+    for epoch in (1, 2):
+        hetis.attn_partial(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, b.max_seq_len, ws,
+                           q_head_begin=begin)
+        hetis.attn_combine_peers(s, b.seq_lens, b.max_seq_len, o_peers, s_peers, rank, epoch, ws,
+                                 q_head_begin=begin, q_head_count=count)
+        torch.cuda.synchronize()
+        barrier.wait(timeout=120)            # both ranks' stores and signals are done
+        hetis.peer_wait(sig, epoch)          # stream-ordered acquire; both signals already >= epoch
+        torch.cuda.synchronize()
+        got = o_full.clone()
+        barrier.wait(timeout=120)
+    # single-device reference on this process (all heads, the same generated data per kv head)
+    full = workload.make_decode_batch(shape, lens, 13, "cuda")
+    hetis.kv_append(s, full.k_new, full.v_new, full.k_pool, full.v_pool, full.block_table, full.seq_lens)
+    wsf = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, H, full.max_seq_len), "cuda")
+    ref = torch.empty((B, H, D), device="cuda")
+    hetis.attn_decode(s, full.q, full.k_pool, full.v_pool, full.block_table, full.seq_lens, full.max_seq_len, ref,
+                      wsf)
+    torch.cuda.synchronize()
+    res.put((rank, bool(torch.equal(got, ref)), float((got - ref).abs().nan_to_num(1e9).max()),
+             int(sig.cpu().min())))
+    barrier.wait(timeout=120)                # keep the shared buffers alive until both ranks are done
+
+
+@pytest.mark.parametrize("shape_args,split", [((64, 8, 128, 16, "bf16"), (48, 16)),
+                                              ((40, 40, 128, 16, "bf16"), (24, 16))])
+def test_combine_peers_two_ranks_one_gpu(shape_args, split):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    a2b, b2a, res = ctx.Queue(), ctx.Queue(), ctx.Queue()
+    barrier = ctx.Barrier(2)
+    ps = [ctx.Process(target=_rank, args=(0, split, shape_args, b2a, a2b, barrier, res)),
+          ctx.Process(target=_rank, args=(1, split, shape_args, a2b, b2a, barrier, res))]
+    for p in ps:
+        p.start()
+    out = [res.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, equal, diff, sig_min in out:
+        assert sig_min == 2, (rank, sig_min)
+        assert equal, (rank, diff)
