@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--o-dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--attn-flags", type=int, default=0, help="HETIS_ATTN_* flags (diagnostics)")
     ap.add_argument("--graph", type=int, default=1, help="N = 1: replay the K timed steps as one CUDA graph")
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1: NCCL all-gather of O (default) or the combine kernel's peer-memory stores")
     return ap.parse_args()
 
 
@@ -254,6 +256,8 @@ def run_ours(args, world, rank, local):
         vn_full = (torch.randn((B, shape.num_kv_heads, shape.head_dim), generator=gq, device=device)
                    .to(shape.torch_dtype) if is_root else None)
         o_full = torch.empty((B, shape.num_q_heads, shape.head_dim), dtype=odt, device=device)
+        if args.gather == "peer":
+            step.setup_peers(o_full)
     else:
         step.buf.q_shard.copy_(batch.q)
         step.buf.k_new.copy_(batch.k_new)
@@ -273,6 +277,13 @@ def run_ours(args, world, rank, local):
                            flags=args.attn_flags)
         if ev_b is not None:
             ev_b.record(torch.cuda.current_stream(device))
+        if world > 1 and args.gather == "peer":
+            # one kernel merges the splits and stores O into every rank's o_full over NVLink
+            step.epoch += 1
+            hetis.attn_combine_peers(step.cshape, batch.seq_lens, max_len, step.o_peers, step.sig_peers, rank,
+                                     step.epoch, step.buf.workspace, q_head_begin=q_begin, q_head_count=q_count)
+            hetis.peer_wait(step.sig, step.epoch)
+            return
         hetis.attn_combine(step.cshape, batch.seq_lens, max_len, step.buf.o_shard, step.buf.workspace,
                            q_head_count=q_count)
         if world > 1:
@@ -428,6 +439,7 @@ def run_ours(args, world, rank, local):
                 "seq_len_range": cfg.seq_len_range, "q_heads": shape.num_q_heads, "kv_heads": shape.num_kv_heads,
                 "head_dim": shape.head_dim, "page_size": shape.page_size, "split": list(split),
                 "o_dtype": args.o_dtype, "layers_rotated": n_layers,
+                "gather": (args.gather if world > 1 else None),
                 "l2": f"inputs larger than L2: {n_layers} layer pool(s) x {kv_bytes_rank / 1e6:.1f} MB KV per rank "
                       f"rotated per step (L2 = 126 MB)",
                 "tokens": "one token = one request's decode step of one layer, all heads"},

@@ -91,3 +91,36 @@ class DecodeStep:
     def gather(self, o_full, root: int = -1, stream=None):
         hetis.gather(self.plan, self.comm_ptr, self.rank, root, self.num_seqs, self.buf.o_shard, o_full,
                      self.buf.comm_ws, stream)
+
+    # ---- fused combine + all-gather over peer memory (NVLink), see hetis_attn_combine_peers
+    def setup_peers(self, o_full: torch.Tensor) -> None:
+        """Map every rank's o_full and signal array into this process (CUDA IPC handles exchanged with
+        torch.distributed; on one NVSwitch box the mappings are NVLink peer memory).  Collective."""
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.o_full = o_full
+        self.sig = torch.zeros(self.world, dtype=torch.int64, device=self.device)
+        mine = (reduce_tensor(o_full), reduce_tensor(self.sig))
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, mine)
+        self.o_peers, self.sig_peers = [], []
+        for i, (ro, rs) in enumerate(everyone):
+            if i == self.rank:
+                self.o_peers.append(o_full)
+                self.sig_peers.append(self.sig)
+            else:
+                self.o_peers.append(ro[0](*ro[1]))
+                self.sig_peers.append(rs[0](*rs[1]))
+        self.epoch = 0
+
+    def attention_gather_peers(self, k_pool, v_pool, block_table, seq_lens, stream=None, flags: int = 0):
+        """Partial attention, then ONE kernel that merges the splits and stores every row into every
+        rank's o_full; returns after a stream-ordered wait for all ranks' rows of this step."""
+        self.epoch += 1
+        hetis.attn_partial(self.cshape, self.buf.q_shard, k_pool, v_pool, block_table, seq_lens, self.max_seq_len,
+                           self.buf.workspace, q_head_begin=self.q_begin, flags=flags, stream=stream)
+        hetis.attn_combine_peers(self.cshape, seq_lens, self.max_seq_len, self.o_peers, self.sig_peers, self.rank,
+                                 self.epoch, self.buf.workspace, q_head_begin=self.q_begin,
+                                 q_head_count=self.q_count, stream=stream)
+        hetis.peer_wait(self.sig, self.epoch, stream=stream)
+        return self.o_full
