@@ -254,6 +254,42 @@ HETIS_API hetis_status hetis_gather(const hetis_plan *plan, void *nccl_comm, int
                           const void *o_shard, void *o_full, void *workspace, size_t workspace_bytes,
                           hetis_stream_t stream);
 
+/* ---- head-granular KV migration (the Hauler) ------- */
+/* Re-dispatching a request moves only the kv-head groups whose device changes
+ * ("only partial cache transmission"): each moved (request, kv
+ * head) is a block-table ROW on the source and one on the destination, and its
+ * cache is the ceil(num_tokens / P) pages those rows list.  For every entry e
+ * and page k < ceil(entries[e].num_tokens / P):
+ *   dst_pool[dst_block_table[dst_row][k]] <- src_pool[src_block_table[src_row][k]]
+ * for both the K and the V pool -- a bit-exact copy of whole pages (the slots
+ * past num_tokens in the last page receive the source page's bytes).
+ *   entries        : device [num_entries] hetis_migration_entry; src_row indexes
+ *                    the rows of src_block_table ([rows][src_max_pages]), dst_row
+ *                    those of dst_block_table ([rows][dst_max_pages])
+ *   src_*_pool     : [pages][page_size][head_dim] kv_dtype, 16-B aligned, readable
+ *                    by the executing device (local, or a peer mapping: pull)
+ *   dst_*_pool     : same layout, writable by the executing device (local, or a
+ *                    peer mapping over NVLink: push)
+ *   the tables and entries must be readable by the executing device; the
+ *   destination pages are allocated by the caller (as for kv_append) and must
+ *   not overlap any source page of the same call.
+ *   max_ctas       : CTAs the copy may occupy (0 = 2 per SM).  The Hauler runs
+ *                    this on a low-priority stream while decode runs (PAPER.md:
+ *                    545); max_ctas bounds its share of the SMs.
+ * num_entries <= 16384 (else HETIS_E_INVALID); 0 launches nothing.  Row and
+ * page ids are contracts on device data (not checked). */
+typedef struct {
+    int32_t src_row;     /* row of src_block_table */
+    int32_t dst_row;     /* row of dst_block_table */
+    int32_t num_tokens;  /* cached tokens of this (request, kv head): L_j */
+} hetis_migration_entry;
+HETIS_API hetis_status hetis_kv_migrate(const hetis_shape *shape, int32_t num_entries,
+                                        const hetis_migration_entry *entries, const void *src_k_pool,
+                                        const void *src_v_pool, const int32_t *src_block_table,
+                                        int32_t src_max_pages, void *dst_k_pool, void *dst_v_pool,
+                                        const int32_t *dst_block_table, int32_t dst_max_pages, int32_t max_ctas,
+                                        hetis_stream_t stream);
+
 /* Number of kernels this library has launched in the calling process (all
  * threads) -- for the bench's gpu_launches accounting. */
 HETIS_API uint64_t hetis_launch_count(void);

@@ -61,8 +61,9 @@ def _load():
                                                                i32, i32, i32, i32, dp, dp]
             lib.oracle_kv_append.argtypes = [i32] * 5 + [vp, vp, vp, vp, i64, vp, i32, vp]
             lib.oracle_lse_merge_f64.argtypes = [i32, i32, dp, dp, dp, dp]
+            lib.oracle_kv_migrate.argtypes = [i32, vp, i32, i32, i32, vp, vp, i64, vp, i32, vp, vp, i64, vp, i32]
             for f in (lib.oracle_decode_f64, lib.oracle_decode_pairs_f64, lib.oracle_decode_range_f64,
-                      lib.oracle_kv_append, lib.oracle_lse_merge_f64):
+                      lib.oracle_kv_append, lib.oracle_lse_merge_f64, lib.oracle_kv_migrate):
                 f.restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -172,3 +173,19 @@ def kv_append(k_new, v_new, k_pool, v_pool, block_table, seq_lens) -> None:
     eb = k_pool.dtype.itemsize
     _check(_load().oracle_kv_append(B, Hkv, D, P, eb, _ptr(k_new), _ptr(v_new), _ptr(k_pool), _ptr(v_pool),
                                     num_pages, _ptr(bt), bt.shape[2], _ptr(sl)))
+
+
+def kv_migrate(entries, src_k, src_v, src_bt, dst_k, dst_v, dst_bt) -> None:
+    """Token-by-token copy of migrated (request, kv head) caches, in place on
+    dst_k / dst_v.  entries: int32 [n][3] (src_row, dst_row, num_tokens); tables are [rows][max_pages]
+    (any leading shape, flattened); pools [num_pages][P][D], same element type (uint16 / float32)."""
+    assert dst_k.flags.c_contiguous and dst_v.flags.c_contiguous
+    en = np.ascontiguousarray(entries, dtype=np.int32).reshape(-1, 3)
+    src_k, src_v = np.ascontiguousarray(src_k), np.ascontiguousarray(src_v)
+    sbt = np.ascontiguousarray(src_bt, dtype=np.int32)
+    dbt = np.ascontiguousarray(dst_bt, dtype=np.int32)
+    _, P, D = src_k.shape
+    assert dst_k.shape[1:] == (P, D) and src_k.dtype == dst_k.dtype
+    _check(_load().oracle_kv_migrate(en.shape[0], _ptr(en), D, P, src_k.dtype.itemsize, _ptr(src_k), _ptr(src_v),
+                                     src_k.shape[0], _ptr(sbt), sbt.shape[-1], _ptr(dst_k), _ptr(dst_v),
+                                     dst_k.shape[0], _ptr(dbt), dbt.shape[-1]))

@@ -320,3 +320,38 @@ int oracle_decode_range_f64(int B, int H, int Hkv, int D, int P, int dtype,
     free(scores);
     return ORACLE_OK;
 }
+
+/*
+ * Head-granular KV migration (the Hauler, "only partial cache
+ * transmission", :545): the cache of one (request, kv head) is the token rows
+ * its block-table row lists.  For every entry e = (src_row, dst_row, n) and
+ * every token t < n, the destination row's token t receives the source row's
+ * token t:
+ *   dst_pool[dst_bt[dst_row][t / P]][t mod P][:] = src_pool[src_bt[src_row][t / P]][t mod P][:]
+ * for the K and the V pool.  Token-by-token byte copy (slots past n untouched).
+ * entries: [num_entries][3] int32.
+ */
+int oracle_kv_migrate(int num_entries, const int32_t *entries, int D, int P, int elem_bytes,
+                      const void *src_k, const void *src_v, int64_t src_pages, const int32_t *src_bt,
+                      int src_max_pages, void *dst_k, void *dst_v, int64_t dst_pages, const int32_t *dst_bt,
+                      int dst_max_pages) {
+    if (num_entries < 0 || D < 1 || P < 1 || (elem_bytes != 2 && elem_bytes != 4)) return ORACLE_E_ARG;
+    if (num_entries == 0) return ORACLE_OK;
+    if (!entries || !src_k || !src_v || !src_bt || !dst_k || !dst_v || !dst_bt) return ORACLE_E_ARG;
+    const size_t row_bytes = (size_t)D * (size_t)elem_bytes;
+    for (int e = 0; e < num_entries; ++e) {
+        const int src_row = entries[3 * e], dst_row = entries[3 * e + 1], n = entries[3 * e + 2];
+        if (src_row < 0 || dst_row < 0 || n < 0) return ORACLE_E_ARG;
+        if (n > src_max_pages * P || n > dst_max_pages * P) return ORACLE_E_LEN;
+        for (int t = 0; t < n; ++t) {
+            const int32_t sp = src_bt[(int64_t)src_row * src_max_pages + t / P];
+            const int32_t dp = dst_bt[(int64_t)dst_row * dst_max_pages + t / P];
+            if (sp < 0 || sp >= src_pages || dp < 0 || dp >= dst_pages) return ORACLE_E_PAGE;
+            const size_t so = ((size_t)sp * P + (size_t)(t % P)) * row_bytes;
+            const size_t d0 = ((size_t)dp * P + (size_t)(t % P)) * row_bytes;
+            memcpy((char *)dst_k + d0, (const char *)src_k + so, row_bytes);
+            memcpy((char *)dst_v + d0, (const char *)src_v + so, row_bytes);
+        }
+    }
+    return ORACLE_OK;
+}

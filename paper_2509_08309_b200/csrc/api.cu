@@ -311,6 +311,31 @@ hetis_status hetis_kv_append(const hetis_shape *shape, int32_t num_seqs, int32_t
     return HETIS_OK;
 }
 
+// ---------------------------------------------------------------- migration (f4)
+hetis_status hetis_kv_migrate(const hetis_shape *shape, int32_t num_entries, const hetis_migration_entry *entries,
+                              const void *src_k_pool, const void *src_v_pool, const int32_t *src_block_table,
+                              int32_t src_max_pages, void *dst_k_pool, void *dst_v_pool,
+                              const int32_t *dst_block_table, int32_t dst_max_pages, int32_t max_ctas,
+                              hetis_stream_t stream) {
+    hetis_status st = check_shape(shape);
+    if (st != HETIS_OK) return st;
+    if (num_entries < 0 || num_entries > 16384) return fail(HETIS_E_INVALID, "num_entries must be in [0, 16384]");
+    if (src_max_pages < 1 || dst_max_pages < 1 || max_ctas < 0) return fail(HETIS_E_INVALID, "bad sizes");
+    if (num_entries == 0) return HETIS_OK;
+    if (!entries || !src_k_pool || !src_v_pool || !src_block_table || !dst_k_pool || !dst_v_pool || !dst_block_table)
+        return fail(HETIS_E_INVALID, "NULL pointer");
+    if (!aligned(src_k_pool, 16) || !aligned(src_v_pool, 16) || !aligned(dst_k_pool, 16) || !aligned(dst_v_pool, 16) ||
+        !aligned(entries, 4))
+        return fail(HETIS_E_INVALID, "pools must be 16-byte aligned");
+    const int page_bytes = shape->page_size * shape->head_dim * esize(shape->kv_dtype);
+    cudaError_t e = hetis::launch_kv_migrate(num_entries, entries, shape->page_size, page_bytes, src_k_pool,
+                                             src_v_pool, src_block_table, src_max_pages, dst_k_pool, dst_v_pool,
+                                             dst_block_table, dst_max_pages, max_ctas,
+                                             reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "kv_migrate launch");
+    return HETIS_OK;
+}
+
 // ---------------------------------------------------------------- attention
 hetis_status hetis_attn_decode_workspace(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_count,
                                          int32_t max_seq_len, size_t *bytes) {

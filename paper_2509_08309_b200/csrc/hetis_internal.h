@@ -77,6 +77,10 @@ cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim,
                                  const float *part_lse, const float *part_o, int o_dtype, const PeerTargets &t,
                                  cudaStream_t s);
 cudaError_t launch_peer_wait(const int64_t *sig, int n, int64_t epoch, cudaStream_t s);
+cudaError_t launch_kv_migrate(int num_entries, const hetis_migration_entry *entries, int page_size, int page_bytes,
+                              const void *src_k, const void *src_v, const int32_t *src_bt, int src_max_pages,
+                              void *dst_k, void *dst_v, const int32_t *dst_bt, int dst_max_pages, int max_ctas,
+                              cudaStream_t s);
 
 void note_launch();
 int num_sms();

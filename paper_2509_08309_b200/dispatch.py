@@ -294,3 +294,62 @@ def brute_force_optimum(devices: list[DeviceState], lens, H: int, r: int) -> flo
 def plan_rows(x: np.ndarray) -> list[int]:
     """Flatten a [N][J] allocation into hetis_plan_create(per_request=1)'s [J][N] row-major x."""
     return [int(v) for v in np.asarray(x).T.reshape(-1)]
+
+
+# ---------------------------------------------------------------- re-dispatch migration (row f4)
+def group_owners(x_row, r: int) -> np.ndarray:
+    """Device of every kv group of one request under a plan row x_i (i = device): device i owns the
+    contiguous head range [b_i, b_i + x_i), b_i = sum_{i' < i} x_i' (reading 3), i.e. groups
+    [b_i / r, (b_i + x_i) / r)."""
+    x = np.asarray(x_row, dtype=np.int64)
+    if (x < 0).any() or (x % r).any():
+        raise ValueError("head counts must be non-negative multiples of r (PAPER.md:454)")
+    return np.repeat(np.arange(len(x)), x // r)
+
+
+@dataclass
+class Migration:
+    """KV movement of one re-dispatched request ("only partial cache transmission").
+
+    moves  : (kv group g, source device, destination device), ascending g -- the groups whose
+             owner changes; every other group's pages stay where they are (reused)
+    reused : number of kv groups that stay on their device
+    """
+    moves: list[tuple[int, int, int]]
+    reused: int
+
+    def moved_bytes(self, seq_len: int, head_dim: int, elem_bytes: int, n_layers: int = 1) -> int:
+        """K and V bytes the moves transfer: groups x L tokens x 2 x d x elem x layers."""
+        return len(self.moves) * seq_len * 2 * head_dim * elem_bytes * n_layers
+
+
+def plan_migration(old_row, new_row, r: int) -> Migration:
+    """Groups of one request that must move when its plan row changes from old_row to new_row.
+
+    Under contiguous head ranges (reading 3) a device keeps exactly the groups in the intersection
+    of its old and new ranges.  sum_i min(old_i, new_i) / r is an upper bound on the reuse, reached
+    for two devices and whenever the ranges nest; reading 17 in DESIGN.md."""
+    old, new = np.asarray(old_row, dtype=np.int64), np.asarray(new_row, dtype=np.int64)
+    if old.shape != new.shape:
+        raise ValueError("plans cover different device counts")
+    if old.sum() != new.sum():
+        raise ValueError("old and new rows must both sum to H (Eq. 5)")
+    o, n = group_owners(old, r), group_owners(new, r)
+    moves = [(int(g), int(o[g]), int(n[g])) for g in range(len(o)) if o[g] != n[g]]
+    return Migration(moves=moves, reused=int((o == n).sum()))
+
+
+def migration_entries(old_units: list[list[tuple[int, int]]], new_units: list[list[tuple[int, int]]],
+                      migrations: dict[int, Migration], seq_lens) -> dict[tuple[int, int], np.ndarray]:
+    """hetis_kv_migrate entries per (source, destination) device pair.
+
+    old_units / new_units: per device, the (request, global kv group) units of the old / new
+    per-request plan (hetis_plan_units order = block-table row order, one row per unit).
+    migrations: request -> Migration.  Returns {(src, dst): int32 [n][3] (src_row, dst_row, L_j)}."""
+    old_row = [{u: k for k, u in enumerate(units)} for units in old_units]
+    new_row = [{u: k for k, u in enumerate(units)} for units in new_units]
+    out: dict[tuple[int, int], list[list[int]]] = {}
+    for j in sorted(migrations):
+        for g, src, dst in migrations[j].moves:
+            out.setdefault((src, dst), []).append([old_row[src][(j, g)], new_row[dst][(j, g)], int(seq_lens[j])])
+    return {k: np.asarray(v, dtype=np.int32) for k, v in out.items()}

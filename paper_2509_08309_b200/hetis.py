@@ -31,7 +31,7 @@ EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_
             "hetis_plan_create", "hetis_plan_destroy", "hetis_plan_heads", "hetis_plan_num_devices", "hetis_plan_units",
             "hetis_plan_check_capacity", "hetis_kv_append", "hetis_attn_decode_workspace", "hetis_attn_partial",
             "hetis_attn_combine", "hetis_attn_decode", "hetis_attn_combine_peers", "hetis_peer_wait",
-            "hetis_comm_workspace", "hetis_scatter_q", "hetis_gather",
+            "hetis_comm_workspace", "hetis_scatter_q", "hetis_gather", "hetis_kv_migrate",
             "hetis_launch_count")
 
 
@@ -89,6 +89,7 @@ def lib() -> ctypes.CDLL:
                 "hetis_comm_workspace": (ctypes.c_int, [vp, i32, i32, P(sz)]),
                 "hetis_scatter_q": (ctypes.c_int, [vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
                 "hetis_gather": (ctypes.c_int, [vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]),
+                "hetis_kv_migrate": (ctypes.c_int, [sp, i32, vp, vp, vp, vp, i32, vp, vp, vp, i32, i32, vp]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)
@@ -207,6 +208,21 @@ def kv_append(shape: CShape, k_new, v_new, k_pool, v_pool, block_table, seq_lens
                                  _dev(k_pool, "k_pool"), _dev(v_pool, "v_pool"), k_pool.shape[0],
                                  _dev(block_table, "block_table"), block_table.shape[2], _dev(seq_lens, "seq_lens"),
                                  _stream(stream)), "hetis_kv_append")
+
+
+def kv_migrate(shape: CShape, entries, src_k_pool, src_v_pool, src_block_table, dst_k_pool, dst_v_pool,
+               dst_block_table, max_ctas: int = 0, stream=None) -> None:
+    """Head-granular KV migration (hetis_kv_migrate).  entries: device int32 [n][3] rows of
+    (src_row, dst_row, num_tokens); the block tables are viewed as [rows][max_pages] (their last
+    dimension is max_pages).  Pools may be peer mappings (CUDA IPC) of another device's pools."""
+    if entries.dtype != torch.int32 or entries.dim() != 2 or entries.shape[1] != 3 or not entries.is_contiguous():
+        raise ValueError("entries must be a contiguous int32 [n][3] tensor")
+    _check(lib().hetis_kv_migrate(ctypes.byref(shape), entries.shape[0], _dev(entries, "entries"),
+                                  _dev(src_k_pool, "src_k_pool"), _dev(src_v_pool, "src_v_pool"),
+                                  _dev(src_block_table, "src_block_table"), src_block_table.shape[-1],
+                                  _dev(dst_k_pool, "dst_k_pool"), _dev(dst_v_pool, "dst_v_pool"),
+                                  _dev(dst_block_table, "dst_block_table"), dst_block_table.shape[-1], max_ctas,
+                                  _stream(stream)), "hetis_kv_migrate")
 
 
 def attn_decode_workspace(shape: CShape, num_seqs: int, q_head_count: int, max_seq_len: int) -> int:

@@ -29,7 +29,7 @@ def declared_symbols():
 
 def test_every_declared_symbol_is_exported(L):
     syms = declared_symbols()
-    assert len(syms) == 21
+    assert len(syms) == 22
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(hetis.EXPORTED)
@@ -179,6 +179,26 @@ def test_kv_append_and_combine_validation(L):
     assert rc == 0                                                          # empty batch
     rc = L.hetis_attn_combine(ctypes.byref(s), 4, 8, vp_(64), 128, vp_(4096), 8 * 64 - 1, vp_(512), 1 << 30, vp_(0))
     assert rc == 1                                                          # stride below a dense row
+
+
+def test_kv_migrate_validation(L):
+    vp_ = ctypes.c_void_p
+    s = hetis.make_shape(workload.Shape(8, 8, 128, 16, "bf16"))
+    ok = [vp_(4096), vp_(8192), vp_(1 << 20), vp_(64), 8, vp_(2 << 20), vp_(3 << 20), vp_(128), 8, 0, vp_(0)]
+    assert L.hetis_kv_migrate(ctypes.byref(s), 0, None, *([None] * 3), 8, None, None, None, 8, 0, vp_(0)) == 0
+    assert L.hetis_kv_migrate(ctypes.byref(s), 16385, *ok) == 1               # above the entry cap
+    assert L.hetis_kv_migrate(ctypes.byref(s), -1, *ok) == 1
+    bad = list(ok)
+    bad[1] = vp_(8192 + 8)
+    assert L.hetis_kv_migrate(ctypes.byref(s), 4, *bad) == 1                 # misaligned source K pool
+    bad = list(ok)
+    bad[6] = None
+    assert L.hetis_kv_migrate(ctypes.byref(s), 4, *bad) == 1                 # NULL destination V pool
+    bad = list(ok)
+    bad[9] = -1
+    assert L.hetis_kv_migrate(ctypes.byref(s), 4, *bad) == 1                 # negative CTA budget
+    s2 = hetis.make_shape(workload.Shape(8, 8, 96, 16, "bf16"))
+    assert L.hetis_kv_migrate(ctypes.byref(s2), 4, *ok) == 5                 # head_dim not built
 
 
 def test_nccl_calls_validate_plan_and_comm(L):

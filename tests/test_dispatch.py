@@ -6,9 +6,13 @@ enumeration on small instances.
 """
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
 import pytest
 
+from paper_2509_08309_b200 import dispatch
 from paper_2509_08309_b200 import dispatch as dp
 from paper_2509_08309_b200 import hetis
 
@@ -139,3 +143,73 @@ def test_small_instance_optimality_against_exhaustive_enumeration():
         assert out.objective <= opt + slack + 1e-12
         exact += out.objective <= opt * (1 + 1e-9)
     assert exact / trials >= 0.85, exact / trials      # measured 0.91 over 300 instances
+
+
+# ---------------------------------------------------------------- re-dispatch migration (f4)
+def test_plan_migration_golden_examples():
+    """SPEC.md:407-418 examples (identity, full move with its byte count, overlap count)."""
+    with open(os.path.join(os.path.dirname(__file__), "golden", "migration_plans.json")) as f:
+        gx = json.load(f)
+    for c in gx["cases"]:
+        m = dispatch.plan_migration(c["old"], c["new"], c["r"])
+        assert len(m.moves) == c["moved"] and m.reused == c["reused"], c
+        pairs = {}
+        for _, s, d in m.moves:
+            pairs[f"{s}->{d}"] = pairs.get(f"{s}->{d}", 0) + 1
+        assert pairs == c["pairs"], c
+        if "moved_bytes" in c:
+            assert m.moved_bytes(c["seq_len"], c["head_dim"], c["elem_bytes"], c["n_layers"]) == c["moved_bytes"]
+
+
+def _owners_brute(x, r):
+    """Owner of each kv group by walking the heads one by one (independent of group_owners)."""
+    own, dev, left = [], 0, list(x)
+    for h in range(sum(x)):
+        while left[dev] == 0:
+            dev += 1
+        left[dev] -= 1
+        if h % r == 0:
+            own.append(dev)
+    return own
+
+
+def test_plan_migration_conservation_and_reuse_bound():
+    """moved + reused = H / r; reuse <= sum_i min(old_i, new_i) / r, with equality for two devices
+    (SPEC.md's set-difference invariant) -- checked on every allocation pair of small instances."""
+    import itertools
+    for N, H, r in ((2, 8, 1), (2, 16, 4), (3, 6, 1), (4, 8, 2)):
+        rows = [x for x in itertools.product(range(0, H + 1, r), repeat=N) if sum(x) == H]
+        for old in rows:
+            for new in rows:
+                m = dispatch.plan_migration(old, new, r)
+                ob, nb = _owners_brute(old, r), _owners_brute(new, r)
+                assert [g for g, _, _ in m.moves] == [g for g in range(H // r) if ob[g] != nb[g]]
+                assert all(ob[g] == s and nb[g] == d for g, s, d in m.moves)
+                assert len(m.moves) + m.reused == H // r
+                bound = sum(min(a, b) for a, b in zip(old, new)) // r
+                assert m.reused <= bound
+                if N == 2:
+                    assert m.reused == bound
+
+
+def test_plan_migration_rejects_inconsistent_rows():
+    with pytest.raises(ValueError):
+        dispatch.plan_migration([8, 0], [4, 2], 1)         # sums differ (Eq. 5)
+    with pytest.raises(ValueError):
+        dispatch.plan_migration([6, 2], [4, 4], 4)         # not multiples of r (PAPER.md:454)
+
+
+def test_migration_entries_follow_plan_unit_rows():
+    """Entries index the units of the old plan on the source and of the new plan on the destination
+    (hetis_plan_units order: requests ascending, kv groups ascending)."""
+    r = 1
+    old = np.array([[4, 0], [2, 2], [0, 4]]).T                 # [N][J]
+    new = old.copy()
+    new[:, 1] = [0, 4]                                         # request 1 re-dispatched to device 1
+    units = lambda x: [[(j, g) for j in range(x.shape[1]) for g in range(4)
+                        if dispatch.group_owners(x[:, j], r)[g] == i] for i in range(2)]
+    mig = {1: dispatch.plan_migration(old[:, 1], new[:, 1], r)}
+    ent = dispatch.migration_entries(units(old), units(new), mig, [10, 33, 7])
+    assert list(ent) == [(0, 1)]
+    # old device 0 units: (0,0..3), (1,0), (1,1) -> rows 4, 5; new device 1 units: (1,0..3), (2,0..3)
+    assert ent[(0, 1)].tolist() == [[4, 0, 33], [5, 1, 33]]

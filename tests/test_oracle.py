@@ -367,3 +367,39 @@ def test_comm_volume_eq4():
     # Eq. 4: d = (2 + 2/r) h; MHA r = 1 -> 4h, GQA r = 8 -> 2.25h
     assert accounting.comm_head_vectors(8, 8) == 18.0
     assert accounting.comm_head_vectors(5, 1) == 20.0
+
+
+def test_kv_migrate_hand_worked_example():
+    """Token-order-preserving head-granular migration against a hand-derived result (golden)."""
+    with open(os.path.join(GOLDEN, "kv_migrate_example.json")) as f:
+        gx = json.load(f)
+    src_k = np.array(gx["src_k"], np.float32)[..., None]            # [pages][P][1]
+    src_v = -src_k
+    dst_k = np.full((4, gx["page_size"], 1), gx["dst_init"], np.float32)
+    dst_v = dst_k.copy()
+    oracle.kv_migrate(np.array(gx["entries"], np.int32), src_k, src_v, np.array(gx["src_bt"], np.int32),
+                      dst_k, dst_v, np.array(gx["dst_bt"], np.int32))
+    exp = np.array(gx["expected_dst_k"], np.float32)
+    assert np.array_equal(dst_k[..., 0], exp)
+    assert np.array_equal(dst_v[..., 0], -exp)
+
+
+def test_kv_migrate_then_decode_equals_decode_in_place():
+    """Moving every (request, kv head) to a freshly permuted pool leaves Eq. 2b's result unchanged."""
+    b = small_batch(H=8, Hkv=2, D=8, dtype="bf16", lens=(1, 16, 17, 40), seed=55)
+    hb = host_batch(b)
+    B, G, mp = hb["block_table"].shape
+    rng = np.random.default_rng(3)
+    npg = hb["k_pool"].shape[0]
+    perm = rng.permutation(npg).astype(np.int32)
+    dst_bt = np.where(hb["block_table"] >= 0, perm[np.maximum(hb["block_table"], 0)], -1).astype(np.int32)
+    dst_bt = dst_bt[::-1].copy()                                   # requests stored in reverse row order
+    lens = hb["seq_lens"]
+    entries = [[j * G + g, (B - 1 - j) * G + g, int(lens[j])] for j in range(B) for g in range(G)]
+    dk = np.full_like(hb["k_pool"], workload.NAN_BF16)
+    dv = np.full_like(hb["v_pool"], workload.NAN_BF16)
+    oracle.kv_migrate(np.array(entries, np.int32), hb["k_pool"], hb["v_pool"], hb["block_table"], dk, dv, dst_bt)
+    ref = oracle.decode(hb["q"], hb["k_pool"], hb["v_pool"], hb["block_table"], lens, num_kv_heads=G,
+                        dtype=oracle.BF16)
+    got = oracle.decode(hb["q"][::-1].copy(), dk, dv, dst_bt, lens[::-1].copy(), num_kv_heads=G, dtype=oracle.BF16)
+    assert np.array_equal(got[::-1], ref)
