@@ -34,9 +34,13 @@
  *   table is [num_seqs][x / r][max_pages] with local kv head g - b / r.
  *   Global head ids appear only in plans, scatter and gather.
  * - Device-data contracts (not checked per call, as in vLLM): every page id a
- *   kernel reads is in [0, num_pages); 1 <= seq_lens[j] <= min(max_seq_len,
+ *   kernel reads is in [0, num_pages); 0 <= seq_lens[j] <= min(max_seq_len,
  *   max_pages * page_size).  Table entries past ceil(L_j / page_size) and
  *   pool slots past L_j are never read into a result (they may hold NaN).
+ *   L_j = 0 is meaningful only on a device that holds none of request j's
+ *   tokens under a sequence split (row f3): kv_append skips the request, the
+ *   combine writes o = 0 (and lse = -inf).  Softmax over no token is
+ *   undefined (reading 10), so a whole-request result needs L_j >= 1.
  * - Builds: head_dim in {64, 128}; page_size 16; kv/q dtype in {bf16, f32}
  *   with q_dtype == kv_dtype; o_dtype in {f32, bf16}; r = H / H_kv in
  *   {1, 2, 4, 8}.  Anything else -> HETIS_E_UNSUPPORTED.  bf16 with r > 1
@@ -147,7 +151,9 @@ HETIS_API hetis_status hetis_plan_check_capacity(const hetis_plan *plan, int32_t
 /* ---- kv append: head-granular store --------------------- */
 /* For every request j and local kv head g: the new row goes to page
  * block_table[j][g][(L_j - 1) / P], slot (L_j - 1) mod P, L_j = seq_lens[j]
- * (length AFTER the append, reading 6).  A bit-exact copy.
+ * (length AFTER the append, reading 6).  A bit-exact copy.  L_j = 0: nothing
+ * is stored for request j (a device that does not own the request's newest
+ * page under a sequence split, see hetis_seq_split_lens).
  *   k_new, v_new : device [num_seqs][kv_head_count][head_dim], kv_dtype
  *   k_pool, v_pool: device [num_pages][page_size][head_dim], 16-B aligned
  *   block_table  : device int32 [num_seqs][kv_head_count][max_pages]
@@ -192,6 +198,16 @@ HETIS_API hetis_status hetis_attn_partial(const hetis_shape *shape, int32_t num_
 HETIS_API hetis_status hetis_attn_combine(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_count,
                                 const int32_t *seq_lens, int32_t max_seq_len, void *o, int64_t o_seq_stride,
                                 const void *workspace, size_t workspace_bytes, hetis_stream_t stream);
+
+/* hetis_attn_combine that also returns, per head, the natural-log normaliser
+ * over the tokens this device holds (the "global softmax attribute" a sequence
+ * split must aggregate):
+ *   lse[j][h] = ln sum_{t < L_j} exp(q_{j,h} . k_t / sqrt(d))
+ * (-inf and o = 0 when L_j = 0).  lse: device float [num_seqs][q_head_count]. */
+HETIS_API hetis_status hetis_attn_combine_lse(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_count,
+                                              const int32_t *seq_lens, int32_t max_seq_len, void *o,
+                                              int64_t o_seq_stride, float *lse, const void *workspace,
+                                              size_t workspace_bytes, hetis_stream_t stream);
 
 /* hetis_attn_partial followed by hetis_attn_combine with a dense o shard. */
 HETIS_API hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
@@ -253,6 +269,54 @@ HETIS_API hetis_status hetis_scatter_q(const hetis_plan *plan, void *nccl_comm, 
 HETIS_API hetis_status hetis_gather(const hetis_plan *plan, void *nccl_comm, int32_t rank, int32_t root, int32_t num_seqs,
                           const void *o_shard, void *o_full, void *workspace, size_t workspace_bytes,
                           hetis_stream_t stream);
+
+/* ---- sequence-wise split across devices (row f3) ------------------------ */
+/* The alternative the paper argues against (PAPER.md:292-304 `fig:head_wise_
+ * advantage`, :356-358): every device attends ALL heads over a subset of each
+ * request's tokens; the partial results are merged with their log-sum-exp
+ * ("aggregate global softmax attributes").  Layout (reading f3):
+ * page k of every (request, kv head) lives on device k mod N ("page striping"):
+ * the device's block table lists its pages k = rank, rank + N, ... in order, so
+ * only its last page can be partial, and the newest token always lands on the
+ * device holding page ceil(L_j / P) - 1.  Nothing moves as a request grows.
+ *
+ * From global lengths L_j (after the append), this device's token count
+ *   local_lens[j]  = sum over its pages of the tokens they hold
+ * and the length to pass to hetis_kv_append (append_lens may be NULL)
+ *   append_lens[j] = local_lens[j] if it owns page ceil(L_j / P) - 1, else 0.
+ * seq_lens, local_lens, append_lens: device int32 [num_seqs].  Integer; exact. */
+HETIS_API hetis_status hetis_seq_split_lens(int32_t num_ranks, int32_t rank, int32_t page_size, int32_t num_seqs,
+                                            const int32_t *seq_lens, int32_t *local_lens, int32_t *append_lens,
+                                            hetis_stream_t stream);
+/* O[j][h] = sum_p e^(lse_p - lse) o_p[j][h], lse = ln sum_p e^(lse_p), over the
+ * num_parts devices' partial results in ascending p (the union-of-subsets
+ * identity; a part with lse = -inf holds no token and is skipped).  One part
+ * reproduces its o bit for bit.
+ *   o_parts   : device float, part p at o_parts + p * o_part_stride, layout
+ *               [num_seqs][q_head_count][head_dim]; 16-byte aligned
+ *   lse_parts : device float, part p at lse_parts + p * lse_part_stride,
+ *               [num_seqs][q_head_count] (natural log, hetis_attn_combine_lse)
+ *   o         : device [num_seqs][q_head_count][head_dim] (o_dtype), rows of
+ *               request j at o + j * o_seq_stride elements */
+HETIS_API hetis_status hetis_seq_merge(const hetis_shape *shape, int32_t num_parts, int32_t num_seqs,
+                                       int32_t q_head_count, const float *o_parts, int64_t o_part_stride,
+                                       const float *lse_parts, int64_t lse_part_stride, void *o,
+                                       int64_t o_seq_stride, hetis_stream_t stream);
+/* The sequence split's input exchange: every device needs q of ALL heads (and
+ * the new k, v rows, which only the owner of the newest page stores): NCCL
+ * broadcast of q [num_seqs][H][d] and k_new, v_new [num_seqs][H_kv][d] from
+ * root, in place.  nccl_comm: ncclComm_t of num_ranks ranks, this one `rank`. */
+HETIS_API hetis_status hetis_seq_broadcast_q(const hetis_shape *shape, void *nccl_comm, int32_t num_ranks,
+                                             int32_t rank, int32_t root, int32_t num_seqs, void *q, void *k_new,
+                                             void *v_new, hetis_stream_t stream);
+/* The sequence split's output exchange: all-gather every device's record
+ *   part = [ o [num_seqs][H][d] float | lse [num_seqs][H] float ]
+ * (hetis_attn_combine_lse with q_head_count = H) into staging [num_ranks][record]
+ * (NCCL, num_seqs * H must be a multiple of 4), then hetis_seq_merge -> o
+ * [num_seqs][H][d] (o_dtype) on every rank. */
+HETIS_API hetis_status hetis_seq_allgather_merge(const hetis_shape *shape, void *nccl_comm, int32_t num_ranks,
+                                                 int32_t rank, int32_t num_seqs, const float *part, float *staging,
+                                                 void *o, int64_t o_seq_stride, hetis_stream_t stream);
 
 /* ---- head-granular KV migration (the Hauler) ------- */
 /* Re-dispatching a request moves only the kv-head groups whose device changes

@@ -422,9 +422,9 @@ hetis_status hetis_attn_partial(const hetis_shape *shape, int32_t num_seqs, int3
     return HETIS_OK;
 }
 
-hetis_status hetis_attn_combine(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_count,
-                                const int32_t *seq_lens, int32_t max_seq_len, void *o, int64_t o_seq_stride,
-                                const void *workspace, size_t workspace_bytes, hetis_stream_t stream) {
+static hetis_status combine_common(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_count,
+                                   const int32_t *seq_lens, int32_t max_seq_len, void *o, int64_t o_seq_stride,
+                                   float *lse, const void *workspace, size_t workspace_bytes, hetis_stream_t stream) {
     hetis_status st = check_shape(shape);
     if (st != HETIS_OK) return st;
     const int r = shape->num_q_heads / shape->num_kv_heads;
@@ -435,6 +435,7 @@ hetis_status hetis_attn_combine(const hetis_shape *shape, int32_t num_seqs, int3
     if (o_seq_stride < (int64_t)q_head_count * shape->head_dim) return fail(HETIS_E_INVALID, "o_seq_stride too small");
     const int oe = esize(shape->o_dtype);
     if (!aligned(o, 8) || (o_seq_stride * oe) % 8) return fail(HETIS_E_INVALID, "o rows must be 8-byte aligned");
+    if (lse && !aligned(lse, 4)) return fail(HETIS_E_INVALID, "lse must be 4-byte aligned");
     if (!aligned(workspace, 256)) return fail(HETIS_E_WORKSPACE, "workspace must be 256-byte aligned");
     hetis::WorkspaceLayout w = hetis::workspace_layout(num_seqs, q_head_count / r, r, shape->head_dim, max_seq_len);
     if (workspace_bytes < w.total) return fail(HETIS_E_WORKSPACE, "workspace too small");
@@ -442,9 +443,25 @@ hetis_status hetis_attn_combine(const hetis_shape *shape, int32_t num_seqs, int3
     cudaError_t e = hetis::launch_combine(
         num_seqs, q_head_count, r, shape->head_dim, seq_lens, reinterpret_cast<const int32_t *>(ws + w.split_off_offset),
         reinterpret_cast<const float *>(ws + w.lse_offset), reinterpret_cast<const float *>(ws + w.o_offset), o,
-        shape->o_dtype, o_seq_stride, reinterpret_cast<cudaStream_t>(stream));
+        shape->o_dtype, o_seq_stride, reinterpret_cast<cudaStream_t>(stream), lse);
     if (e != cudaSuccess) return cuda_fail(e, "combine launch");
     return HETIS_OK;
+}
+
+hetis_status hetis_attn_combine(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_count,
+                                const int32_t *seq_lens, int32_t max_seq_len, void *o, int64_t o_seq_stride,
+                                const void *workspace, size_t workspace_bytes, hetis_stream_t stream) {
+    return combine_common(shape, num_seqs, q_head_count, seq_lens, max_seq_len, o, o_seq_stride, nullptr, workspace,
+                          workspace_bytes, stream);
+}
+
+hetis_status hetis_attn_combine_lse(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_count,
+                                    const int32_t *seq_lens, int32_t max_seq_len, void *o, int64_t o_seq_stride,
+                                    float *lse, const void *workspace, size_t workspace_bytes,
+                                    hetis_stream_t stream) {
+    if (!lse && num_seqs > 0) return fail(HETIS_E_INVALID, "lse is NULL");
+    return combine_common(shape, num_seqs, q_head_count, seq_lens, max_seq_len, o, o_seq_stride, lse, workspace,
+                          workspace_bytes, stream);
 }
 
 hetis_status hetis_attn_combine_peers(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
@@ -663,6 +680,100 @@ hetis_status hetis_gather(const hetis_plan *plan, void *nccl_comm, int32_t rank,
         }
     }
     return HETIS_OK;
+}
+
+// ---------------------------------------------------------------- sequence-wise split (f3)
+hetis_status hetis_seq_split_lens(int32_t num_ranks, int32_t rank, int32_t page_size, int32_t num_seqs,
+                                  const int32_t *seq_lens, int32_t *local_lens, int32_t *append_lens,
+                                  hetis_stream_t stream) {
+    if (num_ranks < 1 || rank < 0 || rank >= num_ranks) return fail(HETIS_E_INVALID, "rank outside [0, num_ranks)");
+    if (page_size < 1 || num_seqs < 0) return fail(HETIS_E_INVALID, "bad sizes");
+    if (num_seqs == 0) return HETIS_OK;
+    if (!seq_lens || !local_lens) return fail(HETIS_E_INVALID, "NULL pointer");
+    cudaError_t e = hetis::launch_seq_split_lens(num_ranks, rank, page_size, num_seqs, seq_lens, local_lens,
+                                                 append_lens, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "seq_split_lens launch");
+    return HETIS_OK;
+}
+
+hetis_status hetis_seq_merge(const hetis_shape *shape, int32_t num_parts, int32_t num_seqs, int32_t q_head_count,
+                             const float *o_parts, int64_t o_part_stride, const float *lse_parts,
+                             int64_t lse_part_stride, void *o, int64_t o_seq_stride, hetis_stream_t stream) {
+    hetis_status st = check_shape(shape);
+    if (st != HETIS_OK) return st;
+    if (num_parts < 1 || num_seqs < 0 || q_head_count < 1) return fail(HETIS_E_INVALID, "bad sizes");
+    if (num_seqs == 0) return HETIS_OK;
+    if (!o_parts || !lse_parts || !o) return fail(HETIS_E_INVALID, "NULL pointer");
+    const int64_t rows = (int64_t)num_seqs * q_head_count;
+    if (num_parts > 1 && (o_part_stride < rows * shape->head_dim || lse_part_stride < rows))
+        return fail(HETIS_E_INVALID, "part strides below one part");
+    if (o_seq_stride < (int64_t)q_head_count * shape->head_dim) return fail(HETIS_E_INVALID, "o_seq_stride too small");
+    if (!aligned(o_parts, 16) || (o_part_stride % 4) || !aligned(lse_parts, 4))
+        return fail(HETIS_E_INVALID, "o_parts must be 16-byte aligned with a part stride multiple of 4");
+    const int oe = esize(shape->o_dtype);
+    if (!aligned(o, 8) || (o_seq_stride * oe) % 8) return fail(HETIS_E_INVALID, "o rows must be 8-byte aligned");
+    cudaError_t e = hetis::launch_seq_merge(num_parts, num_seqs, q_head_count, shape->head_dim, o_parts, o_part_stride,
+                                            lse_parts, lse_part_stride, o, shape->o_dtype, o_seq_stride,
+                                            reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "seq_merge launch");
+    return HETIS_OK;
+}
+
+static hetis_status check_seq_comm(void *comm, int32_t num_ranks, int32_t rank) {
+    if (!comm) return fail(HETIS_E_INVALID, "nccl_comm is NULL");
+    if (num_ranks < 1 || rank < 0 || rank >= num_ranks) return fail(HETIS_E_INVALID, "rank outside [0, num_ranks)");
+    Nccl &nc = nccl();
+    if (!nc.ok) return fail(HETIS_E_NCCL, nc.why);
+    int count = 0, me = -1;
+    NCCL_TRY(nc.commCount(static_cast<ncclComm_t>(comm), &count));
+    NCCL_TRY(nc.commUserRank(static_cast<ncclComm_t>(comm), &me));
+    if (count != num_ranks || me != rank) return fail(HETIS_E_INVALID, "communicator size/rank do not match");
+    return HETIS_OK;
+}
+
+hetis_status hetis_seq_broadcast_q(const hetis_shape *shape, void *nccl_comm, int32_t num_ranks, int32_t rank,
+                                   int32_t root, int32_t num_seqs, void *q, void *k_new, void *v_new,
+                                   hetis_stream_t stream) {
+    hetis_status st = check_shape(shape);
+    if (st != HETIS_OK) return st;
+    st = check_seq_comm(nccl_comm, num_ranks, rank);
+    if (st != HETIS_OK) return st;
+    if (root < 0 || root >= num_ranks || num_seqs < 0) return fail(HETIS_E_INVALID, "bad root / num_seqs");
+    if (num_seqs == 0) return HETIS_OK;
+    if (!q || !k_new || !v_new) return fail(HETIS_E_INVALID, "NULL pointer");
+    const size_t qb = (size_t)num_seqs * shape->num_q_heads * shape->head_dim * esize(shape->q_dtype);
+    const size_t kb = (size_t)num_seqs * shape->num_kv_heads * shape->head_dim * esize(shape->kv_dtype);
+    Nccl &nc = nccl();
+    ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    NCCL_TRY(nc.groupStart());
+    NCCL_TRY(nc.broadcast(q, q, qb, ncclUint8, root, comm, cs));
+    NCCL_TRY(nc.broadcast(k_new, k_new, kb, ncclUint8, root, comm, cs));
+    NCCL_TRY(nc.broadcast(v_new, v_new, kb, ncclUint8, root, comm, cs));
+    NCCL_TRY(nc.groupEnd());
+    return HETIS_OK;
+}
+
+hetis_status hetis_seq_allgather_merge(const hetis_shape *shape, void *nccl_comm, int32_t num_ranks, int32_t rank,
+                                       int32_t num_seqs, const float *part, float *staging, void *o,
+                                       int64_t o_seq_stride, hetis_stream_t stream) {
+    hetis_status st = check_shape(shape);
+    if (st != HETIS_OK) return st;
+    st = check_seq_comm(nccl_comm, num_ranks, rank);
+    if (st != HETIS_OK) return st;
+    if (num_seqs < 0) return fail(HETIS_E_INVALID, "num_seqs < 0");
+    if (num_seqs == 0) return HETIS_OK;
+    if (!part || !staging || !o) return fail(HETIS_E_INVALID, "NULL pointer");
+    if (!aligned(part, 16) || !aligned(staging, 16)) return fail(HETIS_E_INVALID, "part/staging must be 16-byte aligned");
+    const int H = shape->num_q_heads, D = shape->head_dim;
+    const int64_t rows = (int64_t)num_seqs * H;
+    const int64_t per = rows * (D + 1);  // floats of one device's record: o [B][H][D] then lse [B][H]
+    if (per % 4) return fail(HETIS_E_INVALID, "num_seqs * H must be a multiple of 4 (16-byte aligned records)");
+    Nccl &nc = nccl();
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    NCCL_TRY(nc.allGather(part, staging, (size_t)per, ncclFloat32, static_cast<ncclComm_t>(nccl_comm), cs));
+    return hetis_seq_merge(shape, num_ranks, num_seqs, H, staging, per, staging + rows * D, per, o, o_seq_stride,
+                           stream);
 }
 
 }  // extern "C"

@@ -52,7 +52,7 @@ cudaError_t launch_attn_simt(const AttnArgs &a, cudaStream_t s);
 cudaError_t launch_attn_tc(const AttnArgs &a, cudaStream_t s, std::string *err);
 cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const int32_t *seq_lens,
                            const int32_t *split_off, const float *part_lse, const float *part_o, void *o,
-                           int o_dtype, int64_t o_seq_stride, cudaStream_t s);
+                           int o_dtype, int64_t o_seq_stride, cudaStream_t s, float *lse = nullptr);
 cudaError_t launch_kv_append(int num_seqs, int kv_heads, int head_dim, int page_size, int elem_bytes,
                              const void *k_new, const void *v_new, void *k_pool, void *v_pool,
                              const int32_t *block_table, int max_pages, const int32_t *seq_lens, cudaStream_t s);
@@ -76,6 +76,12 @@ struct PeerTargets {
 cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim, const int32_t *split_off,
                                  const float *part_lse, const float *part_o, int o_dtype, const PeerTargets &t,
                                  cudaStream_t s);
+// sequence-wise split (row f3, seq_split.cu)
+cudaError_t launch_seq_split_lens(int num_ranks, int rank, int page_size, int num_seqs, const int32_t *seq_lens,
+                                  int32_t *local_lens, int32_t *append_lens, cudaStream_t s);
+cudaError_t launch_seq_merge(int num_parts, int num_seqs, int q_heads, int head_dim, const float *o_parts,
+                             int64_t o_part_stride, const float *lse_parts, int64_t lse_part_stride, void *o,
+                             int o_dtype, int64_t o_seq_stride, cudaStream_t s);
 cudaError_t launch_peer_wait(const int64_t *sig, int n, int64_t epoch, cudaStream_t s);
 cudaError_t launch_kv_migrate(int num_entries, const hetis_migration_entry *entries, int page_size, int page_bytes,
                               const void *src_k, const void *src_v, const int32_t *src_bt, int src_max_pages,

@@ -28,6 +28,7 @@ __global__ void kv_append_kernel(int num_seqs, int kv_heads, int row_bytes, int 
     if (warp >= num_seqs * kv_heads) return;
     const int j = warp / kv_heads, g = warp - j * kv_heads;
     const int pos = seq_lens[j] - 1;
+    if (pos < 0) return;  // seq_lens[j] == 0: nothing appended for request j on this device (sequence split)
     const int32_t page = block_table[((size_t)j * kv_heads + g) * max_pages + pos / page_size];
     const size_t dst = ((size_t)page * page_size + (size_t)(pos % page_size)) * row_bytes;
     const size_t src = (size_t)warp * row_bytes;
@@ -42,11 +43,16 @@ __global__ void kv_append_kernel(int num_seqs, int kv_heads, int row_bytes, int 
 // One group of D/4 threads per (request, local query head); each thread owns 4 dims.
 template <int D>
 __device__ __forceinline__ float4 combine_row(int j, int h, int q_heads, int r, const int32_t *split_off,
-                                              const float *part_lse, const float *part_o, int d4) {
+                                              const float *part_lse, const float *part_o, int d4,
+                                              float *lse2_out = nullptr) {
     const int kv_heads = q_heads / r;
     const int g = h / r, rr = h - g * r;
     const int s0 = split_off[j];
     const int ns = split_off[j + 1] - s0;
+    if (ns == 0) {  // no tokens (a rank holding none of request j under a sequence split): o = 0, lse = -inf
+        if (lse2_out) *lse2_out = -INFINITY;
+        return make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     float M = -INFINITY;
 #pragma unroll 8
     for (int s = 0; s < ns; ++s) M = fmaxf(M, part_lse[((size_t)(s0 + s) * kv_heads + g) * r + rr]);
@@ -68,6 +74,7 @@ __device__ __forceinline__ float4 combine_row(int j, int h, int q_heads, int r, 
     acc.y = __fdiv_rn(acc.y, wsum);
     acc.z = __fdiv_rn(acc.z, wsum);
     acc.w = __fdiv_rn(acc.w, wsum);
+    if (lse2_out) *lse2_out = M + log2f(wsum);
     return acc;
 }
 
@@ -83,9 +90,13 @@ __device__ __forceinline__ void store_row4(void *o, size_t idx, float4 acc) {
     }
 }
 
+// lse (optional, natural log, [num_seqs][q_heads]): ln sum_t exp(q.k_t / sqrt(d)) of
+// the head over the tokens this launch saw -- the input of the cross-device merge
+// of a sequence split (seq_split.cu).
 template <int D, int OUT_BF16>
 __global__ void combine_kernel(int num_seqs, int q_heads, int r, const int32_t *seq_lens, const int32_t *split_off,
-                               const float *part_lse, const float *part_o, void *o, int64_t o_seq_stride) {
+                               const float *part_lse, const float *part_o, void *o, int64_t o_seq_stride,
+                               float *lse) {
     dev::pdl_wait_then_release();
     constexpr int TPH = D / 4;  // threads per head
     const int heads_per_block = blockDim.x / TPH;
@@ -93,8 +104,10 @@ __global__ void combine_kernel(int num_seqs, int q_heads, int r, const int32_t *
     const int64_t flat = (int64_t)blockIdx.x * heads_per_block + hl;
     if (flat >= (int64_t)num_seqs * q_heads) return;
     const int j = (int)(flat / q_heads), h = (int)(flat - (int64_t)j * q_heads);
-    const float4 acc = combine_row<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4);
+    float lse2;
+    const float4 acc = combine_row<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4, &lse2);
     store_row4<OUT_BF16>(o, (size_t)j * o_seq_stride + (size_t)h * D + 4 * d4, acc);
+    if (lse != nullptr && d4 == 0) lse[flat] = lse2 * 0.69314718055994531f;  // log2 -> natural log
 }
 
 // Combine fused with the all-gather over peer memory (NVLink / NVSwitch): each
@@ -193,7 +206,7 @@ cudaError_t launch_kv_append(int num_seqs, int kv_heads, int head_dim, int page_
 
 cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const int32_t *seq_lens,
                            const int32_t *split_off, const float *part_lse, const float *part_o, void *o,
-                           int o_dtype, int64_t o_seq_stride, cudaStream_t s) {
+                           int o_dtype, int64_t o_seq_stride, cudaStream_t s, float *lse) {
     const int64_t heads = (int64_t)num_seqs * q_heads;
     if (heads == 0) return cudaSuccess;
     const int tph = head_dim / 4;
@@ -203,7 +216,7 @@ cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const
     auto kern = head_dim == 128 ? (o_dtype == HETIS_BF16 ? combine_kernel<128, 1> : combine_kernel<128, 0>)
                                 : (o_dtype == HETIS_BF16 ? combine_kernel<64, 1> : combine_kernel<64, 0>);
     return launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), 0, s, num_seqs, q_heads, r, seq_lens, split_off,
-                      part_lse, part_o, o, o_seq_stride);
+                      part_lse, part_o, o, o_seq_stride, lse);
 }
 
 cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim, const int32_t *split_off,

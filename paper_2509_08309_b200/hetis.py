@@ -32,7 +32,8 @@ EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_
             "hetis_plan_check_capacity", "hetis_kv_append", "hetis_attn_decode_workspace", "hetis_attn_partial",
             "hetis_attn_combine", "hetis_attn_decode", "hetis_attn_combine_peers", "hetis_peer_wait",
             "hetis_comm_workspace", "hetis_scatter_q", "hetis_gather", "hetis_kv_migrate",
-            "hetis_launch_count")
+            "hetis_attn_combine_lse", "hetis_seq_split_lens", "hetis_seq_merge", "hetis_seq_broadcast_q",
+            "hetis_seq_allgather_merge", "hetis_launch_count")
 
 
 class HetisError(RuntimeError):
@@ -90,6 +91,11 @@ def lib() -> ctypes.CDLL:
                 "hetis_scatter_q": (ctypes.c_int, [vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
                 "hetis_gather": (ctypes.c_int, [vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]),
                 "hetis_kv_migrate": (ctypes.c_int, [sp, i32, vp, vp, vp, vp, i32, vp, vp, vp, i32, i32, vp]),
+                "hetis_attn_combine_lse": (ctypes.c_int, [sp, i32, i32, vp, i32, vp, i64, vp, vp, sz, vp]),
+                "hetis_seq_split_lens": (ctypes.c_int, [i32, i32, i32, i32, vp, vp, vp, vp]),
+                "hetis_seq_merge": (ctypes.c_int, [sp, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp]),
+                "hetis_seq_broadcast_q": (ctypes.c_int, [sp, vp, i32, i32, i32, i32, vp, vp, vp, vp]),
+                "hetis_seq_allgather_merge": (ctypes.c_int, [sp, vp, i32, i32, i32, vp, vp, vp, i64, vp]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)
@@ -264,6 +270,22 @@ def attn_combine(shape: CShape, seq_lens, max_seq_len: int, o, workspace, q_head
            "hetis_attn_combine")
 
 
+def attn_combine_lse(shape: CShape, seq_lens, max_seq_len: int, o, lse, workspace, q_head_count: int | None = None,
+                     o_seq_stride: int | None = None, stream=None) -> None:
+    """hetis_attn_combine that also writes lse [B][q_head_count] (natural log) -- the sequence split's input."""
+    B = seq_lens.shape[0]
+    if q_head_count is None:
+        q_head_count = o.shape[1]
+    if o_seq_stride is None:
+        o_seq_stride = o.stride(0)
+    if not o.is_cuda or not lse.is_cuda or lse.dtype != torch.float32:
+        raise ValueError("o and lse (float32) must be CUDA tensors")
+    _check(lib().hetis_attn_combine_lse(ctypes.byref(shape), B, q_head_count, _dev(seq_lens, "seq_lens"), max_seq_len,
+                                        ctypes.c_void_p(o.data_ptr()), o_seq_stride, ctypes.c_void_p(lse.data_ptr()),
+                                        _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(),
+                                        _stream(stream)), "hetis_attn_combine_lse")
+
+
 def attn_decode(shape: CShape, q, k_pool, v_pool, block_table, seq_lens, max_seq_len: int, o, workspace,
                 q_head_begin: int = 0, flags: int = 0, stream=None) -> None:
     B, x, _ = q.shape
@@ -316,3 +338,42 @@ def gather(plan: Plan, comm_ptr: int, rank: int, root: int, num_seqs: int, o_sha
                               _dev(o_full, "o_full"), _dev(workspace, "workspace"),
                               0 if workspace is None else workspace.numel() * workspace.element_size(),
                               _stream(stream)), "hetis_gather")
+
+
+# ---------------------------------------------------------------- sequence-wise split (row f3)
+def seq_split_lens(num_ranks: int, rank: int, page_size: int, seq_lens, local_lens, append_lens=None,
+                   stream=None) -> None:
+    """Page-striped sequence split: this rank's token counts (and append lengths) from global lengths."""
+    _check(lib().hetis_seq_split_lens(num_ranks, rank, page_size, seq_lens.shape[0], _dev(seq_lens, "seq_lens"),
+                                      _dev(local_lens, "local_lens"), _dev(append_lens, "append_lens"),
+                                      _stream(stream)), "hetis_seq_split_lens")
+
+
+def seq_merge(shape: CShape, o_parts, lse_parts, o, stream=None) -> None:
+    """o_parts float [N][B][x][D], lse_parts float [N][B][x] -> o [B][x][D] (o dtype; rows may be strided).
+    Parts may sit at any stride (e.g. views into the all-gather's staging); each part must be dense."""
+    n, B, x, D = o_parts.shape
+    if not (o.is_cuda and o_parts.is_cuda and lse_parts.is_cuda):
+        raise ValueError("o, o_parts and lse_parts must be CUDA tensors")
+    if not (o_parts[0].is_contiguous() and lse_parts[0].is_contiguous()):
+        raise ValueError("each part of o_parts / lse_parts must be dense")
+    if o_parts.dtype != torch.float32 or lse_parts.dtype != torch.float32:
+        raise ValueError("o_parts and lse_parts must be float32")
+    _check(lib().hetis_seq_merge(ctypes.byref(shape), n, B, x, ctypes.c_void_p(o_parts.data_ptr()), o_parts.stride(0),
+                                 ctypes.c_void_p(lse_parts.data_ptr()), lse_parts.stride(0),
+                                 ctypes.c_void_p(o.data_ptr()), o.stride(0), _stream(stream)), "hetis_seq_merge")
+
+
+def seq_broadcast_q(shape: CShape, comm_ptr: int, num_ranks: int, rank: int, root: int, q, k_new, v_new,
+                    stream=None) -> None:
+    _check(lib().hetis_seq_broadcast_q(ctypes.byref(shape), ctypes.c_void_p(comm_ptr), num_ranks, rank, root,
+                                       q.shape[0], _dev(q, "q"), _dev(k_new, "k_new"), _dev(v_new, "v_new"),
+                                       _stream(stream)), "hetis_seq_broadcast_q")
+
+
+def seq_allgather_merge(shape: CShape, comm_ptr: int, num_ranks: int, rank: int, num_seqs: int, part, staging, o,
+                        stream=None) -> None:
+    """part: float [B*H*D + B*H] (o then lse); staging: float [N][same]; o: [B][H][D] (o dtype)."""
+    _check(lib().hetis_seq_allgather_merge(ctypes.byref(shape), ctypes.c_void_p(comm_ptr), num_ranks, rank, num_seqs,
+                                           _dev(part, "part"), _dev(staging, "staging"), _dev(o, "o"), o.stride(0),
+                                           _stream(stream)), "hetis_seq_allgather_merge")

@@ -29,7 +29,7 @@ def declared_symbols():
 
 def test_every_declared_symbol_is_exported(L):
     syms = declared_symbols()
-    assert len(syms) == 22
+    assert len(syms) == 27
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(hetis.EXPORTED)
@@ -219,3 +219,37 @@ def test_binding_refuses_host_tensors(L):
     with pytest.raises(ValueError):
         hetis.attn_decode(s, t, t, t, torch.zeros(4, 8, 8, dtype=torch.int32), torch.ones(4, dtype=torch.int32), 1,
                           t, torch.zeros(1024, dtype=torch.uint8))
+
+
+def test_seq_split_entry_points_validate(L):
+    """Row f3 entry points: argument validation happens before any launch (no GPU needed)."""
+    vp_ = ctypes.c_void_p
+    s = hetis.make_shape(workload.LLAMA2_13B)
+    # split lengths: rank outside [0, N), nothing to do for 0 requests, NULL outputs
+    assert L.hetis_seq_split_lens(2, 2, 16, 4, vp_(256), vp_(512), None, vp_(0)) == 1
+    assert L.hetis_seq_split_lens(0, 0, 16, 4, vp_(256), vp_(512), None, vp_(0)) == 1
+    assert L.hetis_seq_split_lens(2, 1, 16, 0, None, None, None, vp_(0)) == 0
+    assert L.hetis_seq_split_lens(2, 1, 16, 4, vp_(256), None, None, vp_(0)) == 1
+    # merge: part strides below one part, misaligned parts, unsupported head_dim
+    B, H, D = 4, 40, 128
+    ok = (2, B, H, vp_(1 << 20), B * H * D, vp_(1 << 22), B * H, vp_(1 << 24), H * D, vp_(0))
+    bad = list(ok)
+    bad[4] = B * H * D - 1
+    assert L.hetis_seq_merge(ctypes.byref(s), *bad) == 1
+    bad = list(ok)
+    bad[3] = vp_((1 << 20) + 8)
+    assert L.hetis_seq_merge(ctypes.byref(s), *bad) == 1
+    bad = list(ok)
+    bad[8] = H * D - 4
+    assert L.hetis_seq_merge(ctypes.byref(s), *bad) == 1
+    assert L.hetis_seq_merge(ctypes.byref(s), 0, *ok[1:]) == 1
+    s96 = hetis.make_shape(workload.Shape(40, 40, 96, 16, "bf16"))
+    assert L.hetis_seq_merge(ctypes.byref(s96), *ok) == 5
+    # combine with lse: the lse pointer is required
+    assert L.hetis_attn_combine_lse(ctypes.byref(s), 4, H, vp_(256), 64, vp_(1024), H * D, None, vp_(4096),
+                                    1 << 20, vp_(0)) == 1
+    # NCCL exchange: NULL communicator / rank outside the world
+    assert L.hetis_seq_allgather_merge(ctypes.byref(s), vp_(0), 2, 0, 4, vp_(256), vp_(512), vp_(1024), H * D,
+                                       vp_(0)) == 1
+    assert L.hetis_seq_broadcast_q(ctypes.byref(s), vp_(1234), 2, 3, 0, 4, vp_(256), vp_(512), vp_(768),
+                                   vp_(0)) == 1

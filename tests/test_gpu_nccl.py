@@ -72,3 +72,29 @@ def test_gather_rejects_mismatched_communicator(nccl_world1):
     with pytest.raises(hetis.HetisError) as e:
         hetis.gather(plan, nccl_world1, 0, -1, 2, o, full, ws)
     assert e.value.name == "HETIS_E_INVALID"          # 2-device plan on a 1-rank communicator
+
+
+@pytest.mark.parametrize("shape", [workload.LLAMA2_13B, workload.LLAMA2_70B])
+def test_seq_split_broadcast_and_allgather_merge_world1(nccl_world1, shape):
+    """Sequence split (row f3) through its NCCL entry points: hetis_seq_broadcast_q delivers q / new k, v
+    in place and hetis_seq_allgather_merge of one device's (o, lse) record reproduces o bit for bit."""
+    from paper_2509_08309_b200 import seqsplit
+    lens = torch.tensor([300, 17, 1, 1029], dtype=torch.int32)
+    b = workload.make_decode_batch(shape, lens, 11, "cuda")
+    st = seqsplit.SeqSplitStep(shape, 1, 0, len(lens), int(lens.max()), torch.device("cuda", 0),
+                               comm_ptr=nccl_world1)
+    st.q.copy_(b.q)
+    st.k_new.copy_(b.k_new)
+    st.v_new.copy_(b.v_new)
+    st.broadcast()
+    torch.cuda.synchronize()
+    assert torch.equal(st.q, b.q) and torch.equal(st.k_new, b.k_new) and torch.equal(st.v_new, b.v_new)
+    lbt = seqsplit.local_block_table(b.block_table, 1, 0)
+    o = torch.full_like(b.q, float("nan"), dtype=torch.float32)
+    st.run(b.k_pool, b.v_pool, lbt, b.seq_lens, o)
+    staging = torch.empty((1, st.part.numel()), dtype=torch.float32, device="cuda")
+    o2 = torch.full_like(o, float("nan"))
+    hetis.seq_allgather_merge(st.cshape, nccl_world1, 1, 0, len(lens), st.part, staging, o2)
+    torch.cuda.synchronize()
+    assert torch.equal(staging[0], st.part)
+    assert torch.equal(o2, o) and torch.equal(o, st.part_o)
