@@ -443,7 +443,7 @@ static hetis_status combine_common(const hetis_shape *shape, int32_t num_seqs, i
     cudaError_t e = hetis::launch_combine(
         num_seqs, q_head_count, r, shape->head_dim, seq_lens, reinterpret_cast<const int32_t *>(ws + w.split_off_offset),
         reinterpret_cast<const float *>(ws + w.lse_offset), reinterpret_cast<const float *>(ws + w.o_offset), o,
-        shape->o_dtype, o_seq_stride, reinterpret_cast<cudaStream_t>(stream), lse);
+        shape->o_dtype, o_seq_stride, reinterpret_cast<cudaStream_t>(stream), lse, max_seq_len);
     if (e != cudaSuccess) return cuda_fail(e, "combine launch");
     return HETIS_OK;
 }
@@ -504,7 +504,7 @@ hetis_status hetis_attn_combine_peers(const hetis_shape *shape, int32_t num_seqs
     cudaError_t e = hetis::launch_combine_peers(
         num_seqs, q_head_count, r, shape->head_dim, reinterpret_cast<const int32_t *>(ws + w.split_off_offset),
         reinterpret_cast<const float *>(ws + w.lse_offset), reinterpret_cast<const float *>(ws + w.o_offset),
-        shape->o_dtype, t, reinterpret_cast<cudaStream_t>(stream));
+        shape->o_dtype, t, reinterpret_cast<cudaStream_t>(stream), max_seq_len);
     if (e != cudaSuccess) return cuda_fail(e, "combine_peers launch");
     return HETIS_OK;
 }

@@ -158,9 +158,15 @@ __device__ void build_split_offsets(const Params &p, int32_t *s_len, int32_t *s_
     __syncthreads();
     if (tid == 0) s_off[B] = B > 0 ? s_off[B - 1] + (s_len[B - 1] + kC - 1) / kC : 0;
     __syncthreads();
-    if (blockIdx.x == 0) {
-        for (int j = tid; j <= B; j += nt) p.split_off_out[j] = s_off[j];
-    }
+}
+
+// Block 0 publishes the split offsets for the combine kernel.  Called by the
+// producer lanes AFTER griddepcontrol.wait: the previous step's combine, which
+// may still be running while this kernel's prologue executes (it releases its
+// dependents before it waits), reads the same workspace slots.
+__device__ __forceinline__ void publish_split_offsets(const Params &p, const int32_t *s_off, int lane, int lanes) {
+    if (blockIdx.x != 0) return;
+    for (int j = lane; j <= p.num_seqs; j += lanes) p.split_off_out[j] = s_off[j];
 }
 
 // ---------------------------------------------------------------- ring position
@@ -251,7 +257,11 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
     constexpr unsigned kMask = (1u << kProducerLanes) - 1u;
 
     int item = blockIdx.x;
-    if (item >= n_items) return;
+    if (item >= n_items) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        publish_split_offsets(p, s_off, lane, kProducerLanes);
+        return;
+    }
     static_assert((kQSlots & (kQSlots - 1)) == 0, "q slots: power of two");
     Dec cur = decode(item);
     if (lane == 0) issue_q(0, item, cur);
@@ -259,6 +269,7 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
     load_pids(cur, pid);
     RingPos pos{0, 0u};
     asm volatile("griddepcontrol.wait;" ::: "memory");  // pools may hold rows the previous kernel (kv_append) wrote
+    publish_split_offsets(p, s_off, lane, kProducerLanes);
     for (int it = 0; item < n_items; item += gridDim.x, ++it) {
         const int next = item + gridDim.x;
         int32_t pid_next[PPL];
@@ -811,6 +822,7 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         for (int i = 0; i < kPagesPerItem; ++i) sm.pids[(w * 2 + 0) * kPagesPerItem + i] = nxt[i];
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");  // pools may hold rows the previous kernel wrote
+    publish_split_offsets(p, s_off, w, NW);
     if (w == 0) {
         HETIS_TS(2);
     }

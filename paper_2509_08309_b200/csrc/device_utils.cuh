@@ -120,6 +120,16 @@ __device__ __forceinline__ void pdl_wait_then_release() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// Allow the next kernel to be scheduled now, then wait for the previous one.
+// Used by the combine: its dependents (kv_append of the next step, the merge,
+// or an attention launch) all execute griddepcontrol.wait before touching
+// anything the combine or its predecessors write, so they may be resident and
+// waiting while the combine runs.
+__device__ __forceinline__ void pdl_release_then_wait() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- named barriers
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -52,7 +52,7 @@ cudaError_t launch_attn_simt(const AttnArgs &a, cudaStream_t s);
 cudaError_t launch_attn_tc(const AttnArgs &a, cudaStream_t s, std::string *err);
 cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const int32_t *seq_lens,
                            const int32_t *split_off, const float *part_lse, const float *part_o, void *o,
-                           int o_dtype, int64_t o_seq_stride, cudaStream_t s, float *lse = nullptr);
+                           int o_dtype, int64_t o_seq_stride, cudaStream_t s, float *lse, int max_seq_len);
 cudaError_t launch_kv_append(int num_seqs, int kv_heads, int head_dim, int page_size, int elem_bytes,
                              const void *k_new, const void *v_new, void *k_pool, void *v_pool,
                              const int32_t *block_table, int max_pages, const int32_t *seq_lens, cudaStream_t s);
@@ -75,7 +75,7 @@ struct PeerTargets {
 };
 cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim, const int32_t *split_off,
                                  const float *part_lse, const float *part_o, int o_dtype, const PeerTargets &t,
-                                 cudaStream_t s);
+                                 cudaStream_t s, int max_seq_len);
 // sequence-wise split (row f3, seq_split.cu)
 cudaError_t launch_seq_split_lens(int num_ranks, int rank, int page_size, int num_seqs, const int32_t *seq_lens,
                                   int32_t *local_lens, int32_t *append_lens, cudaStream_t s);

@@ -39,43 +39,132 @@ __global__ void kv_append_kernel(int num_seqs, int kv_heads, int row_bytes, int 
 }
 
 // ---------------------------------------------------------------- combine
-// o = sum_s 2^(lse_s - M) o_s / sum_s 2^(lse_s - M), M = max_s lse_s, s ascending.
-// One group of D/4 threads per (request, local query head); each thread owns 4 dims.
+// o = sum_s 2^(lse_s - M) o_s / sum_s 2^(lse_s - M), M = max_s lse_s.
+// A "group" is D/4 threads, each owning 4 dims of the row.  A group folds its
+// splits in chunks of U: the chunk's lse and o rows are loaded together (one
+// memory round trip per chunk) and accumulated with an online max (rescale by
+// 2^(M_old - M_new)).  The arithmetic of a (request, head) pair depends on its
+// split count ns only (hence on L_j only), never on the launch shape:
+//   ns <= kNarrowSplits: one group folds s = 0 .. ns-1;
+//   ns >  kNarrowSplits: the G groups of a 128-thread block fold s = g, g + G,
+//                        ... and their states are merged in ascending g.
+// With one split, w = 2^0 = 1 and every other term is an exact zero, so
+// o = o_0 bit for bit.  Launch shapes: when every request of the batch has
+// <= kNarrowSplits splits, a block serves G pairs (one group each: few blocks,
+// one round trip per pair); otherwise a block serves one pair.
+constexpr int kCombineThreads = 128;
+constexpr int kCombineChunk = 8;
+constexpr int kNarrowSplits = 16;
+
+struct FoldState {
+    float M, wsum;
+    float4 acc;
+};
+
+// fold splits s = first, first + step, ... < ns
 template <int D>
-__device__ __forceinline__ float4 combine_row(int j, int h, int q_heads, int r, const int32_t *split_off,
-                                              const float *part_lse, const float *part_o, int d4,
-                                              float *lse2_out = nullptr) {
-    const int kv_heads = q_heads / r;
-    const int g = h / r, rr = h - g * r;
-    const int s0 = split_off[j];
-    const int ns = split_off[j + 1] - s0;
-    if (ns == 0) {  // no tokens (a rank holding none of request j under a sequence split): o = 0, lse = -inf
-        if (lse2_out) *lse2_out = -INFINITY;
+__device__ __forceinline__ FoldState fold_splits(int first, int step, int ns, int s0, int kv_heads, int g, int r,
+                                                 int rr, const float *part_lse, const float *part_o, int d4) {
+    constexpr int U = kCombineChunk;
+    FoldState f{-INFINITY, 0.f, make_float4(0.f, 0.f, 0.f, 0.f)};
+    for (int base = first; base < ns; base += step * U) {
+        float l[U];
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int sp = base + u * step;
+            if (sp < ns) {
+                const size_t rw = ((size_t)(s0 + sp) * kv_heads + g) * r + rr;
+                l[u] = part_lse[rw];
+                v[u] = reinterpret_cast<const float4 *>(part_o + rw * D)[d4];
+            } else {
+                l[u] = -INFINITY;
+                v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        float mc = l[0];  // finite: split `base` exists
+#pragma unroll
+        for (int u = 1; u < U; ++u) mc = fmaxf(mc, l[u]);
+        const float Mn = fmaxf(f.M, mc);
+        const float alpha = dev::ex2(f.M - Mn);  // 0 on the first chunk (M = -inf)
+        f.wsum *= alpha;
+        f.acc.x *= alpha;
+        f.acc.y *= alpha;
+        f.acc.z *= alpha;
+        f.acc.w *= alpha;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float w = dev::ex2(l[u] - Mn);  // 0 for the padding (l = -inf)
+            f.wsum += w;
+            f.acc.x = fmaf(w, v[u].x, f.acc.x);
+            f.acc.y = fmaf(w, v[u].y, f.acc.y);
+            f.acc.z = fmaf(w, v[u].z, f.acc.z);
+            f.acc.w = fmaf(w, v[u].w, f.acc.w);
+        }
+        f.M = Mn;
+    }
+    return f;
+}
+
+__device__ __forceinline__ float4 finish(const FoldState &f, float *lse2_out) {
+    *lse2_out = f.M + log2f(f.wsum);
+    return make_float4(__fdiv_rn(f.acc.x, f.wsum), __fdiv_rn(f.acc.y, f.wsum), __fdiv_rn(f.acc.z, f.wsum),
+                       __fdiv_rn(f.acc.w, f.wsum));
+}
+
+// Narrow pair: folded by ONE group (the calling group); no block barrier.
+template <int D>
+__device__ __forceinline__ float4 combine_narrow(int j, int h, int q_heads, int r, const int32_t *split_off,
+                                                 const float *part_lse, const float *part_o, int d4,
+                                                 float *lse2_out) {
+    const int kv_heads = q_heads / r, g = h / r, rr = h - g * r;
+    const int s0 = split_off[j], ns = split_off[j + 1] - s0;
+    if (ns == 0) {  // no tokens (a device holding none of request j under a sequence split): o = 0, lse = -inf
+        *lse2_out = -INFINITY;
         return make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    float M = -INFINITY;
-#pragma unroll 8
-    for (int s = 0; s < ns; ++s) M = fmaxf(M, part_lse[((size_t)(s0 + s) * kv_heads + g) * r + rr]);
-    float wsum = 0.f;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
-    for (int s = 0; s < ns; ++s) {
-        const size_t row = ((size_t)(s0 + s) * kv_heads + g) * r + rr;
-        const float w = dev::ex2(part_lse[row] - M);
-        const float4 v = reinterpret_cast<const float4 *>(part_o + row * D)[d4];
-        wsum += w;
-        acc.x = fmaf(w, v.x, acc.x);
-        acc.y = fmaf(w, v.y, acc.y);
-        acc.z = fmaf(w, v.z, acc.z);
-        acc.w = fmaf(w, v.w, acc.w);
+    return finish(fold_splits<D>(0, 1, ns, s0, kv_heads, g, r, rr, part_lse, part_o, d4), lse2_out);
+}
+
+// Wide launch: the whole 128-thread block serves one pair.  Result valid in group 0.
+template <int D>
+__device__ __forceinline__ float4 combine_wide(int j, int h, int q_heads, int r, const int32_t *split_off,
+                                               const float *part_lse, const float *part_o, float *lse2_out) {
+    constexpr int TPH = D / 4, G = kCombineThreads / TPH;
+    __shared__ float4 s_acc[G][TPH];
+    __shared__ float s_m[G], s_w[G];
+    const int tid = threadIdx.x, grp = tid / TPH, d4 = tid % TPH;
+    const int kv_heads = q_heads / r, g = h / r, rr = h - g * r;
+    const int s0 = split_off[j], ns = split_off[j + 1] - s0;
+    if (ns <= kNarrowSplits)  // block-uniform
+        return combine_narrow<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4, lse2_out);
+    const FoldState f = fold_splits<D>(grp, G, ns, s0, kv_heads, g, r, rr, part_lse, part_o, d4);
+    s_acc[grp][d4] = f.acc;
+    if (d4 == 0) {
+        s_m[grp] = f.M;
+        s_w[grp] = f.wsum;
     }
-    // single split: w = 2^0 = 1 exactly, so o = o_0 bit for bit
-    acc.x = __fdiv_rn(acc.x, wsum);
-    acc.y = __fdiv_rn(acc.y, wsum);
-    acc.z = __fdiv_rn(acc.z, wsum);
-    acc.w = __fdiv_rn(acc.w, wsum);
-    if (lse2_out) *lse2_out = M + log2f(wsum);
-    return acc;
+    __syncthreads();
+    float Mall = s_m[0];
+#pragma unroll
+    for (int k = 1; k < G; ++k) Mall = fmaxf(Mall, s_m[k]);
+    FoldState t;
+    const float f0 = dev::ex2(s_m[0] - Mall);
+    const float4 a0 = s_acc[0][d4];
+    t.acc = make_float4(f0 * a0.x, f0 * a0.y, f0 * a0.z, f0 * a0.w);
+    t.wsum = f0 * s_w[0];
+#pragma unroll
+    for (int k = 1; k < G; ++k) {
+        const float fk = dev::ex2(s_m[k] - Mall);  // every group holds >= 1 split here (ns > G)
+        const float4 ak = s_acc[k][d4];
+        t.acc.x = fmaf(fk, ak.x, t.acc.x);
+        t.acc.y = fmaf(fk, ak.y, t.acc.y);
+        t.acc.z = fmaf(fk, ak.z, t.acc.z);
+        t.acc.w = fmaf(fk, ak.w, t.acc.w);
+        t.wsum = fmaf(fk, s_w[k], t.wsum);
+    }
+    t.M = Mall;
+    return finish(t, lse2_out);
 }
 
 template <int OUT_BF16>
@@ -93,19 +182,21 @@ __device__ __forceinline__ void store_row4(void *o, size_t idx, float4 acc) {
 // lse (optional, natural log, [num_seqs][q_heads]): ln sum_t exp(q.k_t / sqrt(d)) of
 // the head over the tokens this launch saw -- the input of the cross-device merge
 // of a sequence split (seq_split.cu).
-template <int D, int OUT_BF16>
-__global__ void combine_kernel(int num_seqs, int q_heads, int r, const int32_t *seq_lens, const int32_t *split_off,
-                               const float *part_lse, const float *part_o, void *o, int64_t o_seq_stride,
-                               float *lse) {
-    dev::pdl_wait_then_release();
-    constexpr int TPH = D / 4;  // threads per head
-    const int heads_per_block = blockDim.x / TPH;
-    const int hl = threadIdx.x / TPH, d4 = threadIdx.x % TPH;
-    const int64_t flat = (int64_t)blockIdx.x * heads_per_block + hl;
-    if (flat >= (int64_t)num_seqs * q_heads) return;
+template <int D, int OUT_BF16, bool WIDE>
+__global__ void __launch_bounds__(kCombineThreads) combine_kernel(int num_seqs, int q_heads, int r,
+                                                                  const int32_t *seq_lens, const int32_t *split_off,
+                                                                  const float *part_lse, const float *part_o, void *o,
+                                                                  int64_t o_seq_stride, float *lse) {
+    dev::pdl_release_then_wait();
+    constexpr int TPH = D / 4, G = kCombineThreads / TPH;
+    const int grp = threadIdx.x / TPH, d4 = threadIdx.x % TPH;
+    const int64_t flat = WIDE ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * G + grp;
+    if (flat >= (int64_t)num_seqs * q_heads) return;  // narrow launches only (wide grids are exact)
     const int j = (int)(flat / q_heads), h = (int)(flat - (int64_t)j * q_heads);
     float lse2;
-    const float4 acc = combine_row<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4, &lse2);
+    const float4 acc = WIDE ? combine_wide<D>(j, h, q_heads, r, split_off, part_lse, part_o, &lse2)
+                            : combine_narrow<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4, &lse2);
+    if (WIDE && grp != 0) return;
     store_row4<OUT_BF16>(o, (size_t)j * o_seq_stride + (size_t)h * D + 4 * d4, acc);
     if (lse != nullptr && d4 == 0) lse[flat] = lse2 * 0.69314718055994531f;  // log2 -> natural log
 }
@@ -114,19 +205,24 @@ __global__ void combine_kernel(int num_seqs, int q_heads, int r, const int32_t *
 // merged O row is stored straight into every rank's o_full at its GLOBAL head
 // index (Eq. 2a Concat), then the last block publishes `epoch` into every
 // rank's signal slot [rank] with a system-scope release store.
-template <int D, int OUT_BF16>
-__global__ void combine_peers_kernel(int num_seqs, int q_heads, int r, const int32_t *split_off, const float *part_lse,
-                                     const float *part_o, PeerTargets t) {
+template <int D, int OUT_BF16, bool WIDE>
+__global__ void __launch_bounds__(kCombineThreads) combine_peers_kernel(int num_seqs, int q_heads, int r,
+                                                                        const int32_t *split_off,
+                                                                        const float *part_lse, const float *part_o,
+                                                                        PeerTargets t) {
     dev::pdl_wait_then_release();
-    constexpr int TPH = D / 4;
-    const int heads_per_block = blockDim.x / TPH;
-    const int hl = threadIdx.x / TPH, d4 = threadIdx.x % TPH;
-    const int64_t flat = (int64_t)blockIdx.x * heads_per_block + hl;
+    constexpr int TPH = D / 4, G = kCombineThreads / TPH;
+    const int grp = threadIdx.x / TPH, d4 = threadIdx.x % TPH;
+    const int64_t flat = WIDE ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * G + grp;
     if (flat < (int64_t)num_seqs * q_heads) {
         const int j = (int)(flat / q_heads), h = (int)(flat - (int64_t)j * q_heads);
-        const float4 acc = combine_row<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4);
-        const size_t idx = (size_t)j * t.o_seq_stride + (size_t)(t.head0 + h) * D + 4 * d4;
-        for (int p = 0; p < t.n; ++p) store_row4<OUT_BF16>(t.o[p], idx, acc);
+        float lse2;
+        const float4 acc = WIDE ? combine_wide<D>(j, h, q_heads, r, split_off, part_lse, part_o, &lse2)
+                                : combine_narrow<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4, &lse2);
+        if (!WIDE || grp == 0) {
+            const size_t idx = (size_t)j * t.o_seq_stride + (size_t)(t.head0 + h) * D + 4 * d4;
+            for (int p = 0; p < t.n; ++p) store_row4<OUT_BF16>(t.o[p], idx, acc);
+        }
     }
     __threadfence_system();  // this thread's peer stores are visible system-wide ...
     __syncthreads();
@@ -206,30 +302,42 @@ cudaError_t launch_kv_append(int num_seqs, int kv_heads, int head_dim, int page_
 
 cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const int32_t *seq_lens,
                            const int32_t *split_off, const float *part_lse, const float *part_o, void *o,
-                           int o_dtype, int64_t o_seq_stride, cudaStream_t s, float *lse) {
-    const int64_t heads = (int64_t)num_seqs * q_heads;
-    if (heads == 0) return cudaSuccess;
-    const int tph = head_dim / 4;
-    const int threads = 128;
-    const int hpb = threads / tph;
-    const int64_t blocks = (heads + hpb - 1) / hpb;
-    auto kern = head_dim == 128 ? (o_dtype == HETIS_BF16 ? combine_kernel<128, 1> : combine_kernel<128, 0>)
-                                : (o_dtype == HETIS_BF16 ? combine_kernel<64, 1> : combine_kernel<64, 0>);
-    return launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), 0, s, num_seqs, q_heads, r, seq_lens, split_off,
-                      part_lse, part_o, o, o_seq_stride, lse);
+                           int o_dtype, int64_t o_seq_stride, cudaStream_t s, float *lse, int max_seq_len) {
+    const int64_t pairs = (int64_t)num_seqs * q_heads;
+    if (pairs == 0) return cudaSuccess;
+    const bool wide = (max_seq_len + kSplitTokens - 1) / kSplitTokens > kNarrowSplits;
+    const int g = kCombineThreads / (head_dim / 4);
+    const int64_t blocks = wide ? pairs : (pairs + g - 1) / g;
+    const bool bf = o_dtype == HETIS_BF16;
+    decltype(&combine_kernel<128, 0, false>) kern;
+    if (head_dim == 128)
+        kern = wide ? (bf ? combine_kernel<128, 1, true> : combine_kernel<128, 0, true>)
+                    : (bf ? combine_kernel<128, 1, false> : combine_kernel<128, 0, false>);
+    else
+        kern = wide ? (bf ? combine_kernel<64, 1, true> : combine_kernel<64, 0, true>)
+                    : (bf ? combine_kernel<64, 1, false> : combine_kernel<64, 0, false>);
+    return launch_pdl(kern, dim3((unsigned)blocks), dim3(kCombineThreads), 0, s, num_seqs, q_heads, r, seq_lens,
+                      split_off, part_lse, part_o, o, o_seq_stride, lse);
 }
 
 cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim, const int32_t *split_off,
                                  const float *part_lse, const float *part_o, int o_dtype, const PeerTargets &t,
-                                 cudaStream_t s) {
-    const int64_t heads = (int64_t)num_seqs * q_heads;
-    if (heads == 0) return cudaSuccess;
-    const int threads = 128;
-    const int64_t blocks = (heads + threads / (head_dim / 4) - 1) / (threads / (head_dim / 4));
-    auto kern = head_dim == 128 ? (o_dtype == HETIS_BF16 ? combine_peers_kernel<128, 1> : combine_peers_kernel<128, 0>)
-                                : (o_dtype == HETIS_BF16 ? combine_peers_kernel<64, 1> : combine_peers_kernel<64, 0>);
-    return launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), 0, s, num_seqs, q_heads, r, split_off, part_lse,
-                      part_o, t);
+                                 cudaStream_t s, int max_seq_len) {
+    const int64_t pairs = (int64_t)num_seqs * q_heads;
+    if (pairs == 0) return cudaSuccess;
+    const bool wide = (max_seq_len + kSplitTokens - 1) / kSplitTokens > kNarrowSplits;
+    const int g = kCombineThreads / (head_dim / 4);
+    const int64_t blocks = wide ? pairs : (pairs + g - 1) / g;
+    const bool bf = o_dtype == HETIS_BF16;
+    decltype(&combine_peers_kernel<128, 0, false>) kern;
+    if (head_dim == 128)
+        kern = wide ? (bf ? combine_peers_kernel<128, 1, true> : combine_peers_kernel<128, 0, true>)
+                    : (bf ? combine_peers_kernel<128, 1, false> : combine_peers_kernel<128, 0, false>);
+    else
+        kern = wide ? (bf ? combine_peers_kernel<64, 1, true> : combine_peers_kernel<64, 0, true>)
+                    : (bf ? combine_peers_kernel<64, 1, false> : combine_peers_kernel<64, 0, false>);
+    return launch_pdl(kern, dim3((unsigned)blocks), dim3(kCombineThreads), 0, s, num_seqs, q_heads, r, split_off,
+                      part_lse, part_o, t);
 }
 
 cudaError_t launch_peer_wait(const int64_t *sig, int n, int64_t epoch, cudaStream_t s) {
