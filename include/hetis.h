@@ -100,6 +100,11 @@ typedef struct {
 /* bf16 GQA tensor-core kernel with the shared page ring and per-item CTA merge
  * (the default gives every consumer warp whole items and its own sub-ring). */
 #define HETIS_ATTN_TC_SHARED_RING 0x2u
+/* bf16 GQA tensor-core kernel: claim work items device-wide instead of dealing
+ * them to SMs round-robin.  For decode that shares the SMs with another kernel
+ * (e.g. hetis_kv_migrate on a low-priority stream, the Hauler): slowed SMs take
+ * fewer items (c3 beside a 16-CTA migration: 1.16x instead of 1.4x step time). */
+#define HETIS_ATTN_DEVICE_CLAIM 0x4u
 /* Diagnostic only: stream every K/V page through the shared-memory ring but
  * skip the math (partials are left unwritten).  Measures the memory-system
  * ceiling of the pipeline; the CUDA-core kernel honours it. */

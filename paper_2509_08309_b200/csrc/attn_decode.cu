@@ -59,11 +59,13 @@ constexpr int kQSlots = 2;
 #ifndef HETIS_MAX_STAGES
 #define HETIS_MAX_STAGES 24
 #endif
-#ifndef HETIS_GLOBAL_CLAIM
-// 0: items dealt to CTAs round-robin, claimed dynamically by the CTA's warps
-// (default: measured best for c3 at N = 2, 4, 8); 1: device-wide claiming
-// (+1.5% at N = 1, -10% at N = 4 on c3).
-#define HETIS_GLOBAL_CLAIM 0
+#ifndef HETIS_STATIC_PCT
+// Work distribution of the per-warp GQA kernel: the first HETIS_STATIC_PCT % of
+// the items are dealt to CTAs round-robin and claimed dynamically by each CTA's
+// warps; a CTA that runs out steals from the rest through a device-wide counter.
+// (Sweep on c3 at N = 1..8: 95 ~ 100 > 85 > 70; HETIS_ATTN_DEVICE_CLAIM switches
+// to device-wide claiming for SMs of unequal speed.)
+#define HETIS_STATIC_PCT 95
 #endif
 #ifndef HETIS_WARP_STAGES
 #define HETIS_WARP_STAGES 4
@@ -787,23 +789,28 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             for (int i = 0; i < kPagesPerItem; ++i) nxt[i] = i < np ? __ldg(row + i) : 0;
         }
     };
-    // Work is claimed dynamically: every lane takes the next item from a
-    // device-wide counter when its worker needs work (HETIS_GLOBAL_CLAIM, the
-    // default), so faster SMs and warps take more items and the kernel ends
-    // within about one item of perfect balance; the alternative deals items to
-    // CTAs round-robin and claims only within the CTA.  One item is claimed
-    // ahead (its page ids load in the background); a claim past the end posts
-    // a sentinel.  The claim order never changes an item's arithmetic.
-    // The first round is static and interleaved over the CTAs (worker (cta, w)
-    // takes item w * gridDim.x + cta), so a problem smaller than one round is
-    // spread evenly over the SMs; claims after that come from the counter.
-#if HETIS_GLOBAL_CLAIM
-    auto claim = [&]() -> int { return (int)gridDim.x * NW + atomicAdd(p.counters, 1); };
-    int item = w * (int)gridDim.x + (int)blockIdx.x;
-#else
-    auto claim = [&]() -> int { return (int)blockIdx.x + atomicAdd(sm.claim, 1) * (int)gridDim.x; };
-    int item = claim();
-#endif
+    // Work is claimed dynamically, one item ahead per worker (its page ids load in
+    // the background); a claim past the end posts a sentinel.  The claim order
+    // never changes an item's arithmetic (split boundaries depend on L_j only).
+    // Device-wide claiming (HETIS_ATTN_DEVICE_CLAIM): the first round is static and
+    // interleaved over the CTAs (worker (cta, w) takes item w * grid + cta), every later
+    // claim comes from the device-wide counter -- SMs slowed by another kernel (e.g. a
+    // migration on a side stream) simply take fewer items.  Default: CTA-local items
+    // [0, n_static) (CTA c: c, c + grid, ...), then stealing from [n_static, n_items).
+    const bool device_claim = (p.flags & HETIS_ATTN_DEVICE_CLAIM) != 0;
+    const int per_cta = device_claim ? 0 : (int)(((long long)n_items * HETIS_STATIC_PCT / 100) / gridDim.x);
+    const int n_static = device_claim ? (int)gridDim.x * NW : per_cta * (int)gridDim.x;
+    auto claim = [&]() -> int {
+        if (!device_claim) {
+            const int k = atomicAdd(sm.claim, 1);
+            if (k < per_cta) return (int)blockIdx.x + k * (int)gridDim.x;
+        }
+        // the device-wide counter is reset by the previous launch's last CTA: never touch it
+        // before that launch has completed (a no-op once this thread has waited)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        return n_static + atomicAdd(p.counters, 1);
+    };
+    int item = device_claim ? w * (int)gridDim.x + (int)blockIdx.x : claim();
     // The next item is claimed lazily, once half of the current item's pages
     // are issued: a worker on a faster SM gets there sooner, which is what
     // balances the device (claiming at the start would hand out every item
@@ -1085,7 +1092,6 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     } else {
         consumer_warp_items<D, R, NW>(p, sm, SW, n_items);
     }
-#if HETIS_GLOBAL_CLAIM
     // the last CTA to finish returns the device-wide counters to zero for the next launch
     __syncwarp();
     __syncthreads();
@@ -1096,7 +1102,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
             p.counters[1] = 0;
         }
     }
-#endif
+
 }
 
 template <int D, int R>

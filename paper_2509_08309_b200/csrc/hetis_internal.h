@@ -96,8 +96,20 @@ int num_sms();
 // this library executes griddepcontrol.wait before its first global-memory
 // access (so stream order is preserved) and then griddepcontrol.launch_dependents,
 // which hides launch latency and CTA scheduling between the step's kernels.
+// Every kernel of the library prefers the maximum shared-memory carveout: the
+// persistent attention kernel needs ~217 KB per SM, and a small kernel (append,
+// combine, migration on a side stream) that lands first on an SM with a smaller
+// carveout would keep the attention CTA off that SM until it drains.
+void prefer_max_smem_once(const void *kern);  // small_kernels.cu: once per kernel (and device)
+
+template <typename... KArgs>
+void prefer_max_smem(void (*kern)(KArgs...)) {
+    prefer_max_smem_once(reinterpret_cast<const void *>(kern));
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args &&...args) {
+    prefer_max_smem(kern);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;

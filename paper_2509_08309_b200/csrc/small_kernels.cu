@@ -8,6 +8,9 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "device_utils.cuh"
 #include "hetis_internal.h"
@@ -275,6 +278,16 @@ __global__ void head_copy_kernel(const uint8_t *src, uint8_t *dst, int num_seqs,
 }  // namespace
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void prefer_max_smem_once(const void *kern) {
+    static std::mutex mu;
+    static std::set<std::pair<int, const void *>> seen;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    if (seen.insert({dev, kern}).second)
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 int num_sms() {

@@ -25,6 +25,7 @@ STATUS = {0: "HETIS_OK", 1: "HETIS_E_INVALID", 2: "HETIS_E_HEAD_INTEGRITY", 3: "
 F32, BF16 = 0, 1
 ATTN_FORCE_SIMT = 0x1
 ATTN_TC_SHARED_RING = 0x2
+ATTN_DEVICE_CLAIM = 0x4
 ATTN_DIAG_STREAM_ONLY = 0x100
 
 EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_split_tokens",
