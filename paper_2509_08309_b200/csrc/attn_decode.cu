@@ -67,6 +67,11 @@ constexpr int kQSlots = 2;
 // to device-wide claiming for SMs of unequal speed.)
 #define HETIS_STATIC_PCT 95
 #endif
+#ifndef HETIS_CLAIM_AT
+// a worker claims its next item once HETIS_CLAIM_AT / 16 of the current item's pages are issued
+// (sweep on c3 N = 1..8 with the static share at 90 / 100: 8, 12 and 16 within +-2%)
+#define HETIS_CLAIM_AT 8
+#endif
 #ifndef HETIS_WARP_STAGES
 #define HETIS_WARP_STAGES 4
 #endif
@@ -198,9 +203,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define HETIS_TS(slot) (g_trace[blockIdx.x & 1023][(slot)] = gtimer())
 #define HETIS_TS_MAX(slot) atomicMax(&g_trace[blockIdx.x & 1023][(slot)], gtimer())
+#define HETIS_TS_ADD(slot) atomicAdd(&g_trace[blockIdx.x & 1023][(slot)], 1ull)
+#define HETIS_TS_SMID(slot)                                  \
+    do {                                                     \
+        unsigned sm_;                                        \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));     \
+        g_trace[blockIdx.x & 1023][(slot)] = sm_;            \
+    } while (0)
 #else
 #define HETIS_TS(slot) ((void)0)
 #define HETIS_TS_MAX(slot) ((void)0)
+#define HETIS_TS_ADD(slot) ((void)0)
+#define HETIS_TS_SMID(slot) ((void)0)
 #endif
 
 // ---------------------------------------------------------------- producer (kProducerLanes threads)
@@ -865,7 +879,7 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
                 HETIS_TS(3);
             }
         }
-        if (next < 0 && 2 * pg >= np) {
+        if (next < 0 && kPagesPerItem * pg >= HETIS_CLAIM_AT * np) {
             next = claim();
             load_next(next);
         }
@@ -919,6 +933,9 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     for (int it = 0;; ++it) {
         dev::mbar_wait(&sm.qfull[w], it & 1);
         const ItemMeta meta = sm.meta[w];
+        if (lane == 0 && meta.item >= 0) {
+            HETIS_TS_ADD(7);
+        }
         if (meta.item < 0) {  // sentinel: the CTA's items are exhausted
             if (lane == 0) {
                 HETIS_TS_MAX(5);
@@ -1080,6 +1097,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     }
     if (threadIdx.x == 0) {
         HETIS_TS(0);
+        HETIS_TS_SMID(6);
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     build_split_offsets(p, s_len, s_off);  // contains __syncthreads

@@ -121,10 +121,10 @@ __device__ __forceinline__ void pdl_wait_then_release() {
 }
 
 // Allow the next kernel to be scheduled now, then wait for the previous one.
-// Used by the combine: its dependents (kv_append of the next step, the merge,
-// or an attention launch) all execute griddepcontrol.wait before touching
-// anything the combine or its predecessors write, so they may be resident and
-// waiting while the combine runs.
+// Used by the combine and kv_append: their dependents execute griddepcontrol.wait
+// before touching anything these kernels or their predecessors write -- except
+// the attention prologue, which reads only q, seq_lens and block tables, and no
+// kernel that releases early writes those (hetis_seq_split_lens never releases).
 __device__ __forceinline__ void pdl_release_then_wait() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");

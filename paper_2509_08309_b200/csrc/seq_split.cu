@@ -27,7 +27,9 @@ namespace {
 
 __global__ void seq_split_lens_kernel(int num_ranks, int rank, int page_size, int num_seqs, const int32_t *seq_lens,
                                       int32_t *local_lens, int32_t *append_lens) {
-    dev::pdl_wait_then_release();
+    // no early release: these lengths are the seq_lens the attention kernel reads in its
+    // prologue before it waits, so dependents may only start once this kernel is complete
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= num_seqs) return;
     const int L = seq_lens[j];

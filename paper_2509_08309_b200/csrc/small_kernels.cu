@@ -25,7 +25,10 @@ std::atomic<uint64_t> g_launches{0};
 __global__ void kv_append_kernel(int num_seqs, int kv_heads, int row_bytes, int page_size, const uint8_t *k_new,
                                  const uint8_t *v_new, uint8_t *k_pool, uint8_t *v_pool, const int32_t *block_table,
                                  int max_pages, const int32_t *seq_lens) {
-    dev::pdl_wait_then_release();
+    // release first: the attention kernel that follows may run its prologue (q, seq_lens and
+    // block tables only -- no library kernel that releases early writes those) while this
+    // kernel waits for its predecessor; its page copies wait for this kernel to complete
+    dev::pdl_release_then_wait();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= num_seqs * kv_heads) return;

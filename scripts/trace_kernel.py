@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--heads", type=int, default=8)
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--len", type=int, default=2048)
+    ap.add_argument("--flags", type=int, default=0)
     a = ap.parse_args()
     shape = workload.LLAMA2_70B
     lens = torch.full((a.batch,), a.len, dtype=torch.int32)
@@ -42,7 +43,7 @@ def main():
         L.hetis_trace_read(buf.ctypes.data, buf.nbytes, 1)          # clear
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-        hetis.attn_partial(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, a.len, ws)
+        hetis.attn_partial(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, a.len, ws, flags=a.flags)
         ev1.record()
         torch.cuda.synchronize()
     L.hetis_trace_read(buf.ctypes.data, buf.nbytes, 0)
@@ -57,7 +58,24 @@ def main():
     for k, name in enumerate(names):
         v = (t[:, k] - t0) / 1e3
         print(f"  {name:22s} min {v.min():8.2f} us  median {np.median(v):8.2f} us  max {v.max():8.2f} us")
+    done = (t[:, 5] - t0) / 1e3
+    smid, items = buf[:n, 6].astype(np.int64), buf[:n, 7].astype(np.int64)
+    print("  finish deciles (us):", " ".join(f"{x:.1f}" for x in np.percentile(done, np.arange(0, 101, 10))))
+    print(f"  items per CTA: min {items.min()} median {int(np.median(items))} max {items.max()} total {items.sum()}")
+    rate = items / np.maximum(done - (t[:, 4] - t0) / 1e3, 1e-3)     # items per us after the first page
+    order = np.argsort(done)
+    print("  slowest CTAs (smid, items, done us):", [(int(smid[i]), int(items[i]), round(float(done[i]), 1))
+                                                    for i in order[-8:]])
+    print("  fastest CTAs (smid, items, done us):", [(int(smid[i]), int(items[i]), round(float(done[i]), 1))
+                                                    for i in order[:8]])
+    # per-SM throughput by SM id bands (two dies: 0..73 / 74..147 if numbered that way)
+    for lo in range(0, n, 37):
+        m = (smid >= lo) & (smid < lo + 37)
+        if m.any():
+            print(f"  smid {lo:3d}-{lo + 36:3d}: items/us median {np.median(rate[m]):.3f}, done median "
+                  f"{np.median(done[m]):.1f} us")
 
 
 if __name__ == "__main__":
     main()
+
