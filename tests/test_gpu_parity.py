@@ -379,3 +379,26 @@ def test_device_claim_flag_is_bit_identical(lens):
     torch.cuda.synchronize()
     for o in outs[1:]:
         assert torch.equal(o, outs[0])
+
+
+# ------------------------------------------------------------------ combine arithmetic is launch-shape independent
+@pytest.mark.parametrize("H,Hkv,D", [(40, 40, 128), (64, 8, 128), (8, 8, 64)])
+def test_combine_narrow_and_wide_launches_give_identical_rows(H, Hkv, D):
+    """The combine folds a request with <= 16 splits with one thread group whatever the launch shape: a
+    batch whose longest request has > 16 splits launches one block per row (wide), a batch without one
+    launches four rows per block (narrow).  The short requests' rows must be bit-identical either way."""
+    dt = "f32" if D == 64 else "bf16"
+    lens = (300, 1029, 17, 4096, 5000)          # 2, 5, 1, 16 and 20 splits of 256
+    b = gpu_batch(H, Hkv, D, dt, lens, 83)
+    s = hetis.make_shape(b.shape)
+    hetis.kv_append(s, b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens)
+    B, x, _ = b.q.shape
+    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, 5000), "cuda")
+    hetis.attn_partial(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, 5000, ws)
+    wide = torch.full((B, x, D), float("nan"), device="cuda")
+    hetis.attn_combine(s, b.seq_lens, 5000, wide, ws)                       # > 16 splits present: wide launch
+    narrow = torch.full((4, x, D), float("nan"), device="cuda")
+    hetis.attn_combine(s, b.seq_lens[:4], 4096, narrow, ws, q_head_count=x)  # <= 16 splits: narrow launch
+    torch.cuda.synchronize()
+    assert torch.equal(wide[:4], narrow)
+    assert_close(wide, oracle_full(b), "combine (wide launch) vs oracle")
