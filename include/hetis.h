@@ -105,6 +105,9 @@ typedef struct {
  * (e.g. hetis_kv_migrate on a low-priority stream, the Hauler): slowed SMs take
  * fewer items (c3 beside a 16-CTA migration: 1.16x instead of 1.4x step time). */
 #define HETIS_ATTN_DEVICE_CLAIM 0x4u
+/* bf16 MHA (r = 1) on the per-warp tensor-core kernel (one valid MMA row)
+ * instead of the CUDA-core kernel. */
+#define HETIS_ATTN_MHA_TC 0x8u
 /* Diagnostic only: stream every K/V page through the shared-memory ring but
  * skip the math (partials are left unwritten).  Measures the memory-system
  * ceiling of the pipeline; the CUDA-core kernel honours it. */

@@ -409,7 +409,8 @@ hetis_status hetis_attn_partial(const hetis_shape *shape, int32_t num_seqs, int3
     if (num_seqs == 0) return HETIS_OK;
     a.flags = flags;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const bool tc = a.dtype == HETIS_BF16 && a.r > 1 && !(flags & HETIS_ATTN_FORCE_SIMT);
+    const bool tc = a.dtype == HETIS_BF16 && (a.r > 1 || (flags & HETIS_ATTN_MHA_TC)) &&
+                    !(flags & HETIS_ATTN_FORCE_SIMT);
     cudaError_t e;
     std::string err;
     if (tc) {

@@ -1373,6 +1373,8 @@ cudaError_t launch_attn_tc(const AttnArgs &a, cudaStream_t s, std::string *err) 
         case 64 * 16 + 2: return launch_gqa_warp<64, 2>(p, a.num_seqs, s, tk, tv, err);
         case 64 * 16 + 4: return launch_gqa_warp<64, 4>(p, a.num_seqs, s, tk, tv, err);
         case 64 * 16 + 8: return launch_gqa_warp<64, 8>(p, a.num_seqs, s, tk, tv, err);
+        case 128 * 16 + 1: return launch_gqa_warp<128, 1>(p, a.num_seqs, s, tk, tv, err);
+        case 64 * 16 + 1: return launch_gqa_warp<64, 1>(p, a.num_seqs, s, tk, tv, err);
         default: break;
     }
     return cudaErrorInvalidValue;

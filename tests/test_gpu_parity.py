@@ -386,19 +386,50 @@ def test_device_claim_flag_is_bit_identical(lens):
 def test_combine_narrow_and_wide_launches_give_identical_rows(H, Hkv, D):
     """The combine folds a request with <= 16 splits with one thread group whatever the launch shape: a
     batch whose longest request has > 16 splits launches one block per row (wide), a batch without one
-    launches four rows per block (narrow).  The short requests' rows must be bit-identical either way."""
+    launches four rows per block (narrow).  The same requests must get bit-identical rows either way."""
     dt = "f32" if D == 64 else "bf16"
     lens = (300, 1029, 17, 4096, 5000)          # 2, 5, 1, 16 and 20 splits of 256
     b = gpu_batch(H, Hkv, D, dt, lens, 83)
     s = hetis.make_shape(b.shape)
     hetis.kv_append(s, b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens)
-    B, x, _ = b.q.shape
-    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, 5000), "cuda")
-    hetis.attn_partial(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, 5000, ws)
-    wide = torch.full((B, x, D), float("nan"), device="cuda")
-    hetis.attn_combine(s, b.seq_lens, 5000, wide, ws)                       # > 16 splits present: wide launch
-    narrow = torch.full((4, x, D), float("nan"), device="cuda")
-    hetis.attn_combine(s, b.seq_lens[:4], 4096, narrow, ws, q_head_count=x)  # <= 16 splits: narrow launch
-    torch.cuda.synchronize()
+    wide = run_gpu(b, append=False)                                          # 20 splits present: wide launch
+    first4 = workload.DecodeBatch(b.shape, 0, H, b.q[:4].contiguous(), b.k_new[:4].contiguous(),
+                                  b.v_new[:4].contiguous(), b.k_pool, b.v_pool, b.block_table[:4].contiguous(),
+                                  b.seq_lens[:4].contiguous())
+    narrow = run_gpu(first4, append=False)                                   # <= 16 splits: narrow launch
     assert torch.equal(wide[:4], narrow)
     assert_close(wide, oracle_full(b), "combine (wide launch) vs oracle")
+
+
+# ------------------------------------------------------------------ MHA on tensor cores (HETIS_ATTN_MHA_TC)
+@pytest.mark.parametrize("D", [128, 64])
+@pytest.mark.parametrize("peaked", [False, True])
+def test_mha_on_tensor_cores_matches_oracle(D, peaked):
+    """r = 1 on the per-warp tensor-core kernel (one valid MMA row, P carried as P_hi + P_lo): within the
+    north-star tolerance of the oracle, including peaked keys (K x 4) that would fail a bf16-rounded P."""
+    lens = (1, 15, 16, 17, 255, 256, 257, 1029)
+    b = gpu_batch(8, 8, D, "bf16", lens, seed=91)
+    if peaked:
+        b.k_pool.mul_(4)
+        b.k_new.mul_(4)
+    o_tc = run_gpu(b, flags=hetis.ATTN_MHA_TC)
+    o_simt = run_gpu(b, append=False)
+    ref = oracle_full(b)
+    assert_close(o_tc, ref, "mha tc")
+    assert (o_tc - o_simt).abs().max().item() < 1e-3
+    # L = 1 returns the V row bit for bit on the tensor-core path too
+    v_row = b.v_new[0].float()
+    assert torch.equal(o_tc[0], v_row)
+
+
+def test_mha_tc_head_partition_bit_identical():
+    shape = workload.Shape(40, 40, 128, 16, "bf16")
+    lens = torch.tensor([600, 5, 1300, 256], dtype=torch.int32)
+    full = workload.make_decode_batch(shape, lens, 23, "cuda")
+    o_full = run_gpu(full, flags=hetis.ATTN_MHA_TC)
+    begin, outs = 0, []
+    for i, x in enumerate((16, 8, 8, 4, 4)):
+        part = workload.make_decode_batch(shape, lens, 23, "cuda", q_begin=begin, q_count=x, rank_salt=i + 1)
+        outs.append(run_gpu(part, flags=hetis.ATTN_MHA_TC))
+        begin += x
+    assert torch.equal(torch.cat(outs, 1), o_full)
