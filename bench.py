@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--graph", type=int, default=1, help="N = 1: replay the K timed steps as one CUDA graph")
     ap.add_argument("--gather", default="nccl", choices=["nccl", "peer"],
                     help="N > 1: NCCL all-gather of O (default) or the combine kernel's peer-memory stores")
+    ap.add_argument("--scatter", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1: 'peer' = every rank pulls its q / new k, v shard from the root's buffers over "
+                         "NVLink (hetis_peer_signal + hetis_scatter_pull) instead of NCCL send/recv")
     return ap.parse_args()
 
 
@@ -256,8 +259,8 @@ def run_ours(args, world, rank, local):
         vn_full = (torch.randn((B, shape.num_kv_heads, shape.head_dim), generator=gq, device=device)
                    .to(shape.torch_dtype) if is_root else None)
         o_full = torch.empty((B, shape.num_q_heads, shape.head_dim), dtype=odt, device=device)
-        if args.gather == "peer":
-            step.setup_peers(o_full)
+        if args.gather == "peer" or args.scatter == "peer":
+            step.setup_peers(o_full, q_full, kn_full, vn_full)
     else:
         step.buf.q_shard.copy_(batch.q)
         step.buf.k_new.copy_(batch.k_new)
@@ -267,7 +270,11 @@ def run_ours(args, world, rank, local):
 
     def one_step(i, ev_a=None, ev_b=None):
         li = i % n_layers
-        if world > 1:
+        if world > 1 and (args.gather == "peer" or args.scatter == "peer"):
+            step.epoch += 1
+        if world > 1 and args.scatter == "peer":
+            step.scatter_peers(step.epoch)
+        elif world > 1:
             step.scatter(q_full, kn_full, vn_full)
         step.append(k_pools[li], v_pools[li], batch.block_table, batch.seq_lens)
         if ev_a is not None:
@@ -279,7 +286,6 @@ def run_ours(args, world, rank, local):
             ev_b.record(torch.cuda.current_stream(device))
         if world > 1 and args.gather == "peer":
             # one kernel merges the splits and stores O into every rank's o_full over NVLink
-            step.epoch += 1
             hetis.attn_combine_peers(step.cshape, batch.seq_lens, max_len, step.o_peers, step.sig_peers, rank,
                                      step.epoch, step.buf.workspace, q_head_begin=q_begin, q_head_count=q_count)
             hetis.peer_wait(step.sig, step.epoch)
@@ -440,6 +446,7 @@ def run_ours(args, world, rank, local):
                 "head_dim": shape.head_dim, "page_size": shape.page_size, "split": list(split),
                 "o_dtype": args.o_dtype, "layers_rotated": n_layers,
                 "gather": (args.gather if world > 1 else None),
+                "scatter": (args.scatter if world > 1 else None),
                 "l2": f"inputs larger than L2: {n_layers} layer pool(s) x {kv_bytes_rank / 1e6:.1f} MB KV per rank "
                       f"rotated per step (L2 = 126 MB)",
                 "tokens": "one token = one request's decode step of one layer, all heads"},

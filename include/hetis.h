@@ -252,6 +252,29 @@ HETIS_API hetis_status hetis_attn_combine_peers(const hetis_shape *shape, int32_
 HETIS_API hetis_status hetis_peer_wait(const int64_t *signal_local, int32_t num_ranks, int64_t epoch,
                                        hetis_stream_t stream);
 
+/* ---- scatter over peer memory (NVLink 5 / NVSwitch) --------------------- */
+/* The Primary's half of a pull-based scatter (a2): once q_full, k_new_full and
+ * v_new_full of step `epoch` are written (everything before this call on the
+ * stream), publish `epoch` into slot [rank] of every rank's signal array
+ * (system-scope release).  signal_peers: host array [num_ranks] of device
+ * pointers to each rank's int64 [num_ranks] array, mapped in this process
+ * (zero-initialised once; epochs strictly increase).  num_ranks <= 8. */
+HETIS_API hetis_status hetis_peer_signal(int64_t *const *signal_peers, int32_t num_ranks, int32_t rank,
+                                         int64_t epoch, hetis_stream_t stream);
+/* The workers' half: wait (stream-ordered, acquire; traps after ~10 s if the
+ * root never signals) until signal_local[root] >= epoch, then copy this
+ * rank's plan range straight from the root's buffers (mapped over NVLink):
+ *   q_full_root [num_seqs][H][d] heads [b, b + x)       -> q_shard [num_seqs][x][d]
+ *   k/v_new_full_root [num_seqs][H_kv][d] [b/r, (b+x)/r) -> k/v_new_shard [num_seqs][x/r][d]
+ * One kernel, no NCCL: the same result as hetis_scatter_q.  The root may
+ * overwrite its buffers only after every rank has consumed them (e.g. after
+ * the step's O exchange, hetis_peer_wait). */
+HETIS_API hetis_status hetis_scatter_pull(const hetis_plan *plan, int32_t rank, int32_t num_seqs,
+                                          const int64_t *signal_local, int32_t root, int64_t epoch,
+                                          const void *q_full_root, const void *k_new_full_root,
+                                          const void *v_new_full_root, void *q_shard, void *k_new_shard,
+                                          void *v_new_shard, hetis_stream_t stream);
+
 /* ---- scatter / gather over NCCL ------------------- */
 /* nccl_comm is an ncclComm_t (e.g. torch ProcessGroupNCCL._comm_ptr()) whose
  * ranks are the plan's devices.  libnccl.so.2 is resolved at first use from

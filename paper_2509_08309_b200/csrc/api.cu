@@ -532,6 +532,52 @@ hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_seqs, int32
                               (int64_t)q_head_count * shape->head_dim, workspace, workspace_bytes, stream);
 }
 
+// ---------------------------------------------------------------- scatter over peer memory
+hetis_status hetis_peer_signal(int64_t *const *signal_peers, int32_t num_ranks, int32_t rank, int64_t epoch,
+                               hetis_stream_t stream) {
+    if (!signal_peers || num_ranks < 1 || num_ranks > hetis::kMaxPeers || rank < 0 || rank >= num_ranks)
+        return fail(HETIS_E_INVALID, "num_ranks must be 1..8 and rank inside it");
+    if (epoch < 1) return fail(HETIS_E_INVALID, "epoch must be >= 1");
+    hetis::PeerSignal t{};
+    for (int p = 0; p < num_ranks; ++p) {
+        if (!signal_peers[p] || !aligned(signal_peers[p], 8)) return fail(HETIS_E_INVALID, "bad signal pointer");
+        t.sig[p] = signal_peers[p];
+    }
+    t.n = num_ranks;
+    t.rank = rank;
+    t.epoch = epoch;
+    cudaError_t e = hetis::launch_peer_signal(t, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "peer_signal launch");
+    return HETIS_OK;
+}
+
+hetis_status hetis_scatter_pull(const hetis_plan *plan, int32_t rank, int32_t num_seqs, const int64_t *signal_local,
+                                int32_t root, int64_t epoch, const void *q_full_root, const void *k_new_full_root,
+                                const void *v_new_full_root, void *q_shard, void *k_new_shard, void *v_new_shard,
+                                hetis_stream_t stream) {
+    if (!plan) return fail(HETIS_E_INVALID, "plan is NULL");
+    if (plan->per_request) return fail(HETIS_E_UNSUPPORTED, "scatter needs a global (per_request = 0) plan");
+    if (rank < 0 || rank >= plan->num_devices || root < 0 || root >= plan->num_devices)
+        return fail(HETIS_E_INVALID, "rank / root outside the plan");
+    if (num_seqs < 0 || epoch < 1) return fail(HETIS_E_INVALID, "bad num_seqs / epoch");
+    if (num_seqs == 0 || plan->x[rank] == 0) return HETIS_OK;
+    if (!signal_local || !q_full_root || !k_new_full_root || !v_new_full_root || !q_shard || !k_new_shard ||
+        !v_new_shard)
+        return fail(HETIS_E_INVALID, "NULL pointer");
+    const void *ptrs[] = {q_full_root, k_new_full_root, v_new_full_root, q_shard, k_new_shard, v_new_shard};
+    for (const void *ptr : ptrs)
+        if (!aligned(ptr, 16)) return fail(HETIS_E_INVALID, "buffers must be 16-byte aligned");
+    const hetis_shape &s = plan->shape;
+    const int r = s.num_q_heads / s.num_kv_heads;
+    const int x = plan->x[rank], b = plan->begin[rank];
+    cudaError_t e = hetis::launch_scatter_pull(
+        signal_local + root, epoch, q_full_root, k_new_full_root, v_new_full_root, num_seqs, s.num_q_heads,
+        s.num_kv_heads, b, x, b / r, x / r, s.head_dim * esize(s.q_dtype), s.head_dim * esize(s.kv_dtype), q_shard,
+        k_new_shard, v_new_shard, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "scatter_pull launch");
+    return HETIS_OK;
+}
+
 // ---------------------------------------------------------------- scatter / gather
 hetis_status hetis_comm_workspace(const hetis_plan *plan, int32_t rank, int32_t num_seqs, size_t *bytes) {
     if (!plan || !bytes) return fail(HETIS_E_INVALID, "NULL argument");

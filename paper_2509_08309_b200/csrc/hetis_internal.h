@@ -82,6 +82,15 @@ cudaError_t launch_seq_split_lens(int num_ranks, int rank, int page_size, int nu
 cudaError_t launch_seq_merge(int num_parts, int num_seqs, int q_heads, int head_dim, const float *o_parts,
                              int64_t o_part_stride, const float *lse_parts, int64_t lse_part_stride, void *o,
                              int o_dtype, int64_t o_seq_stride, cudaStream_t s);
+struct PeerSignal {
+    int64_t *sig[kMaxPeers];   // every rank's signal array, mapped in this process
+    int n, rank;
+    int64_t epoch;
+};
+cudaError_t launch_peer_signal(const PeerSignal &t, cudaStream_t s);
+cudaError_t launch_scatter_pull(const int64_t *sig, int64_t epoch, const void *q_src, const void *k_src,
+                                const void *v_src, int num_seqs, int H, int Hkv, int q0, int nq, int k0, int nk,
+                                int qrow, int kvrow, void *q_dst, void *k_dst, void *v_dst, cudaStream_t s);
 cudaError_t launch_peer_wait(const int64_t *sig, int n, int64_t epoch, cudaStream_t s);
 cudaError_t launch_kv_migrate(int num_entries, const hetis_migration_entry *entries, int page_size, int page_bytes,
                               const void *src_k, const void *src_v, const int32_t *src_bt, int src_max_pages,

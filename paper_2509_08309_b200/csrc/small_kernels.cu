@@ -260,6 +260,68 @@ __global__ void peer_wait_kernel(const int64_t *sig, int n, int64_t epoch) {
     }
 }
 
+// ---------------------------------------------------------------- scatter over peer memory
+// Publish `epoch` into slot [rank] of every rank's signal array (system-scope
+// release) once everything before it on the stream is complete and visible.
+__global__ void peer_signal_kernel(PeerSignal t) {
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int p = 0; p < t.n; ++p)
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(t.sig[p] + t.rank), "l"(t.epoch) : "memory");
+    }
+}
+
+// Pull this rank's shard of the step's inputs straight from the Primary's buffers
+// (mapped over NVLink): every block's thread 0 waits (acquire, bounded) until the
+// Primary published `epoch`, then the block copies 16-byte chunks of
+//   q      [B][H][d]     heads [q0, q0 + nq)   -> q_shard [B][nq][d]
+//   k, v   [B][Hkv][d]   heads [k0, k0 + nk)   -> k/v_shard [B][nk][d]
+__global__ void scatter_pull_kernel(const int64_t *sig, int64_t epoch, const uint8_t *q_src, const uint8_t *k_src,
+                                    const uint8_t *v_src, int num_seqs, int H, int Hkv, int q0, int nq, int k0, int nk,
+                                    int qrow, int kvrow, uint8_t *q_dst, uint8_t *k_dst, uint8_t *v_dst) {
+    if (threadIdx.x == 0) {
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
+            int64_t v;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(sig) : "memory");
+            if (v >= epoch) break;
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 10000000000ull) __trap();
+            __nanosleep(100);
+        }
+    }
+    __syncthreads();
+    const int qc = qrow / 16, kc = kvrow / 16;
+    const int64_t nq_chunks = (int64_t)num_seqs * nq * qc, nk_chunks = (int64_t)num_seqs * nk * kc;
+    const int64_t total = nq_chunks + 2 * nk_chunks;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t *src;
+        uint8_t *dst;
+        if (i < nq_chunks) {
+            const int c = (int)(i % qc);
+            const int64_t row = i / qc;
+            const int h = (int)(row % nq), j = (int)(row / nq);
+            src = q_src + ((size_t)j * H + q0 + h) * qrow + 16 * c;
+            dst = q_dst + ((size_t)j * nq + h) * qrow + 16 * c;
+        } else {
+            const int64_t ii = (i - nq_chunks) % nk_chunks;
+            const bool is_v = (i - nq_chunks) >= nk_chunks;
+            const int c = (int)(ii % kc);
+            const int64_t row = ii / kc;
+            const int h = (int)(row % nk), j = (int)(row / nk);
+            src = (is_v ? v_src : k_src) + ((size_t)j * Hkv + k0 + h) * kvrow + 16 * c;
+            dst = (is_v ? v_dst : k_dst) + ((size_t)j * nk + h) * kvrow + 16 * c;
+        }
+        uint4 v;
+        asm volatile("ld.relaxed.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(src));
+        *reinterpret_cast<uint4 *>(dst) = v;
+    }
+}
+
 // ---------------------------------------------------------------- shard copies
 // src rows [B][src_heads] of row_bytes -> dst rows [B][dst_heads]; copies n heads
 // from src head offset hs to dst head offset hd.  16-byte chunks.
@@ -358,6 +420,28 @@ cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim,
 
 cudaError_t launch_peer_wait(const int64_t *sig, int n, int64_t epoch, cudaStream_t s) {
     peer_wait_kernel<<<1, 32, 0, s>>>(sig, n, epoch);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_peer_signal(const PeerSignal &t, cudaStream_t s) {
+    peer_signal_kernel<<<1, 32, 0, s>>>(t);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_pull(const int64_t *sig, int64_t epoch, const void *q_src, const void *k_src,
+                                const void *v_src, int num_seqs, int H, int Hkv, int q0, int nq, int k0, int nk,
+                                int qrow, int kvrow, void *q_dst, void *k_dst, void *v_dst, cudaStream_t s) {
+    const int64_t total = (int64_t)num_seqs * (nq * (qrow / 16) + 2 * nk * (kvrow / 16));
+    if (total == 0) return cudaSuccess;
+    const int threads = 256;
+    int64_t blocks = (total + threads - 1) / threads;
+    if (blocks > 2 * num_sms()) blocks = 2 * num_sms();
+    scatter_pull_kernel<<<(unsigned)blocks, threads, 0, s>>>(
+        sig, epoch, static_cast<const uint8_t *>(q_src), static_cast<const uint8_t *>(k_src),
+        static_cast<const uint8_t *>(v_src), num_seqs, H, Hkv, q0, nq, k0, nk, qrow, kvrow,
+        static_cast<uint8_t *>(q_dst), static_cast<uint8_t *>(k_dst), static_cast<uint8_t *>(v_dst));
     note_launch();
     return cudaGetLastError();
 }

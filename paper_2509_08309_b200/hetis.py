@@ -35,7 +35,7 @@ EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_
             "hetis_attn_combine", "hetis_attn_decode", "hetis_attn_combine_peers", "hetis_peer_wait",
             "hetis_comm_workspace", "hetis_scatter_q", "hetis_gather", "hetis_kv_migrate",
             "hetis_attn_combine_lse", "hetis_seq_split_lens", "hetis_seq_merge", "hetis_seq_broadcast_q",
-            "hetis_seq_allgather_merge", "hetis_launch_count")
+            "hetis_seq_allgather_merge", "hetis_peer_signal", "hetis_scatter_pull", "hetis_launch_count")
 
 
 class HetisError(RuntimeError):
@@ -98,6 +98,8 @@ def lib() -> ctypes.CDLL:
                 "hetis_seq_merge": (ctypes.c_int, [sp, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp]),
                 "hetis_seq_broadcast_q": (ctypes.c_int, [sp, vp, i32, i32, i32, i32, vp, vp, vp, vp]),
                 "hetis_seq_allgather_merge": (ctypes.c_int, [sp, vp, i32, i32, i32, vp, vp, vp, i64, vp]),
+                "hetis_peer_signal": (ctypes.c_int, [P(vp), i32, i32, i64, vp]),
+                "hetis_scatter_pull": (ctypes.c_int, [vp, i32, i32, vp, i32, i64, vp, vp, vp, vp, vp, vp, vp]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(L, name)
@@ -321,6 +323,24 @@ def attn_combine_peers(shape: CShape, seq_lens, max_seq_len: int, o_full_peers, 
 def peer_wait(signal_local, epoch: int, stream=None) -> None:
     _check(lib().hetis_peer_wait(_dev(signal_local, "signal_local"), signal_local.numel(), epoch, _stream(stream)),
            "hetis_peer_wait")
+
+
+def peer_signal(signal_peers, rank: int, epoch: int, stream=None) -> None:
+    """Publish `epoch` into slot [rank] of every rank's signal array (tensors or raw pointers mapped here)."""
+    n = len(signal_peers)
+    ptr = lambda t: t.data_ptr() if hasattr(t, "data_ptr") else int(t)
+    arr = (ctypes.c_void_p * n)(*[ptr(t) for t in signal_peers])
+    _check(lib().hetis_peer_signal(arr, n, rank, epoch, _stream(stream)), "hetis_peer_signal")
+
+
+def scatter_pull(plan: Plan, rank: int, num_seqs: int, signal_local, root: int, epoch: int, q_full_root,
+                 k_new_full_root, v_new_full_root, q_shard, k_new_shard, v_new_shard, stream=None) -> None:
+    """Wait for the root's epoch, then copy this rank's plan range from the root's (peer-mapped) buffers."""
+    ptr = lambda t: ctypes.c_void_p(t.data_ptr() if hasattr(t, "data_ptr") else int(t))
+    _check(lib().hetis_scatter_pull(plan.handle, rank, num_seqs, _dev(signal_local, "signal_local"), root, epoch,
+                                    ptr(q_full_root), ptr(k_new_full_root), ptr(v_new_full_root),
+                                    _dev(q_shard, "q_shard"), _dev(k_new_shard, "k_new_shard"),
+                                    _dev(v_new_shard, "v_new_shard"), _stream(stream)), "hetis_scatter_pull")
 
 
 # ---------------------------------------------------------------- NCCL scatter / gather

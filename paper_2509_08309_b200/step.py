@@ -92,26 +92,46 @@ class DecodeStep:
         hetis.gather(self.plan, self.comm_ptr, self.rank, root, self.num_seqs, self.buf.o_shard, o_full,
                      self.buf.comm_ws, stream)
 
-    # ---- fused combine + all-gather over peer memory (NVLink), see hetis_attn_combine_peers
-    def setup_peers(self, o_full: torch.Tensor) -> None:
-        """Map every rank's o_full and signal array into this process (CUDA IPC handles exchanged with
-        torch.distributed; on one NVSwitch box the mappings are NVLink peer memory).  Collective."""
+    # ---- exchanges over peer memory (NVLink): pull scatter (hetis_scatter_pull) and the combine fused
+    # with the all-gather (hetis_attn_combine_peers)
+    def setup_peers(self, o_full: torch.Tensor, q_full=None, k_new_full=None, v_new_full=None) -> None:
+        """Map every rank's o_full and signal arrays, and the root's q_full / k_new_full / v_new_full, into
+        this process (CUDA IPC handles exchanged with torch.distributed; on one NVSwitch box the mappings
+        are NVLink peer memory).  Collective; only the root passes the *_full tensors."""
         import torch.distributed as dist
         from torch.multiprocessing.reductions import reduce_tensor
         self.o_full = o_full
-        self.sig = torch.zeros(self.world, dtype=torch.int64, device=self.device)
-        mine = (reduce_tensor(o_full), reduce_tensor(self.sig))
+        self.sig = torch.zeros(self.world, dtype=torch.int64, device=self.device)    # O epochs from every rank
+        self.qsig = torch.zeros(self.world, dtype=torch.int64, device=self.device)   # input epochs from the root
+        root_bufs = None
+        if self.rank == self.root:
+            root_bufs = tuple(reduce_tensor(t) for t in (q_full, k_new_full, v_new_full))
+        mine = (reduce_tensor(o_full), reduce_tensor(self.sig), reduce_tensor(self.qsig), root_bufs)
         everyone = [None] * self.world
         dist.all_gather_object(everyone, mine)
-        self.o_peers, self.sig_peers = [], []
-        for i, (ro, rs) in enumerate(everyone):
+        self.o_peers, self.sig_peers, self.qsig_peers = [], [], []
+        for i, (ro, rs, rq, _) in enumerate(everyone):
             if i == self.rank:
                 self.o_peers.append(o_full)
                 self.sig_peers.append(self.sig)
+                self.qsig_peers.append(self.qsig)
             else:
                 self.o_peers.append(ro[0](*ro[1]))
                 self.sig_peers.append(rs[0](*rs[1]))
+                self.qsig_peers.append(rq[0](*rq[1]))
+        if self.rank == self.root:
+            self.root_bufs = (q_full, k_new_full, v_new_full)
+        else:
+            self.root_bufs = tuple(f(*a) for f, a in everyone[self.root][3])
         self.epoch = 0
+
+    def scatter_peers(self, epoch: int, stream=None):
+        """Root: publish that this step's inputs are written; every rank: pull its heads' q and its kv heads'
+        new k, v straight from the root's buffers (one kernel, waits for the root's epoch)."""
+        if self.rank == self.root:
+            hetis.peer_signal(self.qsig_peers, self.rank, epoch, stream=stream)
+        hetis.scatter_pull(self.plan, self.rank, self.num_seqs, self.qsig, self.root, epoch, *self.root_bufs,
+                           self.buf.q_shard, self.buf.k_new, self.buf.v_new, stream=stream)
 
     def attention_gather_peers(self, k_pool, v_pool, block_table, seq_lens, stream=None, flags: int = 0):
         """Partial attention, then ONE kernel that merges the splits and stores every row into every

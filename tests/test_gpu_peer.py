@@ -83,3 +83,81 @@ def test_combine_peers_two_ranks_one_gpu(shape_args, split):
     for rank, equal, diff, sig_min in out:
         assert sig_min == 2, (rank, sig_min)
         assert equal, (rank, diff)
+
+
+# ------------------------------------------------------------------ pull-based scatter over peer memory
+def _pull_rank(rank, port, shape_args, split, res, barrier):
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_2509_08309_b200 import hetis, workload
+    from paper_2509_08309_b200.step import DecodeStep
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)     # object exchange only; data moves by IPC
+    try:
+        torch.cuda.set_device(0)
+        shape = workload.Shape(*shape_args)
+        B, H, Hkv, D = 7, shape.num_q_heads, shape.num_kv_heads, shape.head_dim
+        plan = hetis.plan_create(hetis.make_shape(shape), 2, split)
+        step = DecodeStep(shape, plan, rank, B, 512, torch.device("cuda", 0))
+        g = torch.Generator(device="cuda").manual_seed(3)
+        mk = lambda *sz: torch.randn(sz, generator=g, device="cuda").to(shape.torch_dtype)
+        q_full, k_full, v_full = mk(B, H, D), mk(B, Hkv, D), mk(B, Hkv, D)   # same bits on both ranks
+        o_full = torch.zeros((B, H, D), device="cuda")
+        if rank == 0:
+            step.setup_peers(o_full, q_full, k_full, v_full)
+        else:
+            step.setup_peers(o_full)
+        ok = True
+        for epoch in (1, 2):
+            if rank == 0:
+                q_full.mul_(-1)                      # new inputs for this step, then signal
+                k_full.mul_(-1)
+                v_full.mul_(-1)
+                hetis.peer_signal(step.qsig_peers, 0, epoch)
+                torch.cuda.synchronize()
+            else:
+                q_full.mul_(-1)
+                k_full.mul_(-1)
+                v_full.mul_(-1)
+            barrier.wait(timeout=120)                # the root's signal is published before anyone pulls
+            step.buf.q_shard.zero_()
+            step.buf.k_new.zero_()
+            step.buf.v_new.zero_()
+            step.scatter_peers(epoch)
+            torch.cuda.synchronize()
+            b, x = plan.heads(rank)
+            r = shape.r
+            ok &= torch.equal(step.buf.q_shard, q_full[:, b:b + x])
+            ok &= torch.equal(step.buf.k_new, k_full[:, b // r:(b + x) // r])
+            ok &= torch.equal(step.buf.v_new, v_full[:, b // r:(b + x) // r])
+            ok &= int(step.qsig[0].item()) == epoch
+            barrier.wait(timeout=120)                # nobody changes the root's buffers while others pull
+        res.put((rank, bool(ok)))
+        barrier.wait(timeout=120)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shape_args,split", [((64, 8, 128, 16, "bf16"), (48, 16)),
+                                              ((40, 40, 128, 16, "bf16"), (24, 16))])
+def test_scatter_pull_two_ranks_one_gpu(shape_args, split):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    ctx = mp.get_context("spawn")
+    res, barrier = ctx.Queue(), ctx.Barrier(2)
+    ps = [ctx.Process(target=_pull_rank, args=(r, port, shape_args, split, res, barrier)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = [res.get(timeout=600) for _ in ps]
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, ok in out:
+        assert ok, rank
