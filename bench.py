@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--graph", type=int, default=1, help="N = 1: replay the K timed steps as one CUDA graph")
     ap.add_argument("--gather", default="nccl", choices=["nccl", "peer"],
                     help="N > 1: NCCL all-gather of O (default) or the combine kernel's peer-memory stores")
+    ap.add_argument("--fused-append", type=int, default=1,
+                    help="1: kv_append fused into the attention kernel (hetis_attn_partial_append); 0: separate")
     ap.add_argument("--scatter", default="nccl", choices=["nccl", "peer"],
                     help="N > 1: 'peer' = every rank pulls its q / new k, v shard from the root's buffers over "
                          "NVLink (hetis_peer_signal + hetis_scatter_pull) instead of NCCL send/recv")
@@ -276,12 +278,18 @@ def run_ours(args, world, rank, local):
             step.scatter_peers(step.epoch)
         elif world > 1:
             step.scatter(q_full, kn_full, vn_full)
-        step.append(k_pools[li], v_pools[li], batch.block_table, batch.seq_lens)
+        if not args.fused_append:
+            step.append(k_pools[li], v_pools[li], batch.block_table, batch.seq_lens)
         if ev_a is not None:
             ev_a.record(torch.cuda.current_stream(device))
-        hetis.attn_partial(step.cshape, step.buf.q_shard, k_pools[li], v_pools[li], batch.block_table,
-                           batch.seq_lens, max_len, step.buf.workspace, q_head_begin=q_begin,
-                           flags=args.attn_flags)
+        if args.fused_append:   # the append happens inside the attention kernel
+            hetis.attn_partial_append(step.cshape, step.buf.q_shard, step.buf.k_new, step.buf.v_new, k_pools[li],
+                                      v_pools[li], batch.block_table, batch.seq_lens, max_len, step.buf.workspace,
+                                      q_head_begin=q_begin, flags=args.attn_flags)
+        else:
+            hetis.attn_partial(step.cshape, step.buf.q_shard, k_pools[li], v_pools[li], batch.block_table,
+                               batch.seq_lens, max_len, step.buf.workspace, q_head_begin=q_begin,
+                               flags=args.attn_flags)
         if ev_b is not None:
             ev_b.record(torch.cuda.current_stream(device))
         if world > 1 and args.gather == "peer":
@@ -425,6 +433,10 @@ def run_ours(args, world, rank, local):
     sb = accounting.step_bytes(seq_lens.tolist(), q_count, shape.r, shape.head_dim, shape.page_size,
                                shape.elem_bytes, shape.elem_bytes, 4)
     alg_bytes = sb.kv + sb.q + sb.table + sb.seq_lens
+    kernel_name = "hetis_attn_partial (split-KV)"
+    if args.fused_append:   # the new rows are read from k_new / v_new and written into the pools
+        alg_bytes += 2 * 2 * B * (q_count // shape.r) * shape.head_dim * shape.elem_bytes
+        kernel_name = "hetis_attn_partial_append (split-KV attention with kv_append fused)"
     achieved = alg_bytes / (attn_ms / 1e3) / 1e9
     peak, peak_src = peaks()
     clocks = sampler.summary()
@@ -447,11 +459,12 @@ def run_ours(args, world, rank, local):
                 "o_dtype": args.o_dtype, "layers_rotated": n_layers,
                 "gather": (args.gather if world > 1 else None),
                 "scatter": (args.scatter if world > 1 else None),
+                "fused_append": bool(args.fused_append),
                 "l2": f"inputs larger than L2: {n_layers} layer pool(s) x {kv_bytes_rank / 1e6:.1f} MB KV per rank "
                       f"rotated per step (L2 = 126 MB)",
                 "tokens": "one token = one request's decode step of one layer, all heads"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "hetis_attn_partial (split-KV)",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name,
                          "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": attn_ms,
                          "avg_launch_ms_max_rank": attn_ms_max, "peak_source": peak_src,
                          "frac_of_8TBps_nominal": achieved / 8000.0},

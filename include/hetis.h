@@ -199,6 +199,21 @@ HETIS_API hetis_status hetis_attn_partial(const hetis_shape *shape, int32_t num_
                                 const int32_t *seq_lens, int32_t max_seq_len, void *workspace,
                                 size_t workspace_bytes, uint32_t flags, hetis_stream_t stream);
 
+/* hetis_kv_append fused into hetis_attn_partial: ONE kernel whose warp that
+ * owns request j's newest page takes the new K/V row of each local kv head
+ * from k_new / v_new (device [num_seqs][q_head_count / r][head_dim]) straight
+ * into its shared-memory copy of the page -- the new token never round-trips
+ * through HBM before it is used -- and stores it into the pool slot
+ * (page block_table[j][g][(L_j - 1) / P], slot (L_j - 1) mod P) for later
+ * steps.  Results and pools are bit-identical to hetis_kv_append followed by
+ * hetis_attn_partial (same arguments otherwise); seq_lens must be >= 1. */
+HETIS_API hetis_status hetis_attn_partial_append(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
+                                                 int32_t q_head_count, const void *q, const void *k_new,
+                                                 const void *v_new, void *k_pool, void *v_pool, int64_t num_pages,
+                                                 const int32_t *block_table, int32_t max_pages,
+                                                 const int32_t *seq_lens, int32_t max_seq_len, void *workspace,
+                                                 size_t workspace_bytes, uint32_t flags, hetis_stream_t stream);
+
 /* Kernel 2 (a5): o = sum_s 2^(lse_s - lse) o_s in ascending s (fixed order).
  *   o : device [num_seqs][q_head_count][head_dim] (o_dtype), rows of request j
  *       start at o + j * o_seq_stride elements (o_seq_stride >= q_head_count *
@@ -216,6 +231,16 @@ HETIS_API hetis_status hetis_attn_combine_lse(const hetis_shape *shape, int32_t 
                                               const int32_t *seq_lens, int32_t max_seq_len, void *o,
                                               int64_t o_seq_stride, float *lse, const void *workspace,
                                               size_t workspace_bytes, hetis_stream_t stream);
+
+/* hetis_attn_partial_append followed by hetis_attn_combine with a dense o shard:
+ * the whole per-device step (a3 + a4 + a5) in two kernels. */
+HETIS_API hetis_status hetis_attn_decode_append(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
+                                                int32_t q_head_count, const void *q, const void *k_new,
+                                                const void *v_new, void *k_pool, void *v_pool, int64_t num_pages,
+                                                const int32_t *block_table, int32_t max_pages,
+                                                const int32_t *seq_lens, int32_t max_seq_len, void *o,
+                                                void *workspace, size_t workspace_bytes, uint32_t flags,
+                                                hetis_stream_t stream);
 
 /* hetis_attn_partial followed by hetis_attn_combine with a dense o shard. */
 HETIS_API hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,

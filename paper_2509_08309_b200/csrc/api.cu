@@ -397,17 +397,20 @@ static hetis_status attn_args(const hetis_shape *shape, int32_t num_seqs, int32_
     return HETIS_OK;
 }
 
-hetis_status hetis_attn_partial(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
-                                int32_t q_head_count, const void *q, const void *k_pool, const void *v_pool,
-                                int64_t num_pages, const int32_t *block_table, int32_t max_pages,
-                                const int32_t *seq_lens, int32_t max_seq_len, void *workspace,
-                                size_t workspace_bytes, uint32_t flags, hetis_stream_t stream) {
+static hetis_status attn_partial_impl(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
+                                      int32_t q_head_count, const void *q, const void *k_new, const void *v_new,
+                                      const void *k_pool, const void *v_pool, int64_t num_pages,
+                                      const int32_t *block_table, int32_t max_pages, const int32_t *seq_lens,
+                                      int32_t max_seq_len, void *workspace, size_t workspace_bytes, uint32_t flags,
+                                      hetis_stream_t stream) {
     hetis::AttnArgs a{};
     hetis_status st = attn_args(shape, num_seqs, q_head_begin, q_head_count, q, k_pool, v_pool, num_pages,
                                 block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes, &a);
     if (st != HETIS_OK) return st;
     if (num_seqs == 0) return HETIS_OK;
     a.flags = flags;
+    a.k_new = k_new;
+    a.v_new = v_new;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const bool tc = a.dtype == HETIS_BF16 && (a.r > 1 || (flags & HETIS_ATTN_MHA_TC)) &&
                     !(flags & HETIS_ATTN_FORCE_SIMT);
@@ -421,6 +424,29 @@ hetis_status hetis_attn_partial(const hetis_shape *shape, int32_t num_seqs, int3
     if (e != cudaSuccess)
         return err.empty() ? cuda_fail(e, "attn_partial launch") : fail(HETIS_E_CUDA, "attn_partial: " + err);
     return HETIS_OK;
+}
+
+hetis_status hetis_attn_partial(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
+                                int32_t q_head_count, const void *q, const void *k_pool, const void *v_pool,
+                                int64_t num_pages, const int32_t *block_table, int32_t max_pages,
+                                const int32_t *seq_lens, int32_t max_seq_len, void *workspace,
+                                size_t workspace_bytes, uint32_t flags, hetis_stream_t stream) {
+    return attn_partial_impl(shape, num_seqs, q_head_begin, q_head_count, q, nullptr, nullptr, k_pool, v_pool,
+                             num_pages, block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes,
+                             flags, stream);
+}
+
+hetis_status hetis_attn_partial_append(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
+                                       int32_t q_head_count, const void *q, const void *k_new, const void *v_new,
+                                       void *k_pool, void *v_pool, int64_t num_pages, const int32_t *block_table,
+                                       int32_t max_pages, const int32_t *seq_lens, int32_t max_seq_len,
+                                       void *workspace, size_t workspace_bytes, uint32_t flags,
+                                       hetis_stream_t stream) {
+    if (num_seqs > 0 && (!k_new || !v_new)) return fail(HETIS_E_INVALID, "k_new / v_new is NULL");
+    if (!aligned(k_new, 16) || !aligned(v_new, 16)) return fail(HETIS_E_INVALID, "k_new / v_new must be 16-B aligned");
+    if (flags & HETIS_ATTN_DIAG_STREAM_ONLY) return fail(HETIS_E_INVALID, "the stream-only diagnostic cannot append");
+    return attn_partial_impl(shape, num_seqs, q_head_begin, q_head_count, q, k_new, v_new, k_pool, v_pool, num_pages,
+                             block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes, flags, stream);
 }
 
 static hetis_status combine_common(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_count,
@@ -516,6 +542,21 @@ hetis_status hetis_peer_wait(const int64_t *signal_local, int32_t num_ranks, int
     cudaError_t e = hetis::launch_peer_wait(signal_local, num_ranks, epoch, reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "peer_wait launch");
     return HETIS_OK;
+}
+
+hetis_status hetis_attn_decode_append(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
+                                      int32_t q_head_count, const void *q, const void *k_new, const void *v_new,
+                                      void *k_pool, void *v_pool, int64_t num_pages, const int32_t *block_table,
+                                      int32_t max_pages, const int32_t *seq_lens, int32_t max_seq_len, void *o,
+                                      void *workspace, size_t workspace_bytes, uint32_t flags,
+                                      hetis_stream_t stream) {
+    if (!o && num_seqs > 0) return fail(HETIS_E_INVALID, "o is NULL");
+    hetis_status st = hetis_attn_partial_append(shape, num_seqs, q_head_begin, q_head_count, q, k_new, v_new, k_pool,
+                                                v_pool, num_pages, block_table, max_pages, seq_lens, max_seq_len,
+                                                workspace, workspace_bytes, flags, stream);
+    if (st != HETIS_OK) return st;
+    return hetis_attn_combine(shape, num_seqs, q_head_count, seq_lens, max_seq_len, o,
+                              (int64_t)q_head_count * shape->head_dim, workspace, workspace_bytes, stream);
 }
 
 hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin, int32_t q_head_count,

@@ -100,12 +100,23 @@ struct Params {
     float scale_log2;  // log2(e) / sqrt(d)
     uint32_t flags;    // HETIS_ATTN_*
     int32_t *counters; // [0] global work-claim counter, [1] CTA-finish counter (zero between launches)
+    // fused kv_append (hetis_attn_partial_append): the new token's K/V rows [B][kv_heads][D];
+    // nullptr = the pools already hold them (hetis_kv_append ran before)
+    const uint8_t *k_new;
+    const uint8_t *v_new;
 };
 
+// new_page >= 0: this item holds request j's newest token (position L_j - 1) in page
+// new_page, slot new_slot of its page new_pg; with a fused append the consumer takes that
+// row from k_new / v_new (it never round-trips through HBM first) and stores it into the pool.
 struct ItemMeta {
     int item;
     int ntok;
     int npages;
+    int new_page;
+    int jg;      // j * kv_heads + g (row of k_new / v_new)
+    int new_pg;  // page index inside the item
+    int new_slot;
     int pad;
 };
 
@@ -254,7 +265,13 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
     auto issue_q = [&](int it, int item, const Dec &d) {
         const int slot = it & (kQSlots - 1);
         dev::mbar_wait(&qempty[slot], ((it / kQSlots) & 1) ^ 1);
-        qmeta[slot] = ItemMeta{item, d.ntok, (d.ntok + kP - 1) / kP, 0};
+        ItemMeta m{item, d.ntok, (d.ntok + kP - 1) / kP, -1, d.j * p.kv_heads + d.g, 0, 0, 0};
+        if (p.k_new != nullptr && d.t0 + d.ntok == s_len[d.j]) {  // the request's last split: append here
+            m.new_pg = (d.ntok - 1) / kP;
+            m.new_slot = (d.ntok - 1) % kP;
+            m.new_page = __ldg(p.block_table + ((size_t)d.j * p.kv_heads + d.g) * p.max_pages + d.t0 / kP + m.new_pg);
+        }
+        qmeta[slot] = m;
         dev::mbar_arrive_expect_tx(&qfull[slot], kQBytes);
         const uint8_t *src = p.q + ((size_t)d.j * p.q_heads + (size_t)d.g * R) * ROW_BYTES;
         dev::bulk_g2s(qbuf + (size_t)slot * kQStride, src, kQBytes, &qfull[slot], pol_stream);
@@ -332,6 +349,48 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
         for (int i = 0; i < PPL; ++i) pid[i] = pid_next[i];
     }
 }
+
+// ---------------------------------------------------------------- fused append
+// Load this lane's share of the new K and V rows (ROW_BYTES each) into registers; the
+// rows are 2 * ROW_BYTES / 16 chunks of 16 B, chunk c = lane + 32 * u (K first, then V).
+template <int ROW_BYTES>
+struct NewRow {
+    static constexpr int kChunks = 2 * ROW_BYTES / 16;
+    static constexpr int kPerLane = (kChunks + 31) / 32;
+    uint4 v[kPerLane];
+    __device__ __forceinline__ void load(const Params &p, int jg, int lane) {
+#pragma unroll
+        for (int u = 0; u < kPerLane; ++u) {
+            const int c = lane + 32 * u;
+            if (c < kChunks) {
+                const uint8_t *src = (c < kChunks / 2 ? p.k_new : p.v_new) + (size_t)jg * ROW_BYTES +
+                                     (c % (kChunks / 2)) * 16;
+                v[u] = __ldg(reinterpret_cast<const uint4 *>(src));
+            }
+        }
+    }
+    // write the rows into the landed stage (K page at kb, V page at vb; `off(t, c)` maps a token row
+    // and 16-B chunk to its byte offset inside a page) and into the pools; warp-synchronous
+    template <typename Off>
+    __device__ __forceinline__ void patch(const Params &p, uint8_t *kb, uint8_t *vb, int page, int slot, int lane,
+                                          Off off) {
+        constexpr int kHalf = kChunks / 2;
+#pragma unroll
+        for (int u = 0; u < kPerLane; ++u) {
+            const int c = lane + 32 * u;
+            if (c < kChunks) {
+                const bool is_k = c < kHalf;
+                const int cc = c % kHalf;
+                *reinterpret_cast<uint4 *>((is_k ? kb : vb) + off(slot, cc)) = v[u];
+                uint8_t *pool = const_cast<uint8_t *>(is_k ? p.k_pool : p.v_pool);
+                *reinterpret_cast<uint4 *>(pool + ((size_t)page * kP + slot) * ROW_BYTES + cc * 16) = v[u];
+            }
+        }
+        // these generic writes must be ordered before the TMA that will refill this stage
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+    }
+};
 
 // ---------------------------------------------------------------- merge of NW warp states
 // mbuf layout (one of two alternating buffers): [NW][R][D + 4] floats:
@@ -449,6 +508,9 @@ __device__ void consumer_simt(const Params &p, const uint8_t *ring, const uint8_
             qv[rr] = *reinterpret_cast<const uint4 *>(qbuf + (size_t)slot * kQStride + rr * ROW_BYTES + lchk * 16);
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(&qempty[slot]);
+        NewRow<ROW_BYTES> nr;
+        const bool my_new = meta.new_page >= 0 && meta.new_pg % NW == cw;
+        if (my_new) nr.load(p, meta.jg, lane);
 
         float m[R], l[R], acc[R][EPL];
 #pragma unroll
@@ -468,6 +530,11 @@ __device__ void consumer_simt(const Params &p, const uint8_t *ring, const uint8_
                 if (lane == 0) dev::mbar_arrive(&empty[pos.stage]);
                 pos.advance(NW, p.stages);
                 continue;
+            }
+            if (my_new && pg == meta.new_pg) {
+                uint8_t *kbp = const_cast<uint8_t *>(ring) + (size_t)pos.stage * kStageBytes;
+                nr.patch(p, kbp, kbp + kPageBytes, meta.new_page, meta.new_slot, lane,
+                         [](int t, int c) { return (uint32_t)(t * ROW_BYTES + c * 16); });
             }
             const uint8_t *kb = ring + (size_t)pos.stage * kStageBytes;
             const uint8_t *vb = kb + kPageBytes;
@@ -634,6 +701,9 @@ __device__ void consumer_tc(const Params &p, const uint8_t *ring, const uint8_t 
         }
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(&qempty[slot]);
+        NewRow<ROW_BYTES> nr;
+        const bool my_new = meta.new_page >= 0 && meta.new_pg % NW == cw;
+        if (my_new) nr.load(p, meta.jg, lane);
 
         float m = -INFINITY, l = 0.f;
         float o[NT_O][4];
@@ -644,6 +714,10 @@ __device__ void consumer_tc(const Params &p, const uint8_t *ring, const uint8_t 
         pos.advance(cw, p.stages);
         for (int pg = cw; pg < meta.npages; pg += NW) {
             dev::mbar_wait(&full[pos.stage], pos.phase);
+            if (my_new && pg == meta.new_pg) {
+                uint8_t *kbp = const_cast<uint8_t *>(ring) + (size_t)pos.stage * kStageBytes;
+                nr.patch(p, kbp, kbp + kPageBytes, meta.new_page, meta.new_slot, lane, swz);
+            }
             if (p.flags & HETIS_ATTN_DIAG_STREAM_ONLY) {  // diagnostic: memory-system ceiling of this pipeline
                 __syncwarp();
                 if (lane == 0) dev::mbar_arrive(&empty[pos.stage]);
@@ -851,14 +925,20 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         if (finished) continue;
         if (item >= n_items) {  // no more work for this worker: post the sentinel when the q slot is free
             if (dev::mbar_test(&sm.qempty[w], (it & 1) ^ 1)) {
-                sm.meta[w] = ItemMeta{-1, 0, 0, 0};
+                sm.meta[w] = ItemMeta{-1, 0, 0, -1, 0, 0, 0, 0};
                 dev::mbar_arrive(&sm.qfull[w]);
                 finished = true;
             }
             continue;
         }
         if (!q_done && dev::mbar_test(&sm.qempty[w], (it & 1) ^ 1)) {
-            sm.meta[w] = ItemMeta{item, ntok, np, 0};
+            ItemMeta m{item, ntok, np, -1, j * p.kv_heads + g, 0, 0, 0};
+            if (p.k_new != nullptr && t0 + ntok == s_len[j]) {  // the request's last split: append here
+                m.new_pg = (ntok - 1) / kP;
+                m.new_slot = (ntok - 1) % kP;
+                m.new_page = sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + m.new_pg];
+            }
+            sm.meta[w] = m;
             dev::mbar_arrive_expect_tx(&sm.qfull[w], kQBytes);
             const uint8_t *src = p.q + ((size_t)j * p.q_heads + (size_t)g * R) * ROW_BYTES;
             dev::bulk_g2s(sm.qbuf + (size_t)w * kQStride, src, kQBytes, &sm.qfull[w], pol);
@@ -958,6 +1038,8 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         }
         __syncwarp();
         if (lane == 0) dev::mbar_arrive(&sm.qempty[w]);
+        NewRow<D * 2> nr;
+        if (meta.new_page >= 0) nr.load(p, meta.jg, lane);  // fused append: the new rows, in flight early
 
         float m = -INFINITY, l = 0.f;
         float o[NT_O][4];
@@ -965,6 +1047,10 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         for (int nt = 0; nt < NT_O; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
         for (int pg = 0; pg < meta.npages; ++pg) {
             dev::mbar_wait(&sm.full[w * SW + pos.stage], pos.phase);
+            if (meta.new_page >= 0 && pg == meta.new_pg) {
+                uint8_t *kbp = sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes;
+                nr.patch(p, kbp, kbp + kPageBytes, meta.new_page, meta.new_slot, lane, swz);
+            }
             if (w == 0 && lane == 0 && it == 0 && pg == 0) {
                 HETIS_TS(4);
             }
@@ -1276,6 +1362,8 @@ Params make_params(const AttnArgs &a) {
     p.scale_log2 = (float)(1.4426950408889634 / std::sqrt((double)a.head_dim));
     p.flags = a.flags;
     p.counters = a.counters;
+    p.k_new = static_cast<const uint8_t *>(a.k_new);
+    p.v_new = static_cast<const uint8_t *>(a.v_new);
     return p;
 }
 

@@ -38,6 +38,8 @@ struct AttnArgs {
     int64_t max_items;
     uint32_t flags;       // HETIS_ATTN_*
     int32_t *counters;    // [2] work-claim and CTA-finish counters; zero between launches
+    const void *k_new;    // fused append: new rows [num_seqs][kv_heads][head_dim], or nullptr
+    const void *v_new;
 };
 
 struct WorkspaceLayout {

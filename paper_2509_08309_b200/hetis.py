@@ -35,7 +35,8 @@ EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_
             "hetis_attn_combine", "hetis_attn_decode", "hetis_attn_combine_peers", "hetis_peer_wait",
             "hetis_comm_workspace", "hetis_scatter_q", "hetis_gather", "hetis_kv_migrate",
             "hetis_attn_combine_lse", "hetis_seq_split_lens", "hetis_seq_merge", "hetis_seq_broadcast_q",
-            "hetis_seq_allgather_merge", "hetis_peer_signal", "hetis_scatter_pull", "hetis_launch_count")
+            "hetis_seq_allgather_merge", "hetis_peer_signal", "hetis_scatter_pull", "hetis_attn_partial_append",
+            "hetis_attn_decode_append", "hetis_launch_count")
 
 
 class HetisError(RuntimeError):
@@ -99,6 +100,10 @@ def lib() -> ctypes.CDLL:
                 "hetis_seq_broadcast_q": (ctypes.c_int, [sp, vp, i32, i32, i32, i32, vp, vp, vp, vp]),
                 "hetis_seq_allgather_merge": (ctypes.c_int, [sp, vp, i32, i32, i32, vp, vp, vp, i64, vp]),
                 "hetis_peer_signal": (ctypes.c_int, [P(vp), i32, i32, i64, vp]),
+                "hetis_attn_partial_append": (ctypes.c_int, [sp, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32, vp,
+                                                             i32, vp, sz, u32, vp]),
+                "hetis_attn_decode_append": (ctypes.c_int, [sp, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32, vp,
+                                                            i32, vp, vp, sz, u32, vp]),
                 "hetis_scatter_pull": (ctypes.c_int, [vp, i32, i32, vp, i32, i64, vp, vp, vp, vp, vp, vp, vp]),
             }
             for name, (res, args) in sig.items():
@@ -288,6 +293,30 @@ def attn_combine_lse(shape: CShape, seq_lens, max_seq_len: int, o, lse, workspac
                                         ctypes.c_void_p(o.data_ptr()), o_seq_stride, ctypes.c_void_p(lse.data_ptr()),
                                         _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(),
                                         _stream(stream)), "hetis_attn_combine_lse")
+
+
+def attn_partial_append(shape: CShape, q, k_new, v_new, k_pool, v_pool, block_table, seq_lens, max_seq_len: int,
+                        workspace, q_head_begin: int = 0, flags: int = 0, stream=None) -> None:
+    """kv_append fused into the split-KV attention kernel (hetis_attn_partial_append)."""
+    B, x, _ = q.shape
+    _check(lib().hetis_attn_partial_append(ctypes.byref(shape), B, q_head_begin, x, _dev(q, "q"), _dev(k_new, "k_new"),
+                                           _dev(v_new, "v_new"), _dev(k_pool, "k_pool"), _dev(v_pool, "v_pool"),
+                                           k_pool.shape[0], _dev(block_table, "block_table"), block_table.shape[2],
+                                           _dev(seq_lens, "seq_lens"), max_seq_len, _dev(workspace, "workspace"),
+                                           workspace.numel() * workspace.element_size(), flags, _stream(stream)),
+           "hetis_attn_partial_append")
+
+
+def attn_decode_append(shape: CShape, q, k_new, v_new, k_pool, v_pool, block_table, seq_lens, max_seq_len: int, o,
+                       workspace, q_head_begin: int = 0, flags: int = 0, stream=None) -> None:
+    """The per-device step in two kernels: attention with the append fused, then the combine."""
+    B, x, _ = q.shape
+    _check(lib().hetis_attn_decode_append(ctypes.byref(shape), B, q_head_begin, x, _dev(q, "q"), _dev(k_new, "k_new"),
+                                          _dev(v_new, "v_new"), _dev(k_pool, "k_pool"), _dev(v_pool, "v_pool"),
+                                          k_pool.shape[0], _dev(block_table, "block_table"), block_table.shape[2],
+                                          _dev(seq_lens, "seq_lens"), max_seq_len, _dev(o, "o"),
+                                          _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(),
+                                          flags, _stream(stream)), "hetis_attn_decode_append")
 
 
 def attn_decode(shape: CShape, q, k_pool, v_pool, block_table, seq_lens, max_seq_len: int, o, workspace,

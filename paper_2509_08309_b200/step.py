@@ -63,7 +63,7 @@ class DecodeStep:
 
     # kernels launched per step by this rank (for gpu_launches accounting)
     def launches_per_step(self) -> int:
-        n = 3  # kv_append, attention partial, combine
+        n = 3  # kv_append, attention partial, combine (2 with the fused append)
         if self.world > 1:
             x = [self.plan.heads(i)[1] for i in range(self.world)]
             if self.rank == self.root:
@@ -84,6 +84,18 @@ class DecodeStep:
         o = self.buf.o_shard if o is None else o
         hetis.attn_partial(self.cshape, q, k_pool, v_pool, block_table, seq_lens, self.max_seq_len,
                            self.buf.workspace, q_head_begin=self.q_begin, flags=flags, stream=stream)
+        hetis.attn_combine(self.cshape, seq_lens, self.max_seq_len, o, self.buf.workspace, q_head_count=self.q_count,
+                           stream=stream)
+        return o
+
+    def append_attention(self, k_pool, v_pool, block_table, seq_lens, q=None, o=None, stream=None, flags: int = 0):
+        """kv_append fused into the attention kernel, then the combine: the per-device step in two kernels
+        (bit-identical to append() followed by attention())."""
+        q = self.buf.q_shard if q is None else q
+        o = self.buf.o_shard if o is None else o
+        hetis.attn_partial_append(self.cshape, q, self.buf.k_new, self.buf.v_new, k_pool, v_pool, block_table, seq_lens,
+                                  self.max_seq_len, self.buf.workspace, q_head_begin=self.q_begin, flags=flags,
+                                  stream=stream)
         hetis.attn_combine(self.cshape, seq_lens, self.max_seq_len, o, self.buf.workspace, q_head_count=self.q_count,
                            stream=stream)
         return o

@@ -42,10 +42,10 @@ def share_time(cfg, n: int, steps: int, warmup: int, device):
 
     def step(i, ea=None, eb=None):
         li = i % n_layers
-        hetis.kv_append(s, b.k_new, b.v_new, kp[li], vp[li], b.block_table, b.seq_lens)
         if ea is not None:
             ea.record()
-        hetis.attn_partial(s, b.q, kp[li], vp[li], b.block_table, b.seq_lens, L, ws)
+        # the per-device step: attention with kv_append fused, then the combine (two kernels)
+        hetis.attn_partial_append(s, b.q, b.k_new, b.v_new, kp[li], vp[li], b.block_table, b.seq_lens, L, ws)
         if eb is not None:
             eb.record()
         hetis.attn_combine(s, b.seq_lens, L, o, ws)

@@ -88,9 +88,15 @@ def main():
         def comb(i):
             hetis.attn_combine(s, b.seq_lens, L, o, ws)
 
+        def fapp(i):    # kv_append fused into the attention kernel, then the combine: two kernels
+            li = i % nl
+            hetis.attn_partial_append(s, b.q, b.k_new, b.v_new, kp[li], vp[li], b.block_table, b.seq_lens, L, ws,
+                                      flags=a.flags)
+            hetis.attn_combine(s, b.seq_lens, L, o, ws)
+
         row = {"config": cfg.name, "n": n, "heads": x, "kv_bytes": kv, "layers": nl,
                "floor_us_at_6550": kv / 6550e3}
-        for name, fn in (("full", full), ("no_app", no_app), ("attn", attn), ("comb", comb)):
+        for name, fn in (("full", full), ("no_app", no_app), ("attn", attn), ("comb", comb), ("fapp", fapp)):
             row[name + "_us"] = graph_us(fn, a.steps)
         print(json.dumps(row), flush=True)
         del kp, vp, b

@@ -433,3 +433,63 @@ def test_mha_tc_head_partition_bit_identical():
         outs.append(run_gpu(part, flags=hetis.ATTN_MHA_TC))
         begin += x
     assert torch.equal(torch.cat(outs, 1), o_full)
+
+
+# ------------------------------------------------------------------ kv_append fused into the attention kernel
+@pytest.mark.parametrize("H,Hkv,D,dtype,flags", [
+    (40, 40, 128, "bf16", 0),                          # CUDA-core MHA
+    (64, 8, 128, "bf16", 0),                           # per-warp tensor-core GQA
+    (16, 4, 64, "bf16", 0),
+    (8, 8, 64, "f32", 0),                              # fp32 CUDA-core
+    (4, 2, 128, "f32", 0),
+    (40, 40, 128, "bf16", hetis.ATTN_MHA_TC),          # MHA on the per-warp tensor-core kernel
+    (64, 8, 128, "bf16", hetis.ATTN_TC_SHARED_RING),   # shared-ring tensor-core kernel
+    (16, 2, 128, "bf16", hetis.ATTN_FORCE_SIMT),
+])
+def test_fused_append_bit_identical_to_append_then_attention(H, Hkv, D, dtype, flags):
+    """hetis_attn_decode_append (the new rows patched into the landed page in shared memory and stored into
+    the pool by the same kernel) == hetis_kv_append + hetis_attn_decode: O and both pools bit for bit."""
+    lens = EDGE_LENS
+    a = gpu_batch(H, Hkv, D, dtype, lens, seed=97)
+    b = gpu_batch(H, Hkv, D, dtype, lens, seed=97)
+    s = hetis.make_shape(a.shape)
+    B, x, _ = a.q.shape
+    L = a.max_seq_len
+    o_ref = run_gpu(a, flags=flags)                                   # kv_append, then attention + combine
+    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), "cuda")
+    o = torch.full((B, x, D), float("nan"), device="cuda")
+    hetis.attn_decode_append(s, b.q, b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, o, ws,
+                             flags=flags)
+    torch.cuda.synchronize()
+    assert torch.equal(o, o_ref)
+    bits = lambda t: t.view(torch.int16) if t.dtype == torch.bfloat16 else t.view(torch.int32)
+    assert torch.equal(bits(b.k_pool), bits(a.k_pool)) and torch.equal(bits(b.v_pool), bits(a.v_pool))
+    # a second step reads the appended rows from the pools like any other token
+    o2 = torch.full_like(o, float("nan"))
+    hetis.attn_decode(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, o2, ws, flags=flags)
+    torch.cuda.synchronize()
+    assert torch.equal(o2, o_ref)
+
+
+def test_decode_step_fused_append_matches_separate_calls():
+    from paper_2509_08309_b200.step import DecodeStep
+    shape = workload.LLAMA2_70B
+    lens = torch.tensor([300, 17, 1, 1029], dtype=torch.int32)
+    a = workload.make_decode_batch(shape, lens, 5, "cuda")
+    b = workload.make_decode_batch(shape, lens, 5, "cuda")
+    plan = hetis.plan_create(hetis.make_shape(shape), 1, [shape.num_q_heads])
+    outs = []
+    for batch, fused in ((a, False), (b, True)):
+        st = DecodeStep(shape, plan, 0, len(lens), int(lens.max()), torch.device("cuda", 0))
+        st.buf.q_shard.copy_(batch.q)
+        st.buf.k_new.copy_(batch.k_new)
+        st.buf.v_new.copy_(batch.v_new)
+        if fused:
+            o = st.append_attention(batch.k_pool, batch.v_pool, batch.block_table, batch.seq_lens)
+        else:
+            st.append(batch.k_pool, batch.v_pool, batch.block_table, batch.seq_lens)
+            o = st.attention(batch.k_pool, batch.v_pool, batch.block_table, batch.seq_lens)
+        outs.append(o.clone())
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    assert torch.equal(a.k_pool.view(torch.int16), b.k_pool.view(torch.int16))
