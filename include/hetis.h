@@ -108,6 +108,12 @@ typedef struct {
 /* bf16 MHA (r = 1) on the per-warp tensor-core kernel (one valid MMA row)
  * instead of the CUDA-core kernel. */
 #define HETIS_ATTN_MHA_TC 0x8u
+/* Pipelined steps: the caller passes two workspaces alternately to consecutive
+ * steps on the stream (at most one kv_append -- fused or not -- per step).
+ * The attention kernel then streams cache pages while the previous step's
+ * combine and attention tail still run: it waits for them only before a page
+ * holding one of the last two positions of a request, and before it ends. */
+#define HETIS_ATTN_PIPELINED 0x10u
 /* Diagnostic only: stream every K/V page through the shared-memory ring but
  * skip the math (partials are left unwritten).  Measures the memory-system
  * ceiling of the pipeline; the CUDA-core kernel honours it. */

@@ -178,6 +178,23 @@ __device__ void build_split_offsets(const Params &p, int32_t *s_len, int32_t *s_
     __syncthreads();
 }
 
+// HETIS_ATTN_PIPELINED: the caller alternates two workspaces between consecutive
+// steps, so nothing in flight reads this launch's workspace and the kernel may
+// stream pages while the previous step's combine (and the tail of its attention)
+// still run.  The only pool rows an in-flight kernel can still be writing are
+// the newest tokens of the previous step(s) (fused or separate kv_append, one
+// token per step), so a producer lane waits only before a page that holds one
+// of the last two positions of its request -- and once more at its end, so this
+// kernel never completes before its predecessors (the next combine relies on it).
+__device__ __forceinline__ bool holds_recent_tokens(int t0, int pg, int L) { return t0 + (pg + 1) * kP >= L - 1; }
+
+__device__ __forceinline__ void pdl_wait_once(bool &waited) {
+    if (!waited) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        waited = true;
+    }
+}
+
 // Block 0 publishes the split offsets for the combine kernel.  Called by the
 // producer lanes AFTER griddepcontrol.wait: the previous step's combine, which
 // may still be running while this kernel's prologue executes (it releases its
@@ -290,8 +307,10 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
     constexpr unsigned kMask = (1u << kProducerLanes) - 1u;
 
     int item = blockIdx.x;
+    const bool pipelined = (p.flags & HETIS_ATTN_PIPELINED) != 0;
+    bool waited = false;
     if (item >= n_items) {
-        asm volatile("griddepcontrol.wait;" ::: "memory");
+        pdl_wait_once(waited);
         publish_split_offsets(p, s_off, lane, kProducerLanes);
         return;
     }
@@ -301,8 +320,10 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
     int32_t pid[PPL];
     load_pids(cur, pid);
     RingPos pos{0, 0u};
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // pools may hold rows the previous kernel (kv_append) wrote
-    publish_split_offsets(p, s_off, lane, kProducerLanes);
+    if (!pipelined) {
+        pdl_wait_once(waited);  // pools may hold rows the previous kernel (kv_append) wrote
+        publish_split_offsets(p, s_off, lane, kProducerLanes);
+    }
     for (int it = 0; item < n_items; item += gridDim.x, ++it) {
         const int next = item + gridDim.x;
         int32_t pid_next[PPL];
@@ -325,6 +346,7 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
                     RingPos my = pos;
                     my.advance(lane, p.stages);
                     const int32_t page = pid[i];
+                    if (pipelined && holds_recent_tokens(cur.t0, pg, s_len[cur.j])) pdl_wait_once(waited);
                     dev::mbar_wait(&empty[my.stage], my.phase ^ 1u);
                     uint8_t *dst = ring + (size_t)my.stage * kStageBytes;
                     dev::mbar_arrive_expect_tx(&full[my.stage], kStageBytes);
@@ -347,6 +369,10 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
         cur = nd;
 #pragma unroll
         for (int i = 0; i < PPL; ++i) pid[i] = pid_next[i];
+    }
+    if (pipelined) {
+        pdl_wait_once(waited);
+        publish_split_offsets(p, s_off, lane, kProducerLanes);
     }
 }
 
@@ -916,8 +942,12 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
 #pragma unroll
         for (int i = 0; i < kPagesPerItem; ++i) sm.pids[(w * 2 + 0) * kPagesPerItem + i] = nxt[i];
     }
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // pools may hold rows the previous kernel wrote
-    publish_split_offsets(p, s_off, w, NW);
+    const bool pipelined = (p.flags & HETIS_ATTN_PIPELINED) != 0;
+    bool waited = false;
+    if (!pipelined) {
+        pdl_wait_once(waited);  // pools may hold rows the previous kernel wrote
+        publish_split_offsets(p, s_off, w, NW);
+    }
     if (w == 0) {
         HETIS_TS(2);
     }
@@ -947,6 +977,7 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         // issue as many pages as the worker's sub-ring has free stages
         while (q_done && pg < np && dev::mbar_test(&sm.empty[w * SW + pos.stage], pos.phase ^ 1u)) {
             const int32_t page = sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + pg];
+            if (pipelined && holds_recent_tokens(t0, pg, s_len[j])) pdl_wait_once(waited);
             uint64_t *bar = &sm.full[w * SW + pos.stage];
             uint8_t *dst = sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes;
             dev::mbar_arrive_expect_tx(bar, kStageBytes);
@@ -976,6 +1007,10 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
                 for (int i = 0; i < kPagesPerItem; ++i) sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + i] = nxt[i];
             }
         }
+    }
+    if (pipelined) {
+        pdl_wait_once(waited);
+        publish_split_offsets(p, s_off, w, NW);
     }
 }
 

@@ -46,7 +46,9 @@ __global__ void __launch_bounds__(kMigrateThreads) kv_migrate_kernel(
     extern __shared__ int32_t prefix[];  // [num_entries + 1]: first flat page of each entry
     __shared__ int32_t warp_tot[kMigrateThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    dev::pdl_wait_then_release();
+    // no early release: a pipelined attention launch reads cache pages before it waits,
+    // so nothing may start after a migration until its copies are complete
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     // block-wide exclusive scan of pages per entry (each thread owns a contiguous run)
     const int per = (num_entries + kMigrateThreads - 1) / kMigrateThreads;

@@ -27,6 +27,7 @@ ATTN_FORCE_SIMT = 0x1
 ATTN_TC_SHARED_RING = 0x2
 ATTN_DEVICE_CLAIM = 0x4
 ATTN_MHA_TC = 0x8
+ATTN_PIPELINED = 0x10
 ATTN_DIAG_STREAM_ONLY = 0x100
 
 EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_split_tokens",

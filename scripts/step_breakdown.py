@@ -69,6 +69,7 @@ def main():
         vp = [b.v_pool] + [b.v_pool.clone() for _ in range(nl - 1)]
         ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), dev)
         o = torch.empty((B, x, shape.head_dim), device=dev)
+        ws2 = [ws, hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), dev)]
 
         def full(i):
             li = i % nl
@@ -94,9 +95,16 @@ def main():
                                       flags=a.flags)
             hetis.attn_combine(s, b.seq_lens, L, o, ws)
 
+        def pipe(i):    # fused append + combine, pipelined: two workspaces alternate between steps
+            li = i % nl
+            w_ = ws2[i % 2]
+            hetis.attn_partial_append(s, b.q, b.k_new, b.v_new, kp[li], vp[li], b.block_table, b.seq_lens, L, w_,
+                                      flags=a.flags | hetis.ATTN_PIPELINED)
+            hetis.attn_combine(s, b.seq_lens, L, o, w_)
+
         row = {"config": cfg.name, "n": n, "heads": x, "kv_bytes": kv, "layers": nl,
                "floor_us_at_6550": kv / 6550e3}
-        for name, fn in (("full", full), ("no_app", no_app), ("attn", attn), ("comb", comb), ("fapp", fapp)):
+        for name, fn in (("full", full), ("no_app", no_app), ("attn", attn), ("comb", comb), ("fapp", fapp), ("pipe", pipe)):
             row[name + "_us"] = graph_us(fn, a.steps)
         print(json.dumps(row), flush=True)
         del kp, vp, b

@@ -493,3 +493,53 @@ def test_decode_step_fused_append_matches_separate_calls():
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1])
     assert torch.equal(a.k_pool.view(torch.int16), b.k_pool.view(torch.int16))
+
+
+# ------------------------------------------------------------------ pipelined steps (HETIS_ATTN_PIPELINED)
+@pytest.mark.parametrize("H,Hkv,D,dtype", [(64, 8, 128, "bf16"), (40, 40, 128, "bf16"), (8, 8, 64, "f32")])
+def test_pipelined_steps_match_serial_steps(H, Hkv, D, dtype):
+    """Several decode steps (each appends one token) back to back on one stream, pipelined with two
+    alternating workspaces, as a CUDA graph so consecutive kernels really overlap: every step's O and the
+    final pools are bit-identical to the same steps run with the default (fully ordered) launches."""
+    lens0 = torch.tensor([1, 15, 16, 17, 255, 256, 900, 2047], dtype=torch.int32)
+    n_steps = 6
+    lens_max = lens0 + n_steps
+    outs = {}
+    for mode in ("serial", "pipelined"):
+        shape = workload.Shape(H, Hkv, D, 16, dtype)
+        b = workload.make_decode_batch(shape, lens_max, 111, "cuda")      # pages for every step's token
+        s = hetis.make_shape(shape)
+        B, x, _ = b.q.shape
+        L = int(lens_max.max())
+        ws = [hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), "cuda") for _ in range(2)]
+        g = torch.Generator(device="cuda").manual_seed(7)
+        kn = [torch.randn(b.k_new.shape, generator=g, device="cuda").to(b.k_new.dtype) for _ in range(n_steps)]
+        vn = [torch.randn(b.v_new.shape, generator=g, device="cuda").to(b.v_new.dtype) for _ in range(n_steps)]
+        sl = [(lens0 + i + 1).to("cuda") for i in range(n_steps)]
+        o = [torch.empty((B, x, D), device="cuda") for _ in range(n_steps)]
+        flags = hetis.ATTN_PIPELINED if mode == "pipelined" else 0
+
+        def run():
+            for i in range(n_steps):
+                w_ = ws[i % 2] if mode == "pipelined" else ws[0]
+                hetis.attn_partial_append(s, b.q, kn[i], vn[i], b.k_pool, b.v_pool, b.block_table, sl[i], L, w_,
+                                          flags=flags)
+                hetis.attn_combine(s, sl[i], L, o[i], w_)
+
+        k0, v0 = b.k_pool.clone(), b.v_pool.clone()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            run()
+        for rep in range(3):                      # replays start from the same pools
+            b.k_pool.copy_(k0)
+            b.v_pool.copy_(v0)
+            graph.replay()
+            torch.cuda.synchronize()
+            outs.setdefault(mode, []).append(([t.clone() for t in o], b.k_pool.clone(), b.v_pool.clone()))
+    bits = lambda t: t.view(torch.int16) if t.dtype == torch.bfloat16 else t.view(torch.int32)   # NaN slack
+    ref_o, ref_k, ref_v = outs["serial"][0]
+    for mode in ("serial", "pipelined"):
+        for os_, k, v in outs[mode]:
+            for i in range(n_steps):
+                assert torch.equal(os_[i], ref_o[i]), (mode, i)
+            assert torch.equal(bits(k), bits(ref_k)) and torch.equal(bits(v), bits(ref_v)), mode
