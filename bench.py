@@ -417,15 +417,76 @@ def run_ours(args, world, rank, local):
             ho.copy_(o_full, non_blocking=True)
 
     e_steps = max(min(args.steps, 50), 3)
-    for i in range(3):
-        e2e_step(i)
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for i in range(e_steps):
-        e2e_step(i)
-    e1.record(stream)
-    barrier()
+    e_mode = "serial"
+    if world == 1:
+        # Overlapped through the same public calls: step i's host->device copies run on a copy stream
+        # while step i-1 computes, and its device->host read on another stream while step i+1
+        # computes -- double-buffered device inputs / outputs and pinned host outputs.  Every step
+        # still moves its own inputs in and its own O out inside the timed region.
+        e_mode = "overlapped (double-buffered inputs/outputs, copy streams)"
+        ins = [(step.buf.q_shard.clone(), step.buf.k_new.clone(), step.buf.v_new.clone(), batch.seq_lens.clone())
+               for _ in range(2)]
+        outs = [torch.empty_like(o_full) for _ in range(2)]
+        hos = [ho, torch.empty_like(ho).pin_memory()]
+        s_in, s_out = torch.cuda.Stream(device), torch.cuda.Stream(device)
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_done = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+
+        def compute(i, q, kn, vn, sl, o):
+            li = i % n_layers
+            if args.fused_append:
+                hetis.attn_partial_append(step.cshape, q, kn, vn, k_pools[li], v_pools[li], batch.block_table, sl,
+                                          max_len, step.buf.workspace, q_head_begin=q_begin, flags=args.attn_flags)
+            else:
+                hetis.kv_append(step.cshape, kn, vn, k_pools[li], v_pools[li], batch.block_table, sl)
+                hetis.attn_partial(step.cshape, q, k_pools[li], v_pools[li], batch.block_table, sl, max_len,
+                                   step.buf.workspace, q_head_begin=q_begin, flags=args.attn_flags)
+            hetis.attn_combine(step.cshape, sl, max_len, o, step.buf.workspace, q_head_count=q_count)
+
+        def run_overlapped(n, start_event=None):
+            if start_event is not None:
+                s_in.wait_event(start_event)
+            for i in range(n):
+                k = i % 2
+                q, kn, vn, sl = ins[k]
+                with torch.cuda.stream(s_in):
+                    if i >= 2:
+                        s_in.wait_event(ev_done[k])          # step i-2 finished reading these buffers
+                    q.copy_(hq, non_blocking=True)
+                    kn.copy_(hk, non_blocking=True)
+                    vn.copy_(hv, non_blocking=True)
+                    sl.copy_(hsl, non_blocking=True)
+                    ev_in[k].record(s_in)
+                stream.wait_event(ev_in[k])
+                if i >= 2:
+                    stream.wait_event(ev_out[k])             # step i-2's O has been read back
+                compute(i, q, kn, vn, sl, outs[k])
+                ev_done[k].record(stream)
+                with torch.cuda.stream(s_out):
+                    s_out.wait_event(ev_done[k])
+                    hos[k].copy_(outs[k], non_blocking=True)
+                    ev_out[k].record(s_out)
+            for k in range(2):
+                stream.wait_event(ev_out[k])
+
+        run_overlapped(4)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run_overlapped(e_steps, e0)
+        e1.record(stream)
+        barrier()
+    else:
+        for i in range(3):
+            e2e_step(i)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(e_steps):
+            e2e_step(i)
+        e1.record(stream)
+        barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e_steps
     e2e_value = B / (e2e_ms / 1e3)
 
@@ -471,7 +532,7 @@ def run_ours(args, world, rank, local):
             "attention_only_tokens_per_s": B / (attn_ms_max / 1e3),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_ms},
+                    "ms_per_step": e2e_ms, "mode": e_mode},
             "gpu_launches": launches,
             "launch_mode": launch_mode,
             "clocks": clocks,
