@@ -117,7 +117,9 @@ struct ItemMeta {
     int jg;      // j * kv_heads + g (row of k_new / v_new)
     int new_pg;  // page index inside the item
     int new_slot;
-    int pad;
+    int defer_from;     // per-warp kernel, HETIS_ATTN_PIPELINED: pages >= defer_from are copied by the consumer
+    int defer_page[2];  // their page ids (the producer may overwrite its page-id buffer before they are copied)
+    int pad[2];
 };
 
 __device__ __forceinline__ int upper_bound_smem(const int32_t *a, int n, int key) {
@@ -342,11 +344,13 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
             const int pg0 = i * kProducerLanes;
             if (pg0 < np) {
                 const int pg = pg0 + lane;
+                // pipelined: wait (all producer lanes together) before a page an in-flight kernel may write
+                if (pipelined && __any_sync(kMask, pg < np && holds_recent_tokens(cur.t0, pg, s_len[cur.j])))
+                    pdl_wait_once(waited);
                 if (pg < np) {
                     RingPos my = pos;
                     my.advance(lane, p.stages);
                     const int32_t page = pid[i];
-                    if (pipelined && holds_recent_tokens(cur.t0, pg, s_len[cur.j])) pdl_wait_once(waited);
                     dev::mbar_wait(&empty[my.stage], my.phase ^ 1u);
                     uint8_t *dst = ring + (size_t)my.stage * kStageBytes;
                     dev::mbar_arrive_expect_tx(&full[my.stage], kStageBytes);
@@ -911,8 +915,15 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     // claim comes from the device-wide counter -- SMs slowed by another kernel (e.g. a
     // migration on a side stream) simply take fewer items.  Default: CTA-local items
     // [0, n_static) (CTA c: c, c + grid, ...), then stealing from [n_static, n_items).
-    const bool device_claim = (p.flags & HETIS_ATTN_DEVICE_CLAIM) != 0;
-    const int per_cta = device_claim ? 0 : (int)(((long long)n_items * HETIS_STATIC_PCT / 100) / gridDim.x);
+    // griddepcontrol.wait must be executed by converged warps only (a lane blocked in it stalls
+    // the whole producer warp -- with the wait pending, lanes that never reach it deadlock the
+    // CTA).  Pipelined launches have not waited up front, so they never steal (no global counter).
+    const bool pipelined_launch = (p.flags & HETIS_ATTN_PIPELINED) != 0;
+    const bool device_claim = (p.flags & HETIS_ATTN_DEVICE_CLAIM) != 0 && !pipelined_launch;
+    const int static_pct = pipelined_launch ? 100 : HETIS_STATIC_PCT;
+    const int per_cta = device_claim       ? 0
+                        : static_pct == 100 ? (n_items + (int)gridDim.x - 1) / (int)gridDim.x
+                                            : (int)(((long long)n_items * static_pct / 100) / gridDim.x);
     const int n_static = device_claim ? (int)gridDim.x * NW : per_cta * (int)gridDim.x;
     auto claim = [&]() -> int {
         if (!device_claim) {
@@ -962,7 +973,12 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             continue;
         }
         if (!q_done && dev::mbar_test(&sm.qempty[w], (it & 1) ^ 1)) {
-            ItemMeta m{item, ntok, np, -1, j * p.kv_heads + g, 0, 0, 0};
+            ItemMeta m{item, ntok, np, -1, j * p.kv_heads + g, 0, 0, np};
+            if (pipelined) {  // the pages holding the request's last two positions: the consumer waits + copies
+                while (m.defer_from > 0 && holds_recent_tokens(t0, m.defer_from - 1, s_len[j])) --m.defer_from;
+                for (int d = 0; d < 2 && m.defer_from + d < np; ++d)
+                    m.defer_page[d] = sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + m.defer_from + d];
+            }
             if (p.k_new != nullptr && t0 + ntok == s_len[j]) {  // the request's last split: append here
                 m.new_pg = (ntok - 1) / kP;
                 m.new_slot = (ntok - 1) % kP;
@@ -977,13 +993,18 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         // issue as many pages as the worker's sub-ring has free stages
         while (q_done && pg < np && dev::mbar_test(&sm.empty[w * SW + pos.stage], pos.phase ^ 1u)) {
             const int32_t page = sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + pg];
-            if (pipelined && holds_recent_tokens(t0, pg, s_len[j])) pdl_wait_once(waited);
+            // pipelined: a page an in-flight kernel may still write is COPIED by the consumer warp after its
+            // own griddepcontrol.wait, so this warp (which feeds every worker) never blocks.  The stage is
+            // still reserved here (empty wait + arrive.expect_tx), so the consumer can never run a ring
+            // phase ahead; its copy may complete before this arrival (the tx-count goes transiently negative).
             uint64_t *bar = &sm.full[w * SW + pos.stage];
-            uint8_t *dst = sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes;
             dev::mbar_arrive_expect_tx(bar, kStageBytes);
-            const int row = page * kP;
-            dev::tma_load_3d(dst, tmap_k, 0, row, 0, bar, pol);
-            dev::tma_load_3d(dst + kPageBytes, tmap_v, 0, row, 0, bar, pol);
+            if (!(pipelined && holds_recent_tokens(t0, pg, s_len[j]))) {
+                uint8_t *dst = sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes;
+                const int row = page * kP;
+                dev::tma_load_3d(dst, tmap_k, 0, row, 0, bar, pol);
+                dev::tma_load_3d(dst + kPageBytes, tmap_v, 0, row, 0, bar, pol);
+            }
             ++pg;
             pos.advance(1, SW);
             if (w == 0 && it == 0 && pg == 1) {
@@ -1015,7 +1036,8 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
 }
 
 template <int D, int R, int NW>
-__device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW, int n_items) {
+__device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW, int n_items, const void *tmap_k,
+                                    const void *tmap_v) {
     constexpr int ROW_BYTES = D * 2;
     constexpr int kPageBytes = kP * ROW_BYTES;
     constexpr int kHalfBytes = kPageBytes / (D / 64);
@@ -1046,7 +1068,18 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     }
     RingPos pos{0, 0u};
     for (int it = 0;; ++it) {
+#ifdef HETIS_DEBUG_HANG
+        {
+            long long n_ = 0;
+            while (!dev::mbar_try_wait(&sm.qfull[w], it & 1))
+                if (++n_ == (1ll << 24)) {
+                    if (lane == 0) printf("hang qfull: blk %d w %d it %d\n", (int)blockIdx.x, w, it);
+                    __trap();
+                }
+        }
+#else
         dev::mbar_wait(&sm.qfull[w], it & 1);
+#endif
         const ItemMeta meta = sm.meta[w];
         if (lane == 0 && meta.item >= 0) {
             HETIS_TS_ADD(7);
@@ -1081,7 +1114,32 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
 #pragma unroll
         for (int nt = 0; nt < NT_O; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
         for (int pg = 0; pg < meta.npages; ++pg) {
+            if (pg >= meta.defer_from) {  // pipelined: this warp waits for the in-flight kernels, then issues
+                asm volatile("griddepcontrol.wait;" ::: "memory");  // all lanes, converged
+                if (lane == 0) {  // the producer reserved the stage (arrive.expect_tx); only the copy is ours
+                    uint64_t *bar = &sm.full[w * SW + pos.stage];
+                    uint8_t *dst = sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes;
+                    const int row = meta.defer_page[pg - meta.defer_from] * kP;
+                    dev::tma_load_3d(dst, tmap_k, 0, row, 0, bar, dev::policy_evict_first());
+                    dev::tma_load_3d(dst + kPageBytes, tmap_v, 0, row, 0, bar, dev::policy_evict_first());
+                }
+                __syncwarp();
+            }
+#ifdef HETIS_DEBUG_HANG
+            {
+                long long n_ = 0;
+                while (!dev::mbar_try_wait(&sm.full[w * SW + pos.stage], pos.phase))
+                    if (++n_ == (1ll << 24)) {
+                        if (lane == 0)
+                            printf("hang full: blk %d w %d it %d item %d pg %d/%d defer_from %d new_pg %d stage %d ph %u\n",
+                                   (int)blockIdx.x, w, it, meta.item, pg, meta.npages, meta.defer_from, meta.new_pg,
+                                   pos.stage, pos.phase);
+                        __trap();
+                    }
+            }
+#else
             dev::mbar_wait(&sm.full[w * SW + pos.stage], pos.phase);
+#endif
             if (meta.new_page >= 0 && pg == meta.new_pg) {
                 uint8_t *kbp = sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes;
                 nr.patch(p, kbp, kbp + kPageBytes, meta.new_page, meta.new_slot, lane, swz);
@@ -1229,7 +1287,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     if (threadIdx.x < 32) {
         if (threadIdx.x < NW) producer_warp_items<ROW_BYTES, R, NW>(p, sm, SW, s_len, s_off, &tmap_k, &tmap_v);
     } else {
-        consumer_warp_items<D, R, NW>(p, sm, SW, n_items);
+        consumer_warp_items<D, R, NW>(p, sm, SW, n_items, &tmap_k, &tmap_v);
     }
     // the last CTA to finish returns the device-wide counters to zero for the next launch
     __syncwarp();

@@ -2,6 +2,8 @@
 // mma.sync, cache policies.  Header-only, device code only.
 #pragma once
 
+#include <cstdio>
+
 #include <cuda_bf16.h>
 #include <stdint.h>
 
@@ -60,10 +62,24 @@ __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
     return ok != 0;
 }
 
+#ifdef HETIS_DEBUG_HANG
+// debug builds: a wait that never completes reports where it is stuck and traps
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    long long n = 0;
+    while (!mbar_try_wait(bar, parity)) {
+        if (++n == (1ll << 24)) {
+            printf("hetis hang: block %d thread %d bar smem+%u parity %u\n", (int)blockIdx.x, (int)threadIdx.x,
+                   smem_u32(bar), parity);
+            __trap();
+        }
+    }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
     }
 }
+#endif
 
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ uint64_t policy_evict_first() {

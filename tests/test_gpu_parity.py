@@ -496,8 +496,10 @@ def test_decode_step_fused_append_matches_separate_calls():
 
 
 # ------------------------------------------------------------------ pipelined steps (HETIS_ATTN_PIPELINED)
-@pytest.mark.parametrize("H,Hkv,D,dtype", [(64, 8, 128, "bf16"), (40, 40, 128, "bf16"), (8, 8, 64, "f32")])
-def test_pipelined_steps_match_serial_steps(H, Hkv, D, dtype):
+@pytest.mark.parametrize("H,Hkv,D,dtype,extra", [(64, 8, 128, "bf16", 0), (40, 40, 128, "bf16", 0),
+                                                 (8, 8, 64, "f32", 0), (40, 40, 128, "bf16", hetis.ATTN_MHA_TC),
+                                                 (16, 4, 64, "bf16", 0)])
+def test_pipelined_steps_match_serial_steps(H, Hkv, D, dtype, extra):
     """Several decode steps (each appends one token) back to back on one stream, pipelined with two
     alternating workspaces, as a CUDA graph so consecutive kernels really overlap: every step's O and the
     final pools are bit-identical to the same steps run with the default (fully ordered) launches."""
@@ -517,7 +519,7 @@ def test_pipelined_steps_match_serial_steps(H, Hkv, D, dtype):
         vn = [torch.randn(b.v_new.shape, generator=g, device="cuda").to(b.v_new.dtype) for _ in range(n_steps)]
         sl = [(lens0 + i + 1).to("cuda") for i in range(n_steps)]
         o = [torch.empty((B, x, D), device="cuda") for _ in range(n_steps)]
-        flags = hetis.ATTN_PIPELINED if mode == "pipelined" else 0
+        flags = (hetis.ATTN_PIPELINED if mode == "pipelined" else 0) | extra
 
         def run():
             for i in range(n_steps):
