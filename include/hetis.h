@@ -41,6 +41,15 @@
  *   tokens under a sequence split (row f3): kv_append skips the request, the
  *   combine writes o = 0 (and lse = -inf).  Softmax over no token is
  *   undefined (reading 10), so a whole-request result needs L_j >= 1.
+ * - Stream ordering: kernels are launched with programmatic dependent launch
+ *   (PDL).  Each waits (griddepcontrol.wait) for its predecessor before it
+ *   touches anything a predecessor writes, so results follow stream order.
+ *   Callers may rely on: the attention kernels read q, seq_lens and block
+ *   tables before that wait (none of this library's kernels that let their
+ *   successor start early writes those -- hetis_seq_split_lens and
+ *   hetis_kv_migrate never do), and with HETIS_ATTN_PIPELINED they also read
+ *   cache pages other than each request's last two positions early.  Work the
+ *   caller enqueues itself (copies, torch kernels) is ordinary stream order.
  * - Builds: head_dim in {64, 128}; page_size 16; kv/q dtype in {bf16, f32}
  *   with q_dtype == kv_dtype; o_dtype in {f32, bf16}; r = H / H_kv in
  *   {1, 2, 4, 8}.  Anything else -> HETIS_E_UNSUPPORTED.  bf16 with r > 1
