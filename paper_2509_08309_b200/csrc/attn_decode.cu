@@ -935,7 +935,13 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         asm volatile("griddepcontrol.wait;" ::: "memory");
         return n_static + atomicAdd(p.counters, 1);
     };
-    int item = device_claim ? w * (int)gridDim.x + (int)blockIdx.x : claim();
+    // The first claim is CTA-local only: a steal touches the device-wide counter, which needs a
+    // griddepcontrol.wait, and that wait must be executed by the converged producer warp (below).
+    int item = device_claim ? w * (int)gridDim.x + (int)blockIdx.x : -2;
+    if (!device_claim) {
+        const int k = atomicAdd(sm.claim, 1);
+        if (k < per_cta) item = (int)blockIdx.x + k * (int)gridDim.x;
+    }
     // The next item is claimed lazily, once half of the current item's pages
     // are issued: a worker on a faster SM gets there sooner, which is what
     // balances the device (claiming at the start would hand out every item
@@ -946,7 +952,7 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     int pg = 0;
     bool q_done = false, finished = false;
     RingPos pos{0, 0u};
-    if (item < n_items) {
+    if (item >= 0 && item < n_items) {
         decode(item, j, g, t0, ntok);
         np = (ntok + kP - 1) / kP;
         load_next(item);
@@ -958,6 +964,17 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     if (!pipelined) {
         pdl_wait_once(waited);  // pools may hold rows the previous kernel wrote
         publish_split_offsets(p, s_off, w, NW);
+    }
+    if (item == -2 && pipelined) item = n_items;  // pipelined launches never steal (no wait was done)
+    if (item == -2) {  // the CTA-local queue was empty from the start: steal
+        item = n_static + atomicAdd(p.counters, 1);
+        if (item < n_items) {
+            decode(item, j, g, t0, ntok);
+            np = (ntok + kP - 1) / kP;
+            load_next(item);
+#pragma unroll
+            for (int i = 0; i < kPagesPerItem; ++i) sm.pids[(w * 2 + 0) * kPagesPerItem + i] = nxt[i];
+        }
     }
     if (w == 0) {
         HETIS_TS(2);
