@@ -188,6 +188,17 @@ HETIS_API hetis_status hetis_kv_append(const hetis_shape *shape, int32_t num_seq
                              const int32_t *block_table, int32_t max_pages, const int32_t *seq_lens,
                              hetis_stream_t stream);
 
+/* ---- debug validation of the device-data contracts -------------------- */
+/* Counts, into *violations (device int32, overwritten), the contract
+ * violations the decode kernels trust not to happen: seq_lens[j] outside
+ * [1, max_pages * P] (reading 10: an empty request has no softmax), and page
+ * ids of pages 0 .. ceil(L_j / P) - 1 of every (request, local kv head)
+ * outside [0, num_pages).  Stream-ordered; read *violations after it.  For
+ * debugging only -- it reads the whole block table. */
+HETIS_API hetis_status hetis_check_tables(const hetis_shape *shape, int32_t num_seqs, int32_t kv_head_count,
+                                          int64_t num_pages, const int32_t *block_table, int32_t max_pages,
+                                          const int32_t *seq_lens, int32_t *violations, hetis_stream_t stream);
+
 /* ---- decode attention (Eq. 2b) --------------------------- */
 /* Workspace bytes for num_seqs requests of length <= max_seq_len and
  * q_head_count local heads (partials of every split + the split offsets). */

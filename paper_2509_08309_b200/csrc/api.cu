@@ -311,6 +311,21 @@ hetis_status hetis_kv_append(const hetis_shape *shape, int32_t num_seqs, int32_t
     return HETIS_OK;
 }
 
+// ---------------------------------------------------------------- debug table validation
+hetis_status hetis_check_tables(const hetis_shape *shape, int32_t num_seqs, int32_t kv_head_count, int64_t num_pages,
+                                const int32_t *block_table, int32_t max_pages, const int32_t *seq_lens,
+                                int32_t *violations, hetis_stream_t stream) {
+    hetis_status st = check_shape(shape);
+    if (st != HETIS_OK) return st;
+    if (num_seqs < 0 || kv_head_count < 1 || num_pages < 1 || max_pages < 1) return fail(HETIS_E_INVALID, "bad sizes");
+    if (!violations || (num_seqs > 0 && (!block_table || !seq_lens))) return fail(HETIS_E_INVALID, "NULL pointer");
+    if (!aligned(violations, 4)) return fail(HETIS_E_INVALID, "violations must be 4-byte aligned");
+    cudaError_t e = hetis::launch_check_tables(num_seqs, kv_head_count, shape->page_size, num_pages, block_table,
+                                               max_pages, seq_lens, violations, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "check_tables launch");
+    return HETIS_OK;
+}
+
 // ---------------------------------------------------------------- migration (f4)
 hetis_status hetis_kv_migrate(const hetis_shape *shape, int32_t num_entries, const hetis_migration_entry *entries,
                               const void *src_k_pool, const void *src_v_pool, const int32_t *src_block_table,

@@ -93,6 +93,9 @@ cudaError_t launch_peer_signal(const PeerSignal &t, cudaStream_t s);
 cudaError_t launch_scatter_pull(const int64_t *sig, int64_t epoch, const void *q_src, const void *k_src,
                                 const void *v_src, int num_seqs, int H, int Hkv, int q0, int nq, int k0, int nk,
                                 int qrow, int kvrow, void *q_dst, void *k_dst, void *v_dst, cudaStream_t s);
+cudaError_t launch_check_tables(int num_seqs, int kv_heads, int page_size, int64_t num_pages,
+                                const int32_t *block_table, int max_pages, const int32_t *seq_lens,
+                                int32_t *violations, cudaStream_t s);
 cudaError_t launch_peer_wait(const int64_t *sig, int n, int64_t epoch, cudaStream_t s);
 cudaError_t launch_kv_migrate(int num_entries, const hetis_migration_entry *entries, int page_size, int page_bytes,
                               const void *src_k, const void *src_v, const int32_t *src_bt, int src_max_pages,

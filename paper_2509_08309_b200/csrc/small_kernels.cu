@@ -260,6 +260,30 @@ __global__ void peer_wait_kernel(const int64_t *sig, int n, int64_t epoch) {
     }
 }
 
+// ---------------------------------------------------------------- table validation (debug)
+// Counts contract violations of the device-side data the decode kernels trust without
+// checking (include/hetis.h): 1 <= seq_lens[j] <= max_pages * P, and every page id a
+// kernel will read (pages 0 .. ceil(L_j / P) - 1 of each (request, kv head)) in [0, num_pages).
+__global__ void check_tables_kernel(int num_seqs, int kv_heads, int page_size, int64_t num_pages,
+                                    const int32_t *block_table, int max_pages, const int32_t *seq_lens,
+                                    int32_t *violations) {
+    const int64_t total = (int64_t)num_seqs * kv_heads * max_pages;
+    int bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i % max_pages);
+        const int64_t row = i / max_pages;
+        const int j = (int)(row / kv_heads);
+        const int L = seq_lens[j];
+        if (k == 0 && row % kv_heads == 0 && (L < 1 || (int64_t)L > (int64_t)max_pages * page_size)) ++bad;
+        const int np = L < 1 ? 0 : (L + page_size - 1) / page_size;
+        if (k < np) {
+            const int32_t pid = block_table[i];
+            if (pid < 0 || (int64_t)pid >= num_pages) ++bad;
+        }
+    }
+    if (bad) atomicAdd(violations, bad);
+}
+
 // ---------------------------------------------------------------- scatter over peer memory
 // Publish `epoch` into slot [rank] of every rank's signal array (system-scope
 // release) once everything before it on the stream is complete and visible.
@@ -420,6 +444,22 @@ cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim,
 
 cudaError_t launch_peer_wait(const int64_t *sig, int n, int64_t epoch, cudaStream_t s) {
     peer_wait_kernel<<<1, 32, 0, s>>>(sig, n, epoch);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_tables(int num_seqs, int kv_heads, int page_size, int64_t num_pages,
+                                const int32_t *block_table, int max_pages, const int32_t *seq_lens,
+                                int32_t *violations, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(violations, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return e;
+    const int64_t total = (int64_t)num_seqs * kv_heads * max_pages;
+    if (total == 0) return cudaSuccess;
+    const int threads = 256;
+    int64_t blocks = (total + threads - 1) / threads;
+    if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
+    check_tables_kernel<<<(unsigned)blocks, threads, 0, s>>>(num_seqs, kv_heads, page_size, num_pages, block_table,
+                                                             max_pages, seq_lens, violations);
     note_launch();
     return cudaGetLastError();
 }

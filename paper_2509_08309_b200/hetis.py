@@ -37,7 +37,7 @@ EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_
             "hetis_comm_workspace", "hetis_scatter_q", "hetis_gather", "hetis_kv_migrate",
             "hetis_attn_combine_lse", "hetis_seq_split_lens", "hetis_seq_merge", "hetis_seq_broadcast_q",
             "hetis_seq_allgather_merge", "hetis_peer_signal", "hetis_scatter_pull", "hetis_attn_partial_append",
-            "hetis_attn_decode_append", "hetis_launch_count")
+            "hetis_attn_decode_append", "hetis_check_tables", "hetis_launch_count")
 
 
 class HetisError(RuntimeError):
@@ -101,6 +101,7 @@ def lib() -> ctypes.CDLL:
                 "hetis_seq_broadcast_q": (ctypes.c_int, [sp, vp, i32, i32, i32, i32, vp, vp, vp, vp]),
                 "hetis_seq_allgather_merge": (ctypes.c_int, [sp, vp, i32, i32, i32, vp, vp, vp, i64, vp]),
                 "hetis_peer_signal": (ctypes.c_int, [P(vp), i32, i32, i64, vp]),
+                "hetis_check_tables": (ctypes.c_int, [sp, i32, i32, i64, vp, i32, vp, vp, vp]),
                 "hetis_attn_partial_append": (ctypes.c_int, [sp, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32, vp,
                                                              i32, vp, sz, u32, vp]),
                 "hetis_attn_decode_append": (ctypes.c_int, [sp, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32, vp,
@@ -224,6 +225,16 @@ def kv_append(shape: CShape, k_new, v_new, k_pool, v_pool, block_table, seq_lens
                                  _dev(k_pool, "k_pool"), _dev(v_pool, "v_pool"), k_pool.shape[0],
                                  _dev(block_table, "block_table"), block_table.shape[2], _dev(seq_lens, "seq_lens"),
                                  _stream(stream)), "hetis_kv_append")
+
+
+def check_tables(shape: CShape, k_pool, block_table, seq_lens, stream=None) -> int:
+    """Number of device-data contract violations (hetis_check_tables); synchronises the stream."""
+    out = torch.empty(1, dtype=torch.int32, device=block_table.device)
+    B, G, M = block_table.shape
+    _check(lib().hetis_check_tables(ctypes.byref(shape), B, G, k_pool.shape[0], _dev(block_table, "block_table"), M,
+                                    _dev(seq_lens, "seq_lens"), _dev(out, "violations"), _stream(stream)),
+           "hetis_check_tables")
+    return int(out.item())
 
 
 def kv_migrate(shape: CShape, entries, src_k_pool, src_v_pool, src_block_table, dst_k_pool, dst_v_pool,

@@ -545,3 +545,17 @@ def test_pipelined_steps_match_serial_steps(H, Hkv, D, dtype, extra):
             for i in range(n_steps):
                 assert torch.equal(os_[i], ref_o[i]), (mode, i)
             assert torch.equal(bits(k), bits(ref_k)) and torch.equal(bits(v), bits(ref_v)), mode
+
+
+def test_check_tables_counts_contract_violations():
+    b = gpu_batch(16, 4, 128, "bf16", (1, 17, 300, 1029), seed=7)
+    s = hetis.make_shape(b.shape)
+    assert hetis.check_tables(s, b.k_pool, b.block_table, b.seq_lens) == 0
+    bt = b.block_table.clone()
+    bt[2, 1, 3] = b.k_pool.shape[0]            # page id out of range, inside the request's pages
+    bt[0, 0, 5] = 10 ** 6                      # beyond request 0's only page: never read -> not a violation
+    assert hetis.check_tables(s, b.k_pool, bt, b.seq_lens) == 1
+    sl = b.seq_lens.clone()
+    sl[1] = 0                                  # empty request (reading 10)
+    sl[3] = b.block_table.shape[2] * 16 + 1    # longer than its table
+    assert hetis.check_tables(s, b.k_pool, b.block_table, sl) == 2
