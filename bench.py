@@ -55,6 +55,11 @@ def parse():
                     help="N > 1: NCCL all-gather of O (default) or the combine kernel's peer-memory stores")
     ap.add_argument("--fused-append", type=int, default=1,
                     help="1: kv_append fused into the attention kernel (hetis_attn_partial_append); 0: separate")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="debug: run the N > 1 code path (NCCL process group, scatter, gather) at N = 1")
+    ap.add_argument("--graph-dist", type=int, default=1,
+                    help="N > 1: replay the timed steps as a CUDA graph too (NCCL calls captured; not with the "
+                         "peer-memory exchanges, whose epochs change every step)")
     ap.add_argument("--scatter", default="nccl", choices=["nccl", "peer"],
                     help="N > 1: 'peer' = every rank pulls its q / new k, v shard from the root's buffers over "
                          "NVLink (hetis_peer_signal + hetis_scatter_pull) instead of NCCL send/recv")
@@ -227,8 +232,19 @@ def run_ours(args, world, rank, local):
     split = cfg.head_split(world)
     comm_ptr = None
     pg = None
-    if world > 1:
+    dist_mode = world > 1 or args.force_dist
+    if dist_mode:
         import torch.distributed as dist
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            if "MASTER_PORT" not in os.environ:
+                import socket
+                so = socket.socket()
+                so.bind(("127.0.0.1", 0))
+                os.environ["MASTER_PORT"] = str(so.getsockname()[1])
+                so.close()
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=device)
         pg = dist.group.WORLD
         dist.barrier()
@@ -253,7 +269,7 @@ def run_ours(args, world, rank, local):
     v_pools = [batch.v_pool] + [batch.v_pool.clone() for _ in range(n_layers - 1)]
     odt = torch.bfloat16 if args.o_dtype == "bf16" else torch.float32
     is_root = rank == 0
-    if world > 1:
+    if dist_mode:
         gq = torch.Generator(device=device).manual_seed(cfg.seed + 17)
         q_full = workload.make_q(shape, B, cfg.seed, device) if is_root else None
         kn_full = (torch.randn((B, shape.num_kv_heads, shape.head_dim), generator=gq, device=device)
@@ -272,11 +288,11 @@ def run_ours(args, world, rank, local):
 
     def one_step(i, ev_a=None, ev_b=None):
         li = i % n_layers
-        if world > 1 and (args.gather == "peer" or args.scatter == "peer"):
+        if dist_mode and (args.gather == "peer" or args.scatter == "peer"):
             step.epoch += 1
-        if world > 1 and args.scatter == "peer":
+        if dist_mode and args.scatter == "peer":
             step.scatter_peers(step.epoch)
-        elif world > 1:
+        elif dist_mode:
             step.scatter(q_full, kn_full, vn_full)
         if not args.fused_append:
             step.append(k_pools[li], v_pools[li], batch.block_table, batch.seq_lens)
@@ -292,7 +308,7 @@ def run_ours(args, world, rank, local):
                                flags=args.attn_flags)
         if ev_b is not None:
             ev_b.record(torch.cuda.current_stream(device))
-        if world > 1 and args.gather == "peer":
+        if dist_mode and args.gather == "peer":
             # one kernel merges the splits and stores O into every rank's o_full over NVLink
             hetis.attn_combine_peers(step.cshape, batch.seq_lens, max_len, step.o_peers, step.sig_peers, rank,
                                      step.epoch, step.buf.workspace, q_head_begin=q_begin, q_head_count=q_count)
@@ -300,11 +316,11 @@ def run_ours(args, world, rank, local):
             return
         hetis.attn_combine(step.cshape, batch.seq_lens, max_len, step.buf.o_shard, step.buf.workspace,
                            q_head_count=q_count)
-        if world > 1:
+        if dist_mode:
             step.gather(o_full, root=-1)
 
     def barrier():
-        if world > 1:
+        if dist_mode:
             import torch.distributed as dist
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize(device)
@@ -327,7 +343,9 @@ def run_ours(args, world, rank, local):
     # the graph is replayed once inside the timed region; per-step events are graph nodes.
     sampler = ClockSampler(local)
     # external=True: inside a capture the records become event-record graph nodes
-    use_graph = bool(args.graph) and world == 1
+    # N > 1: only the NCCL exchanges can be captured -- the peer-memory ones carry a per-step epoch
+    use_graph = bool(args.graph) and (not dist_mode or (bool(args.graph_dist) and args.gather == "nccl"
+                                                         and args.scatter == "nccl"))
     evs_a = [torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(args.steps)]
     evs_b = [torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -339,7 +357,7 @@ def run_ours(args, world, rank, local):
     # for the roofline), replayed in a second timed region.
     graph = graph_ev = None
     graph_launches = 0
-    if args.graph and world == 1:
+    if use_graph:
         try:
             graph = torch.cuda.CUDAGraph()
             c0 = hetis.launch_count()
@@ -383,7 +401,7 @@ def run_ours(args, world, rank, local):
 
     # ---- end to end through the public API with pinned host buffers
     h2d = d2h = 0
-    if world > 1:
+    if dist_mode:
         if is_root:
             hq = q_full.cpu().pin_memory()
             hk = kn_full.cpu().pin_memory()
@@ -402,7 +420,7 @@ def run_ours(args, world, rank, local):
     h2d += hsl.numel() * 4
 
     def e2e_step(i):
-        if world > 1:
+        if dist_mode:
             if is_root:
                 q_full.copy_(hq, non_blocking=True)
                 kn_full.copy_(hk, non_blocking=True)
@@ -418,7 +436,7 @@ def run_ours(args, world, rank, local):
 
     e_steps = max(min(args.steps, 50), 3)
     e_mode = "serial"
-    if world == 1:
+    if not dist_mode:
         # Overlapped through the same public calls: step i's host->device copies run on a copy stream
         # while step i-1 computes, and its device->host read on another stream while step i+1
         # computes -- double-buffered device inputs / outputs and pinned host outputs.  Every step
@@ -531,8 +549,8 @@ def run_ours(args, world, rank, local):
                 "seq_len_range": cfg.seq_len_range, "q_heads": shape.num_q_heads, "kv_heads": shape.num_kv_heads,
                 "head_dim": shape.head_dim, "page_size": shape.page_size, "split": list(split),
                 "o_dtype": args.o_dtype, "layers_rotated": n_layers,
-                "gather": (args.gather if world > 1 else None),
-                "scatter": (args.scatter if world > 1 else None),
+                "gather": (args.gather if dist_mode else None),
+                "scatter": (args.scatter if dist_mode else None),
                 "fused_append": bool(args.fused_append),
                 "l2": f"inputs larger than L2: {n_layers} layer pool(s) x {kv_bytes_rank / 1e6:.1f} MB KV per rank "
                       f"rotated per step (L2 = 126 MB)",
@@ -551,7 +569,7 @@ def run_ours(args, world, rank, local):
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_mode:
         import torch.distributed as dist
         dist.barrier(device_ids=[local])
         dist.destroy_process_group()

@@ -675,6 +675,10 @@ hetis_status hetis_scatter_q(const hetis_plan *plan, void *nccl_comm, int32_t ra
     Nccl &nc = nccl();
     std::vector<uint8_t *> qst(N), kst(N), vst(N);
     if (rank == root) {
+        // every rank's q / new k / new v slices in ONE pack kernel (segments of hetis::CopySegs)
+        if (3 * N > hetis::kMaxCopySegs) return fail(HETIS_E_UNSUPPORTED, "scatter packs at most 16 ranks");
+        hetis::CopySegs segs{};
+        segs.num_seqs = num_seqs;
         uint8_t *w = static_cast<uint8_t *>(workspace);
         for (int i = 0; i < N; ++i) {
             const int x = plan->x[i], b = plan->begin[i];
@@ -695,11 +699,12 @@ hetis_status hetis_scatter_q(const hetis_plan *plan, void *nccl_comm, int32_t ra
             kst[i] = kd;
             vst[i] = vd;
             if (x == 0) continue;
-            cudaError_t e = hetis::launch_head_slice(q_full, qd, num_seqs, H, b, x, qrow, cs);
-            if (e == cudaSuccess) e = hetis::launch_head_slice(k_new_full, kd, num_seqs, Hkv, b / r, x / r, kvrow, cs);
-            if (e == cudaSuccess) e = hetis::launch_head_slice(v_new_full, vd, num_seqs, Hkv, b / r, x / r, kvrow, cs);
-            if (e != cudaSuccess) return cuda_fail(e, "scatter pack");
+            segs.seg[segs.count++] = {static_cast<const uint8_t *>(q_full), qd, H, b, x, 0, x, qrow};
+            segs.seg[segs.count++] = {static_cast<const uint8_t *>(k_new_full), kd, Hkv, b / r, x / r, 0, x / r, kvrow};
+            segs.seg[segs.count++] = {static_cast<const uint8_t *>(v_new_full), vd, Hkv, b / r, x / r, 0, x / r, kvrow};
         }
+        cudaError_t e = hetis::launch_head_copies(segs, cs);
+        if (e != cudaSuccess) return cuda_fail(e, "scatter pack");
     }
     ncclComm_t comm = static_cast<ncclComm_t>(nccl_comm);
     NCCL_TRY(nc.groupStart());
@@ -774,13 +779,18 @@ hetis_status hetis_gather(const hetis_plan *plan, void *nccl_comm, int32_t rank,
         }
         NCCL_TRY(nc.groupEnd());
     }
-    if (receiver) {
+    if (receiver) {  // every rank's shard to its global heads in ONE placement kernel
+        if (N > hetis::kMaxCopySegs) return fail(HETIS_E_UNSUPPORTED, "gather places at most 48 ranks");
+        hetis::CopySegs segs{};
+        segs.num_seqs = num_seqs;
         for (int i = 0; i < N; ++i) {
             if (plan->x[i] == 0) continue;
             const void *src = (root >= 0 && i == rank) ? o_shard : stg[i];
-            cudaError_t e = hetis::launch_head_place(src, o_full, num_seqs, H, plan->begin[i], plan->x[i], orow, cs);
-            if (e != cudaSuccess) return cuda_fail(e, "gather place");
+            segs.seg[segs.count++] = {static_cast<const uint8_t *>(src), static_cast<uint8_t *>(o_full), plan->x[i], 0,
+                                      H, plan->begin[i], plan->x[i], orow};
         }
+        cudaError_t e = hetis::launch_head_copies(segs, cs);
+        if (e != cudaSuccess) return cuda_fail(e, "gather place");
     }
     return HETIS_OK;
 }

@@ -58,6 +58,24 @@ cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const
 cudaError_t launch_kv_append(int num_seqs, int kv_heads, int head_dim, int page_size, int elem_bytes,
                              const void *k_new, const void *v_new, void *k_pool, void *v_pool,
                              const int32_t *block_table, int max_pages, const int32_t *seq_lens, cudaStream_t s);
+// Up to kMaxCopySegs strided head copies in ONE launch (the scatter's pack on the
+// root and the gather's placement: one kernel instead of one per rank and tensor).
+// Segment k copies, for every request j, heads [hs, hs + n) of src rows
+// [num_seqs][src_heads] to heads [hd, hd + n) of dst rows [num_seqs][dst_heads].
+constexpr int kMaxCopySegs = 48;
+struct CopySeg {
+    const uint8_t *src;
+    uint8_t *dst;
+    int src_heads, hs, dst_heads, hd, n, row_bytes;
+};
+struct CopySegs {
+    CopySeg seg[kMaxCopySegs];
+    int64_t start[kMaxCopySegs + 1];  // prefix of 16-byte chunks per segment
+    int count;
+    int num_seqs;
+};
+cudaError_t launch_head_copies(CopySegs &c, cudaStream_t s);
+
 // copy rows [num_seqs][src_heads][d] head slice [h0, h0 + n) -> dense [num_seqs][n][d]
 cudaError_t launch_head_slice(const void *src, void *dst, int num_seqs, int src_heads, int h0, int n,
                               int row_bytes, cudaStream_t s);

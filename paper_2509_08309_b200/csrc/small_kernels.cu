@@ -364,7 +364,41 @@ __global__ void head_copy_kernel(const uint8_t *src, uint8_t *dst, int num_seqs,
     }
 }
 
+// Batched version: chunk i belongs to the segment whose prefix range holds it
+// (linear search: at most 3 N segments).
+__global__ void head_copies_kernel(const CopySegs c) {
+    const int64_t total = c.start[c.count];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int k = 0;
+        while (i >= c.start[k + 1]) ++k;
+        const CopySeg &g = c.seg[k];
+        const int chunks = g.row_bytes / 16;
+        const int64_t li = i - c.start[k];
+        const int ch = (int)(li % chunks);
+        const int64_t rowi = li / chunks;
+        const int hh = (int)(rowi % g.n);
+        const int j = (int)(rowi / g.n);
+        const uint4 v =
+            *reinterpret_cast<const uint4 *>(g.src + (((size_t)j * g.src_heads + g.hs + hh) * g.row_bytes) + 16 * ch);
+        *reinterpret_cast<uint4 *>(g.dst + (((size_t)j * g.dst_heads + g.hd + hh) * g.row_bytes) + 16 * ch) = v;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_head_copies(CopySegs &c, cudaStream_t s) {
+    c.start[0] = 0;
+    for (int k = 0; k < c.count; ++k)
+        c.start[k + 1] = c.start[k] + (int64_t)c.num_seqs * c.seg[k].n * (c.seg[k].row_bytes / 16);
+    const int64_t total = c.start[c.count];
+    if (total == 0) return cudaSuccess;
+    const int threads = 256;
+    int64_t blocks = (total + threads - 1) / threads;
+    if (blocks > 4 * num_sms()) blocks = 4 * num_sms();
+    head_copies_kernel<<<(unsigned)blocks, threads, 0, s>>>(c);
+    note_launch();
+    return cudaGetLastError();
+}
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 

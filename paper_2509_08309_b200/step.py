@@ -67,8 +67,8 @@ class DecodeStep:
         if self.world > 1:
             x = [self.plan.heads(i)[1] for i in range(self.world)]
             if self.rank == self.root:
-                n += 3 * sum(1 for v in x if v > 0)       # scatter packs (incl. own shard)
-            n += sum(1 for v in x if v > 0)               # gather places
+                n += 1                                    # one batched scatter pack (every rank's slices)
+            n += 1                                        # one batched gather placement
         return n
 
     def scatter(self, q_full, k_new_full, v_new_full, stream=None):
