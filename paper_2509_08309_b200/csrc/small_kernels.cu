@@ -59,7 +59,10 @@ __global__ void kv_append_kernel(int num_seqs, int kv_heads, int row_bytes, int 
 // <= kNarrowSplits splits, a block serves G pairs (one group each: few blocks,
 // one round trip per pair); otherwise a block serves one pair.
 constexpr int kCombineThreads = 128;
-constexpr int kCombineChunk = 8;
+#ifndef HETIS_COMBINE_CHUNK
+#define HETIS_COMBINE_CHUNK 8
+#endif
+constexpr int kCombineChunk = HETIS_COMBINE_CHUNK;
 constexpr int kNarrowSplits = 16;
 
 struct FoldState {
