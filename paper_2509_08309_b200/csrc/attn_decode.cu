@@ -1084,6 +1084,7 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         v_off[c2] = swz((mi & 1) * 8 + (lane & 7), 2 * c2 + (mi >> 1));
     }
     RingPos pos{0, 0u};
+    bool c_waited = false;  // this warp has executed griddepcontrol.wait (pipelined deferred pages)
     for (int it = 0;; ++it) {
 #ifdef HETIS_DEBUG_HANG
         {
@@ -1130,18 +1131,29 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         float o[NT_O][4];
 #pragma unroll
         for (int nt = 0; nt < NT_O; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
-        for (int pg = 0; pg < meta.npages; ++pg) {
-            if (pg >= meta.defer_from) {  // pipelined: this warp waits for the in-flight kernels, then issues
+        // Pipelined: this warp copies the item's deferred pages itself (after a converged
+        // griddepcontrol.wait), each as soon as its ring stage is free -- i.e. once the page SW
+        // positions earlier has been consumed -- so they are prefetched as deep as the producer's
+        // pages.  The producer reserves those stages (arrive.expect_tx) in ring order.
+        const RingPos item_base = pos;
+        auto issue_deferred = [&](int d) {
+            if (!c_waited) {  // once per warp: afterwards every predecessor has completed
                 asm volatile("griddepcontrol.wait;" ::: "memory");  // all lanes, converged
-                if (lane == 0) {  // the producer reserved the stage (arrive.expect_tx); only the copy is ours
-                    uint64_t *bar = &sm.full[w * SW + pos.stage];
-                    uint8_t *dst = sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes;
-                    const int row = meta.defer_page[pg - meta.defer_from] * kP;
-                    dev::tma_load_3d(dst, tmap_k, 0, row, 0, bar, dev::policy_evict_first());
-                    dev::tma_load_3d(dst + kPageBytes, tmap_v, 0, row, 0, bar, dev::policy_evict_first());
-                }
-                __syncwarp();
+                c_waited = true;
             }
+            if (lane == 0) {
+                RingPos at = item_base;
+                at.advance(d, SW);
+                uint64_t *bar = &sm.full[w * SW + at.stage];
+                uint8_t *dst = sm.ring + ((size_t)w * SW + at.stage) * kStageBytes;
+                const int row = meta.defer_page[d - meta.defer_from] * kP;
+                dev::tma_load_3d(dst, tmap_k, 0, row, 0, bar, dev::policy_evict_first());
+                dev::tma_load_3d(dst + kPageBytes, tmap_v, 0, row, 0, bar, dev::policy_evict_first());
+            }
+            __syncwarp();
+        };
+        for (int d = meta.defer_from; d < meta.npages && d < SW; ++d) issue_deferred(d);  // stages already free
+        for (int pg = 0; pg < meta.npages; ++pg) {
 #ifdef HETIS_DEBUG_HANG
             {
                 long long n_ = 0;
@@ -1168,6 +1180,7 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
                 __syncwarp();
                 if (lane == 0) dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
                 pos.advance(1, SW);
+                if (pg + SW >= meta.defer_from && pg + SW < meta.npages) issue_deferred(pg + SW);
                 continue;
             }
             const uint32_t kb = dev::smem_u32(sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes);
@@ -1241,6 +1254,7 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             __syncwarp();
             if (lane == 0) dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
             pos.advance(1, SW);
+            if (pg + SW >= meta.defer_from && pg + SW < meta.npages) issue_deferred(pg + SW);  // its stage is free
         }
         // the item's partial: o_s = acc / l and lse_s = m + log2(l) for each of the r heads
         l += __shfl_xor_sync(0xffffffffu, l, 1);
