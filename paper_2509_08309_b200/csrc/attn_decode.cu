@@ -5,28 +5,26 @@
 // (PAPER.md:539).  Each work item is (request j, local kv head g, split s)
 // covering tokens [s C, min((s+1) C, L_j)), C = kSplitTokens (reading 12), and
 // produces, for the r query heads of g, the normalised partial o_s and its
-// log2-sum-exp; attn_combine.cu merges the splits.
+// log2-sum-exp; the combine kernel (small_kernels.cu) merges the splits.
 //
-// Kernel structure (both variants), one persistent CTA per SM:
-//   warp 0      producer: decodes items, streams the item's q rows and every
-//               K/V page of the item into a ring of shared-memory stages with
-//               TMA (cp.async.bulk / cp.async.bulk.tensor) completing on
-//               mbarriers; the block-table entries of the next item are
-//               prefetched while the current item's pages are issued.
-//   warps 1..NW consumers: page p of an item goes to consumer warp p mod NW;
-//               each warp runs an fp32 online softmax over its pages; at the
-//               end of an item the NW partial states are merged in fixed warp
-//               order through shared memory (deterministic; depends on L_j only).
-// Variants:
-//   simt : CUDA cores.  q.k with fma.rn.f32.bf16 (exact bf16 products, fp32
-//          accumulate) or fp32 FFMA; p.v in fp32.  Any r, bf16 or fp32.
-//   tc   : bf16, r in {2,4,8}: the r query heads sharing a kv head form the
-//          M rows of mma.sync.m16n8k16 (rows r..7 zero).  S = Q K^T in bf16 with
-//          fp32 accumulate; P V with P split as P_hi + P_lo (two bf16 terms)
-//          carried in rows 8..15 of the same MMA, so P is effectively
-//          represented to ~2^-16 relative at no extra MMA cost.  K/V pages are
-//          loaded by 2-D TMA with the 128-byte swizzle so ldmatrix is
-//          bank-conflict free.
+// Two kernels, one persistent CTA per SM, warp 0 = TMA producer:
+//   attn_decode_kernel (shared ring; CUDA cores for MHA / fp32, tensor cores with
+//     HETIS_ATTN_TC_SHARED_RING): page p of an item goes to consumer warp
+//     p mod NW; each warp runs an fp32 online softmax over its pages; at the end
+//     of an item the NW states are merged in fixed warp order through shared
+//     memory.  q.k with fma.rn.f32.bf16 (exact bf16 products, fp32 accumulate)
+//     or fp32 FFMA; p.v with FFMA2.
+//   attn_gqa_warp_kernel (bf16 GQA default; MHA with HETIS_ATTN_MHA_TC): every
+//     consumer warp is an independent worker with its own sub-ring and whole
+//     items; the r query heads sharing a kv head are the M rows of
+//     mma.sync.m16n8k16 (rows r..7 zero), P carried as P_hi + P_lo (rows 8..15,
+//     ~2^-16 relative at no extra MMA); one 3-D 128-B-swizzled TMA box per page so
+//     ldmatrix is bank-conflict free; items dealt to CTAs, claimed lazily inside
+//     the CTA, the last 5% stolen device-wide.
+// Both: the arithmetic of an item depends on L_j only (bit-exact partition and
+// page-permutation invariance); optional fused kv_append (the new token's rows
+// patched into the landed page in shared memory and stored into the pool) and
+// pipelined launches (HETIS_ATTN_PIPELINED); see DESIGN.md §6.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
