@@ -76,13 +76,6 @@ struct CopySegs {
 };
 cudaError_t launch_head_copies(CopySegs &c, cudaStream_t s);
 
-// copy rows [num_seqs][src_heads][d] head slice [h0, h0 + n) -> dense [num_seqs][n][d]
-cudaError_t launch_head_slice(const void *src, void *dst, int num_seqs, int src_heads, int h0, int n,
-                              int row_bytes, cudaStream_t s);
-// dense [num_seqs][n][d] -> rows [num_seqs][dst_heads][d] at head offset h0
-cudaError_t launch_head_place(const void *src, void *dst, int num_seqs, int dst_heads, int h0, int n,
-                              int row_bytes, cudaStream_t s);
-
 // Peer-memory targets of the fused combine + all-gather (at most kMaxPeers ranks).
 constexpr int kMaxPeers = 8;
 struct PeerTargets {

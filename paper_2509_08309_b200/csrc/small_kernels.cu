@@ -350,23 +350,8 @@ __global__ void scatter_pull_kernel(const int64_t *sig, int64_t epoch, const uin
 }
 
 // ---------------------------------------------------------------- shard copies
-// src rows [B][src_heads] of row_bytes -> dst rows [B][dst_heads]; copies n heads
-// from src head offset hs to dst head offset hd.  16-byte chunks.
-__global__ void head_copy_kernel(const uint8_t *src, uint8_t *dst, int num_seqs, int src_heads, int hs,
-                                 int dst_heads, int hd, int n, int row_bytes) {
-    const int chunks = row_bytes / 16;
-    const int64_t total = (int64_t)num_seqs * n * chunks;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(i % chunks);
-        const int64_t rowi = i / chunks;
-        const int hh = (int)(rowi % n);
-        const int j = (int)(rowi / n);
-        const uint4 v =
-            *reinterpret_cast<const uint4 *>(src + (((size_t)j * src_heads + hs + hh) * row_bytes) + 16 * c);
-        *reinterpret_cast<uint4 *>(dst + (((size_t)j * dst_heads + hd + hh) * row_bytes) + 16 * c) = v;
-    }
-}
-
+// Strided [B][H][d] <-> dense [B][x][d] head copies around the NCCL scatter /
+// gather, every rank's (and tensor's) segment in one launch.
 // Batched version: chunk i belongs to the segment whose prefix range holds it
 // (linear search: at most 3 N segments).
 __global__ void head_copies_kernel(const CopySegs c) {
@@ -521,30 +506,6 @@ cudaError_t launch_scatter_pull(const int64_t *sig, int64_t epoch, const void *q
         static_cast<uint8_t *>(q_dst), static_cast<uint8_t *>(k_dst), static_cast<uint8_t *>(v_dst));
     note_launch();
     return cudaGetLastError();
-}
-
-static cudaError_t head_copy(const void *src, void *dst, int num_seqs, int src_heads, int hs, int dst_heads, int hd,
-                             int n, int row_bytes, cudaStream_t s) {
-    const int64_t total = (int64_t)num_seqs * n * (row_bytes / 16);
-    if (total == 0) return cudaSuccess;
-    const int threads = 256;
-    int64_t blocks = (total + threads - 1) / threads;
-    if (blocks > 4 * 148) blocks = 4 * 148;
-    head_copy_kernel<<<(unsigned)blocks, threads, 0, s>>>(static_cast<const uint8_t *>(src),
-                                                          static_cast<uint8_t *>(dst), num_seqs, src_heads, hs,
-                                                          dst_heads, hd, n, row_bytes);
-    note_launch();
-    return cudaGetLastError();
-}
-
-cudaError_t launch_head_slice(const void *src, void *dst, int num_seqs, int src_heads, int h0, int n, int row_bytes,
-                              cudaStream_t s) {
-    return head_copy(src, dst, num_seqs, src_heads, h0, n, 0, n, row_bytes, s);
-}
-
-cudaError_t launch_head_place(const void *src, void *dst, int num_seqs, int dst_heads, int h0, int n, int row_bytes,
-                              cudaStream_t s) {
-    return head_copy(src, dst, num_seqs, n, 0, dst_heads, h0, n, row_bytes, s);
 }
 
 }  // namespace hetis
