@@ -70,6 +70,9 @@ constexpr int kQSlots = 2;
 // (sweep on c3 N = 1..8 with the static share at 90 / 100: 8, 12 and 16 within +-2%)
 #define HETIS_CLAIM_AT 8
 #endif
+#ifndef HETIS_PARTIAL_EVICT_LAST
+#define HETIS_PARTIAL_EVICT_LAST 1
+#endif
 #ifndef HETIS_WARP_STAGES
 #define HETIS_WARP_STAGES 4
 #endif
@@ -454,8 +457,15 @@ __device__ __forceinline__ void merge_warp(const Params &p, const float *mbuf, i
         const size_t row = (size_t)item * R + rr;
         float *dst = p.part_o + row * D + lane * DPL;
 #pragma unroll
+#if HETIS_PARTIAL_EVICT_LAST
+        const uint64_t keep = dev::policy_evict_last();
+#pragma unroll
+        for (int k = 0; k < DPL; k += 2) dev::st_hint_f32x2(dst + k, __fdiv_rn(a[k], lsum), __fdiv_rn(a[k + 1], lsum), keep);
+        if (lane == 0) dev::st_hint_f32(p.part_lse + row, M + __log2f(lsum), keep);
+#else
         for (int k = 0; k < DPL; ++k) dst[k] = __fdiv_rn(a[k], lsum);
         if (lane == 0) p.part_lse[row] = M + __log2f(lsum);
+#endif
     }
 }
 
@@ -1260,11 +1270,20 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         if (grp < R && !(p.flags & HETIS_ATTN_DIAG_STREAM_ONLY)) {
             const size_t row = (size_t)meta.item * R + grp;
             float *dst = p.part_o + row * D;
+#if HETIS_PARTIAL_EVICT_LAST
+            const uint64_t keep = dev::policy_evict_last();
+#pragma unroll
+            for (int nt = 0; nt < NT_O; ++nt)
+                dev::st_hint_f32x2(dst + 8 * nt + 2 * tq, __fdiv_rn(o[nt][0] + o[nt][2], l),
+                                   __fdiv_rn(o[nt][1] + o[nt][3], l), keep);
+            if (tq == 0) dev::st_hint_f32(p.part_lse + row, m + __log2f(l), keep);
+#else
 #pragma unroll
             for (int nt = 0; nt < NT_O; ++nt)
                 *reinterpret_cast<float2 *>(dst + 8 * nt + 2 * tq) =
                     make_float2(__fdiv_rn(o[nt][0] + o[nt][2], l), __fdiv_rn(o[nt][1] + o[nt][3], l));
             if (tq == 0) p.part_lse[row] = m + __log2f(l);
+#endif
         }
     }
 }

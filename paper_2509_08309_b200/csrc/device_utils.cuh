@@ -94,6 +94,15 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     return p;
 }
 
+// Stores of the split partials with an L2 cache hint: they are read back by the
+// combine right after, while the K/V stream (evict_first) flows through L2.
+__device__ __forceinline__ void st_hint_f32x2(float *p, float a, float b, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(a), "f"(b), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_hint_f32(float *p, float a, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(a), "l"(pol) : "memory");
+}
+
 // 1-D bulk copy global -> shared, completion counted on an mbarrier (UBLKCP).
 __device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gmem_src, uint32_t bytes, uint64_t *bar,
                                          uint64_t policy) {
