@@ -64,6 +64,9 @@ constexpr int kCombineThreads = 128;
 #endif
 constexpr int kCombineChunk = HETIS_COMBINE_CHUNK;
 constexpr int kNarrowSplits = 16;
+#ifndef HETIS_COMBINE_DISCARD
+#define HETIS_COMBINE_DISCARD 0
+#endif
 
 struct FoldState {
     float M, wsum;
@@ -125,14 +128,27 @@ __device__ __forceinline__ float4 finish(const FoldState &f, float *lse2_out) {
 template <int D>
 __device__ __forceinline__ float4 combine_narrow(int j, int h, int q_heads, int r, const int32_t *split_off,
                                                  const float *part_lse, const float *part_o, int d4,
-                                                 float *lse2_out) {
+                                                 float *lse2_out, bool sole_reader = true) {
     const int kv_heads = q_heads / r, g = h / r, rr = h - g * r;
     const int s0 = split_off[j], ns = split_off[j + 1] - s0;
     if (ns == 0) {  // no tokens (a device holding none of request j under a sequence split): o = 0, lse = -inf
         *lse2_out = -INFINITY;
         return make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    return finish(fold_splits<D>(0, 1, ns, s0, kv_heads, g, r, rr, part_lse, part_o, d4), lse2_out);
+    const FoldState f = fold_splits<D>(0, 1, ns, s0, kv_heads, g, r, rr, part_lse, part_o, d4);
+#if HETIS_COMBINE_DISCARD
+    // the partial rows are dead once folded: drop their (dirty) L2 lines instead of writing them back
+    constexpr int TPH = D / 4, LINES = D * 4 / 128;
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned gmask = (TPH == 32 ? 0xffffffffu : ((1u << TPH) - 1u) << (lane & ~(unsigned)(TPH - 1)));
+    __syncwarp(gmask);
+    for (int i = sole_reader ? d4 : ns * LINES; i < ns * LINES; i += TPH) {
+        const int sp = i / LINES, ln = i % LINES;
+        const float *line = part_o + (((size_t)(s0 + sp) * kv_heads + g) * r + rr) * D + ln * 32;
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
+    }
+#endif
+    return finish(f, lse2_out);
 }
 
 // Wide launch: the whole 128-thread block serves one pair.  Result valid in group 0.
@@ -145,8 +161,8 @@ __device__ __forceinline__ float4 combine_wide(int j, int h, int q_heads, int r,
     const int tid = threadIdx.x, grp = tid / TPH, d4 = tid % TPH;
     const int kv_heads = q_heads / r, g = h / r, rr = h - g * r;
     const int s0 = split_off[j], ns = split_off[j + 1] - s0;
-    if (ns <= kNarrowSplits)  // block-uniform
-        return combine_narrow<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4, lse2_out);
+    if (ns <= kNarrowSplits)  // block-uniform; every group folds the same pair, so none may discard
+        return combine_narrow<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4, lse2_out, false);
     const FoldState f = fold_splits<D>(grp, G, ns, s0, kv_heads, g, r, rr, part_lse, part_o, d4);
     s_acc[grp][d4] = f.acc;
     if (d4 == 0) {

@@ -102,9 +102,16 @@ def main():
                                       flags=a.flags | hetis.ATTN_PIPELINED)
             hetis.attn_combine(s, b.seq_lens, L, o, w_)
 
+        def fapp2(i):   # fused append + combine, NOT pipelined, but with the two alternating workspaces
+            li = i % nl
+            w_ = ws2[i % 2]
+            hetis.attn_partial_append(s, b.q, b.k_new, b.v_new, kp[li], vp[li], b.block_table, b.seq_lens, L, w_,
+                                      flags=a.flags)
+            hetis.attn_combine(s, b.seq_lens, L, o, w_)
+
         row = {"config": cfg.name, "n": n, "heads": x, "kv_bytes": kv, "layers": nl,
                "floor_us_at_6550": kv / 6550e3}
-        for name, fn in (("full", full), ("no_app", no_app), ("attn", attn), ("comb", comb), ("fapp", fapp), ("pipe", pipe)):
+        for name, fn in (("full", full), ("no_app", no_app), ("attn", attn), ("comb", comb), ("fapp", fapp), ("pipe", pipe), ("fapp2", fapp2)):
             row[name + "_us"] = graph_us(fn, a.steps)
         print(json.dumps(row), flush=True)
         del kp, vp, b
