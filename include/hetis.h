@@ -104,7 +104,8 @@ typedef struct {
     int32_t o_dtype;  /* hetis_dtype of o: HETIS_F32 or HETIS_BF16    */
 } hetis_shape;
 
-/* Flags for hetis_attn_partial / hetis_attn_decode. */
+/* Flags for hetis_attn_partial(_append) / hetis_attn_decode(_append).  None of
+ * them changes a result bit: an item's arithmetic depends on L_j only. */
 #define HETIS_ATTN_FORCE_SIMT 0x1u /* bf16 GQA on CUDA cores instead of tensor cores */
 /* bf16 GQA tensor-core kernel with the shared page ring and per-item CTA merge
  * (the default gives every consumer warp whole items and its own sub-ring). */
@@ -112,16 +113,20 @@ typedef struct {
 /* bf16 GQA tensor-core kernel: claim work items device-wide instead of dealing
  * them to SMs round-robin.  For decode that shares the SMs with another kernel
  * (e.g. hetis_kv_migrate on a low-priority stream, the Hauler): slowed SMs take
- * fewer items (c3 beside a 16-CTA migration: 1.16x instead of 1.4x step time). */
+ * fewer items (c3 beside a 16-CTA migration: 1.17x instead of 1.42x step time).
+ * Ignored with HETIS_ATTN_PIPELINED. */
 #define HETIS_ATTN_DEVICE_CLAIM 0x4u
 /* bf16 MHA (r = 1) on the per-warp tensor-core kernel (one valid MMA row)
- * instead of the CUDA-core kernel. */
+ * instead of the CUDA-core kernel (faster for large per-device problems, c5
+ * -4%; slower at small ones, the c2 8-GPU share +5%). */
 #define HETIS_ATTN_MHA_TC 0x8u
 /* Pipelined steps: the caller passes two workspaces alternately to consecutive
  * steps on the stream (at most one kv_append -- fused or not -- per step).
  * The attention kernel then streams cache pages while the previous step's
  * combine and attention tail still run: it waits for them only before a page
- * holding one of the last two positions of a request, and before it ends. */
+ * holding one of the last two positions of a request, and before it ends.
+ * Pays when a device has about one work item per warp (c3 8-GPU share -12%);
+ * costs a few % on large problems.  No work stealing in this mode. */
 #define HETIS_ATTN_PIPELINED 0x10u
 /* Diagnostic only: stream every K/V page through the shared-memory ring but
  * skip the math (partials are left unwritten).  Measures the memory-system
