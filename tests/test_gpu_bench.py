@@ -35,3 +35,21 @@ def test_bench_line_contract(extra):
     assert d["roofline"]["bound"] == "hbm" and d["roofline"]["achieved"] > 0
     if "--force-dist" in extra:
         assert d["config"]["gather"] in ("nccl", "peer")
+
+
+def test_c_abi_example_from_plain_c():
+    """examples/c_decode.c: the library driven from C (cudaMalloc'd buffers, plan, workspace query, the
+    fused step), checked against closed forms of Eq. 2b (L = 1 -> the V row; zero keys -> mean of V)."""
+    import shutil
+    import tempfile
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    exe = os.path.join(tempfile.mkdtemp(), "c_decode")
+    cmd = ["gcc", "-O2", "-std=c11", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(ROOT, "examples", "c_decode.c"), "-L", os.path.join(ROOT, "paper_2509_08309_b200"), "-lhetis",
+           "-L", "/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath," + os.path.join(ROOT, "paper_2509_08309_b200"),
+           "-lm", "-o", exe]
+    b = subprocess.run(cmd, capture_output=True, text=True)
+    assert b.returncode == 0, b.stderr
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "c example ok" in r.stdout, r.stdout + r.stderr
