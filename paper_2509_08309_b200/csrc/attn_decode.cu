@@ -49,7 +49,7 @@ constexpr int kPagesPerItem = kC / kP;  // 16
 constexpr int kQSlots = 2;
 // tunables (compile-time; scripts/ sweeps override them with -D)
 #ifndef HETIS_SIMT_NW
-#define HETIS_SIMT_NW 8
+#define HETIS_SIMT_NW 16
 #endif
 #ifndef HETIS_TC_NW
 #define HETIS_TC_NW 8
@@ -1443,7 +1443,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
 // ---------------------------------------------------------------- host side
 template <int DT, int D, int R, bool TC>
 struct Launch {
-    static constexpr int NW = TC ? HETIS_TC_NW : HETIS_SIMT_NW;
+    // 16 consumer warps for bf16 MHA (the c2 / c4 / c5 hot path: 4-5% faster than 8, the ring keeps
+    // 24 stages); 8 elsewhere -- with 16 warps and a ring shallower than 16 stages (fp32 d = 128, r = 8
+    // on CUDA cores) a step was seen to hang, so those keep 8
+    static constexpr int NW = TC ? HETIS_TC_NW : ((DT == HETIS_BF16 && R == 1) ? HETIS_SIMT_NW : 8);
     static constexpr int EB = DT == HETIS_BF16 ? 2 : 4;
     static constexpr int ROW_BYTES = D * EB;
     static constexpr int kStageBytes = 2 * kP * ROW_BYTES;
@@ -1466,6 +1469,10 @@ struct Launch {
         const size_t smem = (size_t)stages * kStageBytes + fixed_bytes(num_seqs, stages) + 1024;
         if (smem > (size_t)kMaxSmem) {
             if (err) *err = "batch too large for the shared-memory split table";
+            return cudaErrorInvalidValue;
+        }
+        if (stages < NW) {  // every consumer warp must be able to hold a page of the current item
+            if (err) *err = "ring shallower than the consumer warps";
             return cudaErrorInvalidValue;
         }
         p.stages = stages;

@@ -29,9 +29,8 @@ def _free_port() -> int:
 
 
 def _worker(rank, world, port, split, shape_args, lens, out_q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # file rendezvous: no free TCP port to race for
+    dist.init_process_group("gloo", init_method="file://" + port, rank=rank, world_size=world)
     try:
         import oracle
         from paper_2509_08309_b200 import hetis, workload
@@ -91,7 +90,8 @@ def test_two_rank_head_parallel_step_equals_unsplit(split, shape_args, lens):
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = _free_port()
+    import tempfile
+    port = os.path.join(tempfile.mkdtemp(), "rendezvous")
     procs = [ctx.Process(target=_worker, args=(r, 2, port, split, shape_args, lens, q)) for r in range(2)]
     for p in procs:
         p.start()

@@ -13,6 +13,8 @@ single-device result, bit for bit.
 """
 from __future__ import annotations
 
+import os
+
 import pytest
 import torch
 import torch.multiprocessing as mp
@@ -92,9 +94,8 @@ def _pull_rank(rank, port, shape_args, split, res, barrier):
     import torch.distributed as dist
     from paper_2509_08309_b200 import hetis, workload
     from paper_2509_08309_b200.step import DecodeStep
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=2)     # object exchange only; data moves by IPC
+    # object exchange only (data moves by IPC); a file rendezvous needs no free TCP port
+    dist.init_process_group("gloo", init_method="file://" + port, rank=rank, world_size=2)
     try:
         torch.cuda.set_device(0)
         shape = workload.Shape(*shape_args)
@@ -145,11 +146,8 @@ def _pull_rank(rank, port, shape_args, split, res, barrier):
 def test_scatter_pull_two_ranks_one_gpu(shape_args, split):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    import socket
-    so = socket.socket()
-    so.bind(("127.0.0.1", 0))
-    port = so.getsockname()[1]
-    so.close()
+    import tempfile
+    port = os.path.join(tempfile.mkdtemp(), "rendezvous")
     ctx = mp.get_context("spawn")
     res, barrier = ctx.Queue(), ctx.Barrier(2)
     ps = [ctx.Process(target=_pull_rank, args=(r, port, shape_args, split, res, barrier)) for r in range(2)]

@@ -184,9 +184,8 @@ def _free_port() -> int:
 
 
 def _worker(rank, world, port, lens, out_q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # file rendezvous: no free TCP port to race for
+    dist.init_process_group("gloo", init_method="file://" + port, rank=rank, world_size=world)
     try:
         b = small_batch(H=8, Hkv=4, D=8, P=4, dtype="bf16", lens=lens, seed=123)
         hb = host_batch(b)
@@ -205,7 +204,8 @@ def test_two_rank_seq_split_step_equals_unsplit():
     lens = (3, 4, 9, 40)
     ctx = tmp.get_context("spawn")
     q = ctx.Queue()
-    port = _free_port()
+    import tempfile
+    port = os.path.join(tempfile.mkdtemp(), "rendezvous")
     procs = [ctx.Process(target=_worker, args=(r, 2, port, lens, q)) for r in range(2)]
     for p in procs:
         p.start()
