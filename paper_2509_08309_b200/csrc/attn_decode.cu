@@ -81,7 +81,8 @@ constexpr int kQSlots = 2;
 #endif
 constexpr int kProducerLanes = HETIS_PRODUCER_LANES;
 static_assert(kPagesPerItem % kProducerLanes == 0, "producer lanes must divide the pages of an item");
-constexpr int kMaxSmem = 227 * 1024;
+// per-block limit (227 KiB) minus the kernels' static shared memory (build_split_offsets, merge scratch)
+constexpr int kMaxSmem = 227 * 1024 - 2048;
 static_assert(kPagesPerItem <= 32, "one producer lane per page of an item");
 
 struct Params {
