@@ -908,7 +908,7 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     int32_t nxt[kPagesPerItem];  // page ids of the NEXT item, in flight in registers
     auto load_next = [&](int item) {
         int j, g, t0, ntok;
-        if (item < n_items) {
+        if (item >= 0 && item < n_items) {
             decode(item, j, g, t0, ntok);
             const int np = (ntok + kP - 1) / kP;
             const int32_t *row = p.block_table + ((size_t)j * p.kv_heads + g) * p.max_pages + t0 / kP;
@@ -926,10 +926,16 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     // [0, n_static) (CTA c: c, c + grid, ...), then stealing from [n_static, n_items).
     // griddepcontrol.wait must be executed by converged warps only (a lane blocked in it stalls
     // the whole producer warp -- with the wait pending, lanes that never reach it deadlock the
-    // CTA).  Pipelined launches have not waited up front, so they never steal (no global counter).
+    // CTA).  Pipelined launches have not waited up front: a lane whose CTA-local queue is exhausted
+    // posts kNeedSteal and the warp, converged at the top of its issue loop, executes the wait and
+    // only then touches the device-wide counter (by then the predecessors have long completed).
+    // They steal only when every worker has two or more items on average; below that the static
+    // deal is one balanced wave and a wait in the middle of it would stall every worker of the CTA.
+    constexpr int kNeedSteal = -3;
     const bool pipelined_launch = (p.flags & HETIS_ATTN_PIPELINED) != 0;
     const bool device_claim = (p.flags & HETIS_ATTN_DEVICE_CLAIM) != 0 && !pipelined_launch;
-    const int static_pct = pipelined_launch ? 100 : HETIS_STATIC_PCT;
+    const bool pipe_steal = pipelined_launch && n_items >= 2 * (int)gridDim.x * NW;
+    const int static_pct = (pipelined_launch && !pipe_steal) ? 100 : HETIS_STATIC_PCT;
     const int per_cta = device_claim       ? 0
                         : static_pct == 100 ? (n_items + (int)gridDim.x - 1) / (int)gridDim.x
                                             : (int)(((long long)n_items * static_pct / 100) / gridDim.x);
@@ -939,6 +945,7 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             const int k = atomicAdd(sm.claim, 1);
             if (k < per_cta) return (int)blockIdx.x + k * (int)gridDim.x;
         }
+        if (pipelined_launch) return pipe_steal ? kNeedSteal : n_items;
         // the device-wide counter is reset by the previous launch's last CTA: never touch it
         // before that launch has completed (a no-op once this thread has waited)
         asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -974,7 +981,7 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         pdl_wait_once(waited);  // pools may hold rows the previous kernel wrote
         publish_split_offsets(p, s_off, w, NW);
     }
-    if (item == -2 && pipelined) item = n_items;  // pipelined launches never steal (no wait was done)
+    if (item == -2 && pipelined) item = n_items;  // a pipelined launch never steals its first item (no wait was done yet)
     if (item == -2) {  // the CTA-local queue was empty from the start: steal
         item = n_static + atomicAdd(p.counters, 1);
         if (item < n_items) {
@@ -989,6 +996,13 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         HETIS_TS(2);
     }
     while (__any_sync(mask, !finished)) {
+        if (__any_sync(mask, next == kNeedSteal)) {  // uniform branch: the producer lanes are converged
+            pdl_wait_once(waited);  // every predecessor has completed: the device-wide counter is ours
+            if (next == kNeedSteal) {
+                next = n_static + atomicAdd(p.counters, 1);
+                load_next(next);
+            }
+        }
         if (finished) continue;
         if (item >= n_items) {  // no more work for this worker: post the sentinel when the q slot is free
             if (dev::mbar_test(&sm.qempty[w], (it & 1) ^ 1)) {
@@ -1037,11 +1051,11 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
                 HETIS_TS(3);
             }
         }
-        if (next < 0 && kPagesPerItem * pg >= HETIS_CLAIM_AT * np) {
+        if (next == -1 && kPagesPerItem * pg >= HETIS_CLAIM_AT * np) {
             next = claim();
             load_next(next);
         }
-        if (q_done && pg == np) {  // item fully issued: move to the claimed next item
+        if (q_done && pg == np && next != kNeedSteal) {  // item fully issued: move to the claimed next item
             item = next;
             next = -1;
             ++it;
