@@ -19,8 +19,11 @@ import torch  # noqa: E402
 from paper_2509_08309_b200 import hetis, workload  # noqa: E402
 
 
-def run(shape, flags, n_steps, replays, seed=3):
-    lens0 = torch.tensor([1, 15, 16, 17, 255, 256, 257, 900, 2047, 3000] * 4, dtype=torch.int32)
+def run(shape, flags, n_steps, replays, seed=3, large=False):
+    if large:  # ~5000 GQA items (>= 2 per worker): pipelined launches steal too
+        lens0 = torch.tensor([200 + (i * 97) % 2800 for i in range(96)], dtype=torch.int32)
+    else:
+        lens0 = torch.tensor([1, 15, 16, 17, 255, 256, 257, 900, 2047, 3000] * 4, dtype=torch.int32)
     lens_max = lens0 + n_steps
     b = workload.make_decode_batch(shape, lens_max, seed, "cuda")
     s = hetis.make_shape(shape)
@@ -76,6 +79,7 @@ def main():
     a = ap.parse_args()
     cases = [("GQA r=8", workload.Shape(64, 8, 128, 16, "bf16"), 0),
              ("GQA r=8 pipelined", workload.Shape(64, 8, 128, 16, "bf16"), hetis.ATTN_PIPELINED),
+             ("GQA r=8 pipelined large", workload.Shape(64, 8, 128, 16, "bf16"), hetis.ATTN_PIPELINED | 0x10000),
              ("GQA r=8 device claim", workload.Shape(64, 8, 128, 16, "bf16"), hetis.ATTN_DEVICE_CLAIM),
              ("MHA CUDA cores", workload.Shape(40, 40, 128, 16, "bf16"), 0),
              ("MHA CUDA cores pipelined", workload.Shape(40, 40, 128, 16, "bf16"), hetis.ATTN_PIPELINED),
@@ -83,7 +87,7 @@ def main():
              ("fp32 d=64", workload.Shape(8, 8, 64, 16, "f32"), 0)]
     total = 0
     for name, shape, flags in cases:
-        bad = run(shape, flags, a.steps, a.replays)
+        bad = run(shape, flags & 0xFFFF, a.steps, a.replays, large=bool(flags & 0x10000))
         total += bad
         print(f"{name:28s}: {bad} of {a.replays} graph replays differ from the serial run", flush=True)
     print("STRESS", "OK" if total == 0 else f"FAILED ({total})")

@@ -496,14 +496,19 @@ def test_decode_step_fused_append_matches_separate_calls():
 
 
 # ------------------------------------------------------------------ pipelined steps (HETIS_ATTN_PIPELINED)
-@pytest.mark.parametrize("H,Hkv,D,dtype,extra", [(64, 8, 128, "bf16", 0), (40, 40, 128, "bf16", 0),
-                                                 (8, 8, 64, "f32", 0), (40, 40, 128, "bf16", hetis.ATTN_MHA_TC),
-                                                 (16, 4, 64, "bf16", 0)])
-def test_pipelined_steps_match_serial_steps(H, Hkv, D, dtype, extra):
+@pytest.mark.parametrize("H,Hkv,D,dtype,extra,large", [(64, 8, 128, "bf16", 0, False), (40, 40, 128, "bf16", 0, False),
+                                                       (8, 8, 64, "f32", 0, False),
+                                                       (40, 40, 128, "bf16", hetis.ATTN_MHA_TC, False),
+                                                       (16, 4, 64, "bf16", 0, False), (64, 8, 128, "bf16", 0, True)])
+def test_pipelined_steps_match_serial_steps(H, Hkv, D, dtype, extra, large):
     """Several decode steps (each appends one token) back to back on one stream, pipelined with two
     alternating workspaces, as a CUDA graph so consecutive kernels really overlap: every step's O and the
-    final pools are bit-identical to the same steps run with the default (fully ordered) launches."""
-    lens0 = torch.tensor([1, 15, 16, 17, 255, 256, 900, 2047], dtype=torch.int32)
+    final pools are bit-identical to the same steps run with the default (fully ordered) launches.
+    large: 96 ragged requests (~5000 GQA items, >= 2 per worker), so pipelined launches also steal."""
+    if large:
+        lens0 = torch.tensor([200 + (i * 97) % 2800 for i in range(96)], dtype=torch.int32)
+    else:
+        lens0 = torch.tensor([1, 15, 16, 17, 255, 256, 900, 2047], dtype=torch.int32)
     n_steps = 6
     lens_max = lens0 + n_steps
     outs = {}
