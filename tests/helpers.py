@@ -33,6 +33,20 @@ def host_batch(b: workload.DecodeBatch) -> dict:
     return out
 
 
+def host_batch_once(b: workload.DecodeBatch) -> dict:
+    """Like host_batch, but without the second host copy of the pools (full-size configs hold several GB):
+    a device tensor's .cpu() is already a fresh, writable host buffer."""
+    def bits(t):
+        a = workload.to_numpy_bits(t)
+        return a if t.is_cuda else a.copy()
+    out = {k: bits(getattr(b, k)) for k in ("q", "k_new", "v_new", "k_pool", "v_pool")}
+    out["block_table"] = b.block_table.cpu().numpy().astype(np.int32)
+    out["seq_lens"] = b.seq_lens.cpu().numpy().astype(np.int32)
+    oracle.kv_append(out["k_new"], out["v_new"], out["k_pool"], out["v_pool"], out["block_table"],
+                     out["seq_lens"])
+    return out
+
+
 def to_f64(x: np.ndarray) -> np.ndarray:
     """Exact widening of stored bits (uint16 bf16 / float32) to float64 -- test side."""
     if x.dtype == np.uint16:

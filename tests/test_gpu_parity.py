@@ -8,13 +8,16 @@ L = 1 returning the V row, bf16 O == RNE(fp32 O).
 """
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
 import pytest
 import torch
 
 import oracle
 from paper_2509_08309_b200 import hetis, workload
-from tests.helpers import dtype_code, err_stats, host_batch, oracle_full, to_f64
+from tests.helpers import dtype_code, err_stats, host_batch, host_batch_once, oracle_full, to_f64
 
 pytestmark = pytest.mark.gpu
 
@@ -50,6 +53,30 @@ def run_gpu(b: workload.DecodeBatch, o_dtype="f32", flags=0, append=True, o_stri
         o = big
     torch.cuda.synchronize()
     return o
+
+
+def run_gpu_fused(b: workload.DecodeBatch, flags=0):
+    """The bench's per-device step: hetis_attn_decode_append (append fused into the attention kernel) + combine."""
+    s = hetis.make_shape(b.shape)
+    B, x, D = b.q.shape
+    L = b.max_seq_len
+    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), b.q.device)
+    o = torch.full((B, x, D), float("nan"), dtype=torch.float32, device=b.q.device)
+    hetis.attn_decode_append(s, b.q, b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, o, ws,
+                             flags=flags)
+    torch.cuda.synchronize()
+    del ws
+    return o
+
+
+def log_parity(tag: str, b: workload.DecodeBatch, st: dict):
+    rec = {"case": tag, "q_heads": b.q_count, "q_begin": b.q_begin, "batch": int(b.q.shape[0]),
+           "max_seq_len": b.max_seq_len, "elements": int(b.q.numel()), **st}
+    print("parity", json.dumps(rec))
+    path = os.environ.get("HETIS_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(rec) + "\n")
 
 
 def assert_close(got, ref, what=""):
@@ -189,11 +216,10 @@ def test_tensor_core_vs_cuda_core_gqa(lens):
     o_tc = run_gpu(b)
     o_ring = run_gpu(b, flags=hetis.ATTN_TC_SHARED_RING, append=False)
     o_simt = run_gpu(b, flags=hetis.ATTN_FORCE_SIMT, append=False)
-    if len(lens) <= 3:
-        ref = oracle_full(b)
-        assert_close(o_tc, ref, "tc")
-        assert_close(o_ring, ref, "tc shared ring")
-        assert_close(o_simt, ref, "simt")
+    ref = oracle_full(b)                          # every batch, incl. 300 x 2048 and (700, 1, 4095) x 40
+    log_parity(f"gqa-batch-{len(lens)}/tc", b, assert_close(o_tc, ref, "tc"))
+    assert_close(o_ring, ref, "tc shared ring")
+    assert_close(o_simt, ref, "simt")
     assert torch.isfinite(o_tc).all() and torch.isfinite(o_ring).all()
     assert (o_tc - o_ring).abs().max().item() < 1e-5
     assert (o_tc - o_simt).abs().max().item() < 1e-4
@@ -243,57 +269,29 @@ def test_kv_append_memcmp_against_oracle_placement(dtype, D, Hkv):
     assert changed.sum() == 6 * Hkv
 
 
-# ------------------------------------------------------------------ full-size configs, sampled outputs
-def _compact_for_pairs(b: workload.DecodeBatch, pairs):
-    """Host copy of only the pages the sampled (seq, head) pairs read, with a remapped table."""
-    r = b.shape.r
-    jg = sorted({(j, h // r) for j, h in pairs})
-    bt = b.block_table.cpu()
-    lens = b.seq_lens.cpu()
-    P = b.shape.page_size
-    pages, new_bt = [], {}
-    for (j, g) in jg:
-        n = (int(lens[j]) + P - 1) // P
-        ids = bt[j, g, :n]
-        new_bt[(j, g)] = list(range(len(pages), len(pages) + n))
-        pages.extend(ids.tolist())
-    idx = torch.tensor(pages, dtype=torch.long, device=b.k_pool.device)
-    kp = workload.to_numpy_bits(b.k_pool.index_select(0, idx))
-    vp = workload.to_numpy_bits(b.v_pool.index_select(0, idx))
-    B, G = bt.shape[0], bt.shape[1]
-    table = np.full((B, G, bt.shape[2]), -1, np.int32)
-    for (j, g), ids in new_bt.items():
-        table[j, g, :len(ids)] = ids
-    return kp, vp, table
+# ------------------------------------------------------------------ full-size configs, whole O against the oracle
+FULL_SIZE_CASES = [("c2", 1, 0), ("c3", 1, 0), ("c3", 8, 5), ("c4", 5, 0), ("c4", 5, 1), ("c4", 5, 2), ("c4", 5, 3),
+                   ("c4", 5, 4), ("c5", 8, 3)]
 
 
-@pytest.mark.parametrize("name,rank", [("c2", 0), ("c3", 0), ("c4", 0), ("c4", 4), ("c5", 3)])
-def test_full_size_config_sampled(name, rank):
+@pytest.mark.parametrize("name,n_dev,rank", FULL_SIZE_CASES)
+def test_full_size_config_whole_output(name, n_dev, rank):
+    """T10: one rank's share of a config at FULL size (c2 and c3 whole; every share of c4's
+    16/8/8/4/4 split; an 8-GPU share of c3 and c5), run with the bench's launch (kv_append fused into the
+    attention kernel, then the combine), compared with the fp64 oracle on EVERY element of O.  The max-abs
+    location (request, local head, dim) is logged (HETIS_PARITY_LOG) and printed."""
     cfg = workload.CONFIGS[name]
-    n_dev = len(cfg.split) if cfg.split else 1
     split = cfg.head_split(n_dev)
     begin = sum(split[:rank])
     b = workload.make_decode_batch(cfg.shape, cfg.seq_lens(), cfg.seed, "cuda", q_begin=begin,
                                    q_count=split[rank], rank_salt=rank)
-    B, x = b.q.shape[0], b.q.shape[1]
-    g = torch.Generator().manual_seed(5)
-    pairs = sorted({(int(torch.randint(B, (1,), generator=g)), int(torch.randint(x, (1,), generator=g)))
-                    for _ in range(24)} | {(0, 0), (B - 1, x - 1)})
-    # oracle inputs: the pages the pairs read, copied BEFORE the GPU append; the new
-    # token is placed on the host by the oracle's own kv_append
-    kp, vp, table = _compact_for_pairs(b, pairs)
-    kn, vn, sl = workload.to_numpy_bits(b.k_new), workload.to_numpy_bits(b.v_new), b.seq_lens.cpu().numpy()
-    for (j, gg) in sorted({(j, h // b.shape.r) for j, h in pairs}):
-        # one (request, kv head) at a time: only the sampled pairs' pages are in the compact pool
-        oracle.kv_append(kn[j:j + 1, gg:gg + 1], vn[j:j + 1, gg:gg + 1], kp, vp, table[j:j + 1, gg:gg + 1],
-                         sl[j:j + 1])
-    q = workload.to_numpy_bits(b.q)
-    ref = oracle.decode_pairs(q, kp, vp, table, b.seq_lens.cpu().numpy(), pairs, num_kv_heads=b.kv_count,
-                              dtype=dtype_code(b.shape))
-    o = run_gpu(b)                                # appends the new token, then attends
-    assert torch.isfinite(o).all()
-    got = np.stack([o[j, h].cpu().numpy() for j, h in pairs])
-    assert_close(got, ref, name)
+    hb = host_batch_once(b)                       # host copies taken BEFORE the GPU append; oracle places the row
+    o = run_gpu_fused(b)
+    ref = oracle.decode(hb["q"], hb["k_pool"], hb["v_pool"], hb["block_table"], hb["seq_lens"],
+                        num_kv_heads=b.kv_count, dtype=dtype_code(b.shape))
+    del hb
+    st = assert_close(o, ref, f"{name} N={n_dev} rank {rank}")
+    log_parity(f"{name}/N{n_dev}/rank{rank}", b, st)
 
 
 # ------------------------------------------------------------------ per-request (dispatcher) plans via work units

@@ -403,3 +403,45 @@ def test_kv_migrate_then_decode_equals_decode_in_place():
                         dtype=oracle.BF16)
     got = oracle.decode(hb["q"][::-1].copy(), dk, dv, dst_bt, lens[::-1].copy(), num_kv_heads=G, dtype=oracle.BF16)
     assert np.array_equal(got[::-1], ref)
+
+
+# ------------------------------------------------------------------ oracle_decode_pairs_f64 (sampled outputs)
+@pytest.mark.parametrize("H,Hkv,D,dtype", [(8, 4, 8, "bf16"), (4, 4, 4, "f32"), (8, 1, 8, "f32")])
+def test_pairs_brute_force_tiny(H, Hkv, D, dtype):
+    """decode_pairs on shuffled (seq, head) pairs, with repeats, against the mpmath brute force (independent
+    gather, no max subtraction) -- the same pin as the full output, applied to the pairs entry point."""
+    b = small_batch(H=H, Hkv=Hkv, D=D, P=4, dtype=dtype, lens=(1, 7, 40), seed=29 + H + D)
+    hb = host_batch(b)
+    ref = _brute_force(hb, b.shape)
+    rng = np.random.default_rng(3)
+    pairs = [(int(rng.integers(3)), int(rng.integers(H))) for _ in range(20)] + [(2, H - 1), (0, 0), (2, H - 1)]
+    got = oracle.decode_pairs(hb["q"], hb["k_pool"], hb["v_pool"], hb["block_table"], hb["seq_lens"], pairs,
+                              num_kv_heads=Hkv, dtype=dtype_code(b.shape))
+    for i, (j, h) in enumerate(pairs):
+        assert np.max(np.abs(got[i] - ref[j, h])) <= 1e-12, (j, h)
+
+
+@pytest.mark.parametrize("H,Hkv,D,dtype", [(16, 2, 64, "bf16"), (8, 8, 32, "f32"), (12, 4, 16, "bf16")])
+def test_pairs_equal_full_output_rows(H, Hkv, D, dtype):
+    """Every sampled pair equals the pinned full output's row bit for bit (same per-output arithmetic), for
+    GQA and MHA, bf16 and fp32, ragged lengths over several pages and random page ids."""
+    b = small_batch(H=H, Hkv=Hkv, D=D, P=16, dtype=dtype, lens=(1, 16, 17, 300, 65, 2), seed=31 + H)
+    hb = host_batch(b)
+    full = _oracle(hb, b.shape)
+    rng = np.random.default_rng(H * D)
+    pairs = sorted({(int(rng.integers(6)), int(rng.integers(H))) for _ in range(40)} | {(0, 0), (5, H - 1)})
+    got = oracle.decode_pairs(hb["q"], hb["k_pool"], hb["v_pool"], hb["block_table"], hb["seq_lens"], pairs,
+                              num_kv_heads=Hkv, dtype=dtype_code(b.shape), nthreads=3)
+    for i, (j, h) in enumerate(pairs):
+        assert np.array_equal(got[i], full[j, h]), (j, h)
+    # a head's row depends on its own kv group only: a wrong h -> g mapping in the pairs path would differ
+    assert not np.array_equal(full[1, 0], full[1, H - 1])
+
+
+def test_pairs_rejects_out_of_range_pairs():
+    b = small_batch(H=4, Hkv=2, D=8, P=4, dtype="f32", lens=(3, 5), seed=2)
+    hb = host_batch(b)
+    for bad in ([(2, 0)], [(0, 4)], [(-1, 0)]):
+        with pytest.raises(oracle.OracleError):
+            oracle.decode_pairs(hb["q"], hb["k_pool"], hb["v_pool"], hb["block_table"], hb["seq_lens"], bad,
+                                num_kv_heads=2, dtype=oracle.F32)
