@@ -65,7 +65,7 @@
 extern "C" {
 #endif
 
-#define HETIS_ABI_VERSION 1
+#define HETIS_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define HETIS_API __attribute__((visibility("default")))
@@ -280,56 +280,69 @@ HETIS_API hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_s
                                const int32_t *seq_lens, int32_t max_seq_len, void *o, void *workspace,
                                size_t workspace_bytes, uint32_t flags, hetis_stream_t stream);
 
-/* ---- combine fused with the O all-gather over peer memory -------------- */
-/* Kernel 2 (a5) and the gather (a6, Eq. 2a Concat) in ONE kernel:
- * every merged row o[j][h] is stored straight into every rank's o_full at its
- * GLOBAL head index q_head_begin + h (NVLink 5 / NVSwitch peer stores), then the
- * last block publishes `epoch` into signal_peers[p][rank] of every rank p with a
- * system-scope release store.  Same arithmetic as hetis_attn_combine.
- *   o_full_peers : host array [num_ranks] of device pointers, rank p's o_full
- *                  [num_seqs][H][head_dim] (o_dtype) as mapped in THIS process
- *                  (own buffer at [rank]; peers via cudaIpcOpenMemHandle or any
- *                  other peer mapping); rows o_seq_stride elements apart
- *   signal_peers : host array [num_ranks] of device pointers to each rank's
- *                  int64 signal array [num_ranks] (zero-initialised once)
- *   epoch        : > every epoch previously published into these signals
- *   workspace    : the hetis_attn_partial workspace of this step
- * num_ranks <= 8.  The consumer of o_full must hetis_peer_wait first. */
-HETIS_API hetis_status hetis_attn_combine_peers(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
-                                                int32_t q_head_count, const int32_t *seq_lens, int32_t max_seq_len,
-                                                void *const *o_full_peers, int64_t o_seq_stride,
-                                                int64_t *const *signal_peers, int32_t num_ranks, int32_t rank,
-                                                int64_t epoch, void *workspace, size_t workspace_bytes,
-                                                hetis_stream_t stream);
-/* Stream-ordered wait (acquire) until signal_local[p] >= epoch for every rank p:
- * after it, o_full holds every rank's rows of that epoch.  A rank that never
- * signals makes the wait kernel trap after ~10 s (HETIS_E_CUDA on the stream)
- * instead of hanging the device.  signal_local: device int64 [num_ranks]. */
-HETIS_API hetis_status hetis_peer_wait(const int64_t *signal_local, int32_t num_ranks, int64_t epoch,
-                                       hetis_stream_t stream);
-
-/* ---- scatter over peer memory (NVLink 5 / NVSwitch) --------------------- */
-/* The Primary's half of a pull-based scatter (a2): once q_full, k_new_full and
- * v_new_full of step `epoch` are written (everything before this call on the
- * stream), publish `epoch` into slot [rank] of every rank's signal array
- * (system-scope release).  signal_peers: host array [num_ranks] of device
- * pointers to each rank's int64 [num_ranks] array, mapped in this process
- * (zero-initialised once; epochs strictly increase).  num_ranks <= 8. */
-HETIS_API hetis_status hetis_peer_signal(int64_t *const *signal_peers, int32_t num_ranks, int32_t rank,
-                                         int64_t epoch, hetis_stream_t stream);
-/* The workers' half: wait (stream-ordered, acquire; traps after ~10 s if the
- * root never signals) until signal_local[root] >= epoch, then copy this
- * rank's plan range straight from the root's buffers (mapped over NVLink):
+/* ---- the step's exchanges over peer memory (NVLink 5 / NVSwitch) -------- */
+/* The scatter (a2) and the gather (a6, Eq. 2a Concat) without
+ * NCCL: every rank pulls its shard of the step's inputs straight from the
+ * Primary's buffers, and the combine kernel stores every merged O row straight
+ * into every receiving rank's o_full.  One step on every rank is
+ *     hetis_scatter_pull -> hetis_attn_partial(_append) -> hetis_attn_combine_peers
+ *     -> hetis_peer_wait
+ * (the Primary writes q_full, k_new_full, v_new_full before its scatter_pull).
+ * Synchronisation lives in device memory: each rank owns a STATE of
+ * hetis_peer_state_bytes() (zero-filled once by the caller, 64-byte aligned)
+ * holding its step counter and the epochs its peers publish (system-scope
+ * release stores, acquire loads).  No call takes a per-step host argument, so
+ * a step -- or many -- can be captured once in a CUDA graph and replayed.
+ * Every rank must run the same sequence of steps.  Reuse rules enforced on the
+ * device: a rank's O rows go into a peer's o_full only after that peer's
+ * scatter_pull of the same step acknowledged (everything it enqueued before,
+ * i.e. the consumer of the previous step's o_full, has completed); the
+ * Primary's scatter_pull of step e + 1 follows its peer_wait of step e, so the
+ * Primary may overwrite its input buffers after hetis_peer_wait returns on its
+ * stream (every rank has pulled by then).  Bounded waits: a peer that never
+ * publishes makes the waiting kernel trap after ~10 s (HETIS_E_CUDA on the
+ * stream) instead of hanging the device. */
+HETIS_API size_t hetis_peer_state_bytes(void);
+typedef struct hetis_peer_group hetis_peer_group; /* opaque, immutable after create */
+/* plan         : global plan (per_request == 0) of num_devices <= 8 ranks
+ * rank, root   : this rank; the Primary holding the step's inputs
+ * gather_root  : -1 = every rank receives O (all-gather, north star); >= 0 =
+ *                only that rank does (gather to the Primary)
+ * state_peers  : host array [N] of device pointers, rank p's state as mapped
+ *                in THIS process ([rank] = own; peers via cudaIpcOpenMemHandle
+ *                or any other peer mapping)
+ * o_full_peers : host array [N], rank p's o_full [num_seqs][H][head_dim]
+ *                (o_dtype) mapped here; rows o_seq_stride elements apart,
+ *                16-byte aligned.  Entries of non-receiving ranks may be NULL.
+ * q_full_root, k_new_full_root, v_new_full_root : the Primary's [num_seqs][H][d]
+ *                and [num_seqs][H_kv][d] input buffers mapped here
+ * The group copies the pointers; the caller keeps the memory alive. */
+HETIS_API hetis_status hetis_peer_group_create(const hetis_plan *plan, int32_t rank, int32_t root,
+                                               int32_t gather_root, int64_t *const *state_peers,
+                                               void *const *o_full_peers, int64_t o_seq_stride,
+                                               const void *q_full_root, const void *k_new_full_root,
+                                               const void *v_new_full_root, hetis_peer_group **out);
+HETIS_API void hetis_peer_group_destroy(hetis_peer_group *group);
+/* a2: on the Primary, first publish this step's epoch (its inputs are written);
+ * on every rank, acknowledge the previous step's o_full, wait (acquire) for
+ * the Primary's epoch, then copy this rank's plan range straight from the
+ * Primary's buffers:
  *   q_full_root [num_seqs][H][d] heads [b, b + x)       -> q_shard [num_seqs][x][d]
  *   k/v_new_full_root [num_seqs][H_kv][d] [b/r, (b+x)/r) -> k/v_new_shard [num_seqs][x/r][d]
- * One kernel, no NCCL: the same result as hetis_scatter_q.  The root may
- * overwrite its buffers only after every rank has consumed them (e.g. after
- * the step's O exchange, hetis_peer_wait). */
-HETIS_API hetis_status hetis_scatter_pull(const hetis_plan *plan, int32_t rank, int32_t num_seqs,
-                                          const int64_t *signal_local, int32_t root, int64_t epoch,
-                                          const void *q_full_root, const void *k_new_full_root,
-                                          const void *v_new_full_root, void *q_shard, void *k_new_shard,
-                                          void *v_new_shard, hetis_stream_t stream);
+ * One kernel; the same bytes as hetis_scatter_q. */
+HETIS_API hetis_status hetis_scatter_pull(const hetis_peer_group *group, int32_t num_seqs, void *q_shard,
+                                          void *k_new_shard, void *v_new_shard, hetis_stream_t stream);
+/* a5 + a6 in ONE kernel: the split combine of this rank's heads (same
+ * arithmetic as hetis_attn_combine) storing every row o[j][h] at its GLOBAL
+ * head index into every receiving rank's o_full, then publishing the epoch to
+ * them.  workspace: this step's hetis_attn_partial workspace. */
+HETIS_API hetis_status hetis_attn_combine_peers(const hetis_peer_group *group, int32_t num_seqs,
+                                                const int32_t *seq_lens, int32_t max_seq_len, void *workspace,
+                                                size_t workspace_bytes, hetis_stream_t stream);
+/* The step's last kernel: a receiving rank waits until every rank's rows of
+ * this step are in its o_full; every rank then records the step as completed.
+ * Work enqueued after it on the stream may read o_full. */
+HETIS_API hetis_status hetis_peer_wait(const hetis_peer_group *group, hetis_stream_t stream);
 
 /* ---- scatter / gather over NCCL ------------------- */
 /* nccl_comm is an ncclComm_t (e.g. torch ProcessGroupNCCL._comm_ptr()) whose

@@ -8,7 +8,9 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <initializer_list>
 #include <mutex>
+#include <new>
 #include <string>
 #include <vector>
 
@@ -30,6 +32,12 @@ struct hetis_plan {
     int32_t per_request;
     std::vector<int32_t> x;      // [N] or [B][N]
     std::vector<int32_t> begin;  // same layout: first global head on each device
+};
+
+struct hetis_peer_group {
+    hetis_shape shape;
+    int32_t q_count;             // this rank's query heads
+    hetis::PeerGroupDev dev;     // kernel argument (pointers mapped in this process)
 };
 
 namespace {
@@ -506,56 +514,107 @@ hetis_status hetis_attn_combine_lse(const hetis_shape *shape, int32_t num_seqs, 
                           workspace_bytes, stream);
 }
 
-hetis_status hetis_attn_combine_peers(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
-                                      int32_t q_head_count, const int32_t *seq_lens, int32_t max_seq_len,
-                                      void *const *o_full_peers, int64_t o_seq_stride, int64_t *const *signal_peers,
-                                      int32_t num_ranks, int32_t rank, int64_t epoch, void *workspace,
-                                      size_t workspace_bytes, hetis_stream_t stream) {
-    hetis_status st = check_shape(shape);
-    if (st != HETIS_OK) return st;
-    const int H = shape->num_q_heads, r = H / shape->num_kv_heads;
-    if (num_seqs < 0 || q_head_count < 1 || max_seq_len < 1) return fail(HETIS_E_INVALID, "bad sizes");
-    if (q_head_begin < 0 || q_head_begin + q_head_count > H) return fail(HETIS_E_INVALID, "head range outside [0, H)");
-    if (q_head_begin % r || q_head_count % r) return fail(HETIS_E_GROUP_ALIGN, "head range must cover whole kv groups");
-    if (num_ranks < 1 || num_ranks > hetis::kMaxPeers || rank < 0 || rank >= num_ranks)
-        return fail(HETIS_E_INVALID, "num_ranks must be 1..8 and rank inside it");
-    if (epoch < 1) return fail(HETIS_E_INVALID, "epoch must be >= 1");
-    if (!o_full_peers || !signal_peers || !workspace || (num_seqs > 0 && !seq_lens))
+// ---------------------------------------------------------------- exchanges over peer memory
+size_t hetis_peer_state_bytes(void) { return (size_t)hetis::kStSlots * sizeof(int64_t); }
+
+hetis_status hetis_peer_group_create(const hetis_plan *plan, int32_t rank, int32_t root, int32_t gather_root,
+                                     int64_t *const *state_peers, void *const *o_full_peers, int64_t o_seq_stride,
+                                     const void *q_full_root, const void *k_new_full_root,
+                                     const void *v_new_full_root, hetis_peer_group **out) {
+    if (!out) return fail(HETIS_E_INVALID, "out is NULL");
+    *out = nullptr;
+    if (!plan) return fail(HETIS_E_INVALID, "plan is NULL");
+    if (plan->per_request) return fail(HETIS_E_UNSUPPORTED, "peer exchanges need a global (per_request = 0) plan");
+    const int n = plan->num_devices;
+    if (n > hetis::kMaxPeers) return fail(HETIS_E_UNSUPPORTED, "at most 8 ranks");
+    if (rank < 0 || rank >= n || root < 0 || root >= n || gather_root < -1 || gather_root >= n)
+        return fail(HETIS_E_INVALID, "rank / root / gather_root outside the plan");
+    const hetis_shape &s = plan->shape;
+    if (o_seq_stride < (int64_t)s.num_q_heads * s.head_dim) return fail(HETIS_E_INVALID, "o_seq_stride below H * head_dim");
+    if ((o_seq_stride * esize(s.o_dtype)) % 16) return fail(HETIS_E_INVALID, "o rows must be 16-byte aligned");
+    if (!state_peers || !o_full_peers || !q_full_root || !k_new_full_root || !v_new_full_root)
         return fail(HETIS_E_INVALID, "NULL argument");
-    if (o_seq_stride < (int64_t)H * shape->head_dim) return fail(HETIS_E_INVALID, "o_seq_stride below H * head_dim");
-    const int oe = esize(shape->o_dtype);
-    hetis::PeerTargets t{};
-    for (int p = 0; p < num_ranks; ++p) {
-        if (!o_full_peers[p] || !signal_peers[p]) return fail(HETIS_E_INVALID, "NULL peer pointer");
-        if (!aligned(o_full_peers[p], 8) || (o_seq_stride * oe) % 8 || !aligned(signal_peers[p], 8))
-            return fail(HETIS_E_INVALID, "peer buffers must be 8-byte aligned");
-        t.o[p] = o_full_peers[p];
-        t.sig[p] = signal_peers[p];
+    for (const void *ptr : {q_full_root, k_new_full_root, v_new_full_root})
+        if (!aligned(ptr, 16)) return fail(HETIS_E_INVALID, "root buffers must be 16-byte aligned");
+    auto *g = new (std::nothrow) hetis_peer_group{};
+    if (!g) return fail(HETIS_E_INVALID, "out of host memory");
+    hetis::PeerGroupDev &d = g->dev;
+    for (int p = 0; p < n; ++p) {
+        if (!state_peers[p] || !aligned(state_peers[p], 64)) {
+            delete g;
+            return fail(HETIS_E_INVALID, "every state must be non-NULL and 64-byte aligned");
+        }
+        const bool target = gather_root < 0 || p == gather_root;
+        if (target && (!o_full_peers[p] || !aligned(o_full_peers[p], 16))) {
+            delete g;
+            return fail(HETIS_E_INVALID, "every receiving rank's o_full must be non-NULL and 16-byte aligned");
+        }
+        d.state[p] = state_peers[p];
+        d.o[p] = o_full_peers[p];
     }
+    d.q_root = static_cast<const uint8_t *>(q_full_root);
+    d.k_root = static_cast<const uint8_t *>(k_new_full_root);
+    d.v_root = static_cast<const uint8_t *>(v_new_full_root);
+    d.n = n;
+    d.rank = rank;
+    d.root = root;
+    d.gather_root = gather_root;
+    d.head0 = plan->begin[rank];
+    d.o_seq_stride = o_seq_stride;
+    g->shape = s;
+    g->q_count = plan->x[rank];
+    *out = g;
+    return HETIS_OK;
+}
+
+void hetis_peer_group_destroy(hetis_peer_group *g) { delete g; }
+
+hetis_status hetis_attn_combine_peers(const hetis_peer_group *g, int32_t num_seqs, const int32_t *seq_lens,
+                                      int32_t max_seq_len, void *workspace, size_t workspace_bytes,
+                                      hetis_stream_t stream) {
+    if (!g) return fail(HETIS_E_INVALID, "group is NULL");
+    const hetis_shape &s = g->shape;
+    const int r = s.num_q_heads / s.num_kv_heads;
+    if (num_seqs < 0 || max_seq_len < 1) return fail(HETIS_E_INVALID, "bad sizes");
+    if (!workspace || (num_seqs > 0 && !seq_lens)) return fail(HETIS_E_INVALID, "NULL argument");
     if (!aligned(workspace, 256)) return fail(HETIS_E_WORKSPACE, "workspace must be 256-byte aligned");
-    hetis::WorkspaceLayout w = hetis::workspace_layout(num_seqs, q_head_count / r, r, shape->head_dim, max_seq_len);
+    const int qc = std::max(g->q_count, r);  // a rank without heads still takes part in the epoch protocol
+    hetis::WorkspaceLayout w = hetis::workspace_layout(num_seqs, qc / r, r, s.head_dim, max_seq_len);
     if (workspace_bytes < w.total) return fail(HETIS_E_WORKSPACE, "workspace too small");
-    if (num_seqs == 0) return HETIS_OK;
     uint8_t *ws = static_cast<uint8_t *>(workspace);
-    t.n = num_ranks;
-    t.rank = rank;
-    t.head0 = q_head_begin;
-    t.epoch = epoch;
-    t.o_seq_stride = o_seq_stride;
-    t.done = reinterpret_cast<int32_t *>(ws + w.counter_offset) + 2;
     cudaError_t e = hetis::launch_combine_peers(
-        num_seqs, q_head_count, r, shape->head_dim, reinterpret_cast<const int32_t *>(ws + w.split_off_offset),
-        reinterpret_cast<const float *>(ws + w.lse_offset), reinterpret_cast<const float *>(ws + w.o_offset),
-        shape->o_dtype, t, reinterpret_cast<cudaStream_t>(stream), max_seq_len);
+        g->q_count == 0 ? 0 : num_seqs, g->q_count, r, s.head_dim,
+        reinterpret_cast<const int32_t *>(ws + w.split_off_offset), reinterpret_cast<const float *>(ws + w.lse_offset),
+        reinterpret_cast<const float *>(ws + w.o_offset), s.o_dtype, g->dev, reinterpret_cast<cudaStream_t>(stream),
+        max_seq_len);
     if (e != cudaSuccess) return cuda_fail(e, "combine_peers launch");
     return HETIS_OK;
 }
 
-hetis_status hetis_peer_wait(const int64_t *signal_local, int32_t num_ranks, int64_t epoch, hetis_stream_t stream) {
-    if (!signal_local || num_ranks < 1 || num_ranks > 32 || epoch < 1) return fail(HETIS_E_INVALID, "bad arguments");
-    if (!aligned(signal_local, 8)) return fail(HETIS_E_INVALID, "signal array must be 8-byte aligned");
-    cudaError_t e = hetis::launch_peer_wait(signal_local, num_ranks, epoch, reinterpret_cast<cudaStream_t>(stream));
+hetis_status hetis_peer_wait(const hetis_peer_group *g, hetis_stream_t stream) {
+    if (!g) return fail(HETIS_E_INVALID, "group is NULL");
+    cudaError_t e = hetis::launch_peer_wait(g->dev, reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "peer_wait launch");
+    return HETIS_OK;
+}
+
+hetis_status hetis_scatter_pull(const hetis_peer_group *g, int32_t num_seqs, void *q_shard, void *k_new_shard,
+                                void *v_new_shard, hetis_stream_t stream) {
+    if (!g) return fail(HETIS_E_INVALID, "group is NULL");
+    if (num_seqs < 0) return fail(HETIS_E_INVALID, "bad num_seqs");
+    const hetis_shape &s = g->shape;
+    const int r = s.num_q_heads / s.num_kv_heads;
+    const int x = g->q_count, b = g->dev.head0;
+    if (x > 0 && num_seqs > 0) {
+        if (!q_shard || !k_new_shard || !v_new_shard) return fail(HETIS_E_INVALID, "NULL shard");
+        for (const void *ptr : {(const void *)q_shard, (const void *)k_new_shard, (const void *)v_new_shard})
+            if (!aligned(ptr, 16)) return fail(HETIS_E_INVALID, "shards must be 16-byte aligned");
+    }
+    cudaError_t e = hetis::launch_scatter_pull(g->dev, x > 0 ? num_seqs : 0, s.num_q_heads, s.num_kv_heads, b, x,
+                                               b / r, x / r, s.head_dim * esize(s.q_dtype),
+                                               s.head_dim * esize(s.kv_dtype), q_shard, k_new_shard, v_new_shard,
+                                               reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "scatter_pull launch");
     return HETIS_OK;
 }
 
@@ -586,52 +645,6 @@ hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_seqs, int32
     if (st != HETIS_OK) return st;
     return hetis_attn_combine(shape, num_seqs, q_head_count, seq_lens, max_seq_len, o,
                               (int64_t)q_head_count * shape->head_dim, workspace, workspace_bytes, stream);
-}
-
-// ---------------------------------------------------------------- scatter over peer memory
-hetis_status hetis_peer_signal(int64_t *const *signal_peers, int32_t num_ranks, int32_t rank, int64_t epoch,
-                               hetis_stream_t stream) {
-    if (!signal_peers || num_ranks < 1 || num_ranks > hetis::kMaxPeers || rank < 0 || rank >= num_ranks)
-        return fail(HETIS_E_INVALID, "num_ranks must be 1..8 and rank inside it");
-    if (epoch < 1) return fail(HETIS_E_INVALID, "epoch must be >= 1");
-    hetis::PeerSignal t{};
-    for (int p = 0; p < num_ranks; ++p) {
-        if (!signal_peers[p] || !aligned(signal_peers[p], 8)) return fail(HETIS_E_INVALID, "bad signal pointer");
-        t.sig[p] = signal_peers[p];
-    }
-    t.n = num_ranks;
-    t.rank = rank;
-    t.epoch = epoch;
-    cudaError_t e = hetis::launch_peer_signal(t, reinterpret_cast<cudaStream_t>(stream));
-    if (e != cudaSuccess) return cuda_fail(e, "peer_signal launch");
-    return HETIS_OK;
-}
-
-hetis_status hetis_scatter_pull(const hetis_plan *plan, int32_t rank, int32_t num_seqs, const int64_t *signal_local,
-                                int32_t root, int64_t epoch, const void *q_full_root, const void *k_new_full_root,
-                                const void *v_new_full_root, void *q_shard, void *k_new_shard, void *v_new_shard,
-                                hetis_stream_t stream) {
-    if (!plan) return fail(HETIS_E_INVALID, "plan is NULL");
-    if (plan->per_request) return fail(HETIS_E_UNSUPPORTED, "scatter needs a global (per_request = 0) plan");
-    if (rank < 0 || rank >= plan->num_devices || root < 0 || root >= plan->num_devices)
-        return fail(HETIS_E_INVALID, "rank / root outside the plan");
-    if (num_seqs < 0 || epoch < 1) return fail(HETIS_E_INVALID, "bad num_seqs / epoch");
-    if (num_seqs == 0 || plan->x[rank] == 0) return HETIS_OK;
-    if (!signal_local || !q_full_root || !k_new_full_root || !v_new_full_root || !q_shard || !k_new_shard ||
-        !v_new_shard)
-        return fail(HETIS_E_INVALID, "NULL pointer");
-    const void *ptrs[] = {q_full_root, k_new_full_root, v_new_full_root, q_shard, k_new_shard, v_new_shard};
-    for (const void *ptr : ptrs)
-        if (!aligned(ptr, 16)) return fail(HETIS_E_INVALID, "buffers must be 16-byte aligned");
-    const hetis_shape &s = plan->shape;
-    const int r = s.num_q_heads / s.num_kv_heads;
-    const int x = plan->x[rank], b = plan->begin[rank];
-    cudaError_t e = hetis::launch_scatter_pull(
-        signal_local + root, epoch, q_full_root, k_new_full_root, v_new_full_root, num_seqs, s.num_q_heads,
-        s.num_kv_heads, b, x, b / r, x / r, s.head_dim * esize(s.q_dtype), s.head_dim * esize(s.kv_dtype), q_shard,
-        k_new_shard, v_new_shard, reinterpret_cast<cudaStream_t>(stream));
-    if (e != cudaSuccess) return cuda_fail(e, "scatter_pull launch");
-    return HETIS_OK;
 }
 
 // ---------------------------------------------------------------- scatter / gather

@@ -76,38 +76,47 @@ struct CopySegs {
 };
 cudaError_t launch_head_copies(CopySegs &c, cudaStream_t s);
 
-// Peer-memory targets of the fused combine + all-gather (at most kMaxPeers ranks).
+// ---------------------------------------------------------------- exchanges over peer memory
+// Device-resident exchange state of one rank (hetis_peer_state_bytes; the
+// caller zero-fills it once).  int64 slots; every epoch lives in device memory,
+// so a step's kernels take no per-step host argument and a captured CUDA graph
+// replays any number of steps.  Epoch of the step in flight = state[kStStep] + 1
+// (read after stream ordering); hetis_peer_wait, the step's last kernel, stores it.
 constexpr int kMaxPeers = 8;
-struct PeerTargets {
-    void *o[kMaxPeers];        // every rank's o_full [num_seqs][H][d], mapped in this process
-    int64_t *sig[kMaxPeers];   // every rank's signal array [n] (int64), mapped in this process
-    int n, rank, head0;
-    int64_t epoch;
-    int64_t o_seq_stride;      // elements between requests in o_full (>= H * d)
-    int32_t *done;             // block-completion counter (zero between calls)
+constexpr int kStStep = 0;     // steps this rank has completed (written only by its own peer_wait)
+constexpr int kStDone = 8;     // block counter of combine_peers (local, self-cleaning)
+constexpr int kStIn = 16;      // the root's latest published input epoch
+constexpr int kStOut = 32;     // [kMaxPeers] epoch of rank p's rows now in this rank's o_full
+constexpr int kStAck = 48;     // [kMaxPeers] rank p has consumed its o_full through this epoch
+constexpr int kStSlots = 64;   // 512 bytes
+struct PeerGroupDev {
+    int64_t *state[kMaxPeers];  // every rank's state as mapped in this process ([rank] = own)
+    void *o[kMaxPeers];         // every rank's o_full [num_seqs][H][d] (o_dtype), mapped here
+    const uint8_t *q_root, *k_root, *v_root;  // the root's q_full / k_new_full / v_new_full, mapped here
+    int n, rank, root;
+    int gather_root;            // -1: every rank receives O (all-gather); >= 0: only that rank
+    int head0;                  // this rank's first global query head
+    int64_t o_seq_stride;       // elements between requests in o_full (>= H * d)
 };
+// O rows of this rank's heads go to rank p iff gather_root < 0 or p == gather_root
+__host__ __device__ inline bool peer_is_target(const PeerGroupDev &g, int p) {
+    return g.gather_root < 0 || p == g.gather_root;
+}
 cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim, const int32_t *split_off,
-                                 const float *part_lse, const float *part_o, int o_dtype, const PeerTargets &t,
+                                 const float *part_lse, const float *part_o, int o_dtype, const PeerGroupDev &g,
                                  cudaStream_t s, int max_seq_len);
+cudaError_t launch_scatter_pull(const PeerGroupDev &g, int num_seqs, int H, int Hkv, int q0, int nq, int k0, int nk,
+                                int qrow, int kvrow, void *q_dst, void *k_dst, void *v_dst, cudaStream_t s);
+cudaError_t launch_peer_wait(const PeerGroupDev &g, cudaStream_t s);
 // sequence-wise split (row f3, seq_split.cu)
 cudaError_t launch_seq_split_lens(int num_ranks, int rank, int page_size, int num_seqs, const int32_t *seq_lens,
                                   int32_t *local_lens, int32_t *append_lens, cudaStream_t s);
 cudaError_t launch_seq_merge(int num_parts, int num_seqs, int q_heads, int head_dim, const float *o_parts,
                              int64_t o_part_stride, const float *lse_parts, int64_t lse_part_stride, void *o,
                              int o_dtype, int64_t o_seq_stride, cudaStream_t s);
-struct PeerSignal {
-    int64_t *sig[kMaxPeers];   // every rank's signal array, mapped in this process
-    int n, rank;
-    int64_t epoch;
-};
-cudaError_t launch_peer_signal(const PeerSignal &t, cudaStream_t s);
-cudaError_t launch_scatter_pull(const int64_t *sig, int64_t epoch, const void *q_src, const void *k_src,
-                                const void *v_src, int num_seqs, int H, int Hkv, int q0, int nq, int k0, int nk,
-                                int qrow, int kvrow, void *q_dst, void *k_dst, void *v_dst, cudaStream_t s);
 cudaError_t launch_check_tables(int num_seqs, int kv_heads, int page_size, int64_t num_pages,
                                 const int32_t *block_table, int max_pages, const int32_t *seq_lens,
                                 int32_t *violations, cudaStream_t s);
-cudaError_t launch_peer_wait(const int64_t *sig, int n, int64_t epoch, cudaStream_t s);
 cudaError_t launch_kv_migrate(int num_entries, const hetis_migration_entry *entries, int page_size, int page_bytes,
                               const void *src_k, const void *src_v, const int32_t *src_bt, int src_max_pages,
                               void *dst_k, void *dst_v, const int32_t *dst_bt, int dst_max_pages, int max_ctas,

@@ -226,57 +226,91 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(int num_seqs, 
     if (lse != nullptr && d4 == 0) lse[flat] = lse2 * 0.69314718055994531f;  // log2 -> natural log
 }
 
-// Combine fused with the all-gather over peer memory (NVLink / NVSwitch): each
-// merged O row is stored straight into every rank's o_full at its GLOBAL head
-// index (Eq. 2a Concat), then the last block publishes `epoch` into every
-// rank's signal slot [rank] with a system-scope release store.
+// ---------------------------------------------------------------- exchanges over peer memory
+// System-scope acquire / release on int64 epochs (every rank's state is mapped
+// into every process: NVLink peer memory on an NVSwitch box).
+__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
+    int64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(int64_t *p, int64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Bounded spin: a peer that never publishes makes the kernel trap after ~10 s
+// (the error surfaces on the stream) instead of hanging the device.
+__device__ __forceinline__ void spin_until_geq(const int64_t *p, int64_t v) {
+    if (ld_acquire_sys(p) >= v) return;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        __nanosleep(128);
+        if (ld_acquire_sys(p) >= v) return;
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > 10000000000ull) __trap();
+    }
+}
+// Epoch of the step in flight: this rank's completed steps + 1 (the state word
+// is written only by this rank's own hetis_peer_wait, earlier on the stream).
+__device__ __forceinline__ int64_t current_epoch(const PeerGroupDev &g) {
+    return *reinterpret_cast<volatile const int64_t *>(g.state[g.rank] + kStStep) + 1;
+}
+
+// Combine fused with the all-gather over peer memory: each merged O row is
+// stored straight into every target rank's o_full at its GLOBAL head index
+// (Eq. 2a Concat), after that rank has acknowledged it consumed the previous
+// step's o_full; then the last block publishes the epoch into every target's
+// state slot kStOut + rank with a system-scope release store.
 template <int D, int OUT_BF16, bool WIDE>
 __global__ void __launch_bounds__(kCombineThreads) combine_peers_kernel(int num_seqs, int q_heads, int r,
                                                                         const int32_t *split_off,
                                                                         const float *part_lse, const float *part_o,
-                                                                        PeerTargets t) {
+                                                                        PeerGroupDev g) {
     dev::pdl_wait_then_release();
+    const int64_t e = current_epoch(g);
     constexpr int TPH = D / 4, G = kCombineThreads / TPH;
     const int grp = threadIdx.x / TPH, d4 = threadIdx.x % TPH;
     const int64_t flat = WIDE ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * G + grp;
-    if (flat < (int64_t)num_seqs * q_heads) {
-        const int j = (int)(flat / q_heads), h = (int)(flat - (int64_t)j * q_heads);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int j = 0, h = 0;
+    const bool live = flat < (int64_t)num_seqs * q_heads;
+    if (live) {
+        j = (int)(flat / q_heads);
+        h = (int)(flat - (int64_t)j * q_heads);
         float lse2;
-        const float4 acc = WIDE ? combine_wide<D>(j, h, q_heads, r, split_off, part_lse, part_o, &lse2)
-                                : combine_narrow<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4, &lse2);
-        if (!WIDE || grp == 0) {
-            const size_t idx = (size_t)j * t.o_seq_stride + (size_t)(t.head0 + h) * D + 4 * d4;
-            for (int p = 0; p < t.n; ++p) store_row4<OUT_BF16>(t.o[p], idx, acc);
-        }
+        acc = WIDE ? combine_wide<D>(j, h, q_heads, r, split_off, part_lse, part_o, &lse2)
+                   : combine_narrow<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4, &lse2);
+    }
+    // rank p may still read the previous step's o_full until it acknowledges (its scatter_pull of this step)
+    if (threadIdx.x < g.n && peer_is_target(g, threadIdx.x)) spin_until_geq(g.state[g.rank] + kStAck + threadIdx.x, e - 1);
+    __syncthreads();
+    if (live && (!WIDE || grp == 0)) {
+        const size_t idx = (size_t)j * g.o_seq_stride + (size_t)(g.head0 + h) * D + 4 * d4;
+        for (int p = 0; p < g.n; ++p)
+            if (peer_is_target(g, p)) store_row4<OUT_BF16>(g.o[p], idx, acc);
     }
     __threadfence_system();  // this thread's peer stores are visible system-wide ...
     __syncthreads();
     if (threadIdx.x == 0) {  // ... before the block is counted
-        if (atomicAdd(t.done, 1) == (int)gridDim.x - 1) {
+        int64_t *done = g.state[g.rank] + kStDone;
+        if (atomicAdd(reinterpret_cast<unsigned long long *>(done), 1ull) == (unsigned long long)gridDim.x - 1) {
             __threadfence_system();
-            for (int p = 0; p < t.n; ++p)
-                asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(t.sig[p] + t.rank), "l"(t.epoch) : "memory");
-            *t.done = 0;  // self-cleaning for the next call
+            for (int p = 0; p < g.n; ++p)
+                if (peer_is_target(g, p)) st_release_sys(g.state[p] + kStOut + g.rank, e);
+            *done = 0;  // self-cleaning for the next step
         }
     }
 }
 
-// Stream-ordered wait until every rank published `epoch` (acquire), bounded:
-// a peer that never signals traps after ~10 s instead of hanging the device.
-__global__ void peer_wait_kernel(const int64_t *sig, int n, int64_t epoch) {
-    if ((int)threadIdx.x < n) {
-        unsigned long long t0;
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
-        for (;;) {
-            int64_t v;
-            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(sig + threadIdx.x) : "memory");
-            if (v >= epoch) break;
-            unsigned long long t1;
-            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
-            if (t1 - t0 > 10000000000ull) __trap();
-            __nanosleep(200);
-        }
-    }
+// The step's last kernel: a target rank waits (acquire, bounded) until every
+// rank published this epoch's rows into its o_full; every rank then records the
+// step as completed (the next step's kernels derive their epoch from it).
+__global__ void peer_wait_kernel(PeerGroupDev g) {
+    const int64_t e = current_epoch(g);
+    if ((int)threadIdx.x < g.n && peer_is_target(g, g.rank)) spin_until_geq(g.state[g.rank] + kStOut + threadIdx.x, e);
+    __syncthreads();
+    if (threadIdx.x == 0) g.state[g.rank][kStStep] = e;
 }
 
 // ---------------------------------------------------------------- table validation (debug)
@@ -304,37 +338,27 @@ __global__ void check_tables_kernel(int num_seqs, int kv_heads, int page_size, i
 }
 
 // ---------------------------------------------------------------- scatter over peer memory
-// Publish `epoch` into slot [rank] of every rank's signal array (system-scope
-// release) once everything before it on the stream is complete and visible.
-__global__ void peer_signal_kernel(PeerSignal t) {
-    if (threadIdx.x == 0) {
-        __threadfence_system();
-        for (int p = 0; p < t.n; ++p)
-            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(t.sig[p] + t.rank), "l"(t.epoch) : "memory");
-    }
-}
-
-// Pull this rank's shard of the step's inputs straight from the Primary's buffers
-// (mapped over NVLink): every block's thread 0 waits (acquire, bounded) until the
-// Primary published `epoch`, then the block copies 16-byte chunks of
+// Pull this rank's shard of the step's inputs straight from the root's buffers
+// (mapped over NVLink).  Block 0 first publishes, system-wide: on the root, the
+// epoch into every rank's kStIn (everything before this kernel on the root's
+// stream -- the writes of q_full, k_new_full, v_new_full -- is visible); on
+// every rank, its acknowledgement (kStAck + rank = e - 1: everything before this
+// kernel on its stream, including the consumer of the previous step's o_full,
+// has completed).  Every block's thread 0 then waits (acquire, bounded) for the
+// root's epoch and the block copies 16-byte chunks of
 //   q      [B][H][d]     heads [q0, q0 + nq)   -> q_shard [B][nq][d]
 //   k, v   [B][Hkv][d]   heads [k0, k0 + nk)   -> k/v_shard [B][nk][d]
-__global__ void scatter_pull_kernel(const int64_t *sig, int64_t epoch, const uint8_t *q_src, const uint8_t *k_src,
-                                    const uint8_t *v_src, int num_seqs, int H, int Hkv, int q0, int nq, int k0, int nk,
+__global__ void scatter_pull_kernel(PeerGroupDev g, int num_seqs, int H, int Hkv, int q0, int nq, int k0, int nk,
                                     int qrow, int kvrow, uint8_t *q_dst, uint8_t *k_dst, uint8_t *v_dst) {
-    if (threadIdx.x == 0) {
-        unsigned long long t0;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        for (;;) {
-            int64_t v;
-            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(sig) : "memory");
-            if (v >= epoch) break;
-            unsigned long long t1;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            if (t1 - t0 > 10000000000ull) __trap();
-            __nanosleep(100);
+    const int64_t e = current_epoch(g);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        __threadfence_system();
+        for (int p = 0; p < g.n; ++p) {
+            st_release_sys(g.state[p] + kStAck + g.rank, e - 1);
+            if (g.rank == g.root) st_release_sys(g.state[p] + kStIn, e);
         }
     }
+    if (threadIdx.x == 0) spin_until_geq(g.state[g.rank] + kStIn, e);
     __syncthreads();
     const int qc = qrow / 16, kc = kvrow / 16;
     const int64_t nq_chunks = (int64_t)num_seqs * nq * qc, nk_chunks = (int64_t)num_seqs * nk * kc;
@@ -346,7 +370,7 @@ __global__ void scatter_pull_kernel(const int64_t *sig, int64_t epoch, const uin
             const int c = (int)(i % qc);
             const int64_t row = i / qc;
             const int h = (int)(row % nq), j = (int)(row / nq);
-            src = q_src + ((size_t)j * H + q0 + h) * qrow + 16 * c;
+            src = g.q_root + ((size_t)j * H + q0 + h) * qrow + 16 * c;
             dst = q_dst + ((size_t)j * nq + h) * qrow + 16 * c;
         } else {
             const int64_t ii = (i - nq_chunks) % nk_chunks;
@@ -354,7 +378,7 @@ __global__ void scatter_pull_kernel(const int64_t *sig, int64_t epoch, const uin
             const int c = (int)(ii % kc);
             const int64_t row = ii / kc;
             const int h = (int)(row % nk), j = (int)(row / nk);
-            src = (is_v ? v_src : k_src) + ((size_t)j * Hkv + k0 + h) * kvrow + 16 * c;
+            src = (is_v ? g.v_root : g.k_root) + ((size_t)j * Hkv + k0 + h) * kvrow + 16 * c;
             dst = (is_v ? v_dst : k_dst) + ((size_t)j * nk + h) * kvrow + 16 * c;
         }
         uint4 v;
@@ -461,13 +485,13 @@ cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const
 }
 
 cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim, const int32_t *split_off,
-                                 const float *part_lse, const float *part_o, int o_dtype, const PeerTargets &t,
+                                 const float *part_lse, const float *part_o, int o_dtype, const PeerGroupDev &g,
                                  cudaStream_t s, int max_seq_len) {
     const int64_t pairs = (int64_t)num_seqs * q_heads;
-    if (pairs == 0) return cudaSuccess;
     const bool wide = (max_seq_len + kSplitTokens - 1) / kSplitTokens > kNarrowSplits;
-    const int g = kCombineThreads / (head_dim / 4);
-    const int64_t blocks = wide ? pairs : (pairs + g - 1) / g;
+    const int gsz = kCombineThreads / (head_dim / 4);
+    int64_t blocks = wide ? pairs : (pairs + gsz - 1) / gsz;
+    if (blocks < 1) blocks = 1;  // an empty shard still publishes the epoch
     const bool bf = o_dtype == HETIS_BF16;
     decltype(&combine_peers_kernel<128, 0, false>) kern;
     if (head_dim == 128)
@@ -477,11 +501,11 @@ cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim,
         kern = wide ? (bf ? combine_peers_kernel<64, 1, true> : combine_peers_kernel<64, 0, true>)
                     : (bf ? combine_peers_kernel<64, 1, false> : combine_peers_kernel<64, 0, false>);
     return launch_pdl(kern, dim3((unsigned)blocks), dim3(kCombineThreads), 0, s, num_seqs, q_heads, r, split_off,
-                      part_lse, part_o, t);
+                      part_lse, part_o, g);
 }
 
-cudaError_t launch_peer_wait(const int64_t *sig, int n, int64_t epoch, cudaStream_t s) {
-    peer_wait_kernel<<<1, 32, 0, s>>>(sig, n, epoch);
+cudaError_t launch_peer_wait(const PeerGroupDev &g, cudaStream_t s) {
+    peer_wait_kernel<<<1, 32, 0, s>>>(g);
     note_launch();
     return cudaGetLastError();
 }
@@ -502,24 +526,17 @@ cudaError_t launch_check_tables(int num_seqs, int kv_heads, int page_size, int64
     return cudaGetLastError();
 }
 
-cudaError_t launch_peer_signal(const PeerSignal &t, cudaStream_t s) {
-    peer_signal_kernel<<<1, 32, 0, s>>>(t);
-    note_launch();
-    return cudaGetLastError();
-}
-
-cudaError_t launch_scatter_pull(const int64_t *sig, int64_t epoch, const void *q_src, const void *k_src,
-                                const void *v_src, int num_seqs, int H, int Hkv, int q0, int nq, int k0, int nk,
+cudaError_t launch_scatter_pull(const PeerGroupDev &g, int num_seqs, int H, int Hkv, int q0, int nq, int k0, int nk,
                                 int qrow, int kvrow, void *q_dst, void *k_dst, void *v_dst, cudaStream_t s) {
     const int64_t total = (int64_t)num_seqs * (nq * (qrow / 16) + 2 * nk * (kvrow / 16));
-    if (total == 0) return cudaSuccess;
     const int threads = 256;
     int64_t blocks = (total + threads - 1) / threads;
     if (blocks > 2 * num_sms()) blocks = 2 * num_sms();
-    scatter_pull_kernel<<<(unsigned)blocks, threads, 0, s>>>(
-        sig, epoch, static_cast<const uint8_t *>(q_src), static_cast<const uint8_t *>(k_src),
-        static_cast<const uint8_t *>(v_src), num_seqs, H, Hkv, q0, nq, k0, nk, qrow, kvrow,
-        static_cast<uint8_t *>(q_dst), static_cast<uint8_t *>(k_dst), static_cast<uint8_t *>(v_dst));
+    if (blocks < 1) blocks = 1;  // nothing to copy still publishes the signal and the acknowledgement
+    scatter_pull_kernel<<<(unsigned)blocks, threads, 0, s>>>(g, num_seqs, H, Hkv, q0, nq, k0, nk, qrow, kvrow,
+                                                            static_cast<uint8_t *>(q_dst),
+                                                            static_cast<uint8_t *>(k_dst),
+                                                            static_cast<uint8_t *>(v_dst));
     note_launch();
     return cudaGetLastError();
 }

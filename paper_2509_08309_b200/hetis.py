@@ -36,7 +36,8 @@ EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_
             "hetis_attn_combine", "hetis_attn_decode", "hetis_attn_combine_peers", "hetis_peer_wait",
             "hetis_comm_workspace", "hetis_scatter_q", "hetis_gather", "hetis_kv_migrate",
             "hetis_attn_combine_lse", "hetis_seq_split_lens", "hetis_seq_merge", "hetis_seq_broadcast_q",
-            "hetis_seq_allgather_merge", "hetis_peer_signal", "hetis_scatter_pull", "hetis_attn_partial_append",
+            "hetis_seq_allgather_merge", "hetis_peer_state_bytes", "hetis_peer_group_create",
+            "hetis_peer_group_destroy", "hetis_scatter_pull", "hetis_attn_partial_append",
             "hetis_attn_decode_append", "hetis_check_tables", "hetis_launch_count")
 
 
@@ -88,9 +89,11 @@ def lib() -> ctypes.CDLL:
                 "hetis_attn_combine": (ctypes.c_int, [sp, i32, i32, vp, i32, vp, i64, vp, sz, vp]),
                 "hetis_attn_decode": (ctypes.c_int, [sp, i32, i32, i32, vp, vp, vp, i64, vp, i32, vp, i32, vp, vp,
                                                      sz, u32, vp]),
-                "hetis_attn_combine_peers": (ctypes.c_int, [sp, i32, i32, i32, vp, i32, P(vp), i64, P(vp), i32, i32,
-                                                            i64, vp, sz, vp]),
-                "hetis_peer_wait": (ctypes.c_int, [vp, i32, i64, vp]),
+                "hetis_peer_state_bytes": (sz, []),
+                "hetis_peer_group_create": (ctypes.c_int, [vp, i32, i32, i32, P(vp), P(vp), i64, vp, vp, vp, P(vp)]),
+                "hetis_peer_group_destroy": (None, [vp]),
+                "hetis_attn_combine_peers": (ctypes.c_int, [vp, i32, vp, i32, vp, sz, vp]),
+                "hetis_peer_wait": (ctypes.c_int, [vp, vp]),
                 "hetis_comm_workspace": (ctypes.c_int, [vp, i32, i32, P(sz)]),
                 "hetis_scatter_q": (ctypes.c_int, [vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
                 "hetis_gather": (ctypes.c_int, [vp, vp, i32, i32, i32, vp, vp, vp, sz, vp]),
@@ -100,13 +103,12 @@ def lib() -> ctypes.CDLL:
                 "hetis_seq_merge": (ctypes.c_int, [sp, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp]),
                 "hetis_seq_broadcast_q": (ctypes.c_int, [sp, vp, i32, i32, i32, i32, vp, vp, vp, vp]),
                 "hetis_seq_allgather_merge": (ctypes.c_int, [sp, vp, i32, i32, i32, vp, vp, vp, i64, vp]),
-                "hetis_peer_signal": (ctypes.c_int, [P(vp), i32, i32, i64, vp]),
                 "hetis_check_tables": (ctypes.c_int, [sp, i32, i32, i64, vp, i32, vp, vp, vp]),
                 "hetis_attn_partial_append": (ctypes.c_int, [sp, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32, vp,
                                                              i32, vp, sz, u32, vp]),
                 "hetis_attn_decode_append": (ctypes.c_int, [sp, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32, vp,
                                                             i32, vp, vp, sz, u32, vp]),
-                "hetis_scatter_pull": (ctypes.c_int, [vp, i32, i32, vp, i32, i64, vp, vp, vp, vp, vp, vp, vp]),
+                "hetis_scatter_pull": (ctypes.c_int, [vp, i32, vp, vp, vp, vp]),
             }
             for name, (res, args) in sig.items():
                 # an older build loaded through HETIS_LIB (A/B runs) may lack newer entry points;
@@ -146,6 +148,50 @@ def _dev(t: torch.Tensor | None, name: str):
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
     return ctypes.c_void_p(t.data_ptr())
+
+
+_TORCH_OF = {F32: torch.float32, BF16: torch.bfloat16}
+
+
+def _check_args(shape: CShape, q=None, o=None, k_pool=None, v_pool=None, block_table=None, seq_lens=None,
+                k_new=None, v_new=None, kv_heads: int | None = None) -> None:
+    """Host-side dtype / shape agreement with the CShape (the C ABI takes raw pointers and cannot check it):
+    a bf16 o passed with an f32 o_dtype, or a block table with the wrong number of kv heads, would make the
+    kernels read or write past the buffers."""
+    r = shape.num_q_heads // shape.num_kv_heads
+    kvt, qt, ot = _TORCH_OF[shape.kv_dtype], _TORCH_OF[shape.q_dtype], _TORCH_OF[shape.o_dtype]
+    D, P = shape.head_dim, shape.page_size
+    B = None
+    if q is not None:
+        if q.dtype != qt or q.dim() != 3 or q.shape[2] != D or q.shape[1] % r:
+            raise ValueError(f"q must be {qt} [B][x][{D}] with x a multiple of r={r}, got {q.dtype} {tuple(q.shape)}")
+        B, kv_heads = q.shape[0], q.shape[1] // r
+    if o is not None:
+        if o.dtype != ot or o.shape[-1] != D:
+            raise ValueError(f"o must be {ot} [..][{D}] (shape.o_dtype), got {o.dtype} {tuple(o.shape)}")
+        if q is not None and (o.shape[0] != q.shape[0] or o.shape[1] < q.shape[1]):
+            raise ValueError(f"o {tuple(o.shape)} does not cover q {tuple(q.shape)}")
+    for name, pool in (("k_pool", k_pool), ("v_pool", v_pool)):
+        if pool is not None and (pool.dtype != kvt or pool.dim() != 3 or pool.shape[1] != P or pool.shape[2] != D):
+            raise ValueError(f"{name} must be {kvt} [pages][{P}][{D}], got {pool.dtype} {tuple(pool.shape)}")
+    if k_pool is not None and v_pool is not None and k_pool.shape != v_pool.shape:
+        raise ValueError("k_pool and v_pool differ in shape")
+    for name, t in (("k_new", k_new), ("v_new", v_new)):
+        if t is not None:
+            if t.dtype != kvt or t.dim() != 3 or t.shape[2] != D:
+                raise ValueError(f"{name} must be {kvt} [B][kv][{D}], got {t.dtype} {tuple(t.shape)}")
+            if B is not None and (t.shape[0] != B or t.shape[1] != kv_heads):
+                raise ValueError(f"{name} {tuple(t.shape)} does not match q's [B][x/r] = [{B}][{kv_heads}]")
+    if block_table is not None:
+        if block_table.dtype != torch.int32 or block_table.dim() != 3:
+            raise ValueError("block_table must be int32 [B][kv][max_pages]")
+        if B is not None and (block_table.shape[0] != B or block_table.shape[1] != kv_heads):
+            raise ValueError(f"block_table {tuple(block_table.shape)} does not match [B][x/r] = [{B}][{kv_heads}]")
+    if seq_lens is not None:
+        if seq_lens.dtype != torch.int32 or seq_lens.dim() != 1:
+            raise ValueError("seq_lens must be int32 [B]")
+        if B is not None and seq_lens.shape[0] != B:
+            raise ValueError(f"seq_lens has {seq_lens.shape[0]} entries for {B} requests")
 
 
 def _stream(stream) -> ctypes.c_void_p:
@@ -225,6 +271,10 @@ def plan_create(shape: CShape, num_devices: int, x, per_request: bool = False, n
 # ---------------------------------------------------------------- kernels
 def kv_append(shape: CShape, k_new, v_new, k_pool, v_pool, block_table, seq_lens, stream=None) -> None:
     B, G, _ = k_new.shape
+    _check_args(shape, k_pool=k_pool, v_pool=v_pool, k_new=k_new, v_new=v_new, block_table=block_table,
+                seq_lens=seq_lens)
+    if block_table.shape[:2] != k_new.shape[:2] or v_new.shape != k_new.shape or seq_lens.shape[0] != B:
+        raise ValueError("k_new, v_new, block_table and seq_lens disagree on [B][kv]")
     _check(lib().hetis_kv_append(ctypes.byref(shape), B, G, _dev(k_new, "k_new"), _dev(v_new, "v_new"),
                                  _dev(k_pool, "k_pool"), _dev(v_pool, "v_pool"), k_pool.shape[0],
                                  _dev(block_table, "block_table"), block_table.shape[2], _dev(seq_lens, "seq_lens"),
@@ -273,6 +323,7 @@ def alloc_workspace(nbytes: int, device) -> torch.Tensor:
 def attn_partial(shape: CShape, q, k_pool, v_pool, block_table, seq_lens, max_seq_len: int, workspace,
                  q_head_begin: int = 0, flags: int = 0, stream=None) -> None:
     B, x, _ = q.shape
+    _check_args(shape, q=q, k_pool=k_pool, v_pool=v_pool, block_table=block_table, seq_lens=seq_lens)
     _check(lib().hetis_attn_partial(ctypes.byref(shape), B, q_head_begin, x, _dev(q, "q"), _dev(k_pool, "k_pool"),
                                     _dev(v_pool, "v_pool"), k_pool.shape[0], _dev(block_table, "block_table"),
                                     block_table.shape[2], _dev(seq_lens, "seq_lens"), max_seq_len,
@@ -289,6 +340,7 @@ def attn_combine(shape: CShape, seq_lens, max_seq_len: int, o, workspace, q_head
         o_seq_stride = o.stride(0)
     if not o.is_cuda:
         raise ValueError("o must be a CUDA tensor")
+    _check_args(shape, o=o, seq_lens=seq_lens)
     _check(lib().hetis_attn_combine(ctypes.byref(shape), B, q_head_count, _dev(seq_lens, "seq_lens"), max_seq_len,
                                     ctypes.c_void_p(o.data_ptr()), o_seq_stride, _dev(workspace, "workspace"),
                                     workspace.numel() * workspace.element_size(), _stream(stream)),
@@ -305,6 +357,7 @@ def attn_combine_lse(shape: CShape, seq_lens, max_seq_len: int, o, lse, workspac
         o_seq_stride = o.stride(0)
     if not o.is_cuda or not lse.is_cuda or lse.dtype != torch.float32:
         raise ValueError("o and lse (float32) must be CUDA tensors")
+    _check_args(shape, o=o, seq_lens=seq_lens)
     _check(lib().hetis_attn_combine_lse(ctypes.byref(shape), B, q_head_count, _dev(seq_lens, "seq_lens"), max_seq_len,
                                         ctypes.c_void_p(o.data_ptr()), o_seq_stride, ctypes.c_void_p(lse.data_ptr()),
                                         _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(),
@@ -315,6 +368,8 @@ def attn_partial_append(shape: CShape, q, k_new, v_new, k_pool, v_pool, block_ta
                         workspace, q_head_begin: int = 0, flags: int = 0, stream=None) -> None:
     """kv_append fused into the split-KV attention kernel (hetis_attn_partial_append)."""
     B, x, _ = q.shape
+    _check_args(shape, q=q, k_pool=k_pool, v_pool=v_pool, block_table=block_table, seq_lens=seq_lens, k_new=k_new,
+                v_new=v_new)
     _check(lib().hetis_attn_partial_append(ctypes.byref(shape), B, q_head_begin, x, _dev(q, "q"), _dev(k_new, "k_new"),
                                            _dev(v_new, "v_new"), _dev(k_pool, "k_pool"), _dev(v_pool, "v_pool"),
                                            k_pool.shape[0], _dev(block_table, "block_table"), block_table.shape[2],
@@ -327,6 +382,8 @@ def attn_decode_append(shape: CShape, q, k_new, v_new, k_pool, v_pool, block_tab
                        workspace, q_head_begin: int = 0, flags: int = 0, stream=None) -> None:
     """The per-device step in two kernels: attention with the append fused, then the combine."""
     B, x, _ = q.shape
+    _check_args(shape, q=q, o=o, k_pool=k_pool, v_pool=v_pool, block_table=block_table, seq_lens=seq_lens,
+                k_new=k_new, v_new=v_new)
     _check(lib().hetis_attn_decode_append(ctypes.byref(shape), B, q_head_begin, x, _dev(q, "q"), _dev(k_new, "k_new"),
                                           _dev(v_new, "v_new"), _dev(k_pool, "k_pool"), _dev(v_pool, "v_pool"),
                                           k_pool.shape[0], _dev(block_table, "block_table"), block_table.shape[2],
@@ -338,6 +395,7 @@ def attn_decode_append(shape: CShape, q, k_new, v_new, k_pool, v_pool, block_tab
 def attn_decode(shape: CShape, q, k_pool, v_pool, block_table, seq_lens, max_seq_len: int, o, workspace,
                 q_head_begin: int = 0, flags: int = 0, stream=None) -> None:
     B, x, _ = q.shape
+    _check_args(shape, q=q, o=o, k_pool=k_pool, v_pool=v_pool, block_table=block_table, seq_lens=seq_lens)
     _check(lib().hetis_attn_decode(ctypes.byref(shape), B, q_head_begin, x, _dev(q, "q"), _dev(k_pool, "k_pool"),
                                    _dev(v_pool, "v_pool"), k_pool.shape[0], _dev(block_table, "block_table"),
                                    block_table.shape[2], _dev(seq_lens, "seq_lens"), max_seq_len, _dev(o, "o"),
@@ -345,47 +403,65 @@ def attn_decode(shape: CShape, q, k_pool, v_pool, block_table, seq_lens, max_seq
                                    _stream(stream)), "hetis_attn_decode")
 
 
-# ---------------------------------------------------------------- combine fused with the peer all-gather
-def attn_combine_peers(shape: CShape, seq_lens, max_seq_len: int, o_full_peers, signal_peers, rank: int, epoch: int,
-                       workspace, q_head_begin: int, q_head_count: int, stream=None) -> None:
-    """Merge this rank's splits and store every row into every rank's o_full (peer memory), then publish `epoch`.
-
-    o_full_peers / signal_peers: per rank, tensors (or raw device pointers) mapped in this process."""
-    n = len(o_full_peers)
-    ptr = lambda t: t.data_ptr() if hasattr(t, "data_ptr") else int(t)
-    o_arr = (ctypes.c_void_p * n)(*[ptr(t) for t in o_full_peers])
-    s_arr = (ctypes.c_void_p * n)(*[ptr(t) for t in signal_peers])
-    o0 = o_full_peers[rank]
-    stride = o0.stride(0) if hasattr(o0, "stride") else shape.num_q_heads * shape.head_dim
-    B = seq_lens.shape[0]
-    _check(lib().hetis_attn_combine_peers(ctypes.byref(shape), B, q_head_begin, q_head_count,
-                                          _dev(seq_lens, "seq_lens"), max_seq_len, o_arr, stride, s_arr, n, rank,
-                                          epoch, _dev(workspace, "workspace"),
-                                          workspace.numel() * workspace.element_size(), _stream(stream)),
-           "hetis_attn_combine_peers")
+# ---------------------------------------------------------------- the step's exchanges over peer memory
+def peer_state_bytes() -> int:
+    return int(lib().hetis_peer_state_bytes())
 
 
-def peer_wait(signal_local, epoch: int, stream=None) -> None:
-    _check(lib().hetis_peer_wait(_dev(signal_local, "signal_local"), signal_local.numel(), epoch, _stream(stream)),
-           "hetis_peer_wait")
+def alloc_peer_state(device) -> torch.Tensor:
+    """A zero-filled device state for hetis_peer_group_create (int64 slots; torch allocations are 512-B aligned)."""
+    return torch.zeros(peer_state_bytes() // 8, dtype=torch.int64, device=device)
 
 
-def peer_signal(signal_peers, rank: int, epoch: int, stream=None) -> None:
-    """Publish `epoch` into slot [rank] of every rank's signal array (tensors or raw pointers mapped here)."""
-    n = len(signal_peers)
-    ptr = lambda t: t.data_ptr() if hasattr(t, "data_ptr") else int(t)
-    arr = (ctypes.c_void_p * n)(*[ptr(t) for t in signal_peers])
-    _check(lib().hetis_peer_signal(arr, n, rank, epoch, _stream(stream)), "hetis_peer_signal")
+class PeerGroup:
+    """Owned hetis_peer_group: this rank's view of every rank's state and o_full and of the root's inputs."""
+
+    def __init__(self, plan: Plan, rank: int, root: int, gather_root: int, state_peers, o_full_peers,
+                 o_seq_stride: int, q_full_root, k_new_full_root, v_new_full_root):
+        n = plan.num_devices
+        if len(state_peers) != n or len(o_full_peers) != n:
+            raise ValueError("one state and one o_full (or None) per rank")
+        ptr = lambda t: None if t is None else (t.data_ptr() if hasattr(t, "data_ptr") else int(t))
+        st = (ctypes.c_void_p * n)(*[ptr(t) for t in state_peers])
+        of = (ctypes.c_void_p * n)(*[ptr(t) for t in o_full_peers])
+        h = ctypes.c_void_p()
+        _check(lib().hetis_peer_group_create(plan.handle, rank, root, gather_root, st, of, o_seq_stride,
+                                             ptr(q_full_root), ptr(k_new_full_root), ptr(v_new_full_root),
+                                             ctypes.byref(h)), "hetis_peer_group_create")
+        self._h = h
+        self.plan = plan
+        self.rank, self.root, self.gather_root = rank, root, gather_root
+        self._keep = (state_peers, o_full_peers, q_full_root, k_new_full_root, v_new_full_root)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.hetis_peer_group_destroy(h)
+            self._h = None
 
 
-def scatter_pull(plan: Plan, rank: int, num_seqs: int, signal_local, root: int, epoch: int, q_full_root,
-                 k_new_full_root, v_new_full_root, q_shard, k_new_shard, v_new_shard, stream=None) -> None:
-    """Wait for the root's epoch, then copy this rank's plan range from the root's (peer-mapped) buffers."""
-    ptr = lambda t: ctypes.c_void_p(t.data_ptr() if hasattr(t, "data_ptr") else int(t))
-    _check(lib().hetis_scatter_pull(plan.handle, rank, num_seqs, _dev(signal_local, "signal_local"), root, epoch,
-                                    ptr(q_full_root), ptr(k_new_full_root), ptr(v_new_full_root),
-                                    _dev(q_shard, "q_shard"), _dev(k_new_shard, "k_new_shard"),
+def scatter_pull(group: PeerGroup, num_seqs: int, q_shard, k_new_shard, v_new_shard, stream=None) -> None:
+    """a2 over peer memory: (root) publish the step's inputs, acknowledge the previous o_full, wait for the
+    root, copy this rank's range of q / new k, v straight from the root's buffers."""
+    _check(lib().hetis_scatter_pull(group.handle, num_seqs, _dev(q_shard, "q_shard"), _dev(k_new_shard, "k_new_shard"),
                                     _dev(v_new_shard, "v_new_shard"), _stream(stream)), "hetis_scatter_pull")
+
+
+def attn_combine_peers(group: PeerGroup, seq_lens, max_seq_len: int, workspace, stream=None) -> None:
+    """a5 + a6 in one kernel: merge this rank's splits, store every row into every receiving rank's o_full at
+    its global head index, publish the epoch."""
+    _check(lib().hetis_attn_combine_peers(group.handle, seq_lens.shape[0], _dev(seq_lens, "seq_lens"), max_seq_len,
+                                          _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(),
+                                          _stream(stream)), "hetis_attn_combine_peers")
+
+
+def peer_wait(group: PeerGroup, stream=None) -> None:
+    """The step's last kernel: wait for every rank's rows of this step (receiving ranks), record the step."""
+    _check(lib().hetis_peer_wait(group.handle, _stream(stream)), "hetis_peer_wait")
 
 
 # ---------------------------------------------------------------- NCCL scatter / gather

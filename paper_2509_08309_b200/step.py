@@ -104,55 +104,63 @@ class DecodeStep:
         hetis.gather(self.plan, self.comm_ptr, self.rank, root, self.num_seqs, self.buf.o_shard, o_full,
                      self.buf.comm_ws, stream)
 
-    # ---- exchanges over peer memory (NVLink): pull scatter (hetis_scatter_pull) and the combine fused
-    # with the all-gather (hetis_attn_combine_peers)
-    def setup_peers(self, o_full: torch.Tensor, q_full=None, k_new_full=None, v_new_full=None) -> None:
-        """Map every rank's o_full and signal arrays, and the root's q_full / k_new_full / v_new_full, into
-        this process (CUDA IPC handles exchanged with torch.distributed; on one NVSwitch box the mappings
-        are NVLink peer memory).  Collective; only the root passes the *_full tensors."""
+    # ---- exchanges over peer memory (NVLink): pull scatter (hetis_scatter_pull), the combine fused with the
+    # gather (hetis_attn_combine_peers) and the step's closing wait (hetis_peer_wait); epochs live on the device
+    def setup_peers(self, o_full: torch.Tensor | None, q_full=None, k_new_full=None, v_new_full=None,
+                    gather_root: int = -1) -> None:
+        """Map every rank's exchange state and o_full, and the root's q_full / k_new_full / v_new_full, into
+        this process (CUDA IPC handles exchanged over the default torch.distributed group -- gloo or NCCL; on
+        one NVSwitch box the mappings are NVLink peer memory).  Collective.  Only the root passes the *_full
+        tensors; o_full may be None on a rank that receives nothing (gather_root >= 0, not this rank)."""
         import torch.distributed as dist
         from torch.multiprocessing.reductions import reduce_tensor
         self.o_full = o_full
-        self.sig = torch.zeros(self.world, dtype=torch.int64, device=self.device)    # O epochs from every rank
-        self.qsig = torch.zeros(self.world, dtype=torch.int64, device=self.device)   # input epochs from the root
+        self.peer_state = hetis.alloc_peer_state(self.device)
         root_bufs = None
         if self.rank == self.root:
             root_bufs = tuple(reduce_tensor(t) for t in (q_full, k_new_full, v_new_full))
-        mine = (reduce_tensor(o_full), reduce_tensor(self.sig), reduce_tensor(self.qsig), root_bufs)
+        mine = (reduce_tensor(self.peer_state), None if o_full is None else reduce_tensor(o_full), root_bufs)
         everyone = [None] * self.world
         dist.all_gather_object(everyone, mine)
-        self.o_peers, self.sig_peers, self.qsig_peers = [], [], []
-        for i, (ro, rs, rq, _) in enumerate(everyone):
+        states, outs = [], []
+        for i, (rs, ro, _) in enumerate(everyone):
             if i == self.rank:
-                self.o_peers.append(o_full)
-                self.sig_peers.append(self.sig)
-                self.qsig_peers.append(self.qsig)
+                states.append(self.peer_state)
+                outs.append(o_full)
             else:
-                self.o_peers.append(ro[0](*ro[1]))
-                self.sig_peers.append(rs[0](*rs[1]))
-                self.qsig_peers.append(rq[0](*rq[1]))
+                states.append(rs[0](*rs[1]))
+                outs.append(None if ro is None else ro[0](*ro[1]))
         if self.rank == self.root:
-            self.root_bufs = (q_full, k_new_full, v_new_full)
+            root = (q_full, k_new_full, v_new_full)
         else:
-            self.root_bufs = tuple(f(*a) for f, a in everyone[self.root][3])
-        self.epoch = 0
+            root = tuple(f(*a) for f, a in everyone[self.root][2])
+        stride = (o_full.stride(0) if o_full is not None
+                  else self.shape.num_q_heads * self.shape.head_dim)
+        self.group = hetis.PeerGroup(self.plan, self.rank, self.root, gather_root, states, outs, stride, *root)
 
-    def scatter_peers(self, epoch: int, stream=None):
-        """Root: publish that this step's inputs are written; every rank: pull its heads' q and its kv heads'
-        new k, v straight from the root's buffers (one kernel, waits for the root's epoch)."""
-        if self.rank == self.root:
-            hetis.peer_signal(self.qsig_peers, self.rank, epoch, stream=stream)
-        hetis.scatter_pull(self.plan, self.rank, self.num_seqs, self.qsig, self.root, epoch, *self.root_bufs,
-                           self.buf.q_shard, self.buf.k_new, self.buf.v_new, stream=stream)
+    def scatter_peers(self, stream=None):
+        """Every rank pulls its heads' q and its kv heads' new k, v straight from the root's buffers (the root
+        first publishes that this step's inputs are written).  One kernel."""
+        hetis.scatter_pull(self.group, self.num_seqs, self.buf.q_shard, self.buf.k_new, self.buf.v_new, stream=stream)
 
-    def attention_gather_peers(self, k_pool, v_pool, block_table, seq_lens, stream=None, flags: int = 0):
-        """Partial attention, then ONE kernel that merges the splits and stores every row into every
-        rank's o_full; returns after a stream-ordered wait for all ranks' rows of this step."""
-        self.epoch += 1
-        hetis.attn_partial(self.cshape, self.buf.q_shard, k_pool, v_pool, block_table, seq_lens, self.max_seq_len,
-                           self.buf.workspace, q_head_begin=self.q_begin, flags=flags, stream=stream)
-        hetis.attn_combine_peers(self.cshape, seq_lens, self.max_seq_len, self.o_peers, self.sig_peers, self.rank,
-                                 self.epoch, self.buf.workspace, q_head_begin=self.q_begin,
-                                 q_head_count=self.q_count, stream=stream)
-        hetis.peer_wait(self.sig, self.epoch, stream=stream)
+    def attention_gather_peers(self, k_pool, v_pool, block_table, seq_lens, stream=None, flags: int = 0,
+                               fused_append: bool = True):
+        """Partial attention (kv_append fused by default), then ONE kernel that merges the splits and stores
+        every row into every receiving rank's o_full, then the step's closing wait.  Returns o_full."""
+        if fused_append:
+            hetis.attn_partial_append(self.cshape, self.buf.q_shard, self.buf.k_new, self.buf.v_new, k_pool, v_pool,
+                                      block_table, seq_lens, self.max_seq_len, self.buf.workspace,
+                                      q_head_begin=self.q_begin, flags=flags, stream=stream)
+        else:
+            hetis.attn_partial(self.cshape, self.buf.q_shard, k_pool, v_pool, block_table, seq_lens,
+                               self.max_seq_len, self.buf.workspace, q_head_begin=self.q_begin, flags=flags,
+                               stream=stream)
+        hetis.attn_combine_peers(self.group, seq_lens, self.max_seq_len, self.buf.workspace, stream=stream)
+        hetis.peer_wait(self.group, stream=stream)
         return self.o_full
+
+    def step_peers(self, k_pool, v_pool, block_table, seq_lens, stream=None, flags: int = 0):
+        """The whole N > 1 step over peer memory: pull scatter, attention with the append, combine + gather,
+        closing wait (four kernels, no NCCL, no per-step host argument: graph-capturable)."""
+        self.scatter_peers(stream)
+        return self.attention_gather_peers(k_pool, v_pool, block_table, seq_lens, stream=stream, flags=flags)

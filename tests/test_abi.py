@@ -29,7 +29,7 @@ def declared_symbols():
 
 def test_every_declared_symbol_is_exported(L):
     syms = declared_symbols()
-    assert len(syms) == 32
+    assert len(syms) == 34
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(hetis.EXPORTED)
@@ -45,7 +45,7 @@ def test_exported_symbols_match_nm():
 def test_status_strings_and_constants(L):
     for code, name in hetis.STATUS.items():
         assert hetis.status_str(code) == name
-    assert hetis.abi_version() == 1
+    assert hetis.abi_version() == 2
     assert hetis.split_tokens() % 16 == 0
 
 
@@ -253,3 +253,39 @@ def test_seq_split_entry_points_validate(L):
                                        vp_(0)) == 1
     assert L.hetis_seq_broadcast_q(ctypes.byref(s), vp_(1234), 2, 3, 0, 4, vp_(256), vp_(512), vp_(768),
                                    vp_(0)) == 1
+
+
+# ------------------------------------------------------------------ peer-memory exchange group (no launch)
+def _group(plan, rank=0, root=0, gather_root=-1, states=None, outs=None, stride=None, root_bufs=None):
+    n = plan.num_devices
+    states = states if states is not None else [0x100000 * (p + 1) for p in range(n)]
+    outs = outs if outs is not None else [0x4000000 * (p + 1) for p in range(n)]
+    root_bufs = root_bufs if root_bufs is not None else (0x7000000, 0x7100000, 0x7200000)
+    stride = stride if stride is not None else plan.shape.num_q_heads * plan.shape.head_dim
+    return hetis.PeerGroup(plan, rank, root, gather_root, states, outs, stride, *root_bufs)
+
+
+def test_peer_state_bytes(L):
+    assert hetis.peer_state_bytes() == 512
+
+
+def test_peer_group_validation(L):
+    p = hetis.plan_create(SHAPE_13B, 5, [16, 8, 8, 4, 4])
+    g = _group(p, rank=3)                                   # valid: no launch, pointers only recorded
+    assert g.handle.value
+    g2 = _group(p, rank=2, gather_root=0, outs=[0x4000000, None, None, None, None])   # only the receiver's o_full
+    assert g2.handle.value
+    bad = [dict(rank=5), dict(root=-1), dict(gather_root=5), dict(gather_root=-2),
+           dict(states=[0x100000, 0, 0x300000, 0x400000, 0x500000]),             # NULL state
+           dict(states=[0x100008, 0x200000, 0x300000, 0x400000, 0x500000]),      # state not 64-B aligned
+           dict(outs=[0x4000000, None, 0x4000000, 0x4000000, 0x4000000]),         # a receiver without o_full
+           dict(stride=40 * 128 - 1),                                            # stride below H * d
+           dict(root_bufs=(0x7000004, 0x7100000, 0x7200000))]                     # misaligned root q
+    for kw in bad:
+        with pytest.raises(hetis.HetisError) as ei:
+            _group(p, **kw)
+        assert ei.value.name == "HETIS_E_INVALID", kw
+    pr = hetis.plan_create(SHAPE_70B, 2, [64, 0, 32, 32], per_request=True, num_seqs=2)
+    with pytest.raises(hetis.HetisError) as ei:
+        _group(pr)
+    assert ei.value.name == "HETIS_E_UNSUPPORTED"

@@ -1,19 +1,24 @@
-"""Fused combine + all-gather over peer memory (hetis_attn_combine_peers), two ranks.
+"""The N > 1 step over peer memory -- hetis_scatter_pull -> hetis_attn_partial_append ->
+hetis_attn_combine_peers -> hetis_peer_wait -- run by N processes.
 
-Only one GPU is reachable, so the two ranks are two processes on cuda:0 that map
-each other's o_full and signal arrays through CUDA IPC (torch.multiprocessing
-shares CUDA tensors that way) -- the same peer-pointer code path an 8-GPU box
-uses over NVLink, with the data staying on one device.  Each rank runs its own
-heads' attention and stores every merged row into BOTH ranks' o_full at the
-global head index (Eq. 2a Concat), then publishes the epoch.
-Host barriers order the two processes (kernels of two processes time-slice on
-one GPU, so no kernel spin-waits on the other process); hetis_peer_wait runs
-after the barrier and must see both signals.  Both ranks must end with the
-single-device result, bit for bit.
+Only one GPU is reachable, so the N ranks are N processes on cuda:0 that map each
+other's exchange state and o_full, and the root's input buffers, through CUDA
+IPC (the same peer-pointer code path an 8-GPU NVSwitch box uses over NVLink,
+with the data staying on one device).  Nothing orders the processes on the host
+during the steps: every wait is the library's device-side epoch protocol
+(kernels of different processes time-slice on the GPU, so a spinning wait yields
+to the peer it waits for).  Several steps run eagerly, then more steps replayed
+from a captured CUDA graph (no per-step host argument); the root flips the sign
+of q before every step, so each step's O differs and a stale row would show.
+Every receiving rank must end with the single-device result of the final q, bit
+for bit (head-partition invariance; Eq. 2a Concat at the global
+head index), for even, uneven (16/8/8/4/4) and gather-to-root
+plans.
 """
 from __future__ import annotations
 
 import os
+import tempfile
 
 import pytest
 import torch
@@ -21,141 +26,106 @@ import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
 
-LENS = (300, 17, 1029, 2048, 5, 256)
+LENS = (300, 17, 1029, 2048, 5, 256, 1)
+EAGER_STEPS, GRAPH_STEPS, GRAPH_REPLAYS = 3, 2, 2
 
 
-def _rank(rank, split, shape_args, q_in, q_out, barrier, res):
-    import torch
-    from paper_2509_08309_b200 import hetis, workload
-    torch.cuda.set_device(0)
-    shape = workload.Shape(*shape_args)
-    lens = torch.tensor(LENS, dtype=torch.int32)
-    B, H, D = len(LENS), shape.num_q_heads, shape.head_dim
-    begin, count = sum(split[:rank]), split[rank]
-    o_full = torch.full((B, H, D), float("nan"), device="cuda")
-    sig = torch.zeros(2, dtype=torch.int64, device="cuda")
-    q_out.put((o_full, sig))                 # share my buffers with the peer (CUDA IPC)
-    peer_o, peer_sig = q_in.get(timeout=120)
-    o_peers = [o_full, peer_o] if rank == 0 else [peer_o, o_full]
-    s_peers = [sig, peer_sig] if rank == 0 else [peer_sig, sig]
-    b = workload.make_decode_batch(shape, lens, 13, "cuda", q_begin=begin, q_count=count, rank_salt=rank + 1)
-    s = hetis.make_shape(shape)
-    hetis.kv_append(s, b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens)
-    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, count, b.max_seq_len), "cuda")
-    for epoch in (1, 2):
-        hetis.attn_partial(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, b.max_seq_len, ws,
-                           q_head_begin=begin)
-        hetis.attn_combine_peers(s, b.seq_lens, b.max_seq_len, o_peers, s_peers, rank, epoch, ws,
-                                 q_head_begin=begin, q_head_count=count)
-        torch.cuda.synchronize()
-        barrier.wait(timeout=120)            # both ranks' stores and signals are done
-        hetis.peer_wait(sig, epoch)          # stream-ordered acquire; both signals already >= epoch
-        torch.cuda.synchronize()
-        got = o_full.clone()
-        barrier.wait(timeout=120)
-    # single-device reference on this process (all heads, the same generated data per kv head)
-    full = workload.make_decode_batch(shape, lens, 13, "cuda")
-    hetis.kv_append(s, full.k_new, full.v_new, full.k_pool, full.v_pool, full.block_table, full.seq_lens)
-    wsf = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, H, full.max_seq_len), "cuda")
-    ref = torch.empty((B, H, D), device="cuda")
-    hetis.attn_decode(s, full.q, full.k_pool, full.v_pool, full.block_table, full.seq_lens, full.max_seq_len, ref,
-                      wsf)
-    torch.cuda.synchronize()
-    res.put((rank, bool(torch.equal(got, ref)), float((got - ref).abs().nan_to_num(1e9).max()),
-             int(sig.cpu().min())))
-    barrier.wait(timeout=120)                # keep the shared buffers alive until both ranks are done
-
-
-@pytest.mark.parametrize("shape_args,split", [((64, 8, 128, 16, "bf16"), (48, 16)),
-                                              ((40, 40, 128, 16, "bf16"), (24, 16))])
-def test_combine_peers_two_ranks_one_gpu(shape_args, split):
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
-    ctx = mp.get_context("spawn")
-    a2b, b2a, res = ctx.Queue(), ctx.Queue(), ctx.Queue()
-    barrier = ctx.Barrier(2)
-    ps = [ctx.Process(target=_rank, args=(0, split, shape_args, b2a, a2b, barrier, res)),
-          ctx.Process(target=_rank, args=(1, split, shape_args, a2b, b2a, barrier, res))]
-    for p in ps:
-        p.start()
-    out = [res.get(timeout=600) for _ in ps]
-    for p in ps:
-        p.join(timeout=120)
-        assert p.exitcode == 0
-    for rank, equal, diff, sig_min in out:
-        assert sig_min == 2, (rank, sig_min)
-        assert equal, (rank, diff)
-
-
-# ------------------------------------------------------------------ pull-based scatter over peer memory
-def _pull_rank(rank, port, shape_args, split, res, barrier):
-    import os
+def _rank(rank, world, rendezvous, shape_args, split, gather_root, res):
     import torch
     import torch.distributed as dist
     from paper_2509_08309_b200 import hetis, workload
     from paper_2509_08309_b200.step import DecodeStep
-    # object exchange only (data moves by IPC); a file rendezvous needs no free TCP port
-    dist.init_process_group("gloo", init_method="file://" + port, rank=rank, world_size=2)
+    dist.init_process_group("gloo", init_method="file://" + rendezvous, rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
+        dev = torch.device("cuda", 0)
         shape = workload.Shape(*shape_args)
-        B, H, Hkv, D = 7, shape.num_q_heads, shape.num_kv_heads, shape.head_dim
-        plan = hetis.plan_create(hetis.make_shape(shape), 2, split)
-        step = DecodeStep(shape, plan, rank, B, 512, torch.device("cuda", 0))
-        g = torch.Generator(device="cuda").manual_seed(3)
-        mk = lambda *sz: torch.randn(sz, generator=g, device="cuda").to(shape.torch_dtype)
-        q_full, k_full, v_full = mk(B, H, D), mk(B, Hkv, D), mk(B, Hkv, D)   # same bits on both ranks
-        o_full = torch.zeros((B, H, D), device="cuda")
+        lens = torch.tensor(LENS, dtype=torch.int32)
+        B, H, D = len(LENS), shape.num_q_heads, shape.head_dim
+        plan = hetis.plan_create(hetis.make_shape(shape), world, split)
+        begin, count = plan.heads(rank)
+        mine = workload.make_decode_batch(shape, lens, 13, dev, q_begin=begin, q_count=count, rank_salt=rank + 1)
+        full = workload.make_decode_batch(shape, lens, 13, dev)       # the unsplit problem (reference + root inputs)
+        step = DecodeStep(shape, plan, rank, B, int(lens.max()), dev)
+        receives = gather_root < 0 or gather_root == rank
+        o_full = torch.full((B, H, D), float("nan"), device=dev) if receives else None
         if rank == 0:
-            step.setup_peers(o_full, q_full, k_full, v_full)
+            q_full, kn_full, vn_full = full.q.clone(), full.k_new.clone(), full.v_new.clone()
+            step.setup_peers(o_full, q_full, kn_full, vn_full, gather_root=gather_root)
         else:
-            step.setup_peers(o_full)
-        ok = True
-        for epoch in (1, 2):
+            step.setup_peers(o_full, gather_root=gather_root)
+
+        def one_step():
             if rank == 0:
-                q_full.mul_(-1)                      # new inputs for this step, then signal
-                k_full.mul_(-1)
-                v_full.mul_(-1)
-                hetis.peer_signal(step.qsig_peers, 0, epoch)
-                torch.cuda.synchronize()
-            else:
-                q_full.mul_(-1)
-                k_full.mul_(-1)
-                v_full.mul_(-1)
-            barrier.wait(timeout=120)                # the root's signal is published before anyone pulls
-            step.buf.q_shard.zero_()
-            step.buf.k_new.zero_()
-            step.buf.v_new.zero_()
-            step.scatter_peers(epoch)
-            torch.cuda.synchronize()
-            b, x = plan.heads(rank)
-            r = shape.r
-            ok &= torch.equal(step.buf.q_shard, q_full[:, b:b + x])
-            ok &= torch.equal(step.buf.k_new, k_full[:, b // r:(b + x) // r])
-            ok &= torch.equal(step.buf.v_new, v_full[:, b // r:(b + x) // r])
-            ok &= int(step.qsig[0].item()) == epoch
-            barrier.wait(timeout=120)                # nobody changes the root's buffers while others pull
-        res.put((rank, bool(ok)))
-        barrier.wait(timeout=120)
+                q_full.neg_()                   # the step's new inputs, written before the root's pull
+            step.step_peers(mine.k_pool, mine.v_pool, mine.block_table, mine.seq_lens)
+
+        for _ in range(EAGER_STEPS):
+            one_step()
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(graph, stream=s):
+                for _ in range(GRAPH_STEPS):
+                    one_step()
+        torch.cuda.current_stream().wait_stream(s)
+        for _ in range(GRAPH_REPLAYS):
+            graph.replay()
+        torch.cuda.synchronize()
+        n_steps = EAGER_STEPS + GRAPH_STEPS * GRAPH_REPLAYS
+        got = o_full.clone() if receives else None
+        dist.barrier()                          # every rank is done writing into peers' o_full
+        # reference: the unsplit problem with the final q, same launch (append fused) on this process
+        cs = hetis.make_shape(shape)
+        if n_steps % 2:
+            full.q.neg_()
+        ws = hetis.alloc_workspace(hetis.attn_decode_workspace(cs, B, H, int(lens.max())), dev)
+        ref = torch.empty((B, H, D), device=dev)
+        hetis.attn_decode_append(cs, full.q, full.k_new, full.v_new, full.k_pool, full.v_pool, full.block_table,
+                                 full.seq_lens, int(lens.max()), ref, ws)
+        torch.cuda.synchronize()
+        state = step.peer_state.cpu()
+        ok_eq = bool(torch.equal(got, ref)) if receives else True
+        diff = float((got - ref).abs().nan_to_num(1e9).max()) if receives else 0.0
+        # this rank's own shard of the last step went through the pull: bit-exact copy of the root's range
+        r = shape.r
+        q_last = full.q[:, begin:begin + count]
+        ok_pull = bool(torch.equal(step.buf.q_shard, q_last)) and bool(
+            torch.equal(step.buf.k_new, full.k_new[:, begin // r:(begin + count) // r]))
+        res.put((rank, receives, ok_eq, diff, ok_pull, int(state[0]), n_steps))
+        dist.barrier()                          # keep the shared buffers alive until everyone has compared
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("shape_args,split", [((64, 8, 128, 16, "bf16"), (48, 16)),
-                                              ((40, 40, 128, 16, "bf16"), (24, 16))])
-def test_scatter_pull_two_ranks_one_gpu(shape_args, split):
+CASES = [
+    ((64, 8, 128, 16, "bf16"), (32, 32), -1),                 # even GQA, all-gather
+    ((40, 40, 128, 16, "bf16"), (16, 8, 8, 4, 4), -1),        # c4's uneven split, all-gather
+    ((64, 8, 128, 16, "bf16"), (16, 16, 24, 8), 0),           # uneven GQA, gather to the Primary (paper)
+    ((8, 8, 64, 16, "f32"), (4, 4), -1),                      # c1 shape, fp32
+]
+
+
+@pytest.mark.parametrize("shape_args,split,gather_root", CASES)
+def test_peer_step_n_ranks_one_gpu(shape_args, split, gather_root):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    import tempfile
-    port = os.path.join(tempfile.mkdtemp(), "rendezvous")
+    world = len(split)
+    rendezvous = os.path.join(tempfile.mkdtemp(), "rendezvous")
     ctx = mp.get_context("spawn")
-    res, barrier = ctx.Queue(), ctx.Barrier(2)
-    ps = [ctx.Process(target=_pull_rank, args=(r, port, shape_args, split, res, barrier)) for r in range(2)]
+    res = ctx.Queue()
+    ps = [ctx.Process(target=_rank, args=(r, world, rendezvous, shape_args, split, gather_root, res))
+          for r in range(world)]
     for p in ps:
         p.start()
-    out = [res.get(timeout=600) for _ in ps]
+    out = [res.get(timeout=900) for _ in ps]
     for p in ps:
         p.join(timeout=120)
         assert p.exitcode == 0
-    for rank, ok in out:
-        assert ok, rank
+    for rank, receives, ok_eq, diff, ok_pull, steps_done, n_steps in out:
+        assert steps_done == n_steps, (rank, steps_done)
+        assert ok_pull, rank
+        assert ok_eq, (rank, diff)
+    assert sum(o[1] for o in out) == (world if gather_root < 0 else 1)
