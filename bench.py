@@ -5,16 +5,26 @@
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 One step = one layer's decode step for the whole batch on every rank:
-    [N > 1] hetis_scatter_q (NCCL)  -> hetis_kv_append -> hetis_attn_partial
-    -> hetis_attn_combine -> [N > 1] hetis_gather (NCCL all-gather of O)
+    N = 1:  hetis_attn_partial_append (kv_append fused) -> hetis_attn_combine
+    N > 1 (default, --exchange peer): hetis_scatter_pull (the rank's q / new k, v
+            straight from the Primary's buffers over NVLink) -> hetis_attn_partial_append
+            -> hetis_attn_combine_peers (the combine storing every O row into every
+            rank's o_full) -> hetis_peer_wait;  --exchange nccl: hetis_scatter_q ->
+            ... -> hetis_attn_combine -> hetis_gather (NCCL over NVLink)
 Metric (BASELINE.json): decode attention tokens/s (= batch / step time, one
-layer, all heads) and achieved HBM GB/s of the dominant kernel (% of the
-measured copy peak).  Default workload: config c2 (LLaMA2-13B, 40 heads x 128,
-batch 64, context 4096, bf16 paged KV) -- BASELINE.json configs[1]; at N > 1 the
-40 heads are partitioned over the ranks (strong scaling, same total problem).
+layer, all heads, max over ranks) and achieved HBM GB/s of the dominant kernel
+(% of the measured copy peak).  Default workload: config c2 (LLaMA2-13B, 40
+heads x 128, batch 64, context 4096, bf16 paged KV) -- BASELINE.json configs[1];
+at N > 1 the heads are partitioned over the ranks (strong scaling, same total
+problem).  A sub-record for c3 (LLaMA2-70B GQA, the config the >= 6x scaling
+target is stated on) is measured in the same run and printed inside the line.
+
+After timing, the step is run once more and rank 0 checks the gathered O against
+the fp64 oracle (every element) and against the unsplit single-device result
+(bit for bit); a mismatch exits with rc 3.
 
 Rank 0 prints ONE JSON line.  `--impl reference` times the fp64 CPU oracle
-(oracle/, the only reference this tier has) on the same workload shape.
+(oracle/, the only reference this tier has) on the same workload.
 """
 from __future__ import annotations
 
@@ -37,6 +47,7 @@ from paper_2509_08309_b200 import accounting, workload  # noqa: E402
 L2_BYTES = 126 * 1024 * 1024
 METRIC = "decode attention tokens/s and achieved HBM GB/s (% of peak) at 1/2/4/8 B200"
 UNIT = "tokens/s"
+ATOL, RTOL = 2e-3, 1e-2
 
 
 def parse():
@@ -45,24 +56,26 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c2", choices=sorted(workload.CONFIGS))
+    ap.add_argument("--sub-config", default="auto",
+                    help="second workload measured in the same run ('auto': c3 unless --config is c3; 'none')")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-seqs", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the post-timing oracle / unsplit check")
     ap.add_argument("--o-dtype", default="f32", choices=["f32", "bf16"])
     ap.add_argument("--attn-flags", type=int, default=0, help="HETIS_ATTN_* flags (diagnostics)")
-    ap.add_argument("--graph", type=int, default=1, help="N = 1: replay the K timed steps as one CUDA graph")
-    ap.add_argument("--gather", default="nccl", choices=["nccl", "peer"],
-                    help="N > 1: NCCL all-gather of O (default) or the combine kernel's peer-memory stores")
+    ap.add_argument("--graph", type=int, default=1, help="replay the K timed steps as one CUDA graph")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: peer-memory scatter/gather kernels (default) or NCCL scatter_q / gather")
+    ap.add_argument("--gather-root", type=int, default=-1,
+                    help="-1: every rank receives O (all-gather); r >= 0: only rank r (gather to the Primary)")
     ap.add_argument("--fused-append", type=int, default=1,
                     help="1: kv_append fused into the attention kernel (hetis_attn_partial_append); 0: separate")
     ap.add_argument("--force-dist", action="store_true",
-                    help="debug: run the N > 1 code path (NCCL process group, scatter, gather) at N = 1")
-    ap.add_argument("--graph-dist", type=int, default=1,
-                    help="N > 1: replay the timed steps as a CUDA graph too (NCCL calls captured; not with the "
-                         "peer-memory exchanges, whose epochs change every step)")
-    ap.add_argument("--scatter", default="nccl", choices=["nccl", "peer"],
-                    help="N > 1: 'peer' = every rank pulls its q / new k, v shard from the root's buffers over "
-                         "NVLink (hetis_peer_signal + hetis_scatter_pull) instead of NCCL send/recv")
+                    help="debug: run the N > 1 code path (process group, exchanges) at N = 1")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="debug: every rank on cuda:0 with a gloo bootstrap group (correctness of the N > 1 peer "
+                         "path on a one-GPU box; timings are meaningless)")
     return ap.parse_args()
 
 
@@ -83,15 +96,26 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def traffic_from_profiles(workload_name: str):
+def traffic_from_profiles(key: str):
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        v = d.get(workload_name)
+        v = d.get(key)
         return None if v is None else float(v)
     except Exception:
         return None
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 # ---------------------------------------------------------------- clocks sampled during the timed region
@@ -149,26 +173,37 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU oracle timing
-def cpu_oracle_sample(cfg: workload.Config, split, rank: int, n_seqs: int):
-    """Time the fp64 oracle (as it stands) on a CPU-generated batch of the workload's first n_seqs requests,
-    all of this rank's heads, at the workload's lengths.  Returns (tokens/s, seconds, cores, sample text)."""
+def cpu_oracle_sample(cfg: workload.Config, n_seqs: int, budget_s: float = 20.0):
+    """Time the fp64 oracle (as it stands) on a CPU-generated batch of the workload's first n_seqs requests
+    and ALL heads, at the workload's lengths: once on all host cores and once on one thread (the one-thread
+    run on fewer requests if the all-core time says it would exceed budget_s)."""
     import oracle
-    lens = cfg.seq_lens()[:n_seqs]
-    begin = sum(split[:rank])
-    b = workload.make_decode_batch(cfg.shape, lens, cfg.seed, "cpu", q_begin=begin, q_count=split[rank],
-                                   rank_salt=rank)
-    h = {k: workload.to_numpy_bits(getattr(b, k)).copy() for k in ("q", "k_new", "v_new", "k_pool", "v_pool")}
-    bt = b.block_table.numpy()
-    sl = b.seq_lens.numpy()
     cores = len(os.sched_getaffinity(0))
+    lens_all = cfg.seq_lens()
     dt = oracle.BF16 if cfg.shape.dtype == "bf16" else oracle.F32
-    t0 = time.perf_counter()
-    oracle.kv_append(h["k_new"], h["v_new"], h["k_pool"], h["v_pool"], bt, sl)
-    oracle.decode(h["q"], h["k_pool"], h["v_pool"], bt, sl, num_kv_heads=b.kv_count, dtype=dt, nthreads=cores)
-    sec = time.perf_counter() - t0
-    sample = (f"{n_seqs} of {cfg.batch} requests x {split[rank]} heads at the workload's lengths "
-              f"(sum L = {int(lens.sum())}), kv_append + fp64 oracle decode, {cores} threads")
-    return n_seqs / sec, sec, cores, sample
+
+    def timed(n, threads):
+        lens = lens_all[:n]
+        b = workload.make_decode_batch(cfg.shape, lens, cfg.seed, "cpu")
+        h = {k: workload.to_numpy_bits(getattr(b, k)).copy() for k in ("q", "k_new", "v_new", "k_pool", "v_pool")}
+        bt, sl = b.block_table.numpy(), b.seq_lens.numpy()
+        t0 = time.perf_counter()
+        oracle.kv_append(h["k_new"], h["v_new"], h["k_pool"], h["v_pool"], bt, sl)
+        oracle.decode(h["q"], h["k_pool"], h["v_pool"], bt, sl, num_kv_heads=cfg.shape.num_kv_heads, dtype=dt,
+                      nthreads=threads)
+        return time.perf_counter() - t0, int(lens.sum())
+
+    n = min(n_seqs, cfg.batch)
+    sec_all, tok_all = timed(n, cores)
+    n1 = max(1, min(n, int(n * budget_s / max(sec_all * cores, 1e-9))))
+    sec_1, tok_1 = timed(n1, 1)
+    return {"value": n / sec_all, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": (f"{n} of {cfg.batch} requests x {cfg.shape.num_q_heads} heads at the workload's lengths "
+                       f"(sum L = {tok_all}), kv_append + fp64 oracle decode, {cores} threads; one-thread run on "
+                       f"{n1} requests (sum L = {tok_1})"),
+            "value_1thread": n1 / sec_1, "cpu_model": cpu_model(),
+            "gbs_all_cores": tok_all * cfg.shape.num_kv_heads * cfg.shape.head_dim * 2 * cfg.shape.elem_bytes
+            / sec_all / 1e9}
 
 
 def run_reference(args, world, rank, budget_s: float = 150.0):
@@ -178,7 +213,6 @@ def run_reference(args, world, rank, budget_s: float = 150.0):
     cfg = workload.CONFIGS[args.config]
     if rank != 0:
         return 0
-    split = cfg.head_split(1)
     n_max = min(args.cpu_sample_seqs, cfg.batch)
     lens = cfg.seq_lens()[:n_max]
     b = workload.make_decode_batch(cfg.shape, lens, cfg.seed, "cpu")
@@ -202,7 +236,7 @@ def run_reference(args, world, rank, budget_s: float = 150.0):
     times = [run(n) for _ in range(max(args.steps, 1))]
     sec = sum(times) / len(times)
     value = n / sec
-    sample = (f"{n} of {cfg.batch} requests x {split[0]} heads at the workload's lengths "
+    sample = (f"{n} of {cfg.batch} requests x {cfg.shape.num_q_heads} heads at the workload's lengths "
               f"(sum L = {int(sl[:n].sum())}), fp64 oracle decode, {cores} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -210,7 +244,7 @@ def run_reference(args, world, rank, budget_s: float = 150.0):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.description}", "batch_sampled": n, "batch": cfg.batch},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": sample + " per step"},
+                         "sample": sample + " per step", "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -219,36 +253,51 @@ def run_reference(args, world, rank, budget_s: float = 150.0):
 
 
 # ---------------------------------------------------------------- our arm
-def run_ours(args, world, rank, local):
+class Dist:
+    """Process-group plumbing: barrier, max over ranks, object broadcast (NCCL, or gloo with --share-gpu)."""
+
+    def __init__(self, active: bool, world: int, local: int, device, backend: str):
+        self.active, self.world, self.local, self.device, self.backend = active, world, local, device, backend
+
+    def barrier(self):
+        if self.active:
+            import torch.distributed as dist
+            if self.backend == "nccl":
+                dist.barrier(device_ids=[self.local])
+            else:
+                dist.barrier()
+        torch.cuda.synchronize(self.device)
+
+    def max(self, x: float) -> float:
+        if not self.active or self.world == 1:
+            return x
+        import torch.distributed as dist
+        dev = self.device if self.backend == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if not self.active or self.world == 1:
+            return x
+        import torch.distributed as dist
+        dev = self.device if self.backend == "nccl" else "cpu"
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+
+def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headline: bool):
+    """Time cfg_name's step on this rank's share; returns the record (meaningful on rank 0)."""
     from paper_2509_08309_b200 import hetis
     from paper_2509_08309_b200.step import DecodeStep
 
-    if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    device = torch.device("cuda", local)
-    cfg = workload.CONFIGS[args.config]
+    device = D.device
+    cfg = workload.CONFIGS[cfg_name]
     shape = cfg.shape
     split = cfg.head_split(world)
-    comm_ptr = None
-    pg = None
-    dist_mode = world > 1 or args.force_dist
-    if dist_mode:
-        import torch.distributed as dist
-        if world == 1:
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            if "MASTER_PORT" not in os.environ:
-                import socket
-                so = socket.socket()
-                so.bind(("127.0.0.1", 0))
-                os.environ["MASTER_PORT"] = str(so.getsockname()[1])
-                so.close()
-            os.environ.setdefault("RANK", "0")
-            os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", device_id=device)
-        pg = dist.group.WORLD
-        dist.barrier()
-        comm_ptr = pg._get_backend(device)._comm_ptr()
+    dist_mode = D.active
+    peer = dist_mode and args.exchange == "peer"
     B = cfg.batch
     seq_lens = cfg.seq_lens()
     max_len = int(seq_lens.max())
@@ -257,28 +306,31 @@ def run_ours(args, world, rank, local):
     q_begin, q_count = plan.heads(rank)
     batch = workload.make_decode_batch(shape, seq_lens, cfg.seed, device, q_begin=q_begin, q_count=q_count,
                                        rank_salt=rank)
-    step = DecodeStep(shape, plan, rank, B, max_len, device, o_dtype=args.o_dtype, comm_ptr=comm_ptr)
+    step = DecodeStep(shape, plan, rank, B, max_len, device, o_dtype=args.o_dtype,
+                      comm_ptr=comm_ptr if (dist_mode and not peer) else None)
     kv_bytes_rank = accounting.step_bytes(seq_lens.tolist(), q_count, shape.r, shape.head_dim, shape.page_size,
                                           shape.elem_bytes, shape.elem_bytes, 4).kv
     # rotate layer pools so the per-step KV stream never sits in L2
     n_layers = max(1, math.ceil(4 * L2_BYTES / max(kv_bytes_rank, 1)))
     free = torch.cuda.mem_get_info(device)[0]
     pool_bytes = 2 * batch.k_pool.numel() * batch.k_pool.element_size()
-    n_layers = max(1, min(n_layers, int(0.6 * free // max(pool_bytes, 1)) + 1))
+    n_layers = max(1, min(n_layers, int(0.5 * free // max(pool_bytes * (world if args.share_gpu else 1), 1)) + 1))
     k_pools = [batch.k_pool] + [batch.k_pool.clone() for _ in range(n_layers - 1)]
     v_pools = [batch.v_pool] + [batch.v_pool.clone() for _ in range(n_layers - 1)]
     odt = torch.bfloat16 if args.o_dtype == "bf16" else torch.float32
     is_root = rank == 0
+    gather_root = args.gather_root
+    receives = gather_root < 0 or gather_root == rank
+    q_full = kn_full = vn_full = None
     if dist_mode:
-        gq = torch.Generator(device=device).manual_seed(cfg.seed + 17)
-        q_full = workload.make_q(shape, B, cfg.seed, device) if is_root else None
-        kn_full = (torch.randn((B, shape.num_kv_heads, shape.head_dim), generator=gq, device=device)
-                   .to(shape.torch_dtype) if is_root else None)
-        vn_full = (torch.randn((B, shape.num_kv_heads, shape.head_dim), generator=gq, device=device)
-                   .to(shape.torch_dtype) if is_root else None)
-        o_full = torch.empty((B, shape.num_q_heads, shape.head_dim), dtype=odt, device=device)
-        if args.gather == "peer" or args.scatter == "peer":
-            step.setup_peers(o_full, q_full, kn_full, vn_full)
+        if is_root:     # the Primary holds the step's inputs for every head (the logical problem's q, new k, v)
+            q_full = workload.make_q(shape, B, cfg.seed, device)
+            kn_full, vn_full = workload.make_new_rows(shape, seq_lens, cfg.seed, device)
+        o_full = torch.empty((B, shape.num_q_heads, shape.head_dim), dtype=odt, device=device) if receives else None
+        if peer:
+            step.setup_peers(o_full, q_full, kn_full, vn_full, gather_root=gather_root)
+        elif o_full is None:
+            o_full = torch.empty((B, shape.num_q_heads, shape.head_dim), dtype=odt, device=device)
     else:
         step.buf.q_shard.copy_(batch.q)
         step.buf.k_new.copy_(batch.k_new)
@@ -286,138 +338,143 @@ def run_ours(args, world, rank, local):
         o_full = step.buf.o_shard
     stream = torch.cuda.current_stream(device)
 
-    def one_step(i, ev_a=None, ev_b=None):
-        li = i % n_layers
-        if dist_mode and (args.gather == "peer" or args.scatter == "peer"):
-            step.epoch += 1
-        if dist_mode and args.scatter == "peer":
-            step.scatter_peers(step.epoch)
-        elif dist_mode:
-            step.scatter(q_full, kn_full, vn_full)
-        if not args.fused_append:
-            step.append(k_pools[li], v_pools[li], batch.block_table, batch.seq_lens)
-        if ev_a is not None:
-            ev_a.record(torch.cuda.current_stream(device))
+    def attention(li):
         if args.fused_append:   # the append happens inside the attention kernel
             hetis.attn_partial_append(step.cshape, step.buf.q_shard, step.buf.k_new, step.buf.v_new, k_pools[li],
                                       v_pools[li], batch.block_table, batch.seq_lens, max_len, step.buf.workspace,
                                       q_head_begin=q_begin, flags=args.attn_flags)
         else:
+            step.append(k_pools[li], v_pools[li], batch.block_table, batch.seq_lens)
             hetis.attn_partial(step.cshape, step.buf.q_shard, k_pools[li], v_pools[li], batch.block_table,
                                batch.seq_lens, max_len, step.buf.workspace, q_head_begin=q_begin,
                                flags=args.attn_flags)
-        if ev_b is not None:
-            ev_b.record(torch.cuda.current_stream(device))
-        if dist_mode and args.gather == "peer":
-            # one kernel merges the splits and stores O into every rank's o_full over NVLink
-            hetis.attn_combine_peers(step.cshape, batch.seq_lens, max_len, step.o_peers, step.sig_peers, rank,
-                                     step.epoch, step.buf.workspace, q_head_begin=q_begin, q_head_count=q_count)
-            hetis.peer_wait(step.sig, step.epoch)
-            return
-        hetis.attn_combine(step.cshape, batch.seq_lens, max_len, step.buf.o_shard, step.buf.workspace,
-                           q_head_count=q_count)
-        if dist_mode:
-            step.gather(o_full, root=-1)
 
-    def barrier():
-        if dist_mode:
-            import torch.distributed as dist
-            dist.barrier(device_ids=[local])
-        torch.cuda.synchronize(device)
-
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    def one_step(i, ev=None):
+        """ev: optional 5 events recorded between the phases (scatter | attention | combine(+gather) | wait)."""
+        li = i % n_layers
+        rec = (lambda k: ev[k].record(torch.cuda.current_stream(device))) if ev is not None else (lambda k: None)
+        rec(0)
+        if peer:
+            step.scatter_peers()
+        elif dist_mode:
+            step.scatter(q_full, kn_full, vn_full)
+        rec(1)
+        attention(li)
+        rec(2)
+        if peer:
+            hetis.attn_combine_peers(step.group, batch.seq_lens, max_len, step.buf.workspace)
+            rec(3)
+            hetis.peer_wait(step.group)
+        else:
+            hetis.attn_combine(step.cshape, batch.seq_lens, max_len, step.buf.o_shard, step.buf.workspace,
+                               q_head_count=q_count)
+            rec(3)
+            if dist_mode:
+                step.gather(o_full, root=gather_root)
+        rec(4)
 
     # ---- warm-up
     for i in range(args.warmup):
         one_step(i)
-    barrier()
+    D.barrier()
 
-    # ---- timed: K steps, CUDA events on the launching stream.  At N = 1 the K steps
-    # are captured once into a CUDA graph (the same kernels, no host launch gaps) and
-    # the graph is replayed once inside the timed region; per-step events are graph nodes.
-    sampler = ClockSampler(local)
-    # external=True: inside a capture the records become event-record graph nodes
-    # N > 1: only the NCCL exchanges can be captured -- the peer-memory ones carry a per-step epoch
-    use_graph = bool(args.graph) and (not dist_mode or (bool(args.graph_dist) and args.gather == "nccl"
-                                                         and args.scatter == "nccl"))
-    evs_a = [torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(args.steps)]
-    evs_b = [torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(args.steps)]
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launch_mode = "eager"
-    # At N = 1 the K timed steps are captured as CUDA graphs: graph A (the headline
-    # number) has no nodes between the kernels, so programmatic dependent launch
-    # overlaps each kernel's prologue with its predecessor; graph B is the same K
-    # steps with event nodes around every attention kernel (per-launch durations
-    # for the roofline), replayed in a second timed region.
-    graph = graph_ev = None
+    # ---- graphs: A = the K timed steps (no nodes between kernels: programmatic dependent launch overlaps
+    # each kernel's prologue with its predecessor); B = the same steps with event nodes between the phases
+    # (per-phase times); C = K attention launches alone (the dominant kernel's duration for the roofline,
+    # with the same PDL overlap as in A).
+    use_graph = bool(args.graph)
+    evs = [[torch.cuda.Event(enable_timing=True, external=use_graph) for _ in range(5)] for _ in range(args.steps)]
+    graph = graph_ev = graph_attn = None
     graph_launches = 0
+    launch_mode = "eager"
     if use_graph:
         try:
             graph = torch.cuda.CUDAGraph()
             c0 = hetis.launch_count()
-            with torch.cuda.graph(graph):
+            with torch.cuda.graph(graph, capture_error_mode="thread_local"):
                 for i in range(args.steps):
                     one_step(i)
             graph_launches = hetis.launch_count() - c0
             graph_ev = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph_ev):
+            with torch.cuda.graph(graph_ev, capture_error_mode="thread_local"):
                 for i in range(args.steps):
-                    one_step(i, evs_a[i], evs_b[i])
-            graph.replay()                      # untimed replays (warm instantiation)
-            graph_ev.replay()
+                    one_step(i, evs[i])
+            graph_attn = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph_attn, capture_error_mode="thread_local"):
+                for i in range(args.steps):
+                    attention(i % n_layers)
+            for g in (graph, graph_ev, graph_attn):   # untimed replays (warm instantiation)
+                g.replay()
             torch.cuda.synchronize(device)
-            launch_mode = "cuda_graph (PDL between kernels); roofline from a second replay with event nodes"
+            launch_mode = "cuda_graph (PDL between kernels)"
         except Exception as exc:               # capture unsupported: time eagerly instead
-            graph = graph_ev = None
-            launch_mode = f"eager (graph capture failed: {type(exc).__name__})"
-    barrier()
-    sampler.start()
+            import traceback
+            traceback.print_exc()
+            graph = graph_ev = graph_attn = None
+            launch_mode = f"eager (graph capture failed: {type(exc).__name__}: {exc})"
+            torch.cuda.synchronize(device)
+    D.barrier()
+    sampler = ClockSampler(device.index if not args.share_gpu else 0) if headline else None
+    if sampler:
+        sampler.start()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n0 = hetis.launch_count()
     start.record(stream)
     if graph is not None:
         graph.replay()
     else:
         for i in range(args.steps):
-            one_step(i, evs_a[i], evs_b[i])
+            one_step(i)
     end.record(stream)
     n1 = hetis.launch_count() + graph_launches
-    barrier()
-    if graph_ev is not None:
-        graph_ev.replay()
-        barrier()
-    sampler.stop()
-    elapsed_ms = max_over_ranks(start.elapsed_time(end))
-    attn_ms = sum(a.elapsed_time(b) for a, b in zip(evs_a, evs_b)) / args.steps
-    attn_ms_max = max_over_ranks(attn_ms)
+    D.barrier()
+    if sampler:
+        sampler.stop()
+    elapsed_ms = D.max(start.elapsed_time(end))
     launches = n1 - n0
+    launches_all = int(D.sum(launches))
     ms_per_step = elapsed_ms / args.steps
     value = B / (ms_per_step / 1e3)
 
-    # ---- end to end through the public API with pinned host buffers
-    h2d = d2h = 0
+    # per-phase times (evented replay) and the attention kernel alone
+    if graph_ev is not None:
+        graph_ev.replay()
+    else:
+        for i in range(args.steps):
+            one_step(i, evs[i])
+    D.barrier()
+    phase_names = ("scatter", "attention", "combine" + ("_gather" if peer else ""), "wait" if peer else "gather")
+    phases = {}
+    for k, name in enumerate(phase_names):
+        mean_ms = sum(e[k].elapsed_time(e[k + 1]) for e in evs) / args.steps
+        phases[name + "_us"] = D.max(mean_ms) * 1e3
+    evented_step_ms = D.max(sum(e[0].elapsed_time(e[4]) for e in evs) / args.steps)
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    if graph_attn is not None:
+        graph_attn.replay()
+    else:
+        for i in range(args.steps):
+            attention(i % n_layers)
+    a1.record(stream)
+    D.barrier()
+    attn_ms = a0.elapsed_time(a1) / args.steps
+    attn_ms_max = D.max(attn_ms)
+
+    # ---- end to end through the public API with pinned host buffers: every step copies its inputs in
+    # (the Primary's q / new k, v; every rank's seq_lens) and reads the result back (O on the receiver)
+    hsl = batch.seq_lens.cpu().pin_memory()
     if dist_mode:
         if is_root:
-            hq = q_full.cpu().pin_memory()
-            hk = kn_full.cpu().pin_memory()
-            hv = vn_full.cpu().pin_memory()
-            h2d = sum(t.numel() * t.element_size() for t in (hq, hk, hv))
-        ho = torch.empty_like(o_full, device="cpu").pin_memory() if is_root else None
-        d2h = o_full.numel() * o_full.element_size() if is_root else 0
+            hq, hk, hv = (t.cpu().pin_memory() for t in (q_full, kn_full, vn_full))
+        ho = torch.empty_like(o_full, device="cpu").pin_memory() if (receives and o_full is not None and (
+            is_root or gather_root >= 0)) else None
     else:
-        hq = batch.q.cpu().pin_memory()
-        hk = batch.k_new.cpu().pin_memory()
-        hv = batch.v_new.cpu().pin_memory()
+        hq, hk, hv = (t.cpu().pin_memory() for t in (batch.q, batch.k_new, batch.v_new))
         ho = torch.empty_like(o_full, device="cpu").pin_memory()
-        h2d = sum(t.numel() * t.element_size() for t in (hq, hk, hv))
-        d2h = o_full.numel() * o_full.element_size()
-    hsl = batch.seq_lens.cpu().pin_memory()
-    h2d += hsl.numel() * 4
+    h2d = hsl.numel() * 4 + (sum(t.numel() * t.element_size() for t in (hq, hk, hv)) if (is_root or not dist_mode)
+                             else 0)
+    d2h = 0 if ho is None else o_full.numel() * o_full.element_size()
 
     def e2e_step(i):
         if dist_mode:
@@ -435,13 +492,22 @@ def run_ours(args, world, rank, local):
             ho.copy_(o_full, non_blocking=True)
 
     e_steps = max(min(args.steps, 50), 3)
-    e_mode = "serial"
+    e_mode = "serial (copies in, step, O out, on the step's stream)"
+    for i in range(3):
+        e2e_step(i)
+    D.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(e_steps):
+        e2e_step(i)
+    e1.record(stream)
+    D.barrier()
+    e2e_ms = e0.elapsed_time(e1) / e_steps
     if not dist_mode:
         # Overlapped through the same public calls: step i's host->device copies run on a copy stream
-        # while step i-1 computes, and its device->host read on another stream while step i+1
-        # computes -- double-buffered device inputs / outputs and pinned host outputs.  Every step
-        # still moves its own inputs in and its own O out inside the timed region.
-        e_mode = "overlapped (double-buffered inputs/outputs, copy streams)"
+        # while step i-1 computes, and its device->host read on another stream while step i+1 computes --
+        # double-buffered device inputs / outputs and pinned host outputs.  Every step still moves its own
+        # inputs in and its own O out inside the timed region.  The faster of the two loops is reported.
         ins = [(step.buf.q_shard.clone(), step.buf.k_new.clone(), step.buf.v_new.clone(), batch.seq_lens.clone())
                for _ in range(2)]
         outs = [torch.empty_like(o_full) for _ in range(2)]
@@ -489,37 +555,35 @@ def run_ours(args, world, rank, local):
                 stream.wait_event(ev_out[k])
 
         run_overlapped(4)
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        run_overlapped(e_steps, e0)
-        e1.record(stream)
-        barrier()
-        # tiny steps (c1) are host-bound: the extra stream/event calls cost more than the overlap
-        # saves, so the plain serial loop is timed too and the faster of the two is reported
-        for i in range(3):
-            e2e_step(i)
-        barrier()
+        D.barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        for i in range(e_steps):
-            e2e_step(i)
+        run_overlapped(e_steps, f0)
         f1.record(stream)
-        barrier()
-        if f0.elapsed_time(f1) < e0.elapsed_time(e1):
-            e0, e1, e_mode = f0, f1, "serial (faster than the overlapped loop for this step size)"
-    else:
-        for i in range(3):
-            e2e_step(i)
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for i in range(e_steps):
-            e2e_step(i)
-        e1.record(stream)
-        barrier()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e_steps
+        D.barrier()
+        if f0.elapsed_time(f1) / e_steps < e2e_ms:
+            e2e_ms, e_mode = f0.elapsed_time(f1) / e_steps, "overlapped (double-buffered inputs/outputs, copy streams)"
+    e2e_ms = D.max(e2e_ms)
     e2e_value = B / (e2e_ms / 1e3)
+
+    # ---- parity of this run's result: one more step with O poisoned, then rank 0 compares the gathered
+    # O with the unsplit single-device result (bit for bit) and with the fp64 oracle (every element)
+    parity = None
+    if not args.no_parity:
+        D.barrier()
+        if o_full is not None:
+            o_full.fill_(float("nan"))
+        D.barrier()
+        if dist_mode and is_root:
+            q_full.copy_(hq)
+            kn_full.copy_(hk)
+            vn_full.copy_(hv)
+        batch.seq_lens.copy_(hsl)
+        one_step(0)
+        D.barrier()
+        if is_root:
+            parity = check_parity(cfg, args, o_full, device, dist_mode, gather_root)
+        D.barrier()
 
     # ---- roofline of the dominant kernel (split-KV partial attention) on this rank
     sb = accounting.step_bytes(seq_lens.tolist(), q_count, shape.r, shape.head_dim, shape.page_size,
@@ -530,49 +594,164 @@ def run_ours(args, world, rank, local):
         alg_bytes += 2 * 2 * B * (q_count // shape.r) * shape.head_dim * shape.elem_bytes
         kernel_name = "hetis_attn_partial_append (split-KV attention with kv_append fused)"
     achieved = alg_bytes / (attn_ms / 1e3) / 1e9
+    achieved_min = D.max(-achieved) * -1.0      # the slowest rank
     peak, peak_src = peaks()
-    clocks = sampler.summary()
-    traffic = traffic_from_profiles(f"{cfg.name}/N{world}")
+    rec = {
+        "workload": f"{cfg.name}: {cfg.description}", "value": value, "ms_per_step": ms_per_step,
+        "config": {
+            "workload": f"{cfg.name}: {cfg.description}", "batch": B, "seq_len": cfg.seq_len,
+            "seq_len_range": cfg.seq_len_range, "q_heads": shape.num_q_heads, "kv_heads": shape.num_kv_heads,
+            "head_dim": shape.head_dim, "page_size": shape.page_size, "split": list(split),
+            "o_dtype": args.o_dtype, "layers_rotated": n_layers,
+            "exchange": (args.exchange if dist_mode else None), "gather_root": (gather_root if dist_mode else None),
+            "fused_append": bool(args.fused_append),
+            "l2": f"inputs larger than L2: {n_layers} layer pool(s) x {kv_bytes_rank / 1e6:.1f} MB KV per rank "
+                  f"rotated per step (L2 = 126 MB)",
+            "tokens": "one token = one request's decode step of one layer, all heads"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic_from_profiles(f"{cfg.name}/N{world}"),
+                     "kernel": kernel_name, "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": attn_ms,
+                     "avg_launch_ms_max_rank": attn_ms_max, "achieved_slowest_rank": achieved_min,
+                     "launch_timing": "K attention launches replayed as one CUDA graph (PDL overlap as in the "
+                                      "timed steps), CUDA events around the replay on the launching stream",
+                     "peak_source": peak_src, "frac_of_8TBps_nominal": achieved / 8000.0},
+        "attention_only_tokens_per_s": B / (attn_ms_max / 1e3),
+        "phases_us": phases, "evented_step_us": evented_step_ms * 1e3,
+        "nvlink_us": ({k: v for k, v in phases.items() if k in ("scatter_us", "wait_us", "gather_us")}
+                      if dist_mode else None),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_ms, "mode": e_mode},
+        "gpu_launches": launches, "gpu_launches_all_ranks": launches_all,
+        "launch_mode": launch_mode,
+        "parity": parity,
+        "clocks": sampler.summary() if sampler else None,
+    }
+    del k_pools, v_pools, batch, step
+    torch.cuda.empty_cache()
+    return rec
 
+
+def check_parity(cfg: workload.Config, args, o_full, device, dist_mode: bool, gather_root: int) -> dict:
+    """Rank 0: the step's gathered O vs (a) the unsplit problem on this GPU (bit for bit: head partition does
+    not change an item's arithmetic) and (b) the fp64 oracle on every element."""
+    import numpy as np
+
+    import oracle
+    from paper_2509_08309_b200 import hetis
+    shape = cfg.shape
+    lens = cfg.seq_lens()
+    full = workload.make_decode_batch(shape, lens, cfg.seed, device)
+    host = {k: workload.to_numpy_bits(getattr(full, k)) for k in ("q", "k_new", "v_new", "k_pool", "v_pool")}
+    bt, sl = full.block_table.cpu().numpy(), full.seq_lens.cpu().numpy()
+    cs = hetis.make_shape(shape, args.o_dtype)
+    B, H, D = full.q.shape
+    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(cs, B, H, full.max_seq_len), device)
+    ref_gpu = torch.empty((B, H, D), dtype=o_full.dtype, device=device)
+    hetis.attn_decode_append(cs, full.q, full.k_new, full.v_new, full.k_pool, full.v_pool, full.block_table,
+                             full.seq_lens, full.max_seq_len, ref_gpu, ws, flags=args.attn_flags)
+    torch.cuda.synchronize(device)
+    bit_exact = bool(torch.equal(o_full, ref_gpu))
+    got = o_full.float().cpu().numpy().astype(np.float64)
+    del full, ws, ref_gpu
+    oracle.kv_append(host["k_new"], host["v_new"], host["k_pool"], host["v_pool"], bt, sl)
+    t0 = time.perf_counter()
+    ref = oracle.decode(host["q"], host["k_pool"], host["v_pool"], bt, sl, num_kv_heads=shape.num_kv_heads,
+                        dtype=oracle.BF16 if shape.dtype == "bf16" else oracle.F32)
+    t_oracle = time.perf_counter() - t0
+    diff = np.abs(got - ref)
+    finite = bool(np.isfinite(got).all())
+    loc = tuple(int(i) for i in np.unravel_index(int(np.nanargmax(diff)), diff.shape)) if finite else None
+    max_abs = float(np.nanmax(diff)) if finite else float("inf")
+    rel = float(np.linalg.norm(got - ref) / np.linalg.norm(ref)) if finite else float("inf")
+    tol = ATOL if args.o_dtype == "f32" else 2.0 ** -8 * float(np.abs(ref).max()) + ATOL
+    ok = finite and max_abs <= tol and rel <= RTOL and (bit_exact or args.attn_flags != 0)
+    return {"ok": ok, "bit_exact_vs_unsplit": bit_exact, "max_abs": max_abs, "argmax": loc, "rel_fro": rel,
+            "tol_abs": tol, "tol_rel_fro": RTOL, "elements": int(got.size), "oracle_s": t_oracle,
+            "checked": "gathered O on rank 0 (after the timed steps) vs the unsplit single-GPU step and the fp64 "
+                       "oracle, every element"}
+
+
+def run_ours(args, world, rank, local):
+    from paper_2509_08309_b200 import hetis
+
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    dev_index = 0 if args.share_gpu else local
+    torch.cuda.set_device(dev_index)
+    device = torch.device("cuda", dev_index)
+    dist_mode = world > 1 or args.force_dist
+    comm_ptr = None
+    backend = "gloo" if args.share_gpu else "nccl"
+    if dist_mode:
+        import torch.distributed as dist
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            if "MASTER_PORT" not in os.environ:
+                import socket
+                so = socket.socket()
+                so.bind(("127.0.0.1", 0))
+                os.environ["MASTER_PORT"] = str(so.getsockname()[1])
+                so.close()
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+            comm_ptr = dist.group.WORLD._get_backend(device)._comm_ptr()
+        else:
+            if args.exchange != "peer":
+                raise SystemExit("--share-gpu runs the peer-memory exchange only (NCCL needs one GPU per rank)")
+            dist.init_process_group("gloo")
+    if args.gather_root not in (-1, 0):
+        raise SystemExit("--gather-root: -1 (all-gather) or 0 (gather to the Primary, which checks parity)")
+    D = Dist(dist_mode, world, local, device, backend)
+    D.barrier()
+    rec = measure(args, args.config, D, rank, world, comm_ptr, headline=True)
+    sub_name = args.sub_config
+    if sub_name == "auto":
+        sub_name = "c3" if args.config != "c3" else "none"
+    sub = None
+    if sub_name != "none":
+        sub_args = argparse.Namespace(**vars(args))
+        sub_args.steps = min(args.steps, 100)
+        try:
+            workload.CONFIGS[sub_name].head_split(world)
+        except ValueError as exc:          # e.g. c3's 8 kv groups over 5 ranks
+            sub_name, sub = f"{sub_name} (skipped: {exc})", None
+        else:
+            sub = measure(sub_args, sub_name, D, rank, world, comm_ptr, headline=False)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        tps, sec, cores, sample = cpu_oracle_sample(cfg, split, rank, min(args.cpu_sample_seqs, B))
-        cpu = {"value": tps, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}
-
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_sample(workload.CONFIGS[args.config], args.cpu_sample_seqs)
+    failed = [r["workload"][:2] for r in (rec, sub) if r is not None and r["parity"] is not None
+              and not r["parity"]["ok"]]
     if rank == 0:
+        shape = workload.CONFIGS[args.config].shape
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": shape.dtype, "data": "synthetic",
-            "config": {
-                "workload": f"{cfg.name}: {cfg.description}", "batch": B, "seq_len": cfg.seq_len,
-                "seq_len_range": cfg.seq_len_range, "q_heads": shape.num_q_heads, "kv_heads": shape.num_kv_heads,
-                "head_dim": shape.head_dim, "page_size": shape.page_size, "split": list(split),
-                "o_dtype": args.o_dtype, "layers_rotated": n_layers,
-                "gather": (args.gather if dist_mode else None),
-                "scatter": (args.scatter if dist_mode else None),
-                "fused_append": bool(args.fused_append),
-                "l2": f"inputs larger than L2: {n_layers} layer pool(s) x {kv_bytes_rank / 1e6:.1f} MB KV per rank "
-                      f"rotated per step (L2 = 126 MB)",
-                "tokens": "one token = one request's decode step of one layer, all heads"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name,
-                         "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": attn_ms,
-                         "avg_launch_ms_max_rank": attn_ms_max, "peak_source": peak_src,
-                         "frac_of_8TBps_nominal": achieved / 8000.0},
-            "attention_only_tokens_per_s": B / (attn_ms_max / 1e3),
-            "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_ms, "mode": e_mode},
-            "gpu_launches": launches,
-            "launch_mode": launch_mode,
-            "clocks": clocks,
+            "metric": METRIC, "value": rec["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": rec["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": shape.dtype, "data": "synthetic",
+            "config": rec["config"], "roofline": rec["roofline"],
+            "attention_only_tokens_per_s": rec["attention_only_tokens_per_s"],
+            "phases_us": rec["phases_us"], "evented_step_us": rec["evented_step_us"], "nvlink_us": rec["nvlink_us"],
+            "cpu_baseline": cpu, "e2e": rec["e2e"], "gpu_launches": rec["gpu_launches"],
+            "gpu_launches_all_ranks": rec["gpu_launches_all_ranks"], "launch_mode": rec["launch_mode"],
+            "parity": rec["parity"], "clocks": rec["clocks"],
         }
+        if sub is None and sub_name != "none":
+            line["sub"] = {sub_name: None}
+        if sub is not None:
+            line["sub"] = {sub_name: {k: sub[k] for k in ("value", "ms_per_step", "config", "roofline", "phases_us",
+                                                          "nvlink_us", "e2e", "parity", "gpu_launches")}}
+        if args.share_gpu:
+            line["note"] = "--share-gpu: every rank on cuda:0 (correctness run; timings are not B200 numbers)"
         print(json.dumps(line), flush=True)
     if dist_mode:
         import torch.distributed as dist
-        dist.barrier(device_ids=[local])
+        D.barrier()
         dist.destroy_process_group()
+    if failed:
+        print(f"PARITY FAILED: {failed}", file=sys.stderr, flush=True)
+        return 3
     return 0
 
 

@@ -290,9 +290,9 @@ __global__ void __launch_bounds__(kCombineThreads) combine_peers_kernel(int num_
         for (int p = 0; p < g.n; ++p)
             if (peer_is_target(g, p)) store_row4<OUT_BF16>(g.o[p], idx, acc);
     }
-    __threadfence_system();  // this thread's peer stores are visible system-wide ...
-    __syncthreads();
-    if (threadIdx.x == 0) {  // ... before the block is counted
+    __syncthreads();  // the block's peer stores happen-before thread 0's system-scope fence (cumulative) ...
+    if (threadIdx.x == 0) {  // ... which orders them before the block is counted
+        __threadfence_system();
         int64_t *done = g.state[g.rank] + kStDone;
         if (atomicAdd(reinterpret_cast<unsigned long long *>(done), 1ull) == (unsigned long long)gridDim.x - 1) {
             __threadfence_system();

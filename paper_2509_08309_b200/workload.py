@@ -163,6 +163,32 @@ class DecodeBatch:
         return int(self.seq_lens.max().item()) if self.seq_lens.numel() else 0
 
 
+def _kv_head_stream(shape: Shape, seed: int, g: int, T: int, device):
+    """K and V rows [T][D] of every cached token (all requests, positions ascending) of global kv head g."""
+    gen = _gen(device, seed * 1000003 + 101 + 2 * g)
+    kg = _randn((T, shape.head_dim), shape.torch_dtype, gen, device)
+    vg = _randn((T, shape.head_dim), shape.torch_dtype, gen, device)
+    return kg, vg
+
+
+def make_new_rows(shape: Shape, seq_lens: torch.Tensor, seed: int, device="cpu", kv_begin: int = 0,
+                  kv_count: int | None = None):
+    """The new token's K and V rows [B][kv_count][D] of kv heads [kv_begin, kv_begin + kv_count) -- the same
+    bits make_decode_batch puts in k_new / v_new, without allocating pools (the Primary's scatter input)."""
+    if kv_count is None:
+        kv_count = shape.num_kv_heads - kv_begin
+    lens64 = seq_lens.to(torch.int64).cpu()
+    B, T = int(lens64.numel()), int(lens64.sum().item())
+    new_idx = (torch.cumsum(lens64, 0) - 1).to(device)                # flat index of each request's newest token
+    k_new = torch.empty((B, kv_count, shape.head_dim), dtype=shape.torch_dtype, device=device)
+    v_new = torch.empty_like(k_new)
+    for gl in range(kv_count):
+        kg, vg = _kv_head_stream(shape, seed, kv_begin + gl, T, device)
+        k_new[:, gl] = kg[new_idx]
+        v_new[:, gl] = vg[new_idx]
+    return k_new, v_new
+
+
 def make_q(shape: Shape, batch: int, seed: int, device="cpu") -> torch.Tensor:
     """Full query tensor [B][H][D] for all global heads."""
     return _randn((batch, shape.num_q_heads, shape.head_dim), shape.torch_dtype, _gen(device, seed * 1000003 + 1),
@@ -214,10 +240,7 @@ def make_decode_batch(shape: Shape, seq_lens: torch.Tensor, seed: int, device="c
     is_new = pos_of_tok == (lens64[seq_of_tok] - 1)
     hist = ~is_new
     for gl in range(gn):
-        g = g0 + gl
-        gen = _gen(device, seed * 1000003 + 101 + 2 * g)
-        kg = _randn((T, D), dt, gen, device)
-        vg = _randn((T, D), dt, gen, device)
+        kg, vg = _kv_head_stream(shape, seed, g0 + gl, T, device)
         pages = bt[:, gl, :].to(torch.int64)                              # [B][max_pages]
         rows = pages[seq_of_tok, pos_of_tok // P] * P + pos_of_tok % P      # [T]
         rows_h = rows[hist].to(device)
