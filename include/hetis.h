@@ -44,11 +44,14 @@
  * - Stream ordering: kernels are launched with programmatic dependent launch
  *   (PDL).  Each waits (griddepcontrol.wait) for its predecessor before it
  *   touches anything a predecessor writes, so results follow stream order.
- *   Callers may rely on: the attention kernels read q, seq_lens and block
- *   tables before that wait (none of this library's kernels that let their
- *   successor start early writes those -- hetis_seq_split_lens and
- *   hetis_kv_migrate never do), and with HETIS_ATTN_PIPELINED they also read
- *   cache pages other than each request's last two positions early.  Work the
+ *   Callers may rely on: the attention kernels read seq_lens and block tables
+ *   before that wait (none of this library's kernels that let their successor
+ *   start early writes those -- hetis_seq_split_lens and hetis_kv_migrate
+ *   never do) and q only after it (hetis_scatter_pull, which writes q shards,
+ *   releases its successor before its copy completes); with
+ *   HETIS_ATTN_PIPELINED they read q and the cache pages other than each
+ *   request's last two positions early, so a pipelined step's q must not come
+ *   from hetis_scatter_pull.  Work the
  *   caller enqueues itself (copies, torch kernels) is ordinary stream order.
  * - Builds: head_dim in {64, 128}; page_size 16; kv/q dtype in {bf16, f32}
  *   with q_dtype == kv_dtype; o_dtype in {f32, bf16}; r = H / H_kv in

@@ -65,6 +65,10 @@ constexpr int kQSlots = 2;
 // to device-wide claiming for SMs of unequal speed.)
 #define HETIS_STATIC_PCT 95
 #endif
+#ifndef HETIS_STATIC_ALL_BELOW
+// launches with fewer than this many items per consumer warp deal every item statically
+#define HETIS_STATIC_ALL_BELOW 2
+#endif
 #ifndef HETIS_CLAIM_AT
 // a worker claims its next item once HETIS_CLAIM_AT / 16 of the current item's pages are issued
 // (sweep on c3 N = 1..8 with the static share at 90 / 100: 8, 12 and 16 within +-2%)
@@ -320,14 +324,16 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
     }
     static_assert((kQSlots & (kQSlots - 1)) == 0, "q slots: power of two");
     Dec cur = decode(item);
-    if (lane == 0) issue_q(0, item, cur);
     int32_t pid[PPL];
-    load_pids(cur, pid);
+    load_pids(cur, pid);  // block tables: no library kernel that releases its successor early writes them
     RingPos pos{0, 0u};
     if (!pipelined) {
-        pdl_wait_once(waited);  // pools may hold rows the previous kernel (kv_append) wrote
+        // the pools may hold rows the previous kernel (kv_append) wrote, and q may come from the step's
+        // scatter (hetis_scatter_pull releases this kernel before its copy completes)
+        pdl_wait_once(waited);
         publish_split_offsets(p, s_off, lane, kProducerLanes);
     }
+    if (lane == 0) issue_q(0, item, cur);
     for (int it = 0; item < n_items; item += gridDim.x, ++it) {
         const int next = item + gridDim.x;
         int32_t pid_next[PPL];
@@ -935,7 +941,13 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     const bool pipelined_launch = (p.flags & HETIS_ATTN_PIPELINED) != 0;
     const bool device_claim = (p.flags & HETIS_ATTN_DEVICE_CLAIM) != 0 && !pipelined_launch;
     const bool pipe_steal = pipelined_launch && n_items >= 2 * (int)gridDim.x * NW;
-    const int static_pct = (pipelined_launch && !pipe_steal) ? 100 : HETIS_STATIC_PCT;
+    // Below two items per worker every item is dealt statically (no stealing): a steal is claimed once
+    // the thief is half-way through its current item, i.e. at the start of the launch for such small
+    // shares, and piles a second whole item onto a few warps (c3's 8-GPU share: 8 instead of <= 7 items
+    // on some CTAs; attention 28.0 -> 26.2 us, scripts/attn_probe.py)
+    const int static_pct =
+        ((pipelined_launch && !pipe_steal) || n_items < HETIS_STATIC_ALL_BELOW * (int)gridDim.x * NW) ? 100
+                                                                                                       : HETIS_STATIC_PCT;
     const int per_cta = device_claim       ? 0
                         : static_pct == 100 ? (n_items + (int)gridDim.x - 1) / (int)gridDim.x
                                             : (int)(((long long)n_items * static_pct / 100) / gridDim.x);
@@ -1435,10 +1447,12 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         }
         dev::fence_barrier_init();
     }
-    // PDL: seq_lens, block tables and q are never written by this library's
-    // kernels, so the prologue reads them before griddepcontrol.wait; only the
-    // K/V pools (new-token rows from kv_append) must wait -- the producer lanes
-    // execute griddepcontrol.wait before their first page copy.
+    // PDL: seq_lens and block tables are never written by this library's kernels
+    // that release their successors early, so the prologue reads them before
+    // griddepcontrol.wait; the K/V pools (new-token rows from kv_append) and q
+    // (written by hetis_scatter_pull) wait -- the producer lanes execute
+    // griddepcontrol.wait before their first page and q copies (except with
+    // HETIS_ATTN_PIPELINED, where q is read early: see include/hetis.h).
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     build_split_offsets(p, s_len, s_off);  // contains __syncthreads
     const int n_items = s_off[p.num_seqs] * p.kv_heads;

@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(kCombineThreads) combine_peers_kernel(int num_
 // rank published this epoch's rows into its o_full; every rank then records the
 // step as completed (the next step's kernels derive their epoch from it).
 __global__ void peer_wait_kernel(PeerGroupDev g) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL launch: the combine before it has completed
     const int64_t e = current_epoch(g);
     if ((int)threadIdx.x < g.n && peer_is_target(g, g.rank)) spin_until_geq(g.state[g.rank] + kStOut + threadIdx.x, e);
     __syncthreads();
@@ -350,6 +351,11 @@ __global__ void check_tables_kernel(int num_seqs, int kv_heads, int page_size, i
 //   k, v   [B][Hkv][d]   heads [k0, k0 + nk)   -> k/v_shard [B][nk][d]
 __global__ void scatter_pull_kernel(PeerGroupDev g, int num_seqs, int H, int Hkv, int q0, int nq, int k0, int nk,
                                     int qrow, int kvrow, uint8_t *q_dst, uint8_t *k_dst, uint8_t *v_dst) {
+    // PDL launch: wait for the previous step's peer_wait (which wrote the step counter), then let the
+    // attention kernel launch at once -- its prologue overlaps this copy; it reads the shards only
+    // after its own griddepcontrol.wait, i.e. after this kernel has completed.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int64_t e = current_epoch(g);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         __threadfence_system();
@@ -505,9 +511,7 @@ cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim,
 }
 
 cudaError_t launch_peer_wait(const PeerGroupDev &g, cudaStream_t s) {
-    peer_wait_kernel<<<1, 32, 0, s>>>(g);
-    note_launch();
-    return cudaGetLastError();
+    return launch_pdl(peer_wait_kernel, dim3(1), dim3(32), 0, s, g);
 }
 
 cudaError_t launch_check_tables(int num_seqs, int kv_heads, int page_size, int64_t num_pages,
@@ -533,12 +537,9 @@ cudaError_t launch_scatter_pull(const PeerGroupDev &g, int num_seqs, int H, int 
     int64_t blocks = (total + threads - 1) / threads;
     if (blocks > 2 * num_sms()) blocks = 2 * num_sms();
     if (blocks < 1) blocks = 1;  // nothing to copy still publishes the signal and the acknowledgement
-    scatter_pull_kernel<<<(unsigned)blocks, threads, 0, s>>>(g, num_seqs, H, Hkv, q0, nq, k0, nk, qrow, kvrow,
-                                                            static_cast<uint8_t *>(q_dst),
-                                                            static_cast<uint8_t *>(k_dst),
-                                                            static_cast<uint8_t *>(v_dst));
-    note_launch();
-    return cudaGetLastError();
+    return launch_pdl(scatter_pull_kernel, dim3((unsigned)blocks), dim3(threads), 0, s, g, num_seqs, H, Hkv, q0,
+                      nq, k0, nk, qrow, kvrow, static_cast<uint8_t *>(q_dst), static_cast<uint8_t *>(k_dst),
+                      static_cast<uint8_t *>(v_dst));
 }
 
 }  // namespace hetis
