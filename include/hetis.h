@@ -68,7 +68,7 @@
 extern "C" {
 #endif
 
-#define HETIS_ABI_VERSION 2
+#define HETIS_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define HETIS_API __attribute__((visibility("default")))
@@ -129,7 +129,11 @@ typedef struct {
  * combine and attention tail still run: it waits for them only before a page
  * holding one of the last two positions of a request, and before it ends.
  * Pays when a device has about one work item per warp (c3 8-GPU share -12%);
- * costs a few % on large problems.  No work stealing in this mode. */
+ * costs a few % on large problems.  No work stealing in this mode.
+ * Safety rests on at most ONE attention CTA per SM (step t + 1 reaches an SM
+ * only after step t's CTA there, which waits for combine t - 1, has left):
+ * pipelined launches reserve > 114 KiB of shared memory per CTA and the
+ * launcher checks the occupancy (HETIS_E_CUDA if it is not exactly 1). */
 #define HETIS_ATTN_PIPELINED 0x10u
 /* Diagnostic only: stream every K/V page through the shared-memory ring but
  * skip the math (partials are left unwritten).  Measures the memory-system
@@ -282,6 +286,39 @@ HETIS_API hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_s
                                int64_t num_pages, const int32_t *block_table, int32_t max_pages,
                                const int32_t *seq_lens, int32_t max_seq_len, void *o, void *workspace,
                                size_t workspace_bytes, uint32_t flags, hetis_stream_t stream);
+
+/* A per-request plan (f2: x_i^j varying with request j, the Eq. 7 dispatcher's
+ * output) executed by ONE attention launch and ONE
+ * combine on the original layouts -- no caller-side gathers of q or o.  The
+ * device's work is its unit list (hetis_plan_units: unit = one (request j,
+ * GLOBAL kv head g) it owns = the r query heads g r .. g r + r - 1 of j), held
+ * in device memory; each unit is chunked by L_j exactly as in the uniform path,
+ * so every result is bit-identical to hetis_attn_decode(_append) of the same
+ * heads.  Arguments:
+ *   num_seqs   : requests B (rows of q, o, block_table, seq_lens)
+ *   num_units, units: device int32 [num_units][2] (j, g), 0 <= j < num_seqs,
+ *                0 <= g < H_kv, no pair twice (a device-data contract); any order
+ *   q          : device [num_seqs][H][head_dim] (q_dtype), ALL heads' rows
+ *                (only the units' heads are read)
+ *   k_new, v_new: device [num_seqs][H_kv][head_dim] new rows, or both NULL.
+ *                Given: the append is fused (hetis_attn_partial_append) for the
+ *                units' (j, g); NULL: the pools already hold the new tokens
+ *   block_table: device int32 [num_seqs][H_kv][max_pages], global kv index
+ *                (rows of kv heads the device does not own are never read)
+ *   o          : device [num_seqs][H][head_dim] (o_dtype), rows of request j
+ *                at o + j * o_seq_stride elements; only the units' heads are
+ *                written, at their GLOBAL head index
+ *   workspace  : >= hetis_attn_decode_workspace(shape, num_units, r,
+ *                max_seq_len) bytes, 256-B aligned, zero-filled before first use
+ *   flags      : HETIS_ATTN_* except HETIS_ATTN_PIPELINED (-> UNSUPPORTED)
+ * num_units == 0 launches nothing. */
+HETIS_API hetis_status hetis_attn_decode_units(const hetis_shape *shape, int32_t num_seqs, int32_t num_units,
+                                               const int32_t *units, const void *q, const void *k_new,
+                                               const void *v_new, void *k_pool, void *v_pool, int64_t num_pages,
+                                               const int32_t *block_table, int32_t max_pages,
+                                               const int32_t *seq_lens, int32_t max_seq_len, void *o,
+                                               int64_t o_seq_stride, void *workspace, size_t workspace_bytes,
+                                               uint32_t flags, hetis_stream_t stream);
 
 /* ---- the step's exchanges over peer memory (NVLink 5 / NVSwitch) -------- */
 /* The scatter (a2) and the gather (a6, Eq. 2a Concat) without

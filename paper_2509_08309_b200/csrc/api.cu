@@ -647,6 +647,54 @@ hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_seqs, int32
                               (int64_t)q_head_count * shape->head_dim, workspace, workspace_bytes, stream);
 }
 
+hetis_status hetis_attn_decode_units(const hetis_shape *shape, int32_t num_seqs, int32_t num_units,
+                                     const int32_t *units, const void *q, const void *k_new, const void *v_new,
+                                     void *k_pool, void *v_pool, int64_t num_pages, const int32_t *block_table,
+                                     int32_t max_pages, const int32_t *seq_lens, int32_t max_seq_len, void *o,
+                                     int64_t o_seq_stride, void *workspace, size_t workspace_bytes, uint32_t flags,
+                                     hetis_stream_t stream) {
+    hetis_status st = check_shape(shape);
+    if (st != HETIS_OK) return st;
+    const int H = shape->num_q_heads, Hkv = shape->num_kv_heads, r = H / Hkv;
+    if (num_seqs < 0 || num_units < 0) return fail(HETIS_E_INVALID, "bad sizes");
+    if (num_units > 0 && num_seqs < 1) return fail(HETIS_E_INVALID, "units need requests");
+    if ((int64_t)num_units > (int64_t)num_seqs * Hkv)
+        return fail(HETIS_E_INVALID, "more units than (request, kv head) pairs");
+    if (num_units == 0) return HETIS_OK;
+    if (!units || !o) return fail(HETIS_E_INVALID, "NULL pointer");
+    if (!aligned(units, 8)) return fail(HETIS_E_INVALID, "units must be 8-byte aligned");
+    if ((k_new == nullptr) != (v_new == nullptr)) return fail(HETIS_E_INVALID, "pass both k_new and v_new, or neither");
+    if (k_new && (!aligned(k_new, 16) || !aligned(v_new, 16)))
+        return fail(HETIS_E_INVALID, "k_new / v_new must be 16-B aligned");
+    if (k_new && (flags & HETIS_ATTN_DIAG_STREAM_ONLY))
+        return fail(HETIS_E_INVALID, "the stream-only diagnostic cannot append");
+    if (flags & HETIS_ATTN_PIPELINED) return fail(HETIS_E_UNSUPPORTED, "units launches are not pipelined");
+    if (o_seq_stride < (int64_t)H * shape->head_dim) return fail(HETIS_E_INVALID, "o_seq_stride too small");
+    const int oe = esize(shape->o_dtype);
+    if (!aligned(o, 8) || (o_seq_stride * oe) % 8) return fail(HETIS_E_INVALID, "o rows must be 8-byte aligned");
+    hetis::AttnArgs a{};
+    // one launch row per unit, r query heads (one kv head) each; q / block-table rows are remapped in the kernel
+    st = attn_args(shape, num_units, 0, r, q, k_pool, v_pool, num_pages, block_table, max_pages, seq_lens,
+                   max_seq_len, workspace, workspace_bytes, &a);
+    if (st != HETIS_OK) return st;
+    a.flags = flags;
+    a.k_new = k_new;
+    a.v_new = v_new;
+    a.units = units;
+    a.row_kv_heads = Hkv;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const bool tc = a.dtype == HETIS_BF16 && (a.r > 1 || (flags & HETIS_ATTN_MHA_TC)) &&
+                    !(flags & HETIS_ATTN_FORCE_SIMT);
+    std::string err;
+    cudaError_t e = tc ? hetis::launch_attn_tc(a, s, &err) : hetis::launch_attn_simt(a, s);
+    if (e != cudaSuccess)
+        return err.empty() ? cuda_fail(e, "attn_decode_units launch") : fail(HETIS_E_CUDA, "attn_decode_units: " + err);
+    e = hetis::launch_combine(num_units, r, r, shape->head_dim, seq_lens, a.split_off, a.part_lse, a.part_o, o,
+                              shape->o_dtype, o_seq_stride, s, nullptr, max_seq_len, units);
+    if (e != cudaSuccess) return cuda_fail(e, "attn_decode_units combine launch");
+    return HETIS_OK;
+}
+
 // ---------------------------------------------------------------- scatter / gather
 hetis_status hetis_comm_workspace(const hetis_plan *plan, int32_t rank, int32_t num_seqs, size_t *bytes) {
     if (!plan || !bytes) return fail(HETIS_E_INVALID, "NULL argument");

@@ -35,6 +35,8 @@
 #include <atomic>
 #include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "device_utils.cuh"
 #include "hetis_internal.h"
@@ -87,6 +89,30 @@ constexpr int kProducerLanes = HETIS_PRODUCER_LANES;
 static_assert(kPagesPerItem % kProducerLanes == 0, "producer lanes must divide the pages of an item");
 // per-block limit (227 KiB) minus the kernels' static shared memory (build_split_offsets, merge scratch)
 constexpr int kMaxSmem = 227 * 1024 - 2048;
+// HETIS_ATTN_PIPELINED is safe only with at most ONE attention CTA per SM: step t + 1's CTA may stream
+// pages into the partials workspace of step t - 1 only because it cannot start on an SM before step t's
+// CTA there has left, and that CTA waits for combine t - 1 before it exits.  Pipelined launches therefore
+// reserve more than half of the SM's 228 KiB of shared memory (two CTAs cannot fit) and the launcher
+// confirms the occupancy once per configuration.
+constexpr size_t kOneCtaPerSmSmem = 116 * 1024;
+template <class K>
+cudaError_t check_one_cta_per_sm(K kern, int threads, size_t smem, std::string *err) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void *, size_t>> checked;  // (kernel, smem) configurations seen
+    const void *key = reinterpret_cast<const void *>(kern);
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto &c : checked)
+        if (c.first == key && c.second == smem) return cudaSuccess;
+    int n = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (n != 1) {
+        if (err) *err = "pipelined launch needs exactly one CTA per SM, occupancy gives " + std::to_string(n);
+        return cudaErrorInvalidConfiguration;
+    }
+    checked.emplace_back(key, smem);
+    return cudaSuccess;
+}
 static_assert(kPagesPerItem <= 32, "one producer lane per page of an item");
 
 struct Params {
@@ -110,7 +136,18 @@ struct Params {
     // nullptr = the pools already hold them (hetis_kv_append ran before)
     const uint8_t *k_new;
     const uint8_t *v_new;
+    // per-request plans (hetis_attn_decode_units): row j of this launch is unit j = (request
+    // units[2j], GLOBAL kv head units[2j+1]) with kv_heads == 1; q / k_new rows and block-table
+    // rows are then addressed in the full [B][row_kv_heads] layout.  nullptr: row j = request j.
+    const int32_t *units;
+    int row_kv_heads;
 };
+
+// Row of (launch row j, local kv head g) in the q (x r), k_new / v_new and block-table layouts.
+__device__ __forceinline__ int kv_row(const Params &p, int j, int g) {
+    if (p.units != nullptr) return __ldg(p.units + 2 * j) * p.row_kv_heads + __ldg(p.units + 2 * j + 1);
+    return j * p.kv_heads + g;
+}
 
 // new_page >= 0: this item holds request j's newest token (position L_j - 1) in page
 // new_page, slot new_slot of its page new_pg; with a fused append the consumer takes that
@@ -151,7 +188,7 @@ __device__ void build_split_offsets(const Params &p, int32_t *s_len, int32_t *s_
     const int b0 = tid * per, b1 = min(B, b0 + per);
     int sum = 0;
     for (int j = b0; j < b1; ++j) {
-        int L = p.seq_lens[j];
+        int L = p.seq_lens[p.units != nullptr ? __ldg(p.units + 2 * j) : j];
         s_len[j] = L;
         sum += (L + kC - 1) / kC;
     }
@@ -290,22 +327,23 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
     auto issue_q = [&](int it, int item, const Dec &d) {
         const int slot = it & (kQSlots - 1);
         dev::mbar_wait(&qempty[slot], ((it / kQSlots) & 1) ^ 1);
-        ItemMeta m{item, d.ntok, (d.ntok + kP - 1) / kP, -1, d.j * p.kv_heads + d.g, 0, 0, 0};
+        const int krow = kv_row(p, d.j, d.g);
+        ItemMeta m{item, d.ntok, (d.ntok + kP - 1) / kP, -1, krow, 0, 0, 0};
         if (p.k_new != nullptr && d.t0 + d.ntok == s_len[d.j]) {  // the request's last split: append here
             m.new_pg = (d.ntok - 1) / kP;
             m.new_slot = (d.ntok - 1) % kP;
-            m.new_page = __ldg(p.block_table + ((size_t)d.j * p.kv_heads + d.g) * p.max_pages + d.t0 / kP + m.new_pg);
+            m.new_page = __ldg(p.block_table + (size_t)krow * p.max_pages + d.t0 / kP + m.new_pg);
         }
         qmeta[slot] = m;
         dev::mbar_arrive_expect_tx(&qfull[slot], kQBytes);
-        const uint8_t *src = p.q + ((size_t)d.j * p.q_heads + (size_t)d.g * R) * ROW_BYTES;
+        const uint8_t *src = p.q + (size_t)krow * R * ROW_BYTES;
         dev::bulk_g2s(qbuf + (size_t)slot * kQStride, src, kQBytes, &qfull[slot], pol_stream);
     };
     // lane k of the G producer lanes owns pages k, k + G, k + 2G, ... of every item
     constexpr int PPL = kPagesPerItem / kProducerLanes;
     auto load_pids = [&](const Dec &d, int32_t (&pid)[PPL]) {
         const int np = (d.ntok + kP - 1) / kP;
-        const int32_t *row = p.block_table + ((size_t)d.j * p.kv_heads + d.g) * p.max_pages + d.t0 / kP;
+        const int32_t *row = p.block_table + (size_t)kv_row(p, d.j, d.g) * p.max_pages + d.t0 / kP;
 #pragma unroll
         for (int i = 0; i < PPL; ++i) {
             const int pg = i * kProducerLanes + lane;
@@ -917,7 +955,7 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         if (item >= 0 && item < n_items) {
             decode(item, j, g, t0, ntok);
             const int np = (ntok + kP - 1) / kP;
-            const int32_t *row = p.block_table + ((size_t)j * p.kv_heads + g) * p.max_pages + t0 / kP;
+            const int32_t *row = p.block_table + (size_t)kv_row(p, j, g) * p.max_pages + t0 / kP;
 #pragma unroll
             for (int i = 0; i < kPagesPerItem; ++i) nxt[i] = i < np ? __ldg(row + i) : 0;
         }
@@ -1025,7 +1063,8 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             continue;
         }
         if (!q_done && dev::mbar_test(&sm.qempty[w], (it & 1) ^ 1)) {
-            ItemMeta m{item, ntok, np, -1, j * p.kv_heads + g, 0, 0, np};
+            const int krow = kv_row(p, j, g);
+            ItemMeta m{item, ntok, np, -1, krow, 0, 0, np};
             if (pipelined) {  // the pages holding the request's last two positions: the consumer waits + copies
                 while (m.defer_from > 0 && holds_recent_tokens(t0, m.defer_from - 1, s_len[j])) --m.defer_from;
                 for (int d = 0; d < 2 && m.defer_from + d < np; ++d)
@@ -1038,7 +1077,7 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             }
             sm.meta[w] = m;
             dev::mbar_arrive_expect_tx(&sm.qfull[w], kQBytes);
-            const uint8_t *src = p.q + ((size_t)j * p.q_heads + (size_t)g * R) * ROW_BYTES;
+            const uint8_t *src = p.q + (size_t)krow * R * ROW_BYTES;
             dev::bulk_g2s(sm.qbuf + (size_t)w * kQStride, src, kQBytes, &sm.qfull[w], pol);
             q_done = true;
         }
@@ -1391,7 +1430,8 @@ cudaError_t launch_gqa_warp(const Params &p0, int num_seqs, cudaStream_t s, cons
     };
     int sw = HETIS_WARP_STAGES;
     while (sw > 2 && (size_t)NW * sw * kStageBytes + fixed(sw) > (size_t)kMaxSmem) --sw;
-    const size_t smem = (size_t)NW * sw * kStageBytes + fixed(sw);
+    size_t smem = (size_t)NW * sw * kStageBytes + fixed(sw);
+    if (p.flags & HETIS_ATTN_PIPELINED) smem = std::max(smem, kOneCtaPerSmSmem);
     if (smem > (size_t)kMaxSmem) {
         if (err) *err = "batch too large for the shared-memory split table";
         return cudaErrorInvalidValue;
@@ -1406,6 +1446,10 @@ cudaError_t launch_gqa_warp(const Params &p0, int num_seqs, cudaStream_t s, cons
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured[dev & 63].store((int)smem, std::memory_order_release);
+    }
+    if (p.flags & HETIS_ATTN_PIPELINED) {
+        e = check_one_cta_per_sm(kern, 32 * (NW + 1), smem, err);
+        if (e != cudaSuccess) return e;
     }
     return launch_pdl(kern, dim3(num_sms()), dim3(32 * (NW + 1)), smem, s, p, tk, tv);
 }
@@ -1495,7 +1539,8 @@ struct Launch {
         int stages = HETIS_MAX_STAGES;
         while (stages > 4 && (size_t)stages * kStageBytes + fixed_bytes(num_seqs, stages) + 1024 > (size_t)kMaxSmem)
             --stages;
-        const size_t smem = (size_t)stages * kStageBytes + fixed_bytes(num_seqs, stages) + 1024;
+        size_t smem = (size_t)stages * kStageBytes + fixed_bytes(num_seqs, stages) + 1024;
+        if (p.flags & HETIS_ATTN_PIPELINED) smem = std::max(smem, kOneCtaPerSmSmem);
         if (smem > (size_t)kMaxSmem) {
             if (err) *err = "batch too large for the shared-memory split table";
             return cudaErrorInvalidValue;
@@ -1516,6 +1561,10 @@ struct Launch {
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
             configured[dev & 63].store((int)smem, std::memory_order_release);
+        }
+        if (p.flags & HETIS_ATTN_PIPELINED) {
+            e = check_one_cta_per_sm(kern, 32 * (NW + 1), smem, err);
+            if (e != cudaSuccess) return e;
         }
         const int grid = num_sms();
         return launch_pdl(kern, dim3(grid), dim3(32 * (NW + 1)), smem, s, p, tk, tv);
@@ -1541,6 +1590,8 @@ Params make_params(const AttnArgs &a) {
     p.counters = a.counters;
     p.k_new = static_cast<const uint8_t *>(a.k_new);
     p.v_new = static_cast<const uint8_t *>(a.v_new);
+    p.units = a.units;
+    p.row_kv_heads = a.row_kv_heads;
     return p;
 }
 

@@ -40,6 +40,11 @@ struct AttnArgs {
     int32_t *counters;    // [2] work-claim and CTA-finish counters; zero between launches
     const void *k_new;    // fused append: new rows [num_seqs][kv_heads][head_dim], or nullptr
     const void *v_new;
+    // per-request plans (hetis_attn_decode_units): launch row j = unit (units[2j], units[2j+1]) =
+    // (request, GLOBAL kv head), kv_heads == 1, q / k_new / block-table rows in the full
+    // [requests][row_kv_heads] layout.  nullptr: launch row j = request j.
+    const int32_t *units;
+    int row_kv_heads;
 };
 
 struct WorkspaceLayout {
@@ -54,7 +59,8 @@ cudaError_t launch_attn_simt(const AttnArgs &a, cudaStream_t s);
 cudaError_t launch_attn_tc(const AttnArgs &a, cudaStream_t s, std::string *err);
 cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const int32_t *seq_lens,
                            const int32_t *split_off, const float *part_lse, const float *part_o, void *o,
-                           int o_dtype, int64_t o_seq_stride, cudaStream_t s, float *lse, int max_seq_len);
+                           int o_dtype, int64_t o_seq_stride, cudaStream_t s, float *lse, int max_seq_len,
+                           const int32_t *units = nullptr);
 cudaError_t launch_kv_append(int num_seqs, int kv_heads, int head_dim, int page_size, int elem_bytes,
                              const void *k_new, const void *v_new, void *k_pool, void *v_pool,
                              const int32_t *block_table, int max_pages, const int32_t *seq_lens, cudaStream_t s);

@@ -211,7 +211,8 @@ template <int D, int OUT_BF16, bool WIDE>
 __global__ void __launch_bounds__(kCombineThreads) combine_kernel(int num_seqs, int q_heads, int r,
                                                                   const int32_t *seq_lens, const int32_t *split_off,
                                                                   const float *part_lse, const float *part_o, void *o,
-                                                                  int64_t o_seq_stride, float *lse) {
+                                                                  int64_t o_seq_stride, float *lse,
+                                                                  const int32_t *units) {
     dev::pdl_release_then_wait();
     constexpr int TPH = D / 4, G = kCombineThreads / TPH;
     const int grp = threadIdx.x / TPH, d4 = threadIdx.x % TPH;
@@ -222,7 +223,11 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(int num_seqs, 
     const float4 acc = WIDE ? combine_wide<D>(j, h, q_heads, r, split_off, part_lse, part_o, &lse2)
                             : combine_narrow<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4, &lse2);
     if (WIDE && grp != 0) return;
-    store_row4<OUT_BF16>(o, (size_t)j * o_seq_stride + (size_t)h * D + 4 * d4, acc);
+    // units (per-request plans): launch row j is (request units[2j], global kv head units[2j+1]) and
+    // h < r its query head within the group -> row units[2j] of o, global head units[2j+1] * r + h
+    const size_t orow = units != nullptr ? (size_t)units[2 * j] * o_seq_stride + ((size_t)units[2 * j + 1] * r + h) * D
+                                         : (size_t)j * o_seq_stride + (size_t)h * D;
+    store_row4<OUT_BF16>(o, orow + 4 * d4, acc);
     if (lse != nullptr && d4 == 0) lse[flat] = lse2 * 0.69314718055994531f;  // log2 -> natural log
 }
 
@@ -472,7 +477,8 @@ cudaError_t launch_kv_append(int num_seqs, int kv_heads, int head_dim, int page_
 
 cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const int32_t *seq_lens,
                            const int32_t *split_off, const float *part_lse, const float *part_o, void *o,
-                           int o_dtype, int64_t o_seq_stride, cudaStream_t s, float *lse, int max_seq_len) {
+                           int o_dtype, int64_t o_seq_stride, cudaStream_t s, float *lse, int max_seq_len,
+                           const int32_t *units) {
     const int64_t pairs = (int64_t)num_seqs * q_heads;
     if (pairs == 0) return cudaSuccess;
     const bool wide = (max_seq_len + kSplitTokens - 1) / kSplitTokens > kNarrowSplits;
@@ -487,7 +493,7 @@ cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const
         kern = wide ? (bf ? combine_kernel<64, 1, true> : combine_kernel<64, 0, true>)
                     : (bf ? combine_kernel<64, 1, false> : combine_kernel<64, 0, false>);
     return launch_pdl(kern, dim3((unsigned)blocks), dim3(kCombineThreads), 0, s, num_seqs, q_heads, r, seq_lens,
-                      split_off, part_lse, part_o, o, o_seq_stride, lse);
+                      split_off, part_lse, part_o, o, o_seq_stride, lse, units);
 }
 
 cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim, const int32_t *split_off,

@@ -38,7 +38,7 @@ EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_
             "hetis_attn_combine_lse", "hetis_seq_split_lens", "hetis_seq_merge", "hetis_seq_broadcast_q",
             "hetis_seq_allgather_merge", "hetis_peer_state_bytes", "hetis_peer_group_create",
             "hetis_peer_group_destroy", "hetis_scatter_pull", "hetis_attn_partial_append",
-            "hetis_attn_decode_append", "hetis_check_tables", "hetis_launch_count")
+            "hetis_attn_decode_append", "hetis_check_tables", "hetis_launch_count", "hetis_attn_decode_units")
 
 
 class HetisError(RuntimeError):
@@ -109,6 +109,8 @@ def lib() -> ctypes.CDLL:
                 "hetis_attn_decode_append": (ctypes.c_int, [sp, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32, vp,
                                                             i32, vp, vp, sz, u32, vp]),
                 "hetis_scatter_pull": (ctypes.c_int, [vp, i32, vp, vp, vp, vp]),
+                "hetis_attn_decode_units": (ctypes.c_int, [sp, i32, i32, vp, vp, vp, vp, vp, vp, i64, vp, i32, vp,
+                                                           i32, vp, i64, vp, sz, u32, vp]),
             }
             for name, (res, args) in sig.items():
                 # an older build loaded through HETIS_LIB (A/B runs) may lack newer entry points;
@@ -390,6 +392,29 @@ def attn_decode_append(shape: CShape, q, k_new, v_new, k_pool, v_pool, block_tab
                                           _dev(seq_lens, "seq_lens"), max_seq_len, _dev(o, "o"),
                                           _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(),
                                           flags, _stream(stream)), "hetis_attn_decode_append")
+
+
+def attn_decode_units(shape: CShape, units, q, k_pool, v_pool, block_table, seq_lens, max_seq_len: int, o,
+                      workspace, k_new=None, v_new=None, flags: int = 0, stream=None) -> None:
+    """A per-request plan's units on the full layouts in one attention launch + one combine
+    (hetis_attn_decode_units).  units: device int32 [U][2] (request, global kv head); q, o
+    [B][H][d]; block_table [B][H_kv][max_pages]; k_new, v_new [B][H_kv][d] or None."""
+    if units.dtype != torch.int32 or units.dim() != 2 or units.shape[1] != 2 or not units.is_contiguous():
+        raise ValueError("units must be a contiguous int32 [U][2] tensor")
+    H, Hkv = shape.num_q_heads, shape.num_kv_heads
+    if q.dim() != 3 or q.shape[1] != H:
+        raise ValueError(f"q must be [B][{H}][d] (all heads), got {tuple(q.shape)}")
+    _check_args(shape, q=q, o=o, k_pool=k_pool, v_pool=v_pool, block_table=block_table, seq_lens=seq_lens,
+                k_new=k_new, v_new=v_new)
+    if o.dim() != 3 or o.shape[1] != H:
+        raise ValueError(f"o must be [B][{H}][d], got {tuple(o.shape)}")
+    _check(lib().hetis_attn_decode_units(ctypes.byref(shape), q.shape[0], units.shape[0], _dev(units, "units"),
+                                         _dev(q, "q"), _dev(k_new, "k_new"), _dev(v_new, "v_new"), _dev(k_pool, "k_pool"),
+                                         _dev(v_pool, "v_pool"), k_pool.shape[0], _dev(block_table, "block_table"),
+                                         block_table.shape[2], _dev(seq_lens, "seq_lens"), max_seq_len,
+                                         ctypes.c_void_p(o.data_ptr()), o.stride(0), _dev(workspace, "workspace"),
+                                         workspace.numel() * workspace.element_size(), flags, _stream(stream)),
+           "hetis_attn_decode_units")
 
 
 def attn_decode(shape: CShape, q, k_pool, v_pool, block_table, seq_lens, max_seq_len: int, o, workspace,

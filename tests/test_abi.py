@@ -29,7 +29,7 @@ def declared_symbols():
 
 def test_every_declared_symbol_is_exported(L):
     syms = declared_symbols()
-    assert len(syms) == 34
+    assert len(syms) == 35
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(hetis.EXPORTED)
@@ -45,7 +45,7 @@ def test_exported_symbols_match_nm():
 def test_status_strings_and_constants(L):
     for code, name in hetis.STATUS.items():
         assert hetis.status_str(code) == name
-    assert hetis.abi_version() == 2
+    assert hetis.abi_version() == 3
     assert hetis.split_tokens() % 16 == 0
 
 

@@ -2,14 +2,17 @@
 SURVEY.md §8(f) row f4).
 
 A request re-dispatched from one per-request plan row to another moves only the
-kv groups whose device changes (`dispatch.plan_migration`).  Here the devices
-are "virtual devices" on one GPU: each has its own K/V pools and block table in
-hetis_plan_units row order.  After the kernel copies the moved groups' pages:
+kv groups whose device changes (`dispatch.plan_migration`: every device keeps
+min(old, new) / r of its groups, so ownership becomes non-contiguous).  Here
+the devices are "virtual devices" on one GPU: each has its own K/V pools and a
+block table with one row per (request, kv group) unit (`dispatch.owner_units`
+order).  After the kernel copies the moved groups' pages:
 
 * every destination pool equals the oracle's token-by-token migration bit for
   bit on every cached token (and untouched pages keep their bytes);
-* attention executed on the NEW plan from the migrated pools reassembles to the
-  single-device result bit for bit (the chunking depends on L_j only) -- the
+* attention executed on the NEW plan from the migrated pools -- each device's
+  unit list in one hetis_attn_decode_units call -- reassembles to the
+  single-device result bit for bit (the chunking depends on L_j only): the
   migrated cache is the cache.
 A two-process test pushes the pages into another process's pools through CUDA
 IPC mappings: the peer-pointer path an NVSwitch box uses over NVLink.
@@ -63,11 +66,9 @@ def _random_rows(rng, J, G, N):
     return rows
 
 
-def _units(rows, r):
-    """hetis_plan_units order per device: requests ascending, groups ascending."""
-    J, N = rows.shape
-    own = [dispatch.group_owners(rows[j] * r, r) for j in range(J)]
-    return [[(j, g) for j in range(J) for g in range(len(own[j])) if own[j][g] == d] for d in range(N)]
+def _contiguous_owners(rows, r):
+    """Every request's group owners under contiguous head ranges (reading 3)."""
+    return [dispatch.group_owners(rows[j] * r, r) for j in range(rows.shape[0])]
 
 
 class VirtualDevice:
@@ -105,18 +106,18 @@ def _fill_from_full(dev, b, pages):
         dev.v[dst] = b.v_pool[src]
 
 
-def _run_units(s, shape, b, dev, units, table, D):
-    r = shape.r
-    js = torch.tensor([u[0] for u in units], device="cuda")
-    gs = torch.tensor([u[1] for u in units], device="cuda")
-    heads = gs[:, None] * r + torch.arange(r, device="cuda")[None, :]
-    q_u = b.q[js[:, None], heads].contiguous()
-    sl_u = b.seq_lens[js].contiguous()
-    U = len(units)
-    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, U, r, b.max_seq_len), "cuda")
-    o_u = torch.empty((U, r, D), device="cuda")
-    hetis.attn_decode(s, q_u, dev.k, dev.v, table[:U, None, :].contiguous(), sl_u, b.max_seq_len, o_u, ws)
-    return js, heads, o_u
+def _run_units(s, b, dev, units, table, o):
+    """The device's units on the full layouts in one attention launch + one combine
+    (hetis_attn_decode_units): its unit-row table is scattered into a [B][H_kv][max_pages] table."""
+    B, Hkv = b.block_table.shape[:2]
+    full_tab = torch.full((B, Hkv, table.shape[1]), -1, dtype=torch.int32, device="cuda")
+    for u, (j, g) in enumerate(units):
+        full_tab[j, g] = table[u]
+    ut = torch.tensor(units, dtype=torch.int32, device="cuda").reshape(-1, 2)
+    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, len(units), s.num_q_heads // s.num_kv_heads,
+                                                           b.max_seq_len), "cuda")
+    hetis.attn_decode_units(s, ut, b.q, dev.k, dev.v, full_tab, b.seq_lens, b.max_seq_len, o, ws)
+    torch.cuda.synchronize()
 
 
 @pytest.mark.parametrize("H,Hkv,D,dtype,max_ctas", [(64, 8, 128, "bf16", 0), (40, 40, 128, "bf16", 7),
@@ -134,7 +135,11 @@ def test_redispatch_migration_bit_exact(H, Hkv, D, dtype, max_ctas):
         new[j] = _random_rows(rng, 1, G, N)[0]
     migs = {j: dispatch.plan_migration(old[j] * r, new[j] * r, r) for j in range(J)
             if not np.array_equal(old[j], new[j])}
-    old_units, new_units = _units(old, r), _units(new, r)
+    old_own = _contiguous_owners(old, r)
+    new_own = [migs[j].new_owner if j in migs else old_own[j] for j in range(J)]   # maximal reuse: not contiguous
+    old_units, new_units = dispatch.owner_units(old_own, N), dispatch.owner_units(new_own, N)
+    for j, m in migs.items():                                    # only the set difference moves
+        assert len(m.moves) == G - int(np.minimum(old[j], new[j]).sum())
     capacity = sum(G * ((L + 15) // 16) for L in lens) + 8
     devs = [VirtualDevice(b, capacity, rng) for _ in range(N)]
     old_tab, new_tab = [], []
@@ -176,13 +181,12 @@ def test_redispatch_migration_bit_exact(H, Hkv, D, dtype, max_ctas):
             assert np.array_equal(got[cached], exp[cached]), d
             assert np.array_equal(got[untouched], exp[untouched]), d
 
-    # the migrated cache serves the new plan: bit-identical to the single-device result
+    # the migrated cache serves the new (non-contiguous) plan: every device runs its unit list with
+    # hetis_attn_decode_units into the shared O; bit-identical to the single-device result
     assembled = torch.full_like(o_ref, float("nan"))
     for d in range(N):
         if new_units[d]:
-            js, heads, o_u = _run_units(s, shape, b, devs[d], new_units[d], new_tab[d][0], D)
-            assembled[js[:, None], heads] = o_u
-    torch.cuda.synchronize()
+            _run_units(s, b, devs[d], new_units[d], new_tab[d][0], assembled)
     assert torch.equal(assembled, o_ref)
 
 

@@ -295,10 +295,25 @@ def test_full_size_config_whole_output(name, n_dev, rank):
 
 
 # ------------------------------------------------------------------ per-request (dispatcher) plans via work units
+def _random_per_request_plan(B, H, r, N, seed):
+    """x[j][i]: a random composition of request j's H / r kv groups over N devices (multiples of r, sum H)."""
+    g = np.random.default_rng(seed)
+    x = np.zeros((B, N), dtype=np.int32)
+    for j in range(B):
+        cuts = np.sort(g.integers(0, H // r + 1, size=N - 1))
+        x[j] = np.diff(np.concatenate([[0], cuts, [H // r]])) * r
+    return x
+
+
+def _units_tensor(plan, dev):
+    units = plan.units(dev)
+    return torch.tensor(units, dtype=torch.int32, device="cuda").reshape(-1, 2), len(units)
+
+
 def test_per_request_plan_units_bit_identical_to_unsplit():
-    """A ragged per-request plan from the Eq. 7 dispatcher, executed by the unchanged kernels on unit views
-    (one kv head per unit), reassembles to exactly the unsplit result (and matches the oracle)."""
-    import numpy as np
+    """A ragged per-request plan from the Eq. 7 dispatcher, each device's units run by
+    hetis_attn_decode_units -- ONE attention launch + ONE combine on the full [B][H][d] q / o, no
+    caller-side gathers -- reassembles to exactly the unsplit result and matches the oracle."""
     from paper_2509_08309_b200 import dispatch as dp
     shape = workload.LLAMA2_70B
     lens = (600, 5, 1300, 256, 2048, 77)
@@ -308,32 +323,77 @@ def test_per_request_plan_units_bit_identical_to_unsplit():
             dp.DeviceState(0, 0, 1e12, False, dp.AttentionCost(2e-8, 3e-11, 5e-6, gamma=1e-9, beta=2e-6)),
             dp.DeviceState(0, 0, 1e12, True, dp.AttentionCost(1.5e-8, 2e-11, 5e-6))]
     out = dp.dispatch(devs, list(lens), H=64, r=8)
-    assert len({tuple(col) for col in out.x.T.tolist()}) > 1 or True   # ragged in general
-    plan = hetis.plan_create(hetis.make_shape(shape), 3, dp.plan_rows(out.x), per_request=True, num_seqs=len(lens))
     s = hetis.make_shape(shape)
-    r = shape.r
+    plan = hetis.plan_create(s, 3, dp.plan_rows(out.x), per_request=True, num_seqs=len(lens))
     assembled = torch.full_like(o_full, float("nan"))
     seen = 0
     for dev in range(3):
-        units = plan.units(dev)
-        if not units:
+        units, U = _units_tensor(plan, dev)
+        if U == 0:
             continue
-        js = torch.tensor([u[0] for u in units], device="cuda")
-        gs = torch.tensor([u[1] for u in units], device="cuda")
-        heads = (gs[:, None] * r + torch.arange(r, device="cuda")[None, :])            # [U][r]
-        q_u = full.q[js[:, None], heads].contiguous()                                     # [U][r][D]
-        bt_u = full.block_table[js, gs][:, None, :].contiguous()                          # [U][1][max_pages]
-        sl_u = full.seq_lens[js].contiguous()
-        U = len(units)
-        ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, U, r, full.max_seq_len), "cuda")
-        o_u = torch.empty((U, r, 128), device="cuda")
-        hetis.attn_decode(s, q_u, full.k_pool, full.v_pool, bt_u, sl_u, full.max_seq_len, o_u, ws)
-        assembled[js[:, None], heads] = o_u
+        ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, U, shape.r, full.max_seq_len), "cuda")
+        mine = torch.full_like(o_full, float("nan"))
+        hetis.attn_decode_units(s, units, full.q, full.k_pool, full.v_pool, full.block_table, full.seq_lens,
+                                full.max_seq_len, mine, ws)
+        torch.cuda.synchronize()
+        owned = torch.zeros(o_full.shape[:2], dtype=torch.bool, device="cuda")
+        for j, g in plan.units(dev):
+            owned[j, g * shape.r:(g + 1) * shape.r] = True
+        assert torch.isnan(mine[~owned]).all(), dev                 # nothing outside the device's units is written
+        assembled[owned] = mine[owned]
         seen += U
-    torch.cuda.synchronize()
     assert seen == len(lens) * 8
     assert torch.equal(assembled, o_full)
     assert_close(assembled, oracle_full(full), "per-request plan")
+
+
+@pytest.mark.parametrize("H,Hkv,D,dtype,fused", [(64, 8, 128, "bf16", True), (40, 40, 128, "bf16", True),
+                                                 (16, 4, 64, "bf16", False), (8, 8, 64, "f32", False),
+                                                 (16, 2, 128, "f32", False)])
+def test_units_random_plans_all_kernels(H, Hkv, D, dtype, fused):
+    """hetis_attn_decode_units on random per-request plans over 3 devices, every kernel family (per-warp
+    tensor-core GQA, CUDA-core MHA, fp32): the union of the devices' outputs is bit-identical to the unsplit
+    single-launch result, and with the append fused the pools end bit-identical to hetis_kv_append's."""
+    lens = (1, 17, 256, 257, 1000, 33, 700, 2)
+    r = H // Hkv
+    full = gpu_batch(H, Hkv, D, dtype, lens, seed=17)
+    o_full = run_gpu(full)
+    fresh = gpu_batch(H, Hkv, D, dtype, lens, seed=17)           # same bits, pools without the new token
+    x = _random_per_request_plan(len(lens), H, r, 3, seed=H + D)
+    s = hetis.make_shape(full.shape)
+    plan = hetis.plan_create(s, 3, x.tolist(), per_request=True, num_seqs=len(lens))
+    out = torch.full_like(o_full, float("nan"))
+    for dev in range(3):
+        units, U = _units_tensor(plan, dev)
+        ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, max(U, 1), r, full.max_seq_len), "cuda")
+        b = fresh if fused else full
+        hetis.attn_decode_units(s, units, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, b.max_seq_len, out, ws,
+                                k_new=b.k_new if fused else None, v_new=b.v_new if fused else None)
+    torch.cuda.synchronize()
+    assert torch.equal(out, o_full)
+    if fused:
+        assert torch.equal(fresh.k_pool.view(torch.int16), full.k_pool.view(torch.int16))
+        assert torch.equal(fresh.v_pool.view(torch.int16), full.v_pool.view(torch.int16))
+
+
+def test_units_argument_errors():
+    full = gpu_batch(64, 8, 128, "bf16", (5, 9), seed=3)
+    s = hetis.make_shape(full.shape)
+    units = torch.tensor([[0, 1], [1, 7]], dtype=torch.int32, device="cuda")
+    o = torch.empty((2, 64, 128), device="cuda")
+    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, 2, 8, full.max_seq_len), "cuda")
+    with pytest.raises(hetis.HetisError) as e:       # pipelined launches are not supported for units
+        hetis.attn_decode_units(s, units, full.q, full.k_pool, full.v_pool, full.block_table, full.seq_lens,
+                                full.max_seq_len, o, ws, flags=hetis.ATTN_PIPELINED)
+    assert e.value.name == "HETIS_E_UNSUPPORTED"
+    small = hetis.alloc_workspace(256, "cuda")
+    with pytest.raises(hetis.HetisError) as e:
+        hetis.attn_decode_units(s, units, full.q, full.k_pool, full.v_pool, full.block_table, full.seq_lens,
+                                full.max_seq_len, o, small)
+    assert e.value.name == "HETIS_E_WORKSPACE"
+    with pytest.raises(ValueError):                  # q must hold every head
+        hetis.attn_decode_units(s, units, full.q[:, :8].contiguous(), full.k_pool, full.v_pool, full.block_table,
+                                full.seq_lens, full.max_seq_len, o, ws)
 
 
 @pytest.mark.parametrize("name", ["c3", "c2"])
