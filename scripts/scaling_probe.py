@@ -8,6 +8,11 @@ GPUs.  NVLink scatter/gather is NOT included (only one GPU is reachable), so
 `compute_scaling` = t(1) / t(N) is an upper bound for the full-step scaling.
 
     python scripts/scaling_probe.py [--config c3] [--steps 200]
+    python scripts/scaling_probe.py --config c4 --shares     # every rank of the config's uneven split
+
+--shares: the config's fixed split (c4: 16/8/8/4/4, Eq. 5's uneven x_i) -- every
+rank's share (its heads [b_i, b_i + x_i), its own pages) timed the same way; the step of the split
+is the slowest rank's (the critical path), reported against the HBM floor of its KV bytes.
 """
 from __future__ import annotations
 
@@ -24,12 +29,13 @@ import torch  # noqa: E402
 from paper_2509_08309_b200 import accounting, hetis, workload  # noqa: E402
 
 
-def share_time(cfg, n: int, steps: int, warmup: int, device):
-    split = cfg.head_split(n)
+def share_time(cfg, n: int, steps: int, warmup: int, device, split=None, rank: int = 0):
+    split = cfg.head_split(n) if split is None else split
     shape = cfg.shape
-    x = split[0]
+    x = split[rank]
+    q_begin = sum(split[:rank])
     lens = cfg.seq_lens()
-    b = workload.make_decode_batch(shape, lens, cfg.seed, device, q_begin=0, q_count=x)
+    b = workload.make_decode_batch(shape, lens, cfg.seed, device, q_begin=q_begin, q_count=x, rank_salt=rank)
     s = hetis.make_shape(shape)
     B, L = len(lens), int(lens.max())
     kv_bytes = accounting.step_bytes(lens.tolist(), x, shape.r, shape.head_dim, shape.page_size, shape.elem_bytes,
@@ -95,7 +101,10 @@ def share_time(cfg, n: int, steps: int, warmup: int, device):
     t1.record()
     torch.cuda.synchronize()
     step_pipe_ms = t0.elapsed_time(t1) / steps
-    return {"n": n, "heads_per_rank": x, "kv_bytes_per_rank": kv_bytes, "layers_rotated": n_layers,
+    del kp, vp, ws2, b
+    torch.cuda.empty_cache()
+    return {"n": n, "rank": rank, "heads_per_rank": x, "q_begin": q_begin, "kv_bytes_per_rank": kv_bytes,
+            "layers_rotated": n_layers,
             "step_us": step_ms * 1e3, "step_no_events_us": step_noev_ms * 1e3,
             "step_pipelined_us": step_pipe_ms * 1e3, "attn_us": attn_ms * 1e3,
             "attn_gbs": kv_bytes / (attn_ms / 1e3) / 1e9}
@@ -107,9 +116,27 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--ns", default="1,2,4,8")
+    ap.add_argument("--shares", action="store_true", help="every rank of the config's fixed (uneven) split")
     a = ap.parse_args()
     cfg = workload.CONFIGS[a.config]
     dev = torch.device("cuda", 0)
+    if a.shares:
+        split = cfg.split
+        peak = 6550.0
+        rows = [share_time(cfg, len(split), a.steps, a.warmup, dev, split=split, rank=i) for i in range(len(split))]
+        for r in rows:
+            r["floor_us_at_6550"] = r["kv_bytes_per_rank"] / (peak * 1e9) * 1e6
+            r["attn_frac_of_6550"] = r["attn_gbs"] / peak
+            r["config"] = cfg.name
+            r["split"] = list(split)
+            print(json.dumps(r), flush=True)
+        crit = max(rows, key=lambda r: r["step_no_events_us"])
+        print(json.dumps({"config": cfg.name, "split": list(split), "critical_rank": crit["rank"],
+                          "critical_step_us": crit["step_no_events_us"],
+                          "critical_floor_us_at_6550": crit["floor_us_at_6550"],
+                          "critical_step_frac_of_floor": crit["floor_us_at_6550"] / crit["step_no_events_us"],
+                          "tokens_per_s_per_layer": cfg.batch / (crit["step_no_events_us"] * 1e-6)}), flush=True)
+        return
     rows = [share_time(cfg, int(n), a.steps, a.warmup, dev) for n in a.ns.split(",")]
     t1, t1n = rows[0]["step_us"], rows[0]["step_no_events_us"]
     for r in rows:

@@ -361,7 +361,7 @@ def test_units_random_plans_all_kernels(H, Hkv, D, dtype, fused):
     fresh = gpu_batch(H, Hkv, D, dtype, lens, seed=17)           # same bits, pools without the new token
     x = _random_per_request_plan(len(lens), H, r, 3, seed=H + D)
     s = hetis.make_shape(full.shape)
-    plan = hetis.plan_create(s, 3, x.tolist(), per_request=True, num_seqs=len(lens))
+    plan = hetis.plan_create(s, 3, x.reshape(-1).tolist(), per_request=True, num_seqs=len(lens))
     out = torch.full_like(o_full, float("nan"))
     for dev in range(3):
         units, U = _units_tensor(plan, dev)
