@@ -337,9 +337,23 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
         step.buf.v_new.copy_(batch.v_new)
         o_full = step.buf.o_shard
     stream = torch.cuda.current_stream(device)
+    # one kernel per step where the attention kernel also merges the splits (per-warp tensor-core kernel)
+    # (opt-in, --attn-flags 0x20: measured slower than the separate combine)
+    fused = (not peer) and bool(args.fused_append) and hetis.attn_decode_launches(step.cshape, args.attn_flags) == 1
+
+    fused_peer = peer and bool(args.fused_append) and bool(args.attn_flags & hetis.ATTN_FUSED_MERGE) and \
+        step.merge_fused(args.attn_flags)
 
     def attention(li):
-        if args.fused_append:   # the append happens inside the attention kernel
+        if fused_peer:          # append + attention + split merge + the stores into every rank's o_full
+            hetis.attn_decode_peers(step.group, step.buf.q_shard, k_pools[li], v_pools[li], batch.block_table,
+                                    batch.seq_lens, max_len, step.buf.workspace, k_new_shard=step.buf.k_new,
+                                    v_new_shard=step.buf.v_new, flags=args.attn_flags)
+        elif fused:             # append + attention + split merge in ONE kernel, O straight into the shard
+            hetis.attn_decode_append(step.cshape, step.buf.q_shard, step.buf.k_new, step.buf.v_new, k_pools[li],
+                                     v_pools[li], batch.block_table, batch.seq_lens, max_len, step.buf.o_shard,
+                                     step.buf.workspace, q_head_begin=q_begin, flags=args.attn_flags)
+        elif args.fused_append:   # the append happens inside the attention kernel
             hetis.attn_partial_append(step.cshape, step.buf.q_shard, step.buf.k_new, step.buf.v_new, k_pools[li],
                                       v_pools[li], batch.block_table, batch.seq_lens, max_len, step.buf.workspace,
                                       q_head_begin=q_begin, flags=args.attn_flags)
@@ -348,6 +362,17 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
             hetis.attn_partial(step.cshape, step.buf.q_shard, k_pools[li], v_pools[li], batch.block_table,
                                batch.seq_lens, max_len, step.buf.workspace, q_head_begin=q_begin,
                                flags=args.attn_flags)
+
+    def attention_only(li):
+        # the dominant kernel alone (roofline): with the merge + gather fused over peer memory that kernel needs
+        # the step's scatter_pull (it waits for every rank's acknowledgement of the previous o_full), so it is
+        # timed as the same kernel writing the local o shard (identical arithmetic and K/V traffic)
+        if fused_peer:
+            hetis.attn_decode_append(step.cshape, step.buf.q_shard, step.buf.k_new, step.buf.v_new, k_pools[li],
+                                     v_pools[li], batch.block_table, batch.seq_lens, max_len, step.buf.o_shard,
+                                     step.buf.workspace, q_head_begin=q_begin, flags=args.attn_flags)
+        else:
+            attention(li)
 
     def one_step(i, ev=None):
         """ev: optional 5 events recorded between the phases (scatter | attention | combine(+gather) | wait)."""
@@ -362,12 +387,14 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
         attention(li)
         rec(2)
         if peer:
-            hetis.attn_combine_peers(step.group, batch.seq_lens, max_len, step.buf.workspace)
+            if not fused_peer:
+                hetis.attn_combine_peers(step.group, batch.seq_lens, max_len, step.buf.workspace)
             rec(3)
             hetis.peer_wait(step.group)
         else:
-            hetis.attn_combine(step.cshape, batch.seq_lens, max_len, step.buf.o_shard, step.buf.workspace,
-                               q_head_count=q_count)
+            if not fused:
+                hetis.attn_combine(step.cshape, batch.seq_lens, max_len, step.buf.o_shard, step.buf.workspace,
+                                   q_head_count=q_count)
             rec(3)
             if dist_mode:
                 step.gather(o_full, root=gather_root)
@@ -402,7 +429,7 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
             graph_attn = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph_attn, capture_error_mode="thread_local"):
                 for i in range(args.steps):
-                    attention(i % n_layers)
+                    attention_only(i % n_layers)
             for g in (graph, graph_ev, graph_attn):   # untimed replays (warm instantiation)
                 g.replay()
             torch.cuda.synchronize(device)
@@ -455,7 +482,7 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
         graph_attn.replay()
     else:
         for i in range(args.steps):
-            attention(i % n_layers)
+            attention_only(i % n_layers)
     a1.record(stream)
     D.barrier()
     attn_ms = a0.elapsed_time(a1) / args.steps
@@ -519,6 +546,10 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
 
         def compute(i, q, kn, vn, sl, o):
             li = i % n_layers
+            if fused:
+                hetis.attn_decode_append(step.cshape, q, kn, vn, k_pools[li], v_pools[li], batch.block_table, sl,
+                                         max_len, o, step.buf.workspace, q_head_begin=q_begin, flags=args.attn_flags)
+                return
             if args.fused_append:
                 hetis.attn_partial_append(step.cshape, q, kn, vn, k_pools[li], v_pools[li], batch.block_table, sl,
                                           max_len, step.buf.workspace, q_head_begin=q_begin, flags=args.attn_flags)
@@ -593,6 +624,10 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
     if args.fused_append:   # the new rows are read from k_new / v_new and written into the pools
         alg_bytes += 2 * 2 * B * (q_count // shape.r) * shape.head_dim * shape.elem_bytes
         kernel_name = "hetis_attn_partial_append (split-KV attention with kv_append fused)"
+    if fused or fused_peer:   # the kernel also writes O
+        alg_bytes += sb.o
+        kernel_name = ("hetis_attn_decode_append (ONE kernel: kv_append + split-KV attention + split merge; "
+                       "O written by the kernel)")
     achieved = alg_bytes / (attn_ms / 1e3) / 1e9
     achieved_min = D.max(-achieved) * -1.0      # the slowest rank
     peak, peak_src = peaks()
@@ -604,7 +639,7 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
             "head_dim": shape.head_dim, "page_size": shape.page_size, "split": list(split),
             "o_dtype": args.o_dtype, "layers_rotated": n_layers,
             "exchange": (args.exchange if dist_mode else None), "gather_root": (gather_root if dist_mode else None),
-            "fused_append": bool(args.fused_append),
+            "fused_append": bool(args.fused_append), "merge_fused": bool(fused or fused_peer),
             "l2": f"inputs larger than L2: {n_layers} layer pool(s) x {kv_bytes_rank / 1e6:.1f} MB KV per rank "
                   f"rotated per step (L2 = 126 MB)",
             "tokens": "one token = one request's decode step of one layer, all heads"},

@@ -135,6 +135,16 @@ typedef struct {
  * pipelined launches reserve > 114 KiB of shared memory per CTA and the
  * launcher checks the occupancy (HETIS_E_CUDA if it is not exactly 1). */
 #define HETIS_ATTN_PIPELINED 0x10u
+/* hetis_attn_decode / _decode_append / _decode_units / _decode_peers with the
+ * per-warp tensor-core kernel: fold each (request, kv head) pair's splits in
+ * the attention kernel itself (the warp that finishes the pair's last split;
+ * the combine's arithmetic, bit-identical) -- ONE launch per step, and over
+ * peer memory the merged rows go straight into every rank's o_full.  Measured
+ * SLOWER than the separate combine on B200 (c3: 200 vs 188 us at N = 1, 33.1
+ * vs 30.7 us for the 8-GPU share; without the fold 182 / 27.7 us -- the fold's
+ * L2 round trips under a saturated memory system stall the merging warp), so
+ * opt-in. */
+#define HETIS_ATTN_FUSED_MERGE 0x20u
 /* Diagnostic only: stream every K/V page through the shared-memory ring but
  * skip the math (partials are left unwritten).  Measures the memory-system
  * ceiling of the pipeline; the CUDA-core kernel honours it. */
@@ -270,8 +280,15 @@ HETIS_API hetis_status hetis_attn_combine_lse(const hetis_shape *shape, int32_t 
                                               int64_t o_seq_stride, float *lse, const void *workspace,
                                               size_t workspace_bytes, hetis_stream_t stream);
 
-/* hetis_attn_partial_append followed by hetis_attn_combine with a dense o shard:
- * the whole per-device step (a3 + a4 + a5) in two kernels. */
+/* The whole per-device step (a3 + a4 + a5) with a dense o shard: results
+ * bit-identical to hetis_attn_partial_append followed by hetis_attn_combine.
+ * With HETIS_ATTN_FUSED_MERGE and the per-warp tensor-core kernel (bf16 and
+ * r > 1, or HETIS_ATTN_MHA_TC; not with HETIS_ATTN_FORCE_SIMT /
+ * _TC_SHARED_RING / _PIPELINED / _DIAG_STREAM_ONLY) it is ONE kernel: the warp
+ * that finishes the last split of a (request, kv head) pair folds the pair's
+ * splits (the combine's arithmetic, same order) and stores its r rows; a
+ * one-split pair stores its rows straight from registers.  Otherwise two
+ * kernels.  o must be 16-byte aligned. */
 HETIS_API hetis_status hetis_attn_decode_append(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
                                                 int32_t q_head_count, const void *q, const void *k_new,
                                                 const void *v_new, void *k_pool, void *v_pool, int64_t num_pages,
@@ -280,12 +297,18 @@ HETIS_API hetis_status hetis_attn_decode_append(const hetis_shape *shape, int32_
                                                 void *workspace, size_t workspace_bytes, uint32_t flags,
                                                 hetis_stream_t stream);
 
-/* hetis_attn_partial followed by hetis_attn_combine with a dense o shard. */
+/* hetis_attn_partial followed by hetis_attn_combine with a dense o shard (one
+ * kernel under the same conditions as hetis_attn_decode_append). */
 HETIS_API hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
                                int32_t q_head_count, const void *q, const void *k_pool, const void *v_pool,
                                int64_t num_pages, const int32_t *block_table, int32_t max_pages,
                                const int32_t *seq_lens, int32_t max_seq_len, void *o, void *workspace,
                                size_t workspace_bytes, uint32_t flags, hetis_stream_t stream);
+
+/* Kernels hetis_attn_decode / _decode_append / _decode_units launch for this
+ * shape and these flags: 1 (merge fused into the attention kernel) or 2
+ * (attention + combine); -1 for an invalid shape. */
+HETIS_API int32_t hetis_attn_decode_launches(const hetis_shape *shape, uint32_t flags);
 
 /* A per-request plan (f2: x_i^j varying with request j, the Eq. 7 dispatcher's
  * output) executed by ONE attention launch and ONE
@@ -311,7 +334,8 @@ HETIS_API hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_s
  *   workspace  : >= hetis_attn_decode_workspace(shape, num_units, r,
  *                max_seq_len) bytes, 256-B aligned, zero-filled before first use
  *   flags      : HETIS_ATTN_* except HETIS_ATTN_PIPELINED (-> UNSUPPORTED)
- * num_units == 0 launches nothing. */
+ * One kernel when hetis_attn_decode_launches says 1 and o rows are 16-byte
+ * aligned; else two.  num_units == 0 launches nothing. */
 HETIS_API hetis_status hetis_attn_decode_units(const hetis_shape *shape, int32_t num_seqs, int32_t num_units,
                                                const int32_t *units, const void *q, const void *k_new,
                                                const void *v_new, void *k_pool, void *v_pool, int64_t num_pages,
@@ -374,14 +398,39 @@ HETIS_API hetis_status hetis_scatter_pull(const hetis_peer_group *group, int32_t
                                           void *k_new_shard, void *v_new_shard, hetis_stream_t stream);
 /* a5 + a6 in ONE kernel: the split combine of this rank's heads (same
  * arithmetic as hetis_attn_combine) storing every row o[j][h] at its GLOBAL
- * head index into every receiving rank's o_full, then publishing the epoch to
- * them.  workspace: this step's hetis_attn_partial workspace. */
+ * head index into every receiving rank's o_full (after that rank acknowledged
+ * the previous step).  workspace: this step's hetis_attn_partial workspace. */
 HETIS_API hetis_status hetis_attn_combine_peers(const hetis_peer_group *group, int32_t num_seqs,
                                                 const int32_t *seq_lens, int32_t max_seq_len, void *workspace,
                                                 size_t workspace_bytes, hetis_stream_t stream);
-/* The step's last kernel: a receiving rank waits until every rank's rows of
- * this step are in its o_full; every rank then records the step as completed.
- * Work enqueued after it on the stream may read o_full. */
+/* a3 + a4 + a5 + a6 in ONE kernel: this rank's attention over its shard
+ * (hetis_attn_partial_append when k/v_new_shard are given, else
+ * hetis_attn_partial; q_shard [num_seqs][x][d], block table / pools / seq_lens
+ * as there) whose merge of each (request, kv head) pair's splits (the
+ * combine's arithmetic) stores the pair's rows straight into every receiving
+ * rank's o_full at the GLOBAL head index, after that rank acknowledged the
+ * previous step -- the work of hetis_attn_partial(_append) +
+ * hetis_attn_combine_peers, bit-identical, one launch.  One step per rank is
+ * then
+ *     hetis_scatter_pull -> hetis_attn_decode_peers -> hetis_peer_wait.
+ * It belongs to a step: before its first O store it waits (bounded, traps after
+ * ~10 s) for every receiving rank's acknowledgement published by that rank's
+ * hetis_scatter_pull of the same step, so it cannot be replayed alone.
+ * Only where hetis_attn_decode_launches(shape, flags | HETIS_ATTN_FUSED_MERGE)
+ * == 1 (the per-warp tensor-core kernel; the flag is implied) and the rank
+ * holds >= 1 head and >= 1 request; else HETIS_E_UNSUPPORTED (use the
+ * two-kernel path).  o_full rows 16-B aligned. */
+HETIS_API hetis_status hetis_attn_decode_peers(const hetis_peer_group *group, int32_t num_seqs, const void *q_shard,
+                                               const void *k_new_shard, const void *v_new_shard, void *k_pool,
+                                               void *v_pool, int64_t num_pages, const int32_t *block_table,
+                                               int32_t max_pages, const int32_t *seq_lens, int32_t max_seq_len,
+                                               void *workspace, size_t workspace_bytes, uint32_t flags,
+                                               hetis_stream_t stream);
+/* The step's last kernel: every rank publishes (one system-scope fence, then
+ * release stores) that the rows the previous kernel stored are in every
+ * receiving rank's o_full; a receiving rank then waits until every rank has
+ * published; every rank records the step as completed.  Work enqueued after it
+ * on the stream may read o_full. */
 HETIS_API hetis_status hetis_peer_wait(const hetis_peer_group *group, hetis_stream_t stream);
 
 /* ---- scatter / gather over NCCL ------------------- */

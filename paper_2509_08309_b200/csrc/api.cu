@@ -154,7 +154,8 @@ WorkspaceLayout workspace_layout(int num_seqs, int kv_heads, int r, int head_dim
     w.lse_offset = round256((size_t)(num_seqs + 1) * 4);
     w.o_offset = w.lse_offset + round256((size_t)w.max_items * r * 4);
     w.counter_offset = w.o_offset + round256((size_t)w.max_items * r * head_dim * 4);
-    w.total = w.counter_offset + 256;
+    w.pair_cnt_offset = w.counter_offset + 256;
+    w.total = w.pair_cnt_offset + round256((size_t)num_seqs * kv_heads * 4);
     return w;
 }
 }  // namespace hetis
@@ -417,7 +418,19 @@ static hetis_status attn_args(const hetis_shape *shape, int32_t num_seqs, int32_
     a->part_o = reinterpret_cast<float *>(ws + w.o_offset);
     a->max_items = w.max_items;
     a->counters = reinterpret_cast<int32_t *>(ws + w.counter_offset);
+    a->pair_cnt = reinterpret_cast<int32_t *>(ws + w.pair_cnt_offset);
     return HETIS_OK;
+}
+
+// HETIS_ATTN_FUSED_MERGE: the per-warp tensor-core kernel (bf16, r > 1 or HETIS_ATTN_MHA_TC) folds
+// each (request, kv head) pair's splits itself: the decode calls are then ONE launch.  Pipelined
+// steps keep the separate combine (its stream order keeps consecutive steps' O writes ordered).
+static bool fused_merge_ok(const hetis_shape *shape, uint32_t flags) {
+    const int r = shape->num_q_heads / shape->num_kv_heads;
+    return (flags & HETIS_ATTN_FUSED_MERGE) && shape->kv_dtype == HETIS_BF16 &&
+           (r > 1 || (flags & HETIS_ATTN_MHA_TC)) &&
+           !(flags & (HETIS_ATTN_FORCE_SIMT | HETIS_ATTN_TC_SHARED_RING | HETIS_ATTN_PIPELINED |
+                      HETIS_ATTN_DIAG_STREAM_ONLY));
 }
 
 static hetis_status attn_partial_impl(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
@@ -425,7 +438,7 @@ static hetis_status attn_partial_impl(const hetis_shape *shape, int32_t num_seqs
                                       const void *k_pool, const void *v_pool, int64_t num_pages,
                                       const int32_t *block_table, int32_t max_pages, const int32_t *seq_lens,
                                       int32_t max_seq_len, void *workspace, size_t workspace_bytes, uint32_t flags,
-                                      hetis_stream_t stream) {
+                                      hetis_stream_t stream, void *o_out = nullptr, int64_t o_seq_stride = 0) {
     hetis::AttnArgs a{};
     hetis_status st = attn_args(shape, num_seqs, q_head_begin, q_head_count, q, k_pool, v_pool, num_pages,
                                 block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes, &a);
@@ -434,6 +447,9 @@ static hetis_status attn_partial_impl(const hetis_shape *shape, int32_t num_seqs
     a.flags = flags;
     a.k_new = k_new;
     a.v_new = v_new;
+    a.o_out = o_out;
+    a.o_seq_stride = o_seq_stride;
+    a.o_dtype = shape->o_dtype;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const bool tc = a.dtype == HETIS_BF16 && (a.r > 1 || (flags & HETIS_ATTN_MHA_TC)) &&
                     !(flags & HETIS_ATTN_FORCE_SIMT);
@@ -591,6 +607,43 @@ hetis_status hetis_attn_combine_peers(const hetis_peer_group *g, int32_t num_seq
     return HETIS_OK;
 }
 
+hetis_status hetis_attn_decode_peers(const hetis_peer_group *g, int32_t num_seqs, const void *q_shard,
+                                     const void *k_new_shard, const void *v_new_shard, void *k_pool, void *v_pool,
+                                     int64_t num_pages, const int32_t *block_table, int32_t max_pages,
+                                     const int32_t *seq_lens, int32_t max_seq_len, void *workspace,
+                                     size_t workspace_bytes, uint32_t flags, hetis_stream_t stream) {
+    if (!g) return fail(HETIS_E_INVALID, "group is NULL");
+    const hetis_shape &s = g->shape;
+    flags |= HETIS_ATTN_FUSED_MERGE;
+    if (!fused_merge_ok(&s, flags))
+        return fail(HETIS_E_UNSUPPORTED, "the merge is fused only into the per-warp tensor-core kernel "
+                                         "(bf16, r > 1 or HETIS_ATTN_MHA_TC; see hetis_attn_decode_launches)");
+    if (g->q_count < 1) return fail(HETIS_E_UNSUPPORTED, "a rank without heads uses hetis_attn_combine_peers");
+    if (num_seqs < 1) return fail(HETIS_E_UNSUPPORTED, "no requests: use hetis_attn_combine_peers");
+    if ((k_new_shard == nullptr) != (v_new_shard == nullptr))
+        return fail(HETIS_E_INVALID, "pass both k_new_shard and v_new_shard, or neither");
+    if (k_new_shard && (!aligned(k_new_shard, 16) || !aligned(v_new_shard, 16)))
+        return fail(HETIS_E_INVALID, "k_new / v_new must be 16-B aligned");
+    if ((g->dev.o_seq_stride * esize(s.o_dtype)) % 16) return fail(HETIS_E_INVALID, "o_full rows must be 16-B aligned");
+    for (int p = 0; p < g->dev.n; ++p)
+        if (hetis::peer_is_target(g->dev, p) && !aligned(g->dev.o[p], 16))
+            return fail(HETIS_E_INVALID, "o_full must be 16-byte aligned");
+    hetis::AttnArgs a{};
+    hetis_status st = attn_args(&s, num_seqs, g->dev.head0, g->q_count, q_shard, k_pool, v_pool, num_pages,
+                                block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes, &a);
+    if (st != HETIS_OK) return st;
+    a.flags = flags;
+    a.k_new = k_new_shard;
+    a.v_new = v_new_shard;
+    a.o_dtype = s.o_dtype;
+    a.peer = &g->dev;
+    std::string err;
+    cudaError_t e = hetis::launch_attn_tc(a, reinterpret_cast<cudaStream_t>(stream), &err);
+    if (e != cudaSuccess)
+        return err.empty() ? cuda_fail(e, "attn_decode_peers launch") : fail(HETIS_E_CUDA, "attn_decode_peers: " + err);
+    return HETIS_OK;
+}
+
 hetis_status hetis_peer_wait(const hetis_peer_group *g, hetis_stream_t stream) {
     if (!g) return fail(HETIS_E_INVALID, "group is NULL");
     cudaError_t e = hetis::launch_peer_wait(g->dev, reinterpret_cast<cudaStream_t>(stream));
@@ -618,6 +671,11 @@ hetis_status hetis_scatter_pull(const hetis_peer_group *g, int32_t num_seqs, voi
     return HETIS_OK;
 }
 
+int32_t hetis_attn_decode_launches(const hetis_shape *shape, uint32_t flags) {
+    if (!shape || check_shape(shape) != HETIS_OK) return -1;
+    return fused_merge_ok(shape, flags) ? 1 : 2;
+}
+
 hetis_status hetis_attn_decode_append(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
                                       int32_t q_head_count, const void *q, const void *k_new, const void *v_new,
                                       void *k_pool, void *v_pool, int64_t num_pages, const int32_t *block_table,
@@ -625,6 +683,15 @@ hetis_status hetis_attn_decode_append(const hetis_shape *shape, int32_t num_seqs
                                       void *workspace, size_t workspace_bytes, uint32_t flags,
                                       hetis_stream_t stream) {
     if (!o && num_seqs > 0) return fail(HETIS_E_INVALID, "o is NULL");
+    if (shape && check_shape(shape) == HETIS_OK && fused_merge_ok(shape, flags)) {
+        if (num_seqs > 0 && (!k_new || !v_new)) return fail(HETIS_E_INVALID, "k_new / v_new is NULL");
+        if (!aligned(k_new, 16) || !aligned(v_new, 16))
+            return fail(HETIS_E_INVALID, "k_new / v_new must be 16-B aligned");
+        if (!aligned(o, 16)) return fail(HETIS_E_INVALID, "o must be 16-byte aligned");
+        return attn_partial_impl(shape, num_seqs, q_head_begin, q_head_count, q, k_new, v_new, k_pool, v_pool,
+                                 num_pages, block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes,
+                                 flags, stream, o, (int64_t)q_head_count * shape->head_dim);
+    }
     hetis_status st = hetis_attn_partial_append(shape, num_seqs, q_head_begin, q_head_count, q, k_new, v_new, k_pool,
                                                 v_pool, num_pages, block_table, max_pages, seq_lens, max_seq_len,
                                                 workspace, workspace_bytes, flags, stream);
@@ -639,6 +706,12 @@ hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_seqs, int32
                                int32_t max_seq_len, void *o, void *workspace, size_t workspace_bytes, uint32_t flags,
                                hetis_stream_t stream) {
     if (!o && num_seqs > 0) return fail(HETIS_E_INVALID, "o is NULL");
+    if (shape && check_shape(shape) == HETIS_OK && fused_merge_ok(shape, flags)) {
+        if (!aligned(o, 16)) return fail(HETIS_E_INVALID, "o must be 16-byte aligned");
+        return attn_partial_impl(shape, num_seqs, q_head_begin, q_head_count, q, nullptr, nullptr, k_pool, v_pool,
+                                 num_pages, block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes,
+                                 flags, stream, o, (int64_t)q_head_count * shape->head_dim);
+    }
     hetis_status st = hetis_attn_partial(shape, num_seqs, q_head_begin, q_head_count, q, k_pool, v_pool, num_pages,
                                          block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes,
                                          flags, stream);
@@ -682,6 +755,12 @@ hetis_status hetis_attn_decode_units(const hetis_shape *shape, int32_t num_seqs,
     a.v_new = v_new;
     a.units = units;
     a.row_kv_heads = Hkv;
+    const bool fused = fused_merge_ok(shape, flags) && aligned(o, 16) && (o_seq_stride * oe) % 16 == 0;
+    if (fused) {  // one launch: the merge runs in the per-warp kernel
+        a.o_out = o;
+        a.o_seq_stride = o_seq_stride;
+        a.o_dtype = shape->o_dtype;
+    }
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const bool tc = a.dtype == HETIS_BF16 && (a.r > 1 || (flags & HETIS_ATTN_MHA_TC)) &&
                     !(flags & HETIS_ATTN_FORCE_SIMT);
@@ -689,6 +768,7 @@ hetis_status hetis_attn_decode_units(const hetis_shape *shape, int32_t num_seqs,
     cudaError_t e = tc ? hetis::launch_attn_tc(a, s, &err) : hetis::launch_attn_simt(a, s);
     if (e != cudaSuccess)
         return err.empty() ? cuda_fail(e, "attn_decode_units launch") : fail(HETIS_E_CUDA, "attn_decode_units: " + err);
+    if (fused) return HETIS_OK;
     e = hetis::launch_combine(num_units, r, r, shape->head_dim, seq_lens, a.split_off, a.part_lse, a.part_o, o,
                               shape->o_dtype, o_seq_stride, s, nullptr, max_seq_len, units);
     if (e != cudaSuccess) return cuda_fail(e, "attn_decode_units combine launch");

@@ -38,6 +38,8 @@
 #include <utility>
 #include <vector>
 
+#include "combine_fold.cuh"
+#include "peer_sync.cuh"
 #include "device_utils.cuh"
 #include "hetis_internal.h"
 
@@ -141,6 +143,19 @@ struct Params {
     // rows are then addressed in the full [B][row_kv_heads] layout.  nullptr: row j = request j.
     const int32_t *units;
     int row_kv_heads;
+    // merge fused into the per-warp kernel (hetis_attn_decode / _append / _units): the last warp to
+    // finish a (request, kv head) pair folds its splits (combine_fold.cuh, the combine's arithmetic)
+    // and stores the pair's r output rows.  nullptr: partials only (the combine kernel merges).
+    void *o_out;
+    int64_t o_seq_stride;  // elements between requests in o_out (or in every o_full, peer mode)
+    int o_bf16;
+    int32_t *pair_cnt;     // [num_seqs * kv_heads] finished splits per pair; zero between launches
+    // peer mode (hetis_attn_decode_peers): the rows go to EVERY target rank's o_full at the GLOBAL head
+    // index o_head0 + local head, after that rank acknowledged the previous step's o_full; the last CTA
+    // then publishes the epoch to them (hetis_attn_combine_peers' protocol, folded into this kernel)
+    int peer_mode;
+    int o_head0;
+    PeerGroupDev peer;
 };
 
 // Row of (launch row j, local kv head g) in the q (x r), k_new / v_new and block-table layouts.
@@ -1126,9 +1141,91 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     }
 }
 
+// Fused-merge output: N consecutive floats of an O row at element index idx, into o_out -- or, in peer
+// mode, into every target rank's o_full (NVLink stores on an NVSwitch box).
+template <int N>
+__device__ __forceinline__ void put_out(const Params &p, size_t idx, const float (&v)[N]) {
+    static_assert(N == 2 || N == 4, "2 or 4 floats");
+    auto put = [&](void *base) {
+        if (p.o_bf16) {
+            __nv_bfloat16 *o = static_cast<__nv_bfloat16 *>(base) + idx;
+            if constexpr (N == 2) {
+                *reinterpret_cast<uint32_t *>(o) = dev::pack_bf16x2(v[0], v[1]);
+            } else {
+                *reinterpret_cast<uint2 *>(o) = make_uint2(dev::pack_bf16x2(v[0], v[1]), dev::pack_bf16x2(v[2], v[3]));
+            }
+        } else {
+            float *o = static_cast<float *>(base) + idx;
+            if constexpr (N == 2) {
+                *reinterpret_cast<float2 *>(o) = make_float2(v[0], v[1]);
+            } else {
+                *reinterpret_cast<float4 *>(o) = make_float4(v[0], v[1], v[2], v[3]);
+            }
+        }
+    };
+    if (!p.peer_mode) {
+        put(p.o_out);
+        return;
+    }
+    for (int t = 0; t < p.peer.n; ++t)
+        if (peer_is_target(p.peer, t)) put(p.peer.o[t]);
+}
+
+// Peer mode: before this warp's first O store, every target rank must have acknowledged that it
+// consumed the previous step's o_full (its scatter_pull of this step) -- bounded spin, once per warp.
+__device__ __forceinline__ void await_peer_acks(const Params &p, int64_t epoch, bool &acked, int lane) {
+    if (!p.peer_mode || acked) return;
+    if (lane < p.peer.n && peer_is_target(p.peer, lane))
+        spin_until_geq(p.peer.state[p.peer.rank] + kStAck + lane, epoch - 1);
+    __syncwarp();
+    acked = true;
+}
+
+// Fused merge: run by the warp that finished the last split of pair (j, g); lanes own 4 dims of a
+// row (D = 128: one row per pass, D = 64: two).  Same fold as the combine kernel.
+#ifndef HETIS_MERGE_ROWS
+#define HETIS_MERGE_ROWS 4
+#endif
+template <int D, int R>
+__device__ __forceinline__ void merge_pair_rows(const Params &p, int ns, int s0, int g, size_t obase, int lane) {
+    constexpr int TPH = D / 4, RPP = 32 / TPH;  // rows per pass
+    if (ns <= kNarrowSplits) {  // NR rows per memory round trip
+        constexpr int NR = (R / RPP) < HETIS_MERGE_ROWS ? (R / RPP > 0 ? R / RPP : 1) : HETIS_MERGE_ROWS;
+        const int sub = lane / TPH, d4 = lane % TPH;
+#pragma unroll 1
+        for (int rr0 = 0; rr0 < R; rr0 += RPP * NR) {
+            FoldState f[NR];
+            // lanes of row group `sub` take rows rr0 + sub * NR .. + NR - 1
+            const int rb = rr0 + sub * NR;
+            if (rb < R) {
+                fold_rows_narrow<D, true, NR>(ns, s0, p.kv_heads, g, R, rb, p.part_lse, p.part_o, d4, f);
+#pragma unroll
+                for (int k = 0; k < NR; ++k) {
+                    float lse2;
+                    const float4 acc = finish(f[k], &lse2);
+                    const float v[4] = {acc.x, acc.y, acc.z, acc.w};
+                    put_out<4>(p, obase + (size_t)(rb + k) * D + 4 * d4, v);
+                }
+            }
+        }
+        return;
+    }
+#pragma unroll 1
+    for (int rr0 = 0; rr0 < R; rr0 += RPP) {
+        const int rr = rr0 + lane / TPH, d4 = lane % TPH;
+        if (rr < R) {
+            float lse2;
+            const float4 acc =
+                fold_row<D, true>(ns, s0, p.kv_heads, g, R, rr, p.part_lse, p.part_o, d4, &lse2);
+            const float v[4] = {acc.x, acc.y, acc.z, acc.w};
+            put_out<4>(p, obase + (size_t)rr * D + 4 * d4, v);
+        }
+    }
+}
+
 template <int D, int R, int NW>
 __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW, int n_items, const void *tmap_k,
-                                    const void *tmap_v) {
+                                    const void *tmap_v, const int32_t *s_off) {
     constexpr int ROW_BYTES = D * 2;
     constexpr int kPageBytes = kP * ROW_BYTES;
     constexpr int kHalfBytes = kPageBytes / (D / 64);
@@ -1159,6 +1256,9 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     }
     RingPos pos{0, 0u};
     bool c_waited = false;  // this warp has executed griddepcontrol.wait (pipelined deferred pages)
+    const bool fused_out = p.o_out != nullptr || p.peer_mode;
+    const int64_t epoch = p.peer_mode ? current_epoch(p.peer) : 0;  // the previous step's peer_wait wrote it
+    bool acked = false;
     for (int it = 0;; ++it) {
 #ifdef HETIS_DEBUG_HANG
         {
@@ -1333,7 +1433,30 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         // the item's partial: o_s = acc / l and lse_s = m + log2(l) for each of the r heads
         l += __shfl_xor_sync(0xffffffffu, l, 1);
         l += __shfl_xor_sync(0xffffffffu, l, 2);
-        if (grp < R && !(p.flags & HETIS_ATTN_DIAG_STREAM_ONLY)) {
+        // fused merge: which pair, how many splits, where its O rows go
+        int ns = 0, s0 = 0, pair = 0, gk = 0;
+        size_t obase = 0;
+        if (fused_out) {
+            const int k = meta.item / p.kv_heads;
+            gk = meta.item - k * p.kv_heads;
+            const int j = upper_bound_smem(s_off, p.num_seqs + 1, k) - 1;
+            s0 = s_off[j];
+            ns = s_off[j + 1] - s0;
+            pair = j * p.kv_heads + gk;
+            const int jr = p.units != nullptr ? __ldg(p.units + 2 * j) : j;
+            const int gr = p.units != nullptr ? __ldg(p.units + 2 * j + 1) : gk;
+            obase = (size_t)jr * p.o_seq_stride + ((size_t)p.o_head0 + (size_t)gr * R) * D;
+        }
+        if (ns == 1) {  // one split: O = the partial, bit for bit (the fold of one split is exact)
+            await_peer_acks(p, epoch, acked, lane);
+            if (grp < R) {
+#pragma unroll
+                for (int nt = 0; nt < NT_O; ++nt) {
+                    const float v[2] = {__fdiv_rn(o[nt][0] + o[nt][2], l), __fdiv_rn(o[nt][1] + o[nt][3], l)};
+                    put_out<2>(p, obase + (size_t)grp * D + 8 * nt + 2 * tq, v);
+                }
+            }
+        } else if (grp < R && !(p.flags & HETIS_ATTN_DIAG_STREAM_ONLY)) {
             const size_t row = (size_t)meta.item * R + grp;
             float *dst = p.part_o + row * D;
 #if HETIS_PARTIAL_EVICT_LAST
@@ -1350,6 +1473,24 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
                     make_float2(__fdiv_rn(o[nt][0] + o[nt][2], l), __fdiv_rn(o[nt][1] + o[nt][3], l));
             if (tq == 0) p.part_lse[row] = m + __log2f(l);
 #endif
+        }
+        if (ns > 1) {  // publish this split; the pair's last split folds them all
+            __syncwarp();
+            int last = 0;
+            if (lane == 0) {
+                __threadfence();  // this warp's partial rows before the count
+                last = atomicAdd(p.pair_cnt + pair, 1) == ns - 1;
+                if (last) {
+                    p.pair_cnt[pair] = 0;  // zero again for the next launch
+                    __threadfence();       // every other split's rows are visible from here on
+                }
+            }
+            if (__shfl_sync(0xffffffffu, last, 0)) {
+                await_peer_acks(p, epoch, acked, lane);
+#ifndef HETIS_DIAG_SKIP_MERGE  // diagnostic builds only: the cost of the hand-off without the fold
+                merge_pair_rows<D, R>(p, ns, s0, gk, obase, lane);
+#endif
+            }
         }
     }
 }
@@ -1401,9 +1542,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     if (threadIdx.x < 32) {
         if (threadIdx.x < NW) producer_warp_items<ROW_BYTES, R, NW>(p, sm, SW, s_len, s_off, &tmap_k, &tmap_v);
     } else {
-        consumer_warp_items<D, R, NW>(p, sm, SW, n_items, &tmap_k, &tmap_v);
+        consumer_warp_items<D, R, NW>(p, sm, SW, n_items, &tmap_k, &tmap_v, s_off);
     }
-    // the last CTA to finish returns the device-wide counters to zero for the next launch
+    // the last CTA to finish returns the device-wide counters to zero for the next launch (in peer mode
+    // hetis_peer_wait, the next kernel, publishes the epoch once this grid has completed)
     __syncwarp();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1592,6 +1734,16 @@ Params make_params(const AttnArgs &a) {
     p.v_new = static_cast<const uint8_t *>(a.v_new);
     p.units = a.units;
     p.row_kv_heads = a.row_kv_heads;
+    p.o_out = a.o_out;
+    p.o_seq_stride = a.o_seq_stride;
+    p.o_bf16 = a.o_dtype == HETIS_BF16;
+    p.pair_cnt = a.pair_cnt;
+    if (a.peer != nullptr) {
+        p.peer_mode = 1;
+        p.peer = *a.peer;
+        p.o_head0 = a.peer->head0;
+        p.o_seq_stride = a.peer->o_seq_stride;
+    }
     return p;
 }
 
@@ -1677,6 +1829,10 @@ cudaError_t launch_attn_tc(const AttnArgs &a, cudaStream_t s, std::string *err) 
     // Default: whole items per warp (no per-item CTA merge); the shared-ring
     // kernel that splits every item over the CTA's warps stays selectable.
     const bool shared_ring = (a.flags & HETIS_ATTN_TC_SHARED_RING) != 0;
+    if (shared_ring && (a.o_out != nullptr || a.peer != nullptr)) {
+        if (err) *err = "the fused merge runs in the per-warp kernel only";
+        return cudaErrorInvalidValue;
+    }
     if (shared_ring) {
         if (a.head_dim == 128) return dispatch_r<HETIS_BF16, 128, true>(a, p, s, tk, tv, err);
         if (a.head_dim == 64) return dispatch_r<HETIS_BF16, 64, true>(a, p, s, tk, tv, err);

@@ -45,10 +45,18 @@ struct AttnArgs {
     // [requests][row_kv_heads] layout.  nullptr: launch row j = request j.
     const int32_t *units;
     int row_kv_heads;
+    // merge fused into the per-warp kernel: O rows of every (request, kv head) pair written by the
+    // pair's last split (nullptr: partials only, hetis_attn_combine merges)
+    void *o_out;
+    int64_t o_seq_stride;
+    int o_dtype;
+    int32_t *pair_cnt;    // [num_seqs * kv_heads], zero between launches (self-cleaning)
+    // fused merge + gather over peer memory: the rows go to every target rank's o_full (nullptr: o_out)
+    const struct PeerGroupDev *peer;
 };
 
 struct WorkspaceLayout {
-    size_t split_off_offset, lse_offset, o_offset, counter_offset, total;
+    size_t split_off_offset, lse_offset, o_offset, counter_offset, pair_cnt_offset, total;
     int64_t max_items;
 };
 
@@ -90,7 +98,7 @@ cudaError_t launch_head_copies(CopySegs &c, cudaStream_t s);
 // (read after stream ordering); hetis_peer_wait, the step's last kernel, stores it.
 constexpr int kMaxPeers = 8;
 constexpr int kStStep = 0;     // steps this rank has completed (written only by its own peer_wait)
-constexpr int kStDone = 8;     // block counter of combine_peers (local, self-cleaning)
+constexpr int kStDone = 8;     // reserved (was combine_peers' block counter; peer_wait publishes now)
 constexpr int kStIn = 16;      // the root's latest published input epoch
 constexpr int kStOut = 32;     // [kMaxPeers] epoch of rank p's rows now in this rank's o_full
 constexpr int kStAck = 48;     // [kMaxPeers] rank p has consumed its o_full through this epoch

@@ -12,6 +12,8 @@
 #include <set>
 #include <utility>
 
+#include "combine_fold.cuh"
+#include "peer_sync.cuh"
 #include "device_utils.cuh"
 #include "hetis_internal.h"
 
@@ -45,84 +47,13 @@ __global__ void kv_append_kernel(int num_seqs, int kv_heads, int row_bytes, int 
 }
 
 // ---------------------------------------------------------------- combine
-// o = sum_s 2^(lse_s - M) o_s / sum_s 2^(lse_s - M), M = max_s lse_s.
-// A "group" is D/4 threads, each owning 4 dims of the row.  A group folds its
-// splits in chunks of U: the chunk's lse and o rows are loaded together (one
-// memory round trip per chunk) and accumulated with an online max (rescale by
-// 2^(M_old - M_new)).  The arithmetic of a (request, head) pair depends on its
-// split count ns only (hence on L_j only), never on the launch shape:
-//   ns <= kNarrowSplits: one group folds s = 0 .. ns-1;
-//   ns >  kNarrowSplits: the G groups of a 128-thread block fold s = g, g + G,
-//                        ... and their states are merged in ascending g.
-// With one split, w = 2^0 = 1 and every other term is an exact zero, so
-// o = o_0 bit for bit.  Launch shapes: when every request of the batch has
-// <= kNarrowSplits splits, a block serves G pairs (one group each: few blocks,
-// one round trip per pair); otherwise a block serves one pair.
-constexpr int kCombineThreads = 128;
-#ifndef HETIS_COMBINE_CHUNK
-#define HETIS_COMBINE_CHUNK 8
-#endif
-constexpr int kCombineChunk = HETIS_COMBINE_CHUNK;
-constexpr int kNarrowSplits = 16;
+// The merge arithmetic lives in combine_fold.cuh (shared with the merge fused into the per-warp
+// attention kernel).  Launch shapes: when every request of the batch has <= kNarrowSplits splits,
+// a block serves G pairs (one group each: few blocks, one round trip per pair); otherwise a block
+// serves one pair and its G groups fold it together.
 #ifndef HETIS_COMBINE_DISCARD
 #define HETIS_COMBINE_DISCARD 0
 #endif
-
-struct FoldState {
-    float M, wsum;
-    float4 acc;
-};
-
-// fold splits s = first, first + step, ... < ns
-template <int D>
-__device__ __forceinline__ FoldState fold_splits(int first, int step, int ns, int s0, int kv_heads, int g, int r,
-                                                 int rr, const float *part_lse, const float *part_o, int d4) {
-    constexpr int U = kCombineChunk;
-    FoldState f{-INFINITY, 0.f, make_float4(0.f, 0.f, 0.f, 0.f)};
-    for (int base = first; base < ns; base += step * U) {
-        float l[U];
-        float4 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int sp = base + u * step;
-            if (sp < ns) {
-                const size_t rw = ((size_t)(s0 + sp) * kv_heads + g) * r + rr;
-                l[u] = part_lse[rw];
-                v[u] = reinterpret_cast<const float4 *>(part_o + rw * D)[d4];
-            } else {
-                l[u] = -INFINITY;
-                v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        }
-        float mc = l[0];  // finite: split `base` exists
-#pragma unroll
-        for (int u = 1; u < U; ++u) mc = fmaxf(mc, l[u]);
-        const float Mn = fmaxf(f.M, mc);
-        const float alpha = dev::ex2(f.M - Mn);  // 0 on the first chunk (M = -inf)
-        f.wsum *= alpha;
-        f.acc.x *= alpha;
-        f.acc.y *= alpha;
-        f.acc.z *= alpha;
-        f.acc.w *= alpha;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const float w = dev::ex2(l[u] - Mn);  // 0 for the padding (l = -inf)
-            f.wsum += w;
-            f.acc.x = fmaf(w, v[u].x, f.acc.x);
-            f.acc.y = fmaf(w, v[u].y, f.acc.y);
-            f.acc.z = fmaf(w, v[u].z, f.acc.z);
-            f.acc.w = fmaf(w, v[u].w, f.acc.w);
-        }
-        f.M = Mn;
-    }
-    return f;
-}
-
-__device__ __forceinline__ float4 finish(const FoldState &f, float *lse2_out) {
-    *lse2_out = f.M + log2f(f.wsum);
-    return make_float4(__fdiv_rn(f.acc.x, f.wsum), __fdiv_rn(f.acc.y, f.wsum), __fdiv_rn(f.acc.z, f.wsum),
-                       __fdiv_rn(f.acc.w, f.wsum));
-}
 
 // Narrow pair: folded by ONE group (the calling group); no block barrier.
 template <int D>
@@ -170,38 +101,15 @@ __device__ __forceinline__ float4 combine_wide(int j, int h, int q_heads, int r,
         s_w[grp] = f.wsum;
     }
     __syncthreads();
-    float Mall = s_m[0];
+    float m[G], w[G];
+    float4 a[G];
 #pragma unroll
-    for (int k = 1; k < G; ++k) Mall = fmaxf(Mall, s_m[k]);
-    FoldState t;
-    const float f0 = dev::ex2(s_m[0] - Mall);
-    const float4 a0 = s_acc[0][d4];
-    t.acc = make_float4(f0 * a0.x, f0 * a0.y, f0 * a0.z, f0 * a0.w);
-    t.wsum = f0 * s_w[0];
-#pragma unroll
-    for (int k = 1; k < G; ++k) {
-        const float fk = dev::ex2(s_m[k] - Mall);  // every group holds >= 1 split here (ns > G)
-        const float4 ak = s_acc[k][d4];
-        t.acc.x = fmaf(fk, ak.x, t.acc.x);
-        t.acc.y = fmaf(fk, ak.y, t.acc.y);
-        t.acc.z = fmaf(fk, ak.z, t.acc.z);
-        t.acc.w = fmaf(fk, ak.w, t.acc.w);
-        t.wsum = fmaf(fk, s_w[k], t.wsum);
+    for (int k = 0; k < G; ++k) {
+        m[k] = s_m[k];
+        w[k] = s_w[k];
+        a[k] = s_acc[k][d4];
     }
-    t.M = Mall;
-    return finish(t, lse2_out);
-}
-
-template <int OUT_BF16>
-__device__ __forceinline__ void store_row4(void *o, size_t idx, float4 acc) {
-    if (OUT_BF16) {
-        uint2 pk;
-        pk.x = dev::pack_bf16x2(acc.x, acc.y);
-        pk.y = dev::pack_bf16x2(acc.z, acc.w);
-        *reinterpret_cast<uint2 *>(static_cast<__nv_bfloat16 *>(o) + idx) = pk;
-    } else {
-        *reinterpret_cast<float4 *>(static_cast<float *>(o) + idx) = acc;
-    }
+    return finish(merge_groups<G>(m, w, a), lse2_out);
 }
 
 // lse (optional, natural log, [num_seqs][q_heads]): ln sum_t exp(q.k_t / sqrt(d)) of
@@ -232,35 +140,7 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(int num_seqs, 
 }
 
 // ---------------------------------------------------------------- exchanges over peer memory
-// System-scope acquire / release on int64 epochs (every rank's state is mapped
-// into every process: NVLink peer memory on an NVSwitch box).
-__device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
-    int64_t v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_sys(int64_t *p, int64_t v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-// Bounded spin: a peer that never publishes makes the kernel trap after ~10 s
-// (the error surfaces on the stream) instead of hanging the device.
-__device__ __forceinline__ void spin_until_geq(const int64_t *p, int64_t v) {
-    if (ld_acquire_sys(p) >= v) return;
-    unsigned long long t0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    for (;;) {
-        __nanosleep(128);
-        if (ld_acquire_sys(p) >= v) return;
-        unsigned long long t1;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        if (t1 - t0 > 10000000000ull) __trap();
-    }
-}
-// Epoch of the step in flight: this rank's completed steps + 1 (the state word
-// is written only by this rank's own hetis_peer_wait, earlier on the stream).
-__device__ __forceinline__ int64_t current_epoch(const PeerGroupDev &g) {
-    return *reinterpret_cast<volatile const int64_t *>(g.state[g.rank] + kStStep) + 1;
-}
+// (system-scope epoch helpers: peer_sync.cuh)
 
 // Combine fused with the all-gather over peer memory: each merged O row is
 // stored straight into every target rank's o_full at its GLOBAL head index
@@ -276,44 +156,47 @@ __global__ void __launch_bounds__(kCombineThreads) combine_peers_kernel(int num_
     const int64_t e = current_epoch(g);
     constexpr int TPH = D / 4, G = kCombineThreads / TPH;
     const int grp = threadIdx.x / TPH, d4 = threadIdx.x % TPH;
-    const int64_t flat = WIDE ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * G + grp;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    int j = 0, h = 0;
-    const bool live = flat < (int64_t)num_seqs * q_heads;
-    if (live) {
-        j = (int)(flat / q_heads);
-        h = (int)(flat - (int64_t)j * q_heads);
-        float lse2;
-        acc = WIDE ? combine_wide<D>(j, h, q_heads, r, split_off, part_lse, part_o, &lse2)
-                   : combine_narrow<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4, &lse2);
-    }
     // rank p may still read the previous step's o_full until it acknowledges (its scatter_pull of this step)
     if (threadIdx.x < g.n && peer_is_target(g, threadIdx.x)) spin_until_geq(g.state[g.rank] + kStAck + threadIdx.x, e - 1);
     __syncthreads();
-    if (live && (!WIDE || grp == 0)) {
-        const size_t idx = (size_t)j * g.o_seq_stride + (size_t)(g.head0 + h) * D + 4 * d4;
-        for (int p = 0; p < g.n; ++p)
-            if (peer_is_target(g, p)) store_row4<OUT_BF16>(g.o[p], idx, acc);
-    }
-    __syncthreads();  // the block's peer stores happen-before thread 0's system-scope fence (cumulative) ...
-    if (threadIdx.x == 0) {  // ... which orders them before the block is counted
-        __threadfence_system();
-        int64_t *done = g.state[g.rank] + kStDone;
-        if (atomicAdd(reinterpret_cast<unsigned long long *>(done), 1ull) == (unsigned long long)gridDim.x - 1) {
-            __threadfence_system();
+    // one row per group (narrow) or per block (wide); the grid-stride loop only matters for huge launches
+    const int64_t total = (int64_t)num_seqs * q_heads;
+    const int64_t first = WIDE ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * G + grp;
+    const int64_t stride = WIDE ? (int64_t)gridDim.x : (int64_t)gridDim.x * G;
+    for (int64_t flat = first; WIDE ? flat < total : true; flat += stride) {
+        if (!WIDE && flat >= total) break;
+        const int j = (int)(flat / q_heads);
+        const int h = (int)(flat - (int64_t)j * q_heads);
+        float lse2;
+        const float4 acc = WIDE ? combine_wide<D>(j, h, q_heads, r, split_off, part_lse, part_o, &lse2)
+                                : combine_narrow<D>(j, h, q_heads, r, split_off, part_lse, part_o, d4, &lse2);
+        if (!WIDE || grp == 0) {
+            const size_t idx = (size_t)j * g.o_seq_stride + (size_t)(g.head0 + h) * D + 4 * d4;
             for (int p = 0; p < g.n; ++p)
-                if (peer_is_target(g, p)) st_release_sys(g.state[p] + kStOut + g.rank, e);
-            *done = 0;  // self-cleaning for the next step
+                if (peer_is_target(g, p)) store_row4<OUT_BF16>(g.o[p], idx, acc);
         }
+        if (WIDE) __syncthreads();  // combine_wide's shared state is reused by the next row
     }
+    // no per-block completion protocol: hetis_peer_wait, the next kernel on this rank's stream, publishes
+    // the epoch after this grid has completed (one system-scope fence per step instead of one per block)
 }
 
-// The step's last kernel: a target rank waits (acquire, bounded) until every
-// rank published this epoch's rows into its o_full; every rank then records the
-// step as completed (the next step's kernels derive their epoch from it).
+// The step's last kernel.  Every rank first publishes that its rows of this
+// epoch are in every target's o_full: the kernel that stored them (the combine,
+// or the attention kernel with the merge fused) has completed before
+// griddepcontrol.wait returns, so its stores happen-before this thread's
+// system-scope fence, which orders them before the release stores of the epoch
+// into the targets' kStOut slots.  A target rank then waits (acquire, bounded)
+// until every rank has published, and every rank records the step as completed
+// (the next step's kernels derive their epoch from it).
 __global__ void peer_wait_kernel(PeerGroupDev g) {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL launch: the combine before it has completed
     const int64_t e = current_epoch(g);
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int p = 0; p < g.n; ++p)
+            if (peer_is_target(g, p)) st_release_sys(g.state[p] + kStOut + g.rank, e);
+    }
     if ((int)threadIdx.x < g.n && peer_is_target(g, g.rank)) spin_until_geq(g.state[g.rank] + kStOut + threadIdx.x, e);
     __syncthreads();
     if (threadIdx.x == 0) g.state[g.rank][kStStep] = e;
@@ -374,9 +257,7 @@ __global__ void scatter_pull_kernel(PeerGroupDev g, int num_seqs, int H, int Hkv
     const int qc = qrow / 16, kc = kvrow / 16;
     const int64_t nq_chunks = (int64_t)num_seqs * nq * qc, nk_chunks = (int64_t)num_seqs * nk * kc;
     const int64_t total = nq_chunks + 2 * nk_chunks;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint8_t *src;
-        uint8_t *dst;
+    auto addr = [&](int64_t i, const uint8_t *&src, uint8_t *&dst) {
         if (i < nq_chunks) {
             const int c = (int)(i % qc);
             const int64_t row = i / qc;
@@ -392,11 +273,27 @@ __global__ void scatter_pull_kernel(PeerGroupDev g, int num_seqs, int H, int Hkv
             src = (is_v ? g.v_root : g.k_root) + ((size_t)j * Hkv + k0 + h) * kvrow + 16 * c;
             dst = (is_v ? v_dst : k_dst) + ((size_t)j * nk + h) * kvrow + 16 * c;
         }
-        uint4 v;
-        asm volatile("ld.relaxed.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                     : "l"(src));
-        *reinterpret_cast<uint4 *>(dst) = v;
+    };
+    // the root's epoch was acquired above (thread 0, then the barrier): plain L2 loads (.cg, never a stale L1
+    // line of the previous step), four 16-byte chunks in flight per thread
+    constexpr int U = 4;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += U * step) {
+        uint4 v[U];
+        uint8_t *dst[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + u * step;
+            dst[u] = nullptr;
+            if (i < total) {
+                const uint8_t *src;
+                addr(i, src, dst[u]);
+                v[u] = __ldcg(reinterpret_cast<const uint4 *>(src));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (dst[u] != nullptr) *reinterpret_cast<uint4 *>(dst[u]) = v[u];
     }
 }
 
@@ -502,8 +399,8 @@ cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim,
     const int64_t pairs = (int64_t)num_seqs * q_heads;
     const bool wide = (max_seq_len + kSplitTokens - 1) / kSplitTokens > kNarrowSplits;
     const int gsz = kCombineThreads / (head_dim / 4);
-    int64_t blocks = wide ? pairs : (pairs + gsz - 1) / gsz;
-    if (blocks < 1) blocks = 1;  // an empty shard still publishes the epoch
+    int64_t blocks = wide ? pairs : (pairs + gsz - 1) / gsz;  // every row in flight at once (one fold each)
+    if (blocks < 1) blocks = 1;
     const bool bf = o_dtype == HETIS_BF16;
     decltype(&combine_peers_kernel<128, 0, false>) kern;
     if (head_dim == 128)

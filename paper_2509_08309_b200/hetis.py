@@ -28,6 +28,7 @@ ATTN_TC_SHARED_RING = 0x2
 ATTN_DEVICE_CLAIM = 0x4
 ATTN_MHA_TC = 0x8
 ATTN_PIPELINED = 0x10
+ATTN_FUSED_MERGE = 0x20
 ATTN_DIAG_STREAM_ONLY = 0x100
 
 EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_split_tokens",
@@ -38,7 +39,8 @@ EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_
             "hetis_attn_combine_lse", "hetis_seq_split_lens", "hetis_seq_merge", "hetis_seq_broadcast_q",
             "hetis_seq_allgather_merge", "hetis_peer_state_bytes", "hetis_peer_group_create",
             "hetis_peer_group_destroy", "hetis_scatter_pull", "hetis_attn_partial_append",
-            "hetis_attn_decode_append", "hetis_check_tables", "hetis_launch_count", "hetis_attn_decode_units")
+            "hetis_attn_decode_append", "hetis_check_tables", "hetis_launch_count", "hetis_attn_decode_units",
+            "hetis_attn_decode_launches", "hetis_attn_decode_peers")
 
 
 class HetisError(RuntimeError):
@@ -109,6 +111,9 @@ def lib() -> ctypes.CDLL:
                 "hetis_attn_decode_append": (ctypes.c_int, [sp, i32, i32, i32, vp, vp, vp, vp, vp, i64, vp, i32, vp,
                                                             i32, vp, vp, sz, u32, vp]),
                 "hetis_scatter_pull": (ctypes.c_int, [vp, i32, vp, vp, vp, vp]),
+                "hetis_attn_decode_launches": (i32, [sp, u32]),
+                "hetis_attn_decode_peers": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, vp, i64, vp, i32, vp, i32, vp, sz,
+                                                           u32, vp]),
                 "hetis_attn_decode_units": (ctypes.c_int, [sp, i32, i32, vp, vp, vp, vp, vp, vp, i64, vp, i32, vp,
                                                            i32, vp, i64, vp, sz, u32, vp]),
             }
@@ -394,6 +399,14 @@ def attn_decode_append(shape: CShape, q, k_new, v_new, k_pool, v_pool, block_tab
                                           flags, _stream(stream)), "hetis_attn_decode_append")
 
 
+def attn_decode_launches(shape: CShape, flags: int = 0) -> int:
+    """1 when hetis_attn_decode(_append) fuses the split merge into the attention kernel, else 2."""
+    n = lib().hetis_attn_decode_launches(ctypes.byref(shape), flags)
+    if n < 0:
+        raise ValueError("invalid shape")
+    return n
+
+
 def attn_decode_units(shape: CShape, units, q, k_pool, v_pool, block_table, seq_lens, max_seq_len: int, o,
                       workspace, k_new=None, v_new=None, flags: int = 0, stream=None) -> None:
     """A per-request plan's units on the full layouts in one attention launch + one combine
@@ -482,6 +495,19 @@ def attn_combine_peers(group: PeerGroup, seq_lens, max_seq_len: int, workspace, 
     _check(lib().hetis_attn_combine_peers(group.handle, seq_lens.shape[0], _dev(seq_lens, "seq_lens"), max_seq_len,
                                           _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(),
                                           _stream(stream)), "hetis_attn_combine_peers")
+
+
+def attn_decode_peers(group: PeerGroup, q_shard, k_pool, v_pool, block_table, seq_lens, max_seq_len: int, workspace,
+                      k_new_shard=None, v_new_shard=None, flags: int = 0, stream=None) -> None:
+    """a3 + a4 + a5 + a6 in one kernel: attention (append fused when k/v_new_shard are given) whose split
+    merge stores every row into every receiving rank's o_full and publishes the epoch (hetis_attn_decode_peers)."""
+    _check(lib().hetis_attn_decode_peers(group.handle, q_shard.shape[0], _dev(q_shard, "q_shard"),
+                                         _dev(k_new_shard, "k_new_shard"), _dev(v_new_shard, "v_new_shard"),
+                                         _dev(k_pool, "k_pool"), _dev(v_pool, "v_pool"), k_pool.shape[0],
+                                         _dev(block_table, "block_table"), block_table.shape[2],
+                                         _dev(seq_lens, "seq_lens"), max_seq_len, _dev(workspace, "workspace"),
+                                         workspace.numel() * workspace.element_size(), flags, _stream(stream)),
+           "hetis_attn_decode_peers")
 
 
 def peer_wait(group: PeerGroup, stream=None) -> None:

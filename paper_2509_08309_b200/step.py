@@ -143,10 +143,26 @@ class DecodeStep:
         first publishes that this step's inputs are written).  One kernel."""
         hetis.scatter_pull(self.group, self.num_seqs, self.buf.q_shard, self.buf.k_new, self.buf.v_new, stream=stream)
 
+    def merge_fused(self, flags: int = 0) -> bool:
+        """True when the attention kernel itself merges the splits and stores O into every receiving rank
+        (hetis_attn_decode_peers: the per-warp tensor-core kernel, a rank holding heads)."""
+        return self.q_count > 0 and self.num_seqs > 0 and hetis.attn_decode_launches(
+            self.cshape, flags | hetis.ATTN_FUSED_MERGE) == 1
+
     def attention_gather_peers(self, k_pool, v_pool, block_table, seq_lens, stream=None, flags: int = 0,
-                               fused_append: bool = True):
-        """Partial attention (kv_append fused by default), then ONE kernel that merges the splits and stores
-        every row into every receiving rank's o_full, then the step's closing wait.  Returns o_full."""
+                               fused_append: bool = True, merge_fused: bool | None = None):
+        """Attention (kv_append fused by default) whose split merge stores every row into every receiving
+        rank's o_full -- ONE kernel (hetis_attn_decode_peers) where the per-warp kernel runs, else the partial
+        kernel + hetis_attn_combine_peers -- then the step's closing wait.  Returns o_full."""
+        if merge_fused is None:                 # opt-in: measured slower than the separate combine (DESIGN §6)
+            merge_fused = bool(flags & hetis.ATTN_FUSED_MERGE) and self.merge_fused(flags)
+        if merge_fused:
+            hetis.attn_decode_peers(self.group, self.buf.q_shard, k_pool, v_pool, block_table, seq_lens,
+                                    self.max_seq_len, self.buf.workspace,
+                                    k_new_shard=self.buf.k_new if fused_append else None,
+                                    v_new_shard=self.buf.v_new if fused_append else None, flags=flags, stream=stream)
+            hetis.peer_wait(self.group, stream=stream)
+            return self.o_full
         if fused_append:
             hetis.attn_partial_append(self.cshape, self.buf.q_shard, self.buf.k_new, self.buf.v_new, k_pool, v_pool,
                                       block_table, seq_lens, self.max_seq_len, self.buf.workspace,
@@ -159,8 +175,10 @@ class DecodeStep:
         hetis.peer_wait(self.group, stream=stream)
         return self.o_full
 
-    def step_peers(self, k_pool, v_pool, block_table, seq_lens, stream=None, flags: int = 0):
-        """The whole N > 1 step over peer memory: pull scatter, attention with the append, combine + gather,
-        closing wait (four kernels, no NCCL, no per-step host argument: graph-capturable)."""
+    def step_peers(self, k_pool, v_pool, block_table, seq_lens, stream=None, flags: int = 0,
+                   merge_fused: bool | None = None):
+        """The whole N > 1 step over peer memory: pull scatter, attention with the append and the merge +
+        gather (one kernel, or two), closing wait -- no NCCL, no per-step host argument: graph-capturable."""
         self.scatter_peers(stream)
-        return self.attention_gather_peers(k_pool, v_pool, block_table, seq_lens, stream=stream, flags=flags)
+        return self.attention_gather_peers(k_pool, v_pool, block_table, seq_lens, stream=stream, flags=flags,
+                                           merge_fused=merge_fused)

@@ -9,6 +9,10 @@ requests at fixed heads and cache (fig:execution_time_modeling (a)
 h = query heads resident on the device (sum over requests), g = cached K/V
 head-vectors (2 * tokens * kv heads, Eq. 8's unit).  tau = one decode step's
 hetis_attn_partial + hetis_attn_combine, CUDA-graph replayed, KV larger than L2.
+Negative fitted terms are clamped to 0 and refitted.  Accuracy
+is reported over the grid, over its small-share half (the steps of a device in
+an 8-way split, where the fixed cost c dominates -- reported with its minimum,
+not only the mean) and for a separate fit of that half.
 
     python scripts/cost_model_fit.py [--shape 13b|70b] > gpurun_out/cost_model.json
 """
@@ -85,9 +89,15 @@ def main():
     h = np.array([q["h"] for q in rows], dtype=np.float64)
     g = np.array([q["g"] for q in rows], dtype=np.float64)
     tau = np.array([q["tau_s"] for q in rows])
-    m = dispatch.fit_attention_cost(h, g, tau)
+    m = dispatch.fit_attention_cost(h, g, tau)          # OLS, negative terms clamped to 0 and refitted
     pred = np.array([m.attention_time(hh, gg) for hh, gg in zip(h, g)])
     acc = dispatch.model_accuracy(pred, tau)
+    # the small-share regime (the half of the grid with the shortest steps -- where a device of an
+    # 8-way split lives and where the fixed cost c dominates) reported on its own, and fitted on its own
+    small = tau <= np.median(tau)
+    m_small = dispatch.fit_attention_cost(h[small], g[small], tau[small])
+    acc_small_own = dispatch.model_accuracy(
+        [m_small.attention_time(hh, gg) for hh, gg in zip(h[small], g[small])], tau[small])
     # batch independence at fixed h and g (fig:execution_time_modeling (a))
     hx = shape.num_q_heads * 16
     batch_rows = []
@@ -104,6 +114,12 @@ def main():
         "fit": {"a_s_per_head": m.a, "b_s_per_headvector": m.b, "c_s": m.c,
                 "implied_GBps_from_b": shape.head_dim * shape.elem_bytes / m.b / 1e9},
         "accuracy": {"mean": float(acc.mean()), "min": float(acc.min()), "max": float(acc.max())},
+        "accuracy_small_share": {"tau_max_us": float(tau[small].max() * 1e6), "points": int(small.sum()),
+                                 "mean": float(acc[small].mean()), "min": float(acc[small].min())},
+        "accuracy_large_share": {"mean": float(acc[~small].mean()), "min": float(acc[~small].min())},
+        "fit_small_share": {"a_s_per_head": m_small.a, "b_s_per_headvector": m_small.b, "c_s": m_small.c,
+                            "accuracy_mean": float(acc_small_own.mean()),
+                            "accuracy_min": float(acc_small_own.min())},
         "batch_independence": {"rows": batch_rows,
                                "spread_pct": float(100 * (bt.max() - bt.min()) / bt.mean()) if len(bt) else None},
     }

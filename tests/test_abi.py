@@ -29,7 +29,7 @@ def declared_symbols():
 
 def test_every_declared_symbol_is_exported(L):
     syms = declared_symbols()
-    assert len(syms) == 35
+    assert len(syms) == 37
     for s in syms:
         assert hasattr(L, s), s
     assert set(syms) == set(hetis.EXPORTED)
@@ -135,7 +135,8 @@ def test_workspace_formula(L):
     n = hetis.attn_decode_workspace(SHAPE_13B, 64, 40, 4096)
     items = 64 * (4096 // C) * 40
     r256 = lambda b: (b + 255) // 256 * 256
-    assert n == r256(65 * 4) + r256(items * 4) + r256(items * 128 * 4) + 256     # + work-claim counters
+    # split offsets + partial lse + partial o + work-claim counters + per-pair split counters (fused merge)
+    assert n == r256(65 * 4) + r256(items * 4) + r256(items * 128 * 4) + 256 + r256(64 * 40 * 4)
     with pytest.raises(hetis.HetisError) as e:
         hetis.attn_decode_workspace(SHAPE_70B, 64, 12, 4096)     # 12 heads = 1.5 kv groups
     assert e.value.name == "HETIS_E_GROUP_ALIGN"

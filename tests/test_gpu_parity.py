@@ -347,10 +347,12 @@ def test_per_request_plan_units_bit_identical_to_unsplit():
     assert_close(assembled, oracle_full(full), "per-request plan")
 
 
-@pytest.mark.parametrize("H,Hkv,D,dtype,fused", [(64, 8, 128, "bf16", True), (40, 40, 128, "bf16", True),
-                                                 (16, 4, 64, "bf16", False), (8, 8, 64, "f32", False),
-                                                 (16, 2, 128, "f32", False)])
-def test_units_random_plans_all_kernels(H, Hkv, D, dtype, fused):
+@pytest.mark.parametrize("H,Hkv,D,dtype,fused,flags", [(64, 8, 128, "bf16", True, 0), (40, 40, 128, "bf16", True, 0),
+                                                       (16, 4, 64, "bf16", False, 0), (8, 8, 64, "f32", False, 0),
+                                                       (16, 2, 128, "f32", False, 0),
+                                                       (64, 8, 128, "bf16", True, hetis.ATTN_FUSED_MERGE),
+                                                       (16, 4, 64, "bf16", False, hetis.ATTN_FUSED_MERGE)])
+def test_units_random_plans_all_kernels(H, Hkv, D, dtype, fused, flags):
     """hetis_attn_decode_units on random per-request plans over 3 devices, every kernel family (per-warp
     tensor-core GQA, CUDA-core MHA, fp32): the union of the devices' outputs is bit-identical to the unsplit
     single-launch result, and with the append fused the pools end bit-identical to hetis_kv_append's."""
@@ -368,7 +370,7 @@ def test_units_random_plans_all_kernels(H, Hkv, D, dtype, fused):
         ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, max(U, 1), r, full.max_seq_len), "cuda")
         b = fresh if fused else full
         hetis.attn_decode_units(s, units, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, b.max_seq_len, out, ws,
-                                k_new=b.k_new if fused else None, v_new=b.v_new if fused else None)
+                                k_new=b.k_new if fused else None, v_new=b.v_new if fused else None, flags=flags)
     torch.cuda.synchronize()
     assert torch.equal(out, o_full)
     if fused:
@@ -527,6 +529,41 @@ def test_fused_append_bit_identical_to_append_then_attention(H, Hkv, D, dtype, f
     hetis.attn_decode(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, o2, ws, flags=flags)
     torch.cuda.synchronize()
     assert torch.equal(o2, o_ref)
+
+
+FM = hetis.ATTN_FUSED_MERGE
+
+
+@pytest.mark.parametrize("H,Hkv,D,flags,odt", [(64, 8, 128, FM, "f32"), (16, 2, 128, FM, "f32"), (16, 4, 64, FM, "f32"),
+                                              (8, 1, 128, FM, "bf16"), (40, 40, 128, FM | hetis.ATTN_MHA_TC, "f32"),
+                                              (8, 4, 128, FM | hetis.ATTN_DEVICE_CLAIM, "bf16")])
+def test_merge_fused_into_attention_bit_identical_to_combine_kernel(H, Hkv, D, flags, odt):
+    """hetis_attn_decode with HETIS_ATTN_FUSED_MERGE and the per-warp tensor-core kernel is ONE launch: the
+    last warp of a (request, kv head) pair folds the pair's splits (one split: the rows straight from registers).  Its O is bit-identical
+    to the two-kernel path (hetis_attn_partial + hetis_attn_combine) for one split, the narrow fold (<= 16
+    splits) and the wide fold (17, 20, 36 splits), and a second launch on the same workspace (the per-pair
+    counters returned to zero) repeats it."""
+    lens = EDGE_LENS + (4097, 5000, 9000)
+    b = gpu_batch(H, Hkv, D, "bf16", lens, seed=123)
+    s = hetis.make_shape(b.shape, odt)
+    assert hetis.attn_decode_launches(s, flags) == 1
+    B, x, _ = b.q.shape
+    L = b.max_seq_len
+    hetis.kv_append(s, b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens)
+    odtype = torch.bfloat16 if odt == "bf16" else torch.float32
+    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), "cuda")
+    ref = torch.full((B, x, D), float("nan"), dtype=odtype, device="cuda")
+    hetis.attn_partial(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, ws, flags=flags)
+    hetis.attn_combine(s, b.seq_lens, L, ref, ws)
+    for rep in range(2):
+        got = torch.full_like(ref, float("nan"))
+        n0 = hetis.launch_count()
+        hetis.attn_decode(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, got, ws, flags=flags)
+        assert hetis.launch_count() - n0 == 1
+        torch.cuda.synchronize()
+        assert torch.equal(got.view(torch.int16), ref.view(torch.int16)), rep
+    if odt == "f32":
+        assert_close(got, oracle_full(b), "fused merge")
 
 
 def test_decode_step_fused_append_matches_separate_calls():

@@ -30,7 +30,7 @@ LENS = (300, 17, 1029, 2048, 5, 256, 1)
 EAGER_STEPS, GRAPH_STEPS, GRAPH_REPLAYS = 3, 2, 2
 
 
-def _rank(rank, world, rendezvous, shape_args, split, gather_root, res):
+def _rank(rank, world, rendezvous, shape_args, split, gather_root, merge_fused, res):
     import torch
     import torch.distributed as dist
     from paper_2509_08309_b200 import hetis, workload
@@ -58,7 +58,7 @@ def _rank(rank, world, rendezvous, shape_args, split, gather_root, res):
         def one_step():
             if rank == 0:
                 q_full.neg_()                   # the step's new inputs, written before the root's pull
-            step.step_peers(mine.k_pool, mine.v_pool, mine.block_table, mine.seq_lens)
+            step.step_peers(mine.k_pool, mine.v_pool, mine.block_table, mine.seq_lens, merge_fused=merge_fused)
 
         for _ in range(EAGER_STEPS):
             one_step()
@@ -100,23 +100,28 @@ def _rank(rank, world, rendezvous, shape_args, split, gather_root, res):
         dist.destroy_process_group()
 
 
+# merge_fused: True = hetis_attn_decode_peers (attention, split merge and the stores into every rank's
+# o_full in ONE kernel), False / None = partial kernel + hetis_attn_combine_peers (the default)
 CASES = [
-    ((64, 8, 128, 16, "bf16"), (32, 32), -1),                 # even GQA, all-gather
-    ((40, 40, 128, 16, "bf16"), (16, 8, 8, 4, 4), -1),        # c4's uneven split, all-gather
-    ((64, 8, 128, 16, "bf16"), (16, 16, 24, 8), 0),           # uneven GQA, gather to the Primary (paper)
-    ((8, 8, 64, 16, "f32"), (4, 4), -1),                      # c1 shape, fp32
+    ((64, 8, 128, 16, "bf16"), (32, 32), -1, None),           # even GQA, all-gather
+    ((64, 8, 128, 16, "bf16"), (32, 32), -1, True),           # the same with the merge + gather fused
+    ((40, 40, 128, 16, "bf16"), (16, 8, 8, 4, 4), -1, None),  # c4's uneven split, all-gather (CUDA-core MHA)
+    ((64, 8, 128, 16, "bf16"), (16, 16, 24, 8), 0, None),     # uneven GQA, gather to the Primary (paper)
+    ((64, 8, 128, 16, "bf16"), (16, 16, 24, 8), 0, True),     # ... fused
+    ((16, 2, 64, 16, "bf16"), (8, 8), -1, True),              # GQA d = 64, fused
+    ((8, 8, 64, 16, "f32"), (4, 4), -1, None),                # c1 shape, fp32
 ]
 
 
-@pytest.mark.parametrize("shape_args,split,gather_root", CASES)
-def test_peer_step_n_ranks_one_gpu(shape_args, split, gather_root):
+@pytest.mark.parametrize("shape_args,split,gather_root,merge_fused", CASES)
+def test_peer_step_n_ranks_one_gpu(shape_args, split, gather_root, merge_fused):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     world = len(split)
     rendezvous = os.path.join(tempfile.mkdtemp(), "rendezvous")
     ctx = mp.get_context("spawn")
     res = ctx.Queue()
-    ps = [ctx.Process(target=_rank, args=(r, world, rendezvous, shape_args, split, gather_root, res))
+    ps = [ctx.Process(target=_rank, args=(r, world, rendezvous, shape_args, split, gather_root, merge_fused, res))
           for r in range(world)]
     for p in ps:
         p.start()
