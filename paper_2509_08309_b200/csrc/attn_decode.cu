@@ -58,6 +58,21 @@ constexpr int kQSlots = 2;
 #ifndef HETIS_TC_NW
 #define HETIS_TC_NW 8
 #endif
+// Per-warp GQA kernel, large launches: more consumer warps (with fewer ring stages each) keep more of
+// the per-page math in flight, which is what bounds the kernel once every worker has several items;
+// at about one item per worker the deeper per-warp ring wins.  Measured attention us (c3 shares,
+// scripts/attn_probe.py; 8 warps x 3 stages / 10 x 2 / 12 x 2):
+//   64 heads 180.9 / 174.9 / 173.2;  32 heads 95.2 / 89.1 / 95.7;  16 heads 51.3 / 51.5 / 56.7;
+//   8 heads 26.8 / 27.6 / 29.9.
+// The warp count never changes an item's arithmetic (bit-identical either way).  0 disables it.
+#ifndef HETIS_TC_NW_LARGE
+#define HETIS_TC_NW_LARGE 10
+#endif
+// ... taken when the launch has at least this many items (upper bound from max_seq_len) per warp
+// worker of the large configuration
+#ifndef HETIS_TC_LARGE_ITEMS_PER_WORKER
+#define HETIS_TC_LARGE_ITEMS_PER_WORKER 2
+#endif
 #ifndef HETIS_MAX_STAGES
 #define HETIS_MAX_STAGES 24
 #endif
@@ -1558,10 +1573,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
 
 }
 
-template <int D, int R>
-cudaError_t launch_gqa_warp(const Params &p0, int num_seqs, cudaStream_t s, const CUtensorMap &tk,
+template <int D, int R, int NW>
+cudaError_t launch_gqa_warp_nw(const Params &p0, int num_seqs, cudaStream_t s, const CUtensorMap &tk,
                             const CUtensorMap &tv, std::string *err) {
-    constexpr int NW = HETIS_TC_NW;
     constexpr int ROW_BYTES = D * 2;
     constexpr int kStageBytes = 2 * kP * ROW_BYTES;
     constexpr int kQStride = (R * ROW_BYTES + 127) / 128 * 128;
@@ -1594,6 +1608,18 @@ cudaError_t launch_gqa_warp(const Params &p0, int num_seqs, cudaStream_t s, cons
         if (e != cudaSuccess) return e;
     }
     return launch_pdl(kern, dim3(num_sms()), dim3(32 * (NW + 1)), smem, s, p, tk, tv);
+}
+
+// warp count of the per-warp kernel for this launch (see HETIS_TC_NW_LARGE)
+template <int D, int R>
+cudaError_t launch_gqa_warp(const Params &p, int num_seqs, int max_seq_len, cudaStream_t s, const CUtensorMap &tk,
+                            const CUtensorMap &tv, std::string *err) {
+#if HETIS_TC_NW_LARGE > 0
+    const int64_t est_items = (int64_t)num_seqs * p.kv_heads * ((max_seq_len + kC - 1) / kC);
+    if (est_items >= (int64_t)HETIS_TC_LARGE_ITEMS_PER_WORKER * num_sms() * HETIS_TC_NW_LARGE)
+        return launch_gqa_warp_nw<D, R, HETIS_TC_NW_LARGE>(p, num_seqs, s, tk, tv, err);
+#endif
+    return launch_gqa_warp_nw<D, R, HETIS_TC_NW>(p, num_seqs, s, tk, tv, err);
 }
 
 // ---------------------------------------------------------------- kernels
@@ -1839,14 +1865,14 @@ cudaError_t launch_attn_tc(const AttnArgs &a, cudaStream_t s, std::string *err) 
         return cudaErrorInvalidValue;
     }
     switch (a.head_dim * 16 + a.r) {
-        case 128 * 16 + 2: return launch_gqa_warp<128, 2>(p, a.num_seqs, s, tk, tv, err);
-        case 128 * 16 + 4: return launch_gqa_warp<128, 4>(p, a.num_seqs, s, tk, tv, err);
-        case 128 * 16 + 8: return launch_gqa_warp<128, 8>(p, a.num_seqs, s, tk, tv, err);
-        case 64 * 16 + 2: return launch_gqa_warp<64, 2>(p, a.num_seqs, s, tk, tv, err);
-        case 64 * 16 + 4: return launch_gqa_warp<64, 4>(p, a.num_seqs, s, tk, tv, err);
-        case 64 * 16 + 8: return launch_gqa_warp<64, 8>(p, a.num_seqs, s, tk, tv, err);
-        case 128 * 16 + 1: return launch_gqa_warp<128, 1>(p, a.num_seqs, s, tk, tv, err);
-        case 64 * 16 + 1: return launch_gqa_warp<64, 1>(p, a.num_seqs, s, tk, tv, err);
+        case 128 * 16 + 2: return launch_gqa_warp<128, 2>(p, a.num_seqs, a.max_seq_len, s, tk, tv, err);
+        case 128 * 16 + 4: return launch_gqa_warp<128, 4>(p, a.num_seqs, a.max_seq_len, s, tk, tv, err);
+        case 128 * 16 + 8: return launch_gqa_warp<128, 8>(p, a.num_seqs, a.max_seq_len, s, tk, tv, err);
+        case 64 * 16 + 2: return launch_gqa_warp<64, 2>(p, a.num_seqs, a.max_seq_len, s, tk, tv, err);
+        case 64 * 16 + 4: return launch_gqa_warp<64, 4>(p, a.num_seqs, a.max_seq_len, s, tk, tv, err);
+        case 64 * 16 + 8: return launch_gqa_warp<64, 8>(p, a.num_seqs, a.max_seq_len, s, tk, tv, err);
+        case 128 * 16 + 1: return launch_gqa_warp<128, 1>(p, a.num_seqs, a.max_seq_len, s, tk, tv, err);
+        case 64 * 16 + 1: return launch_gqa_warp<64, 1>(p, a.num_seqs, a.max_seq_len, s, tk, tv, err);
         default: break;
     }
     return cudaErrorInvalidValue;

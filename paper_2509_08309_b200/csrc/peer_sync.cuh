@@ -20,6 +20,20 @@ __device__ __forceinline__ int64_t ld_acquire_sys(const int64_t *p) {
 __device__ __forceinline__ void st_release_sys(int64_t *p, int64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Before publishing an epoch with st.release.sys: the release store is itself cumulative over every
+// write that happens-before it (the predecessor kernels' stores, through the kernel boundary), so the
+// extra fence is a belt-and-braces choice: HETIS_PEER_FENCE 1 = fence.sc.sys (__threadfence_system),
+// 2 = fence.acq_rel.sys, 0 = none.
+#ifndef HETIS_PEER_FENCE
+#define HETIS_PEER_FENCE 1
+#endif
+__device__ __forceinline__ void peer_publish_fence() {
+#if HETIS_PEER_FENCE == 1
+    __threadfence_system();
+#elif HETIS_PEER_FENCE == 2
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+#endif
+}
 // Bounded spin: a peer that never publishes makes the kernel trap after ~10 s
 // (the error surfaces on the stream) instead of hanging the device.
 __device__ __forceinline__ void spin_until_geq(const int64_t *p, int64_t v) {

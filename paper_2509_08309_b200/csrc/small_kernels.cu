@@ -193,7 +193,7 @@ __global__ void peer_wait_kernel(PeerGroupDev g) {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL launch: the combine before it has completed
     const int64_t e = current_epoch(g);
     if (threadIdx.x == 0) {
-        __threadfence_system();
+        peer_publish_fence();
         for (int p = 0; p < g.n; ++p)
             if (peer_is_target(g, p)) st_release_sys(g.state[p] + kStOut + g.rank, e);
     }
@@ -246,7 +246,7 @@ __global__ void scatter_pull_kernel(PeerGroupDev g, int num_seqs, int H, int Hkv
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int64_t e = current_epoch(g);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        __threadfence_system();
+        peer_publish_fence();
         for (int p = 0; p < g.n; ++p) {
             st_release_sys(g.state[p] + kStAck + g.rank, e - 1);
             if (g.rank == g.root) st_release_sys(g.state[p] + kStIn, e);

@@ -47,8 +47,12 @@ def main():
         o = torch.empty((B, x, shape.head_dim), device=dev)
         for fl in [int(v, 0) for v in a.flags.split(",")]:
             def attn(i):
-                hetis.attn_partial_append(s, b.q, b.k_new, b.v_new, kp[i % n_layers], vp[i % n_layers],
-                                          b.block_table, b.seq_lens, L, ws, flags=fl)
+                if fl & hetis.ATTN_DIAG_STREAM_ONLY:   # the stream-only diagnostic cannot append
+                    hetis.attn_partial(s, b.q, kp[i % n_layers], vp[i % n_layers], b.block_table, b.seq_lens, L,
+                                       ws, flags=fl)
+                else:
+                    hetis.attn_partial_append(s, b.q, b.k_new, b.v_new, kp[i % n_layers], vp[i % n_layers],
+                                              b.block_table, b.seq_lens, L, ws, flags=fl)
 
             def step(i):
                 attn(i)
