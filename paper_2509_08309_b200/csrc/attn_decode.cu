@@ -1238,7 +1238,9 @@ __device__ __forceinline__ void merge_pair_rows(const Params &p, int ns, int s0,
     }
 }
 
-template <int D, int R, int NW>
+// FUSED: the instantiation that merges (Params::o_out / peer mode); the default one carries no merge
+// code at all (the merge's registers cost the hot loop ~2% when merely compiled in)
+template <int D, int R, int NW, bool FUSED>
 __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW, int n_items, const void *tmap_k,
                                     const void *tmap_v, const int32_t *s_off) {
     constexpr int ROW_BYTES = D * 2;
@@ -1271,7 +1273,7 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     }
     RingPos pos{0, 0u};
     bool c_waited = false;  // this warp has executed griddepcontrol.wait (pipelined deferred pages)
-    const bool fused_out = p.o_out != nullptr || p.peer_mode;
+    constexpr bool fused_out = FUSED;
     const int64_t epoch = p.peer_mode ? current_epoch(p.peer) : 0;  // the previous step's peer_wait wrote it
     bool acked = false;
     for (int it = 0;; ++it) {
@@ -1451,7 +1453,7 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         // fused merge: which pair, how many splits, where its O rows go
         int ns = 0, s0 = 0, pair = 0, gk = 0;
         size_t obase = 0;
-        if (fused_out) {
+        if constexpr (fused_out) {
             const int k = meta.item / p.kv_heads;
             gk = meta.item - k * p.kv_heads;
             const int j = upper_bound_smem(s_off, p.num_seqs + 1, k) - 1;
@@ -1510,7 +1512,7 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     }
 }
 
-template <int D, int R, int NW>
+template <int D, int R, int NW, bool FUSED>
 __global__ void __launch_bounds__(32 * (NW + 1), 1)
     attn_gqa_warp_kernel(const Params p, const __grid_constant__ CUtensorMap tmap_k,
                          const __grid_constant__ CUtensorMap tmap_v) {
@@ -1557,7 +1559,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     if (threadIdx.x < 32) {
         if (threadIdx.x < NW) producer_warp_items<ROW_BYTES, R, NW>(p, sm, SW, s_len, s_off, &tmap_k, &tmap_v);
     } else {
-        consumer_warp_items<D, R, NW>(p, sm, SW, n_items, &tmap_k, &tmap_v, s_off);
+        consumer_warp_items<D, R, NW, FUSED>(p, sm, SW, n_items, &tmap_k, &tmap_v, s_off);
     }
     // the last CTA to finish returns the device-wide counters to zero for the next launch (in peer mode
     // hetis_peer_wait, the next kernel, publishes the epoch once this grid has completed)
@@ -1573,7 +1575,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
 
 }
 
-template <int D, int R, int NW>
+template <int D, int R, int NW, bool FUSED>
 cudaError_t launch_gqa_warp_nw(const Params &p0, int num_seqs, cudaStream_t s, const CUtensorMap &tk,
                             const CUtensorMap &tv, std::string *err) {
     constexpr int ROW_BYTES = D * 2;
@@ -1593,7 +1595,7 @@ cudaError_t launch_gqa_warp_nw(const Params &p0, int num_seqs, cudaStream_t s, c
         return cudaErrorInvalidValue;
     }
     p.stages = sw;
-    auto kern = attn_gqa_warp_kernel<D, R, NW>;
+    auto kern = attn_gqa_warp_kernel<D, R, NW, FUSED>;
     static std::atomic<int> configured[64];
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -1614,12 +1616,14 @@ cudaError_t launch_gqa_warp_nw(const Params &p0, int num_seqs, cudaStream_t s, c
 template <int D, int R>
 cudaError_t launch_gqa_warp(const Params &p, int num_seqs, int max_seq_len, cudaStream_t s, const CUtensorMap &tk,
                             const CUtensorMap &tv, std::string *err) {
+    if (p.o_out != nullptr || p.peer_mode)  // the opt-in fused merge: one configuration
+        return launch_gqa_warp_nw<D, R, HETIS_TC_NW, true>(p, num_seqs, s, tk, tv, err);
 #if HETIS_TC_NW_LARGE > 0
     const int64_t est_items = (int64_t)num_seqs * p.kv_heads * ((max_seq_len + kC - 1) / kC);
     if (est_items >= (int64_t)HETIS_TC_LARGE_ITEMS_PER_WORKER * num_sms() * HETIS_TC_NW_LARGE)
-        return launch_gqa_warp_nw<D, R, HETIS_TC_NW_LARGE>(p, num_seqs, s, tk, tv, err);
+        return launch_gqa_warp_nw<D, R, HETIS_TC_NW_LARGE, false>(p, num_seqs, s, tk, tv, err);
 #endif
-    return launch_gqa_warp_nw<D, R, HETIS_TC_NW>(p, num_seqs, s, tk, tv, err);
+    return launch_gqa_warp_nw<D, R, HETIS_TC_NW, false>(p, num_seqs, s, tk, tv, err);
 }
 
 // ---------------------------------------------------------------- kernels

@@ -115,8 +115,11 @@ __device__ __forceinline__ float4 combine_wide(int j, int h, int q_heads, int r,
 // lse (optional, natural log, [num_seqs][q_heads]): ln sum_t exp(q.k_t / sqrt(d)) of
 // the head over the tokens this launch saw -- the input of the cross-device merge
 // of a sequence split (seq_split.cu).
+#ifndef HETIS_COMBINE_MIN_BLOCKS
+#define HETIS_COMBINE_MIN_BLOCKS 1
+#endif
 template <int D, int OUT_BF16, bool WIDE>
-__global__ void __launch_bounds__(kCombineThreads) combine_kernel(int num_seqs, int q_heads, int r,
+__global__ void __launch_bounds__(kCombineThreads, HETIS_COMBINE_MIN_BLOCKS) combine_kernel(int num_seqs, int q_heads, int r,
                                                                   const int32_t *seq_lens, const int32_t *split_off,
                                                                   const float *part_lse, const float *part_o, void *o,
                                                                   int64_t o_seq_stride, float *lse,
