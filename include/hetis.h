@@ -367,6 +367,12 @@ HETIS_API hetis_status hetis_attn_decode_units(const hetis_shape *shape, int32_t
  * publishes makes the waiting kernel trap after ~10 s (HETIS_E_CUDA on the
  * stream) instead of hanging the device. */
 HETIS_API size_t hetis_peer_state_bytes(void);
+/* Let kernels on the CURRENT device dereference memory of peer_device (NVLink
+ * peer access; needed for the peer pointers of a group whose ranks sit on
+ * other GPUs of the box).  OK when already enabled or peer_device is the
+ * current device; HETIS_E_UNSUPPORTED when the devices cannot access each
+ * other.  Host-side, once per pair. */
+HETIS_API hetis_status hetis_peer_access(int32_t peer_device);
 typedef struct hetis_peer_group hetis_peer_group; /* opaque, immutable after create */
 /* plan         : global plan (per_request == 0) of num_devices <= 8 ranks
  * rank, root   : this rank; the Primary holding the step's inputs

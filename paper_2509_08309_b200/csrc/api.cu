@@ -533,6 +533,27 @@ hetis_status hetis_attn_combine_lse(const hetis_shape *shape, int32_t num_seqs, 
 // ---------------------------------------------------------------- exchanges over peer memory
 size_t hetis_peer_state_bytes(void) { return (size_t)hetis::kStSlots * sizeof(int64_t); }
 
+hetis_status hetis_peer_access(int32_t peer_device) {
+    int dev = 0, n = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) return cuda_fail(e, "peer_access");
+    if (peer_device < 0 || peer_device >= n) return fail(HETIS_E_INVALID, "peer device outside [0, device count)");
+    if (peer_device == dev) return HETIS_OK;
+    int ok = 0;
+    e = cudaDeviceCanAccessPeer(&ok, dev, peer_device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceCanAccessPeer");
+    if (!ok) return fail(HETIS_E_UNSUPPORTED, "no peer access from device " + std::to_string(dev) + " to " +
+                                                  std::to_string(peer_device));
+    e = cudaDeviceEnablePeerAccess(peer_device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        (void)cudaGetLastError();  // clear the sticky-free error state
+        return HETIS_OK;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+    return HETIS_OK;
+}
+
 hetis_status hetis_peer_group_create(const hetis_plan *plan, int32_t rank, int32_t root, int32_t gather_root,
                                      int64_t *const *state_peers, void *const *o_full_peers, int64_t o_seq_stride,
                                      const void *q_full_root, const void *k_new_full_root,

@@ -40,7 +40,7 @@ EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_
             "hetis_seq_allgather_merge", "hetis_peer_state_bytes", "hetis_peer_group_create",
             "hetis_peer_group_destroy", "hetis_scatter_pull", "hetis_attn_partial_append",
             "hetis_attn_decode_append", "hetis_check_tables", "hetis_launch_count", "hetis_attn_decode_units",
-            "hetis_attn_decode_launches", "hetis_attn_decode_peers")
+            "hetis_attn_decode_launches", "hetis_attn_decode_peers", "hetis_peer_access")
 
 
 class HetisError(RuntimeError):
@@ -112,6 +112,7 @@ def lib() -> ctypes.CDLL:
                                                             i32, vp, vp, sz, u32, vp]),
                 "hetis_scatter_pull": (ctypes.c_int, [vp, i32, vp, vp, vp, vp]),
                 "hetis_attn_decode_launches": (i32, [sp, u32]),
+                "hetis_peer_access": (ctypes.c_int, [i32]),
                 "hetis_attn_decode_peers": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, vp, i64, vp, i32, vp, i32, vp, sz,
                                                            u32, vp]),
                 "hetis_attn_decode_units": (ctypes.c_int, [sp, i32, i32, vp, vp, vp, vp, vp, vp, i64, vp, i32, vp,
@@ -444,6 +445,11 @@ def attn_decode(shape: CShape, q, k_pool, v_pool, block_table, seq_lens, max_seq
 # ---------------------------------------------------------------- the step's exchanges over peer memory
 def peer_state_bytes() -> int:
     return int(lib().hetis_peer_state_bytes())
+
+
+def peer_access(peer_device: int) -> None:
+    """Enable kernels on the current device to dereference peer_device's memory (hetis_peer_access)."""
+    _check(lib().hetis_peer_access(int(peer_device)), "hetis_peer_access")
 
 
 def alloc_peer_state(device) -> torch.Tensor:

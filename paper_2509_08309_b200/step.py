@@ -134,6 +134,11 @@ class DecodeStep:
             root = (q_full, k_new_full, v_new_full)
         else:
             root = tuple(f(*a) for f, a in everyone[self.root][2])
+        # the peers' buffers live on their own GPUs: this device's kernels load / store them over NVLink
+        with torch.cuda.device(self.device):
+            for t in [*states, *outs, *root]:
+                if t is not None and t.device.index != torch.cuda.current_device():
+                    hetis.peer_access(t.device.index)
         stride = (o_full.stride(0) if o_full is not None
                   else self.shape.num_q_heads * self.shape.head_dim)
         self.group = hetis.PeerGroup(self.plan, self.rank, self.root, gather_root, states, outs, stride, *root)

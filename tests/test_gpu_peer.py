@@ -134,3 +134,22 @@ def test_peer_step_n_ranks_one_gpu(shape_args, split, gather_root, merge_fused):
         assert ok_pull, rank
         assert ok_eq, (rank, diff)
     assert sum(o[1] for o in out) == (world if gather_root < 0 else 1)
+
+
+def test_peer_access_contract():
+    """hetis_peer_access: the current device itself is OK (no-op), a device index outside the box is
+    HETIS_E_INVALID, and every other device of the box is enabled or reported unsupported."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2509_08309_b200 import hetis
+    torch.cuda.set_device(0)
+    hetis.peer_access(0)
+    with pytest.raises(hetis.HetisError) as e:
+        hetis.peer_access(torch.cuda.device_count())
+    assert e.value.name == "HETIS_E_INVALID"
+    for d in range(1, torch.cuda.device_count()):
+        try:
+            hetis.peer_access(d)
+            hetis.peer_access(d)                   # already enabled: still OK
+        except hetis.HetisError as exc:
+            assert exc.name == "HETIS_E_UNSUPPORTED"
