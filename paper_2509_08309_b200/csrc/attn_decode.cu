@@ -65,6 +65,9 @@ constexpr int kQSlots = 2;
 //   64 heads 180.9 / 174.9 / 173.2;  32 heads 95.2 / 89.1 / 95.7;  16 heads 51.3 / 51.5 / 56.7;
 //   8 heads 26.8 / 27.6 / 29.9.
 // The warp count never changes an item's arithmetic (bit-identical either way).  0 disables it.
+#ifndef HETIS_PROLOGUE_PREFETCH
+#define HETIS_PROLOGUE_PREFETCH 0
+#endif
 #ifndef HETIS_TC_NW_LARGE
 #define HETIS_TC_NW_LARGE 10
 #endif
@@ -1057,6 +1060,21 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     }
     const bool pipelined = (p.flags & HETIS_ATTN_PIPELINED) != 0;
     bool waited = false;
+#if HETIS_PROLOGUE_PREFETCH > 0
+    // warm L2 with the first pages of the worker's first item while the predecessor still runs (a
+    // prefetch is a hint: the real TMA loads come after griddepcontrol.wait and read whatever the
+    // predecessor wrote -- L2 is the point of coherence)
+    if (!pipelined && item >= 0 && item < n_items) {
+#pragma unroll
+        for (int i = 0; i < HETIS_PROLOGUE_PREFETCH; ++i) {
+            if (i < np) {
+                const int row = sm.pids[(w * 2 + 0) * kPagesPerItem + i] * kP;
+                dev::tma_prefetch_3d(tmap_k, 0, row, 0);
+                dev::tma_prefetch_3d(tmap_v, 0, row, 0);
+            }
+        }
+    }
+#endif
     if (!pipelined) {
         pdl_wait_once(waited);  // pools may hold rows the previous kernel wrote
         publish_split_offsets(p, s_off, w, NW);

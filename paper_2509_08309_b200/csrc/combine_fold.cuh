@@ -53,11 +53,11 @@ __device__ __forceinline__ float4 ld_f4(const float *p) {
     return CG ? __ldcg(reinterpret_cast<const float4 *>(p)) : *reinterpret_cast<const float4 *>(p);
 }
 
-// fold splits s = first, first + step, ... < ns of row rr of kv head g, request split offset s0;
-// partial row of split s: ((s0 + s) * kv_heads + g) * r + rr
-template <int D, bool CG = false>
-__device__ __forceinline__ FoldState fold_splits(int first, int step, int ns, int s0, int kv_heads, int g, int r,
-                                                 int rr, const float *part_lse, const float *part_o, int d4) {
+// fold splits s = first, first + step, ... < ns; load(s, l, v) fetches split s's log2-sum-exp and
+// this lane's 4 dims of its partial row (from global memory, or from a shared-memory staging copy --
+// the arithmetic below is the same code either way)
+template <class Load>
+__device__ __forceinline__ FoldState fold_splits_with(int first, int step, int ns, Load load) {
     constexpr int U = kCombineChunk;
     FoldState f{-INFINITY, 0.f, make_float4(0.f, 0.f, 0.f, 0.f)};
     for (int base = first; base < ns; base += step * U) {
@@ -67,9 +67,7 @@ __device__ __forceinline__ FoldState fold_splits(int first, int step, int ns, in
         for (int u = 0; u < U; ++u) {
             const int sp = base + u * step;
             if (sp < ns) {
-                const size_t rw = ((size_t)(s0 + sp) * kv_heads + g) * r + rr;
-                l[u] = ld_f<CG>(part_lse + rw);
-                v[u] = ld_f4<CG>(part_o + rw * D + 4 * d4);
+                load(sp, l[u], v[u]);
             } else {
                 l[u] = -INFINITY;
                 v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -91,6 +89,17 @@ __device__ __forceinline__ FoldState fold_splits(int first, int step, int ns, in
         f.M = Mn;
     }
     return f;
+}
+
+// split s's partial row of row rr of kv head g, request split offset s0: ((s0 + s) * kv_heads + g) * r + rr
+template <int D, bool CG = false>
+__device__ __forceinline__ FoldState fold_splits(int first, int step, int ns, int s0, int kv_heads, int g, int r,
+                                                 int rr, const float *part_lse, const float *part_o, int d4) {
+    return fold_splits_with(first, step, ns, [&](int sp, float &l, float4 &v) {
+        const size_t rw = ((size_t)(s0 + sp) * kv_heads + g) * r + rr;
+        l = ld_f<CG>(part_lse + rw);
+        v = ld_f4<CG>(part_o + rw * D + 4 * d4);
+    });
 }
 
 // NR rows at once (rows rr0 .. rr0 + NR - 1 of the same pair, lane d4 of each): the loads of every

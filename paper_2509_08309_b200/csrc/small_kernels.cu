@@ -118,6 +118,9 @@ __device__ __forceinline__ float4 combine_wide(int j, int h, int q_heads, int r,
 #ifndef HETIS_COMBINE_MIN_BLOCKS
 #define HETIS_COMBINE_MIN_BLOCKS 1
 #endif
+#ifndef HETIS_COMBINE_STAGED
+#define HETIS_COMBINE_STAGED 1
+#endif
 template <int D, int OUT_BF16, bool WIDE>
 __global__ void __launch_bounds__(kCombineThreads, HETIS_COMBINE_MIN_BLOCKS) combine_kernel(int num_seqs, int q_heads, int r,
                                                                   const int32_t *seq_lens, const int32_t *split_off,
@@ -375,13 +378,98 @@ cudaError_t launch_kv_append(int num_seqs, int kv_heads, int head_dim, int page_
                       seq_lens);
 }
 
+// Narrow combine with the partials staged in shared memory: lane 0 of a warp issues one bulk copy
+// (cp.async.bulk, completion on an mbarrier) per split row of the warp's rows, the row's lanes < ns
+// copy the split lse values, and the fold reads shared memory.  No register staging, so ~4 KiB of
+// loads per row are in flight with ~40 registers per thread: c3's 8192 rows fit in one wave (the
+// register-staged kernel needs 72 registers per thread and two waves).  Same fold code, same order:
+// bit-identical to combine_kernel.
+constexpr int kStagedWarps = 4;
+template <int D, int OUT_BF16>
+__global__ void __launch_bounds__(32 * kStagedWarps) combine_staged_kernel(
+    int num_seqs, int q_heads, int r, int ns_max, const int32_t *split_off, const float *part_lse,
+    const float *part_o, void *o, int64_t o_seq_stride, float *lse, const int32_t *units) {
+    constexpr int TPH = D / 4, RPW = 32 / TPH;  // lanes per row, rows per warp
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, sub = lane / TPH, d4 = lane % TPH;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
+    float *stage = reinterpret_cast<float *>(smem + 128) + (size_t)warp * RPW * ns_max * (D + 4);
+    float *rowbuf = stage + (size_t)sub * ns_max * (D + 4);  // [ns_max][D] partial rows, then [ns_max] lse
+    float *lsebuf = rowbuf + (size_t)ns_max * D;
+    if (threadIdx.x < kStagedWarps) dev::mbar_init(&bar[threadIdx.x], 1);
+    dev::fence_barrier_init();
+    __syncthreads();
+    dev::pdl_release_then_wait();
+    const int64_t total = (int64_t)num_seqs * q_heads;
+    const int64_t flat = ((int64_t)blockIdx.x * kStagedWarps + warp) * RPW + sub;
+    const bool live = flat < total;
+    int j = 0, h = 0, s0 = 0, ns = 0, kv_heads = q_heads / r, g = 0, rr = 0;
+    if (live) {
+        j = (int)(flat / q_heads);
+        h = (int)(flat - (int64_t)j * q_heads);
+        g = h / r;
+        rr = h - g * r;
+        s0 = split_off[j];
+        ns = split_off[j + 1] - s0;
+    }
+    // bytes of the warp's rows (lane 0 of each row group reports its row's count)
+    uint32_t bytes = (live && d4 == 0) ? (uint32_t)ns * D * 4 : 0u;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, off);
+    if (lane == 0) dev::mbar_arrive_expect_tx(&bar[warp], bytes);
+    __syncwarp();
+    if (live && d4 < ns) {  // lane d4 < ns: split d4's bulk copy and lse (ns <= kNarrowSplits <= TPH)
+        const size_t rw = ((size_t)(s0 + d4) * kv_heads + g) * r + rr;
+        dev::bulk_g2s(rowbuf + (size_t)d4 * D, part_o + rw * D, D * 4, &bar[warp], dev::policy_evict_first());
+        lsebuf[d4] = part_lse[rw];
+    }
+    dev::mbar_wait(&bar[warp], 0);
+    __syncwarp();
+    if (!live) return;
+    float4 acc;
+    float lse2;
+    if (ns == 0) {  // a device holding none of request j's tokens (sequence split): o = 0, lse = -inf
+        acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        lse2 = -INFINITY;
+    } else {
+        acc = finish(fold_splits_with(0, 1, ns,
+                                      [&](int sp, float &l, float4 &v) {
+                                          l = lsebuf[sp];
+                                          v = *reinterpret_cast<const float4 *>(rowbuf + (size_t)sp * D + 4 * d4);
+                                      }),
+                     &lse2);
+    }
+    const size_t orow = units != nullptr ? (size_t)units[2 * j] * o_seq_stride + ((size_t)units[2 * j + 1] * r + h) * D
+                                         : (size_t)j * o_seq_stride + (size_t)h * D;
+    store_row4<OUT_BF16>(o, orow + 4 * d4, acc);
+    if (lse != nullptr && d4 == 0) lse[flat] = lse2 * 0.69314718055994531f;  // log2 -> natural log
+}
+
 cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const int32_t *seq_lens,
                            const int32_t *split_off, const float *part_lse, const float *part_o, void *o,
                            int o_dtype, int64_t o_seq_stride, cudaStream_t s, float *lse, int max_seq_len,
                            const int32_t *units) {
     const int64_t pairs = (int64_t)num_seqs * q_heads;
     if (pairs == 0) return cudaSuccess;
-    const bool wide = (max_seq_len + kSplitTokens - 1) / kSplitTokens > kNarrowSplits;
+    const int ns_max = (max_seq_len + kSplitTokens - 1) / kSplitTokens;
+    const bool wide = ns_max > kNarrowSplits;
+#if HETIS_COMBINE_STAGED
+    // shared-memory staged fold when the register-staged kernel would need more than one wave (~7 of its
+    // 4-row blocks fit an SM at 72 registers per thread): c3 at N = 1, 8192 rows, -1 us per step; for
+    // one-wave launches the bulk-copy round trip is the slower one (c3's 8-GPU share: +1.7 us)
+    if (!wide && pairs > (int64_t)7 * 4 * num_sms()) {
+        const int rpw = 32 / (head_dim / 4);
+        const size_t smem = 128 + (size_t)kStagedWarps * rpw * ns_max * (head_dim + 4) * sizeof(float);
+        const int64_t warps = (pairs + rpw - 1) / rpw;
+        const int64_t blocks = (warps + kStagedWarps - 1) / kStagedWarps;
+        const bool bf = o_dtype == HETIS_BF16;
+        decltype(&combine_staged_kernel<128, 0>) kern =
+            head_dim == 128 ? (bf ? combine_staged_kernel<128, 1> : combine_staged_kernel<128, 0>)
+                            : (bf ? combine_staged_kernel<64, 1> : combine_staged_kernel<64, 0>);
+        return launch_pdl(kern, dim3((unsigned)blocks), dim3(32 * kStagedWarps), smem, s, num_seqs, q_heads, r,
+                          ns_max, split_off, part_lse, part_o, o, o_seq_stride, lse, units);
+    }
+#endif
     const int g = kCombineThreads / (head_dim / 4);
     const int64_t blocks = wide ? pairs : (pairs + g - 1) / g;
     const bool bf = o_dtype == HETIS_BF16;

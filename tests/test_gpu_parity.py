@@ -461,6 +461,24 @@ def test_combine_narrow_and_wide_launches_give_identical_rows(H, Hkv, D):
     assert_close(wide, oracle_full(b), "combine (wide launch) vs oracle")
 
 
+def test_combine_shared_memory_staged_matches_register_staged():
+    """Launches with more rows than one wave of the register-staged combine use the shared-memory staged
+    one (bulk copies of the split rows, the same fold code): a 5120-row batch (staged) and its first 6
+    requests (384 rows, register-staged) give bit-identical rows for those requests, for f32 and bf16 O."""
+    lens = tuple(int(v) for v in (1 + (torch.arange(80) * 977) % 4000))    # 1 .. 16 splits, ragged
+    b = gpu_batch(64, 8, 128, "bf16", lens, 29)
+    hetis.kv_append(hetis.make_shape(b.shape), b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens)
+    for odt in ("f32", "bf16"):
+        big = run_gpu(b, o_dtype=odt, append=False)
+        sub = workload.DecodeBatch(b.shape, 0, 64, b.q[:6].contiguous(), b.k_new[:6].contiguous(),
+                                   b.v_new[:6].contiguous(), b.k_pool, b.v_pool, b.block_table[:6].contiguous(),
+                                   b.seq_lens[:6].contiguous())
+        small = run_gpu(sub, o_dtype=odt, append=False)
+        assert torch.equal(big[:6].view(torch.int16), small.view(torch.int16)), odt
+        if odt == "f32":
+            assert_close(big, oracle_full(b), "staged combine vs oracle")
+
+
 # ------------------------------------------------------------------ MHA on tensor cores (HETIS_ATTN_MHA_TC)
 @pytest.mark.parametrize("D", [128, 64])
 @pytest.mark.parametrize("peaked", [False, True])
