@@ -65,8 +65,11 @@ constexpr int kQSlots = 2;
 //   64 heads 180.9 / 174.9 / 173.2;  32 heads 95.2 / 89.1 / 95.7;  16 heads 51.3 / 51.5 / 56.7;
 //   8 heads 26.8 / 27.6 / 29.9.
 // The warp count never changes an item's arithmetic (bit-identical either way).  0 disables it.
+#ifndef HETIS_EARLY_RELEASE
+#define HETIS_EARLY_RELEASE 0
+#endif
 #ifndef HETIS_PROLOGUE_PREFETCH
-#define HETIS_PROLOGUE_PREFETCH 0
+#define HETIS_PROLOGUE_PREFETCH 2
 #endif
 #ifndef HETIS_TC_NW_LARGE
 #define HETIS_TC_NW_LARGE 10
@@ -1395,6 +1398,14 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             const uint32_t kb = dev::smem_u32(sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes);
             const uint32_t vb = kb + kPageBytes;
             const int valid = min(kP, meta.ntok - pg * kP);
+#if HETIS_EARLY_RELEASE
+            // the page's V fragments go to registers first and the stage is released right after S = Q K^T:
+            // a stage is held for the smem reads and the q.k chain, not for the softmax and P V -- with 2-3
+            // stages per warp the ring's bytes in flight, not the math, bound the stream (Little's law)
+            uint32_t vf[NT_O / 2][4];
+#pragma unroll
+            for (int c2 = 0; c2 < NT_O / 2; ++c2) dev::ldmatrix_x4_trans(vf[c2], vb + v_off[c2]);
+#endif
             float s[2][4];
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
@@ -1407,6 +1418,12 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
                     dev::mma_bf16_16816(s[nt], qa[2 * q4 + 1][0], 0u, qa[2 * q4 + 1][1], 0u, b[2], b[3]);
                 }
             }
+#if HETIS_EARLY_RELEASE
+            __syncwarp();
+            if (lane == 0) dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
+            pos.advance(1, SW);
+            if (pg + SW >= meta.defer_from && pg + SW < meta.npages) issue_deferred(pg + SW);  // its stage is free
+#endif
             float sc[4];
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt)
@@ -1455,15 +1472,21 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             }
 #pragma unroll
             for (int c2 = 0; c2 < NT_O / 2; ++c2) {
+#if HETIS_EARLY_RELEASE
+                const uint32_t(&b)[4] = vf[c2];
+#else
                 uint32_t b[4];
                 dev::ldmatrix_x4_trans(b, vb + v_off[c2]);
+#endif
                 dev::mma_bf16_16816(o[2 * c2], pa[0], pa[1], pa[2], pa[3], b[0] & mk0, b[1] & mk1);
                 dev::mma_bf16_16816(o[2 * c2 + 1], pa[0], pa[1], pa[2], pa[3], b[2] & mk0, b[3] & mk1);
             }
+#if !HETIS_EARLY_RELEASE
             __syncwarp();
             if (lane == 0) dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
             pos.advance(1, SW);
             if (pg + SW >= meta.defer_from && pg + SW < meta.npages) issue_deferred(pg + SW);  // its stage is free
+#endif
         }
         // the item's partial: o_s = acc / l and lse_s = m + log2(l) for each of the r heads
         l += __shfl_xor_sync(0xffffffffu, l, 1);
