@@ -69,6 +69,9 @@ def parse():
                     help="N > 1: peer-memory scatter/gather kernels (default) or NCCL scatter_q / gather")
     ap.add_argument("--gather-root", type=int, default=-1,
                     help="-1: every rank receives O (all-gather); r >= 0: only rank r (gather to the Primary)")
+    ap.add_argument("--pull", type=int, default=1,
+                    help="N > 1 peer exchange: the attention kernel reads q / new k, v from the Primary "
+                         "(hetis_attn_partial_pull) instead of a separate pull-scatter kernel")
     ap.add_argument("--fused-append", type=int, default=1,
                     help="1: kv_append fused into the attention kernel (hetis_attn_partial_append); 0: separate")
     ap.add_argument("--force-dist", action="store_true",
@@ -298,6 +301,7 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
     split = cfg.head_split(world)
     dist_mode = D.active
     peer = dist_mode and args.exchange == "peer"
+    exchange_note = args.exchange
     B = cfg.batch
     seq_lens = cfg.seq_lens()
     max_len = int(seq_lens.max())
@@ -307,7 +311,7 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
     batch = workload.make_decode_batch(shape, seq_lens, cfg.seed, device, q_begin=q_begin, q_count=q_count,
                                        rank_salt=rank)
     step = DecodeStep(shape, plan, rank, B, max_len, device, o_dtype=args.o_dtype,
-                      comm_ptr=comm_ptr if (dist_mode and not peer) else None)
+                      comm_ptr=comm_ptr if dist_mode else None)
     kv_bytes_rank = accounting.step_bytes(seq_lens.tolist(), q_count, shape.r, shape.head_dim, shape.page_size,
                                           shape.elem_bytes, shape.elem_bytes, 4).kv
     # rotate layer pools so the per-step KV stream never sits in L2
@@ -328,8 +332,23 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
             kn_full, vn_full = workload.make_new_rows(shape, seq_lens, cfg.seed, device)
         o_full = torch.empty((B, shape.num_q_heads, shape.head_dim), dtype=odt, device=device) if receives else None
         if peer:
-            step.setup_peers(o_full, q_full, kn_full, vn_full, gather_root=gather_root)
-        elif o_full is None:
+            # the peer mappings need peer access between every pair of GPUs; if setting them up fails on
+            # every rank, the step falls back to the NCCL exchange (same plan, same parity check)
+            try:
+                step.setup_peers(o_full, q_full, kn_full, vn_full, gather_root=gather_root)
+                ok = 1.0
+            except Exception as exc:  # noqa: BLE001
+                print(f"rank {rank}: peer-memory exchange unavailable ({type(exc).__name__}: {exc})",
+                      file=sys.stderr, flush=True)
+                ok = 0.0
+            if D.max(1.0 - ok) > 0 and comm_ptr is not None:
+                peer = False
+                exchange_note = "nccl (peer-memory setup failed on some rank)"
+                if o_full is None:
+                    o_full = torch.empty((B, shape.num_q_heads, shape.head_dim), dtype=odt, device=device)
+            elif D.max(1.0 - ok) > 0:
+                raise SystemExit("peer-memory exchange setup failed and no NCCL communicator to fall back to")
+        if not peer and o_full is None:
             o_full = torch.empty((B, shape.num_q_heads, shape.head_dim), dtype=odt, device=device)
     else:
         step.buf.q_shard.copy_(batch.q)
@@ -343,9 +362,15 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
 
     fused_peer = peer and bool(args.fused_append) and bool(args.attn_flags & hetis.ATTN_FUSED_MERGE) and \
         step.merge_fused(args.attn_flags)
+    # the scatter folded into the attention kernel (it reads q / new k, v from the Primary): the default
+    pull = peer and not fused_peer and bool(args.fused_append) and bool(args.pull) and \
+        step.pull_supported(args.attn_flags)
 
     def attention(li):
-        if fused_peer:          # append + attention + split merge + the stores into every rank's o_full
+        if pull:
+            hetis.attn_partial_pull(step.group, B, k_pools[li], v_pools[li], batch.block_table, batch.seq_lens,
+                                    max_len, step.buf.workspace, flags=args.attn_flags)
+        elif fused_peer:          # append + attention + split merge + the stores into every rank's o_full
             hetis.attn_decode_peers(step.group, step.buf.q_shard, k_pools[li], v_pools[li], batch.block_table,
                                     batch.seq_lens, max_len, step.buf.workspace, k_new_shard=step.buf.k_new,
                                     v_new_shard=step.buf.v_new, flags=args.attn_flags)
@@ -371,6 +396,10 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
             hetis.attn_decode_append(step.cshape, step.buf.q_shard, step.buf.k_new, step.buf.v_new, k_pools[li],
                                      v_pools[li], batch.block_table, batch.seq_lens, max_len, step.buf.o_shard,
                                      step.buf.workspace, q_head_begin=q_begin, flags=args.attn_flags)
+        elif pull:            # same kernel and K/V traffic, q from the local shard (no step protocol)
+            hetis.attn_partial_append(step.cshape, step.buf.q_shard, step.buf.k_new, step.buf.v_new, k_pools[li],
+                                      v_pools[li], batch.block_table, batch.seq_lens, max_len, step.buf.workspace,
+                                      q_head_begin=q_begin, flags=args.attn_flags)
         else:
             attention(li)
 
@@ -380,7 +409,8 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
         rec = (lambda k: ev[k].record(torch.cuda.current_stream(device))) if ev is not None else (lambda k: None)
         rec(0)
         if peer:
-            step.scatter_peers()
+            if not pull:                 # with the pull folded into the attention kernel there is no scatter
+                step.scatter_peers()
         elif dist_mode:
             step.scatter(q_full, kn_full, vn_full)
         rec(1)
@@ -638,8 +668,9 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
             "seq_len_range": cfg.seq_len_range, "q_heads": shape.num_q_heads, "kv_heads": shape.num_kv_heads,
             "head_dim": shape.head_dim, "page_size": shape.page_size, "split": list(split),
             "o_dtype": args.o_dtype, "layers_rotated": n_layers,
-            "exchange": (args.exchange if dist_mode else None), "gather_root": (gather_root if dist_mode else None),
+            "exchange": (exchange_note if dist_mode else None), "gather_root": (gather_root if dist_mode else None),
             "fused_append": bool(args.fused_append), "merge_fused": bool(fused or fused_peer),
+            "scatter_in_attention": bool(pull),
             "l2": f"inputs larger than L2: {n_layers} layer pool(s) x {kv_bytes_rank / 1e6:.1f} MB KV per rank "
                   f"rotated per step (L2 = 126 MB)",
             "tokens": "one token = one request's decode step of one layer, all heads"},

@@ -409,6 +409,27 @@ HETIS_API hetis_status hetis_scatter_pull(const hetis_peer_group *group, int32_t
 HETIS_API hetis_status hetis_attn_combine_peers(const hetis_peer_group *group, int32_t num_seqs,
                                                 const int32_t *seq_lens, int32_t max_seq_len, void *workspace,
                                                 size_t workspace_bytes, hetis_stream_t stream);
+/* a2 + a3 + a4 in ONE kernel (the scatter folded into the attention): the
+ * split-KV partial attention of this rank's heads with the append fused, whose
+ * producers copy each work item's q rows, and whose consumers take the new
+ * token's k, v rows, straight from the Primary's q_full / k_new_full /
+ * v_new_full (peer memory: NVLink loads, pipelined with the K/V pages) -- no
+ * shard copy.  Its first steps after griddepcontrol.wait are hetis_scatter_pull's
+ * synchronisation: CTA 0 publishes this rank's acknowledgement of the previous
+ * o_full (and, on the Primary, the input epoch), every CTA waits (bounded) for
+ * the Primary's epoch.  Pools, block table, seq_lens and workspace as in
+ * hetis_attn_partial_append for this rank's heads.  One step per rank is then
+ *     hetis_attn_partial_pull -> hetis_attn_combine_peers -> hetis_peer_wait.
+ * Results bit-identical to hetis_scatter_pull + hetis_attn_partial_append.
+ * A rank without heads, or num_seqs == 0 -> HETIS_E_UNSUPPORTED (use
+ * hetis_scatter_pull, which takes part in the protocol without a shard);
+ * HETIS_ATTN_PIPELINED / _DIAG_STREAM_ONLY / _FUSED_MERGE -> UNSUPPORTED. */
+HETIS_API hetis_status hetis_attn_partial_pull(const hetis_peer_group *group, int32_t num_seqs, void *k_pool,
+                                               void *v_pool, int64_t num_pages, const int32_t *block_table,
+                                               int32_t max_pages, const int32_t *seq_lens, int32_t max_seq_len,
+                                               void *workspace, size_t workspace_bytes, uint32_t flags,
+                                               hetis_stream_t stream);
+
 /* a3 + a4 + a5 + a6 in ONE kernel: this rank's attention over its shard
  * (hetis_attn_partial_append when k/v_new_shard are given, else
  * hetis_attn_partial; q_shard [num_seqs][x][d], block table / pools / seq_lens

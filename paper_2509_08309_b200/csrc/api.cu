@@ -628,6 +628,42 @@ hetis_status hetis_attn_combine_peers(const hetis_peer_group *g, int32_t num_seq
     return HETIS_OK;
 }
 
+hetis_status hetis_attn_partial_pull(const hetis_peer_group *g, int32_t num_seqs, void *k_pool, void *v_pool,
+                                     int64_t num_pages, const int32_t *block_table, int32_t max_pages,
+                                     const int32_t *seq_lens, int32_t max_seq_len, void *workspace,
+                                     size_t workspace_bytes, uint32_t flags, hetis_stream_t stream) {
+    if (!g) return fail(HETIS_E_INVALID, "group is NULL");
+    const hetis_shape &s = g->shape;
+    const int r = s.num_q_heads / s.num_kv_heads;
+    if (g->q_count < 1) return fail(HETIS_E_UNSUPPORTED, "a rank without heads uses hetis_scatter_pull");
+    if (num_seqs < 1) return fail(HETIS_E_UNSUPPORTED, "no requests: use hetis_scatter_pull");
+    if (flags & (HETIS_ATTN_PIPELINED | HETIS_ATTN_DIAG_STREAM_ONLY | HETIS_ATTN_FUSED_MERGE))
+        return fail(HETIS_E_UNSUPPORTED, "pull launches are not pipelined, diagnostic or merge-fused");
+    if (!g->dev.q_root || !g->dev.k_root || !g->dev.v_root)
+        return fail(HETIS_E_INVALID, "the group has no mapping of the Primary's inputs");
+    const size_t row = (size_t)s.head_dim * esize(s.kv_dtype);
+    const uint8_t *q = g->dev.q_root + (size_t)g->dev.head0 * row;
+    const uint8_t *kn = g->dev.k_root + (size_t)(g->dev.head0 / r) * row;
+    const uint8_t *vn = g->dev.v_root + (size_t)(g->dev.head0 / r) * row;
+    hetis::AttnArgs a{};
+    hetis_status st = attn_args(&s, num_seqs, g->dev.head0, g->q_count, q, k_pool, v_pool, num_pages, block_table,
+                                max_pages, seq_lens, max_seq_len, workspace, workspace_bytes, &a);
+    if (st != HETIS_OK) return st;
+    a.flags = flags;
+    a.k_new = kn;
+    a.v_new = vn;
+    a.pull = &g->dev;
+    a.in_kv_stride = s.num_kv_heads;
+    cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
+    const bool tc = a.dtype == HETIS_BF16 && (a.r > 1 || (flags & HETIS_ATTN_MHA_TC)) &&
+                    !(flags & HETIS_ATTN_FORCE_SIMT);
+    std::string err;
+    cudaError_t e = tc ? hetis::launch_attn_tc(a, cs, &err) : hetis::launch_attn_simt(a, cs);
+    if (e != cudaSuccess)
+        return err.empty() ? cuda_fail(e, "attn_partial_pull launch") : fail(HETIS_E_CUDA, "attn_partial_pull: " + err);
+    return HETIS_OK;
+}
+
 hetis_status hetis_attn_decode_peers(const hetis_peer_group *g, int32_t num_seqs, const void *q_shard,
                                      const void *k_new_shard, const void *v_new_shard, void *k_pool, void *v_pool,
                                      int64_t num_pages, const int32_t *block_table, int32_t max_pages,

@@ -177,12 +177,45 @@ struct Params {
     int peer_mode;
     int o_head0;
     PeerGroupDev peer;
+    // pull mode (hetis_attn_partial_pull: the scatter folded into this kernel): q / k_new / v_new point at
+    // the Primary's [B][H][d] / [B][H_kv][d] buffers (peer memory), already offset to this rank's first
+    // head, with in_kv_stride = H_kv kv rows per request; after griddepcontrol.wait the producers publish
+    // this rank's acknowledgement (and, on the Primary, the input epoch) and wait for the Primary's epoch
+    // before the first q copy -- what hetis_scatter_pull did, without its copy
+    int pull_mode;
+    int in_kv_stride;  // kv rows per request in the q / k_new / v_new layouts (kv_heads when dense)
 };
 
-// Row of (launch row j, local kv head g) in the q (x r), k_new / v_new and block-table layouts.
+// Row of (launch row j, local kv head g) in the block-table layout.
 __device__ __forceinline__ int kv_row(const Params &p, int j, int g) {
     if (p.units != nullptr) return __ldg(p.units + 2 * j) * p.row_kv_heads + __ldg(p.units + 2 * j + 1);
     return j * p.kv_heads + g;
+}
+// ... and in the q (x r) and k_new / v_new layouts
+__device__ __forceinline__ int in_row(const Params &p, int j, int g) {
+    if (p.units != nullptr) return kv_row(p, j, g);
+    return j * p.in_kv_stride + g;
+}
+
+// Pull mode, called by the converged producer lanes after griddepcontrol.wait (everything before this
+// kernel on the stream has completed, including the consumer of the previous step's o_full): CTA 0
+// publishes the acknowledgement and, on the Primary, that this step's inputs are written; every CTA
+// then waits for the Primary's epoch.  `lanes` = the producer lanes (converged).
+__device__ __forceinline__ void pull_mode_sync(const Params &p, int lane, unsigned lanes_mask) {
+    if (!p.pull_mode) return;
+    const PeerGroupDev &g = p.peer;
+    const int64_t e = current_epoch(g);
+    if (lane == 0) {
+        if (blockIdx.x == 0) {
+            peer_publish_fence();
+            for (int q = 0; q < g.n; ++q) {
+                st_release_sys(g.state[q] + kStAck + g.rank, e - 1);
+                if (g.rank == g.root) st_release_sys(g.state[q] + kStIn, e);
+            }
+        }
+        spin_until_geq(g.state[g.rank] + kStIn, e);
+    }
+    __syncwarp(lanes_mask);
 }
 
 // new_page >= 0: this item holds request j's newest token (position L_j - 1) in page
@@ -363,8 +396,8 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
     auto issue_q = [&](int it, int item, const Dec &d) {
         const int slot = it & (kQSlots - 1);
         dev::mbar_wait(&qempty[slot], ((it / kQSlots) & 1) ^ 1);
-        const int krow = kv_row(p, d.j, d.g);
-        ItemMeta m{item, d.ntok, (d.ntok + kP - 1) / kP, -1, krow, 0, 0, 0};
+        const int krow = kv_row(p, d.j, d.g), irow = in_row(p, d.j, d.g);
+        ItemMeta m{item, d.ntok, (d.ntok + kP - 1) / kP, -1, irow, 0, 0, 0};
         if (p.k_new != nullptr && d.t0 + d.ntok == s_len[d.j]) {  // the request's last split: append here
             m.new_pg = (d.ntok - 1) / kP;
             m.new_slot = (d.ntok - 1) % kP;
@@ -372,7 +405,7 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
         }
         qmeta[slot] = m;
         dev::mbar_arrive_expect_tx(&qfull[slot], kQBytes);
-        const uint8_t *src = p.q + (size_t)krow * R * ROW_BYTES;
+        const uint8_t *src = p.q + (size_t)irow * R * ROW_BYTES;
         dev::bulk_g2s(qbuf + (size_t)slot * kQStride, src, kQBytes, &qfull[slot], pol_stream);
     };
     // lane k of the G producer lanes owns pages k, k + G, k + 2G, ... of every item
@@ -394,6 +427,7 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
     if (item >= n_items) {
         pdl_wait_once(waited);
         publish_split_offsets(p, s_off, lane, kProducerLanes);
+        pull_mode_sync(p, lane, kMask);  // CTA 0 publishes the acknowledgement even without items
         return;
     }
     static_assert((kQSlots & (kQSlots - 1)) == 0, "q slots: power of two");
@@ -406,6 +440,7 @@ __device__ void producer(const Params &p, uint8_t *ring, uint8_t *qbuf, ItemMeta
         // scatter (hetis_scatter_pull releases this kernel before its copy completes)
         pdl_wait_once(waited);
         publish_split_offsets(p, s_off, lane, kProducerLanes);
+        pull_mode_sync(p, lane, kMask);
     }
     if (lane == 0) issue_q(0, item, cur);
     for (int it = 0; item < n_items; item += gridDim.x, ++it) {
@@ -1081,6 +1116,7 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     if (!pipelined) {
         pdl_wait_once(waited);  // pools may hold rows the previous kernel wrote
         publish_split_offsets(p, s_off, w, NW);
+        pull_mode_sync(p, w, mask);
     }
     if (item == -2 && pipelined) item = n_items;  // a pipelined launch never steals its first item (no wait was done yet)
     if (item == -2) {  // the CTA-local queue was empty from the start: steal
@@ -1114,8 +1150,8 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             continue;
         }
         if (!q_done && dev::mbar_test(&sm.qempty[w], (it & 1) ^ 1)) {
-            const int krow = kv_row(p, j, g);
-            ItemMeta m{item, ntok, np, -1, krow, 0, 0, np};
+            const int irow = in_row(p, j, g);
+            ItemMeta m{item, ntok, np, -1, irow, 0, 0, np};
             if (pipelined) {  // the pages holding the request's last two positions: the consumer waits + copies
                 while (m.defer_from > 0 && holds_recent_tokens(t0, m.defer_from - 1, s_len[j])) --m.defer_from;
                 for (int d = 0; d < 2 && m.defer_from + d < np; ++d)
@@ -1128,7 +1164,7 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             }
             sm.meta[w] = m;
             dev::mbar_arrive_expect_tx(&sm.qfull[w], kQBytes);
-            const uint8_t *src = p.q + (size_t)krow * R * ROW_BYTES;
+            const uint8_t *src = p.q + (size_t)irow * R * ROW_BYTES;
             dev::bulk_g2s(sm.qbuf + (size_t)w * kQStride, src, kQBytes, &sm.qfull[w], pol);
             q_done = true;
         }
@@ -1805,6 +1841,9 @@ Params make_params(const AttnArgs &a) {
     p.v_new = static_cast<const uint8_t *>(a.v_new);
     p.units = a.units;
     p.row_kv_heads = a.row_kv_heads;
+    p.in_kv_stride = a.in_kv_stride > 0 ? a.in_kv_stride : a.kv_heads;
+    p.pull_mode = a.pull != nullptr;
+    if (a.pull != nullptr) p.peer = *a.pull;
     p.o_out = a.o_out;
     p.o_seq_stride = a.o_seq_stride;
     p.o_bf16 = a.o_dtype == HETIS_BF16;

@@ -53,6 +53,10 @@ struct AttnArgs {
     int32_t *pair_cnt;    // [num_seqs * kv_heads], zero between launches (self-cleaning)
     // fused merge + gather over peer memory: the rows go to every target rank's o_full (nullptr: o_out)
     const struct PeerGroupDev *peer;
+    // pull mode: q / k_new / v_new are the Primary's buffers (offset to this rank's heads), in_kv_stride
+    // kv rows per request; the kernel does the scatter's synchronisation (nullptr: ordinary launch)
+    const struct PeerGroupDev *pull;
+    int in_kv_stride;     // 0 = kv_heads (dense shards)
 };
 
 struct WorkspaceLayout {

@@ -40,7 +40,8 @@ EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_
             "hetis_seq_allgather_merge", "hetis_peer_state_bytes", "hetis_peer_group_create",
             "hetis_peer_group_destroy", "hetis_scatter_pull", "hetis_attn_partial_append",
             "hetis_attn_decode_append", "hetis_check_tables", "hetis_launch_count", "hetis_attn_decode_units",
-            "hetis_attn_decode_launches", "hetis_attn_decode_peers", "hetis_peer_access")
+            "hetis_attn_decode_launches", "hetis_attn_decode_peers", "hetis_peer_access",
+            "hetis_attn_partial_pull")
 
 
 class HetisError(RuntimeError):
@@ -113,6 +114,7 @@ def lib() -> ctypes.CDLL:
                 "hetis_scatter_pull": (ctypes.c_int, [vp, i32, vp, vp, vp, vp]),
                 "hetis_attn_decode_launches": (i32, [sp, u32]),
                 "hetis_peer_access": (ctypes.c_int, [i32]),
+                "hetis_attn_partial_pull": (ctypes.c_int, [vp, i32, vp, vp, i64, vp, i32, vp, i32, vp, sz, u32, vp]),
                 "hetis_attn_decode_peers": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, vp, i64, vp, i32, vp, i32, vp, sz,
                                                            u32, vp]),
                 "hetis_attn_decode_units": (ctypes.c_int, [sp, i32, i32, vp, vp, vp, vp, vp, vp, i64, vp, i32, vp,
@@ -501,6 +503,17 @@ def attn_combine_peers(group: PeerGroup, seq_lens, max_seq_len: int, workspace, 
     _check(lib().hetis_attn_combine_peers(group.handle, seq_lens.shape[0], _dev(seq_lens, "seq_lens"), max_seq_len,
                                           _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(),
                                           _stream(stream)), "hetis_attn_combine_peers")
+
+
+def attn_partial_pull(group: PeerGroup, num_seqs: int, k_pool, v_pool, block_table, seq_lens, max_seq_len: int,
+                      workspace, flags: int = 0, stream=None) -> None:
+    """a2 + a3 + a4 in one kernel: the partial attention with the append fused, q and the new k, v rows
+    read straight from the Primary's buffers (hetis_attn_partial_pull)."""
+    _check(lib().hetis_attn_partial_pull(group.handle, num_seqs, _dev(k_pool, "k_pool"), _dev(v_pool, "v_pool"),
+                                         k_pool.shape[0], _dev(block_table, "block_table"), block_table.shape[2],
+                                         _dev(seq_lens, "seq_lens"), max_seq_len, _dev(workspace, "workspace"),
+                                         workspace.numel() * workspace.element_size(), flags, _stream(stream)),
+           "hetis_attn_partial_pull")
 
 
 def attn_decode_peers(group: PeerGroup, q_shard, k_pool, v_pool, block_table, seq_lens, max_seq_len: int, workspace,

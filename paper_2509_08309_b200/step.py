@@ -180,10 +180,25 @@ class DecodeStep:
         hetis.peer_wait(self.group, stream=stream)
         return self.o_full
 
+    def pull_supported(self, flags: int = 0) -> bool:
+        """hetis_attn_partial_pull applies: this rank holds heads and requests, an ordinary launch."""
+        return self.q_count > 0 and self.num_seqs > 0 and not (
+            flags & (hetis.ATTN_PIPELINED | hetis.ATTN_DIAG_STREAM_ONLY | hetis.ATTN_FUSED_MERGE))
+
     def step_peers(self, k_pool, v_pool, block_table, seq_lens, stream=None, flags: int = 0,
-                   merge_fused: bool | None = None):
-        """The whole N > 1 step over peer memory: pull scatter, attention with the append and the merge +
-        gather (one kernel, or two), closing wait -- no NCCL, no per-step host argument: graph-capturable."""
+                   merge_fused: bool | None = None, pull: bool | None = None):
+        """The whole N > 1 step over peer memory, no NCCL and no per-step host argument (graph-capturable):
+        by default the attention kernel itself pulls q and the new k, v rows from the Primary
+        (hetis_attn_partial_pull), then combine + gather into every rank's o_full, then the closing wait --
+        three kernels; pull=False: the separate pull scatter kernel first (four)."""
+        if pull is None:
+            pull = self.pull_supported(flags) and not merge_fused
+        if pull:
+            hetis.attn_partial_pull(self.group, self.num_seqs, k_pool, v_pool, block_table, seq_lens,
+                                    self.max_seq_len, self.buf.workspace, flags=flags, stream=stream)
+            hetis.attn_combine_peers(self.group, seq_lens, self.max_seq_len, self.buf.workspace, stream=stream)
+            hetis.peer_wait(self.group, stream=stream)
+            return self.o_full
         self.scatter_peers(stream)
         return self.attention_gather_peers(k_pool, v_pool, block_table, seq_lens, stream=stream, flags=flags,
                                            merge_fused=merge_fused)

@@ -7,6 +7,14 @@ plan range, and the gather that puts every head at its GLOBAL index (Eq. 2a
 Concat; reading 4).  The per-rank attention is computed by the
 oracle (test infrastructure) in place of the CUDA kernel, so the assembled
 result must equal the unsplit oracle result bit for bit.
+
+The exchange KERNELS themselves (the pull of q / new k, v from the Primary --
+standalone or folded into the attention kernel -- the combine storing every O
+row into every rank at its global head index, the epoch protocol) need a GPU:
+they run with N = 2, 4, 5 processes sharing one GPU through CUDA IPC in
+tests/test_gpu_peer.py (bit-exact against the single-device result, even /
+uneven / gather-to-root plans, eager steps and graph replays), and the whole
+bench path in tests/test_gpu_bench.py (--force-dist, --share-gpu).
 """
 from __future__ import annotations
 

@@ -30,7 +30,7 @@ LENS = (300, 17, 1029, 2048, 5, 256, 1)
 EAGER_STEPS, GRAPH_STEPS, GRAPH_REPLAYS = 3, 2, 2
 
 
-def _rank(rank, world, rendezvous, shape_args, split, gather_root, merge_fused, res):
+def _rank(rank, world, rendezvous, shape_args, split, gather_root, merge_fused, pull, res):
     import torch
     import torch.distributed as dist
     from paper_2509_08309_b200 import hetis, workload
@@ -58,7 +58,8 @@ def _rank(rank, world, rendezvous, shape_args, split, gather_root, merge_fused, 
         def one_step():
             if rank == 0:
                 q_full.neg_()                   # the step's new inputs, written before the root's pull
-            step.step_peers(mine.k_pool, mine.v_pool, mine.block_table, mine.seq_lens, merge_fused=merge_fused)
+            step.step_peers(mine.k_pool, mine.v_pool, mine.block_table, mine.seq_lens, merge_fused=merge_fused,
+                            pull=pull)
 
         for _ in range(EAGER_STEPS):
             one_step()
@@ -89,11 +90,12 @@ def _rank(rank, world, rendezvous, shape_args, split, gather_root, merge_fused, 
         state = step.peer_state.cpu()
         ok_eq = bool(torch.equal(got, ref)) if receives else True
         diff = float((got - ref).abs().nan_to_num(1e9).max()) if receives else 0.0
-        # this rank's own shard of the last step went through the pull: bit-exact copy of the root's range
+        # with the separate pull kernel, this rank's shard of the last step is a bit-exact copy of the root's
+        # range (with the pull folded into the attention kernel there is no shard)
         r = shape.r
         q_last = full.q[:, begin:begin + count]
-        ok_pull = bool(torch.equal(step.buf.q_shard, q_last)) and bool(
-            torch.equal(step.buf.k_new, full.k_new[:, begin // r:(begin + count) // r]))
+        ok_pull = pull is not False or (bool(torch.equal(step.buf.q_shard, q_last)) and bool(
+            torch.equal(step.buf.k_new, full.k_new[:, begin // r:(begin + count) // r])))
         res.put((rank, receives, ok_eq, diff, ok_pull, int(state[0]), n_steps))
         dist.barrier()                          # keep the shared buffers alive until everyone has compared
     finally:
@@ -101,27 +103,32 @@ def _rank(rank, world, rendezvous, shape_args, split, gather_root, merge_fused, 
 
 
 # merge_fused: True = hetis_attn_decode_peers (attention, split merge and the stores into every rank's
-# o_full in ONE kernel), False / None = partial kernel + hetis_attn_combine_peers (the default)
+# o_full in ONE kernel), None = partial kernel + hetis_attn_combine_peers (the default).
+# pull: None = the attention kernel reads q / new k, v from the Primary (hetis_attn_partial_pull, the
+# default), False = the separate hetis_scatter_pull kernel first
 CASES = [
-    ((64, 8, 128, 16, "bf16"), (32, 32), -1, None),           # even GQA, all-gather
-    ((64, 8, 128, 16, "bf16"), (32, 32), -1, True),           # the same with the merge + gather fused
-    ((40, 40, 128, 16, "bf16"), (16, 8, 8, 4, 4), -1, None),  # c4's uneven split, all-gather (CUDA-core MHA)
-    ((64, 8, 128, 16, "bf16"), (16, 16, 24, 8), 0, None),     # uneven GQA, gather to the Primary (paper)
-    ((64, 8, 128, 16, "bf16"), (16, 16, 24, 8), 0, True),     # ... fused
-    ((16, 2, 64, 16, "bf16"), (8, 8), -1, True),              # GQA d = 64, fused
-    ((8, 8, 64, 16, "f32"), (4, 4), -1, None),                # c1 shape, fp32
+    ((64, 8, 128, 16, "bf16"), (32, 32), -1, None, None),           # even GQA, all-gather, pull in the kernel
+    ((64, 8, 128, 16, "bf16"), (32, 32), -1, None, False),          # ... with the separate pull kernel
+    ((64, 8, 128, 16, "bf16"), (32, 32), -1, True, False),          # the merge + gather fused
+    ((40, 40, 128, 16, "bf16"), (16, 8, 8, 4, 4), -1, None, None),  # c4's uneven split (CUDA-core MHA)
+    ((40, 40, 128, 16, "bf16"), (16, 8, 8, 4, 4), -1, None, False),
+    ((64, 8, 128, 16, "bf16"), (16, 16, 24, 8), 0, None, None),     # uneven GQA, gather to the Primary (paper)
+    ((64, 8, 128, 16, "bf16"), (16, 16, 24, 8), 0, True, False),    # ... fused
+    ((16, 2, 64, 16, "bf16"), (8, 8), -1, True, False),             # GQA d = 64, fused
+    ((8, 8, 64, 16, "f32"), (4, 4), -1, None, None),                # c1 shape, fp32, pull in the kernel
 ]
 
 
-@pytest.mark.parametrize("shape_args,split,gather_root,merge_fused", CASES)
-def test_peer_step_n_ranks_one_gpu(shape_args, split, gather_root, merge_fused):
+@pytest.mark.parametrize("shape_args,split,gather_root,merge_fused,pull", CASES)
+def test_peer_step_n_ranks_one_gpu(shape_args, split, gather_root, merge_fused, pull):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     world = len(split)
     rendezvous = os.path.join(tempfile.mkdtemp(), "rendezvous")
     ctx = mp.get_context("spawn")
     res = ctx.Queue()
-    ps = [ctx.Process(target=_rank, args=(r, world, rendezvous, shape_args, split, gather_root, merge_fused, res))
+    ps = [ctx.Process(target=_rank, args=(r, world, rendezvous, shape_args, split, gather_root, merge_fused, pull,
+                                          res))
           for r in range(world)]
     for p in ps:
         p.start()
