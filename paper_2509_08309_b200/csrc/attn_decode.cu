@@ -213,7 +213,8 @@ __device__ __forceinline__ void pull_mode_sync(const Params &p, int lane, unsign
                 if (g.rank == g.root) st_release_sys(g.state[q] + kStIn, e);
             }
         }
-        spin_until_geq(g.state[g.rank] + kStIn, e);
+        // the Primary's own inputs were written before griddepcontrol.wait returned: it has nothing to wait for
+        if (g.rank != g.root) spin_until_geq(g.state[g.rank] + kStIn, e);
     }
     __syncwarp(lanes_mask);
 }

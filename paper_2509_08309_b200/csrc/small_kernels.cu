@@ -258,7 +258,8 @@ __global__ void scatter_pull_kernel(PeerGroupDev g, int num_seqs, int H, int Hkv
             if (g.rank == g.root) st_release_sys(g.state[p] + kStIn, e);
         }
     }
-    if (threadIdx.x == 0) spin_until_geq(g.state[g.rank] + kStIn, e);
+    // the Primary's own inputs were written before griddepcontrol.wait returned: it has nothing to wait for
+    if (threadIdx.x == 0 && g.rank != g.root) spin_until_geq(g.state[g.rank] + kStIn, e);
     __syncthreads();
     const int qc = qrow / 16, kc = kvrow / 16;
     const int64_t nq_chunks = (int64_t)num_seqs * nq * qc, nk_chunks = (int64_t)num_seqs * nk * kc;
