@@ -21,9 +21,10 @@ timeout -s KILL 900 python scripts/cost_model_fit.py --shape 70b --batch 64 > gp
 timeout -s KILL 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
   --master-port 29541 scripts/transfer_model_fit.py --exchange peer --share-gpu --grid 4 --steps 20 \
   > gpurun_out/transfer_fit_${TAG}_share.json 2> gpurun_out/transfer_fit_${TAG}_share.err
-for X in peer nccl; do
-  timeout -s KILL 400 python bench.py --config c3 --force-dist --exchange $X --steps 100 --warmup 5 \
-    --no-cpu-baseline > gpurun_out/bench_${TAG}_forcedist_$X.log 2>&1
+for X in "peer" "peer --pull 0" "nccl"; do
+  N=$(echo $X | tr -d ' -')
+  timeout -s KILL 400 python bench.py --config c3 --sub-config none --force-dist --exchange $X --steps 100 \
+    --warmup 5 --no-cpu-baseline > gpurun_out/bench_${TAG}_forcedist_$N.log 2>&1
 done
 bash scripts/sanitizer_repro/run.sh > /dev/null 2>&1
 nvidia-smi -q -d CLOCK,PERFORMANCE > gpurun_out/clocks_${TAG}.txt 2>&1
