@@ -356,9 +356,11 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
         step.buf.v_new.copy_(batch.v_new)
         o_full = step.buf.o_shard
     stream = torch.cuda.current_stream(device)
-    # one kernel per step where the attention kernel also merges the splits (per-warp tensor-core kernel)
-    # (opt-in, --attn-flags 0x20: measured slower than the separate combine)
-    fused = (not peer) and bool(args.fused_append) and hetis.attn_decode_launches(step.cshape, args.attn_flags) == 1
+    # the local step (N = 1, and the NCCL exchange) through hetis_attn_decode_append, which picks the
+    # combine: streaming beside the per-warp kernel, the fused merge (opt-in, --attn-flags 0x20: one kernel,
+    # measured slower), or the combine kernel after the attention kernel
+    fused = (not peer) and bool(args.fused_append)
+    merge_in_kernel = fused and hetis.attn_decode_launches(step.cshape, args.attn_flags) == 1
 
     fused_peer = peer and bool(args.fused_append) and bool(args.attn_flags & hetis.ATTN_FUSED_MERGE) and \
         step.merge_fused(args.attn_flags)
@@ -374,7 +376,7 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
             hetis.attn_decode_peers(step.group, step.buf.q_shard, k_pools[li], v_pools[li], batch.block_table,
                                     batch.seq_lens, max_len, step.buf.workspace, k_new_shard=step.buf.k_new,
                                     v_new_shard=step.buf.v_new, flags=args.attn_flags)
-        elif fused:             # append + attention + split merge in ONE kernel, O straight into the shard
+        elif fused:             # append + attention + split merge, O straight into the shard
             hetis.attn_decode_append(step.cshape, step.buf.q_shard, step.buf.k_new, step.buf.v_new, k_pools[li],
                                      v_pools[li], batch.block_table, batch.seq_lens, max_len, step.buf.o_shard,
                                      step.buf.workspace, q_head_begin=q_begin, flags=args.attn_flags)
@@ -396,7 +398,7 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
             hetis.attn_decode_append(step.cshape, step.buf.q_shard, step.buf.k_new, step.buf.v_new, k_pools[li],
                                      v_pools[li], batch.block_table, batch.seq_lens, max_len, step.buf.o_shard,
                                      step.buf.workspace, q_head_begin=q_begin, flags=args.attn_flags)
-        elif pull:            # same kernel and K/V traffic, q from the local shard (no step protocol)
+        elif pull or (fused and not merge_in_kernel):   # the attention kernel alone (same K/V traffic)
             hetis.attn_partial_append(step.cshape, step.buf.q_shard, step.buf.k_new, step.buf.v_new, k_pools[li],
                                       v_pools[li], batch.block_table, batch.seq_lens, max_len, step.buf.workspace,
                                       q_head_begin=q_begin, flags=args.attn_flags)
@@ -654,7 +656,7 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
     if args.fused_append:   # the new rows are read from k_new / v_new and written into the pools
         alg_bytes += 2 * 2 * B * (q_count // shape.r) * shape.head_dim * shape.elem_bytes
         kernel_name = "hetis_attn_partial_append (split-KV attention with kv_append fused)"
-    if fused or fused_peer:   # the kernel also writes O
+    if merge_in_kernel or fused_peer:   # the kernel also writes O
         alg_bytes += sb.o
         kernel_name = ("hetis_attn_decode_append (ONE kernel: kv_append + split-KV attention + split merge; "
                        "O written by the kernel)")
@@ -669,7 +671,7 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
             "head_dim": shape.head_dim, "page_size": shape.page_size, "split": list(split),
             "o_dtype": args.o_dtype, "layers_rotated": n_layers,
             "exchange": (exchange_note if dist_mode else None), "gather_root": (gather_root if dist_mode else None),
-            "fused_append": bool(args.fused_append), "merge_fused": bool(fused or fused_peer),
+            "fused_append": bool(args.fused_append), "merge_fused": bool(merge_in_kernel or fused_peer),
             "scatter_in_attention": bool(pull),
             "l2": f"inputs larger than L2: {n_layers} layer pool(s) x {kv_bytes_rank / 1e6:.1f} MB KV per rank "
                   f"rotated per step (L2 = 126 MB)",

@@ -16,6 +16,11 @@
  *                     heads (Eq. 2b) = hetis_attn_partial (split-KV
  *                     partial attention) + hetis_attn_combine (LSE merge)
  *   hetis_gather      Attention_j = Concat_i result_{i,j} (Eq. 2a)
+ * Over peer memory (NVLink, no NCCL; the bench default at N > 1):
+ *   hetis_attn_partial_pull -> hetis_attn_combine_peers -> hetis_peer_wait
+ *                     (the scatter folded into the attention kernel, the gather
+ *                     into the combine; hetis_scatter_pull is the standalone pull)
+ * Per-request plans (Eq. 7, x_i^j varying with j): hetis_attn_decode_units.
  *
  * Conventions
  * -----------

@@ -171,6 +171,11 @@ struct Params {
     int64_t o_seq_stride;  // elements between requests in o_out (or in every o_full, peer mode)
     int o_bf16;
     int32_t *pair_cnt;     // [num_seqs * kv_heads] finished splits per pair; zero between launches
+    // streaming combine (hetis_attn_decode(_append) with the per-warp kernel): every finished split
+    // is counted in pair_done[j * kv_heads + g] (release), so the combine -- launched early, running
+    // beside this kernel -- folds a pair as soon as its last split lands instead of after the whole
+    // grid; the combine returns the counters to zero.  nullptr: no counting.
+    int32_t *pair_done;
     // peer mode (hetis_attn_decode_peers): the rows go to EVERY target rank's o_full at the GLOBAL head
     // index o_head0 + local head, after that rank acknowledged the previous step's o_full; the last CTA
     // then publishes the epoch to them (hetis_attn_combine_peers' protocol, folded into this kernel)
@@ -1116,6 +1121,7 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
 #endif
     if (!pipelined) {
         pdl_wait_once(waited);  // pools may hold rows the previous kernel wrote
+        if (p.pair_done != nullptr) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         publish_split_offsets(p, s_off, w, NW);
         pull_mode_sync(p, w, mask);
     }
@@ -1569,6 +1575,18 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             if (tq == 0) p.part_lse[row] = m + __log2f(l);
 #endif
         }
+        if constexpr (!fused_out) {
+            if (p.pair_done != nullptr) {  // streaming combine: count this split once its rows are written
+                const int k = meta.item / p.kv_heads;
+                const int gk2 = meta.item - k * p.kv_heads;
+                const int j = upper_bound_smem(s_off, p.num_seqs + 1, k) - 1;
+                __syncwarp();
+                if (lane == 0) {
+                    __threadfence();
+                    atomicAdd(p.pair_done + j * p.kv_heads + gk2, 1);
+                }
+            }
+        }
         if (ns > 1) {  // publish this split; the pair's last split folds them all
             __syncwarp();
             int last = 0;
@@ -1628,7 +1646,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         HETIS_TS(0);
         HETIS_TS_SMID(6);
     }
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // streaming combine: the dependent combine must not start before this kernel's wait for ITS
+    // predecessor (the previous step's combine, which returns the split counters to zero and writes the
+    // same O): the producer triggers after that wait; otherwise trigger at once
+    if (p.pair_done == nullptr) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     build_split_offsets(p, s_len, s_off);  // contains __syncthreads
     if (threadIdx.x == 0) {
         HETIS_TS(1);
@@ -1849,6 +1870,7 @@ Params make_params(const AttnArgs &a) {
     p.o_seq_stride = a.o_seq_stride;
     p.o_bf16 = a.o_dtype == HETIS_BF16;
     p.pair_cnt = a.pair_cnt;
+    p.pair_done = a.stream_combine ? a.pair_cnt : nullptr;
     if (a.peer != nullptr) {
         p.peer_mode = 1;
         p.peer = *a.peer;
