@@ -356,9 +356,9 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
         step.buf.v_new.copy_(batch.v_new)
         o_full = step.buf.o_shard
     stream = torch.cuda.current_stream(device)
-    # the local step (N = 1, and the NCCL exchange) through hetis_attn_decode_append, which picks the
-    # combine: streaming beside the per-warp kernel, the fused merge (opt-in, --attn-flags 0x20: one kernel,
-    # measured slower), or the combine kernel after the attention kernel
+    # the local step (N = 1, and the NCCL exchange) through the library's one-call step,
+    # hetis_attn_decode_append: the attention kernel with the append fused, then the combine kernel (or,
+    # opt-in with --attn-flags 0x20, the merge fused into the attention kernel: one kernel, measured slower)
     fused = (not peer) and bool(args.fused_append)
     merge_in_kernel = fused and hetis.attn_decode_launches(step.cshape, args.attn_flags) == 1
 

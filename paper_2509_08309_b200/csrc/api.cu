@@ -155,8 +155,7 @@ WorkspaceLayout workspace_layout(int num_seqs, int kv_heads, int r, int head_dim
     w.o_offset = w.lse_offset + round256((size_t)w.max_items * r * 4);
     w.counter_offset = w.o_offset + round256((size_t)w.max_items * r * head_dim * 4);
     w.pair_cnt_offset = w.counter_offset + 256;
-    w.rows_done_offset = w.pair_cnt_offset + round256((size_t)num_seqs * kv_heads * 4);
-    w.total = w.rows_done_offset + round256((size_t)num_seqs * kv_heads * 4);
+    w.total = w.pair_cnt_offset + round256((size_t)num_seqs * kv_heads * 4);
     return w;
 }
 }  // namespace hetis
@@ -434,26 +433,12 @@ static bool fused_merge_ok(const hetis_shape *shape, uint32_t flags) {
                       HETIS_ATTN_DIAG_STREAM_ONLY));
 }
 
-// Streaming combine (HETIS_STREAM_COMBINE): the per-warp kernel counts finished splits per pair and a
-// combine launched beside it folds each pair as its last split lands (two kernels, no grid-wide wait).
-#ifndef HETIS_STREAM_COMBINE
-#define HETIS_STREAM_COMBINE 1
-#endif
-static bool stream_combine_ok(const hetis_shape *shape, uint32_t flags, int32_t max_seq_len) {
-    const int r = shape->num_q_heads / shape->num_kv_heads;
-    return HETIS_STREAM_COMBINE && shape->kv_dtype == HETIS_BF16 && (r > 1 || (flags & HETIS_ATTN_MHA_TC)) &&
-           !(flags & (HETIS_ATTN_FORCE_SIMT | HETIS_ATTN_TC_SHARED_RING | HETIS_ATTN_PIPELINED |
-                      HETIS_ATTN_DIAG_STREAM_ONLY | HETIS_ATTN_FUSED_MERGE)) &&
-           (max_seq_len + hetis::kSplitTokens - 1) / hetis::kSplitTokens <= 16;
-}
-
 static hetis_status attn_partial_impl(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
                                       int32_t q_head_count, const void *q, const void *k_new, const void *v_new,
                                       const void *k_pool, const void *v_pool, int64_t num_pages,
                                       const int32_t *block_table, int32_t max_pages, const int32_t *seq_lens,
                                       int32_t max_seq_len, void *workspace, size_t workspace_bytes, uint32_t flags,
-                                      hetis_stream_t stream, void *o_out = nullptr, int64_t o_seq_stride = 0,
-                                      bool stream_combine = false) {
+                                      hetis_stream_t stream, void *o_out = nullptr, int64_t o_seq_stride = 0) {
     hetis::AttnArgs a{};
     hetis_status st = attn_args(shape, num_seqs, q_head_begin, q_head_count, q, k_pool, v_pool, num_pages,
                                 block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes, &a);
@@ -465,7 +450,6 @@ static hetis_status attn_partial_impl(const hetis_shape *shape, int32_t num_seqs
     a.o_out = o_out;
     a.o_seq_stride = o_seq_stride;
     a.o_dtype = shape->o_dtype;
-    a.stream_combine = stream_combine;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const bool tc = a.dtype == HETIS_BF16 && (a.r > 1 || (flags & HETIS_ATTN_MHA_TC)) &&
                     !(flags & HETIS_ATTN_FORCE_SIMT);
@@ -478,15 +462,6 @@ static hetis_status attn_partial_impl(const hetis_shape *shape, int32_t num_seqs
     }
     if (e != cudaSuccess)
         return err.empty() ? cuda_fail(e, "attn_partial launch") : fail(HETIS_E_CUDA, "attn_partial: " + err);
-    if (stream_combine) {
-        uint8_t *ws = static_cast<uint8_t *>(workspace);
-        hetis::WorkspaceLayout w = hetis::workspace_layout(num_seqs, a.kv_heads, a.r, a.head_dim, max_seq_len);
-        e = hetis::launch_combine_stream(num_seqs, q_head_count, a.r, a.head_dim, seq_lens, a.part_lse, a.part_o,
-                                         o_out, shape->o_dtype, o_seq_stride,
-                                         reinterpret_cast<int32_t *>(ws + w.pair_cnt_offset),
-                                         reinterpret_cast<int32_t *>(ws + w.rows_done_offset), s, max_seq_len);
-        if (e != cudaSuccess) return cuda_fail(e, "combine (streaming) launch");
-    }
     return HETIS_OK;
 }
 
@@ -774,15 +749,6 @@ hetis_status hetis_attn_decode_append(const hetis_shape *shape, int32_t num_seqs
                                  num_pages, block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes,
                                  flags, stream, o, (int64_t)q_head_count * shape->head_dim);
     }
-    if (shape && check_shape(shape) == HETIS_OK && stream_combine_ok(shape, flags, max_seq_len)) {
-        if (num_seqs > 0 && (!k_new || !v_new)) return fail(HETIS_E_INVALID, "k_new / v_new is NULL");
-        if (!aligned(k_new, 16) || !aligned(v_new, 16))
-            return fail(HETIS_E_INVALID, "k_new / v_new must be 16-B aligned");
-        if (!aligned(o, 16)) return fail(HETIS_E_INVALID, "o must be 16-byte aligned");
-        return attn_partial_impl(shape, num_seqs, q_head_begin, q_head_count, q, k_new, v_new, k_pool, v_pool,
-                                 num_pages, block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes,
-                                 flags, stream, o, (int64_t)q_head_count * shape->head_dim, true);
-    }
     hetis_status st = hetis_attn_partial_append(shape, num_seqs, q_head_begin, q_head_count, q, k_new, v_new, k_pool,
                                                 v_pool, num_pages, block_table, max_pages, seq_lens, max_seq_len,
                                                 workspace, workspace_bytes, flags, stream);
@@ -802,12 +768,6 @@ hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_seqs, int32
         return attn_partial_impl(shape, num_seqs, q_head_begin, q_head_count, q, nullptr, nullptr, k_pool, v_pool,
                                  num_pages, block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes,
                                  flags, stream, o, (int64_t)q_head_count * shape->head_dim);
-    }
-    if (shape && check_shape(shape) == HETIS_OK && stream_combine_ok(shape, flags, max_seq_len)) {
-        if (!aligned(o, 16)) return fail(HETIS_E_INVALID, "o must be 16-byte aligned");
-        return attn_partial_impl(shape, num_seqs, q_head_begin, q_head_count, q, nullptr, nullptr, k_pool, v_pool,
-                                 num_pages, block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes,
-                                 flags, stream, o, (int64_t)q_head_count * shape->head_dim, true);
     }
     hetis_status st = hetis_attn_partial(shape, num_seqs, q_head_begin, q_head_count, q, k_pool, v_pool, num_pages,
                                          block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes,

@@ -65,6 +65,9 @@ constexpr int kQSlots = 2;
 //   64 heads 180.9 / 174.9 / 173.2;  32 heads 95.2 / 89.1 / 95.7;  16 heads 51.3 / 51.5 / 56.7;
 //   8 heads 26.8 / 27.6 / 29.9.
 // The warp count never changes an item's arithmetic (bit-identical either way).  0 disables it.
+#ifndef HETIS_RESCALE_THRESHOLD
+#define HETIS_RESCALE_THRESHOLD 0
+#endif
 #ifndef HETIS_EARLY_RELEASE
 #define HETIS_EARLY_RELEASE 0
 #endif
@@ -171,11 +174,6 @@ struct Params {
     int64_t o_seq_stride;  // elements between requests in o_out (or in every o_full, peer mode)
     int o_bf16;
     int32_t *pair_cnt;     // [num_seqs * kv_heads] finished splits per pair; zero between launches
-    // streaming combine (hetis_attn_decode(_append) with the per-warp kernel): every finished split
-    // is counted in pair_done[j * kv_heads + g] (release), so the combine -- launched early, running
-    // beside this kernel -- folds a pair as soon as its last split lands instead of after the whole
-    // grid; the combine returns the counters to zero.  nullptr: no counting.
-    int32_t *pair_done;
     // peer mode (hetis_attn_decode_peers): the rows go to EVERY target rank's o_full at the GLOBAL head
     // index o_head0 + local head, after that rank acknowledged the previous step's o_full; the last CTA
     // then publishes the epoch to them (hetis_attn_combine_peers' protocol, folded into this kernel)
@@ -1121,7 +1119,6 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
 #endif
     if (!pipelined) {
         pdl_wait_once(waited);  // pools may hold rows the previous kernel wrote
-        if (p.pair_done != nullptr) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         publish_split_offsets(p, s_off, w, NW);
         pull_mode_sync(p, w, mask);
     }
@@ -1479,16 +1476,22 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
             mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
             const float m_new = fmaxf(m, mx);
-            // o and l are still zero before the first page: nothing to rescale
-            if (__any_sync(0xffffffffu, m_new != m && m != -INFINITY)) {
+            // o and l are still zero before the first page: nothing to rescale.  Lazy rescaling: the
+            // running max m is only a reference; it moves (and o, l are rescaled) when some row's max
+            // grew by more than HETIS_RESCALE_THRESHOLD (log2 units), so the weights 2^(s - m) of a page
+            // stay below 2^threshold (fp32 accumulation; the bf16 P_hi + P_lo split keeps ~2^-16 relative
+            // at any magnitude).  The arithmetic of an item still depends on its data only.
+            if (m == -INFINITY) {
+                m = m_new;
+            } else if (__any_sync(0xffffffffu, m_new - m > (float)HETIS_RESCALE_THRESHOLD)) {
                 const float alpha = dev::ex2(m - m_new);
                 l *= alpha;
 #pragma unroll
                 for (int nt = 0; nt < NT_O; ++nt) {
                     o[nt][0] *= alpha; o[nt][1] *= alpha; o[nt][2] *= alpha; o[nt][3] *= alpha;
                 }
+                m = m_new;
             }
-            m = m_new;
             float pp[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -1575,18 +1578,6 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             if (tq == 0) p.part_lse[row] = m + __log2f(l);
 #endif
         }
-        if constexpr (!fused_out) {
-            if (p.pair_done != nullptr) {  // streaming combine: count this split once its rows are written
-                const int k = meta.item / p.kv_heads;
-                const int gk2 = meta.item - k * p.kv_heads;
-                const int j = upper_bound_smem(s_off, p.num_seqs + 1, k) - 1;
-                __syncwarp();
-                if (lane == 0) {
-                    __threadfence();
-                    atomicAdd(p.pair_done + j * p.kv_heads + gk2, 1);
-                }
-            }
-        }
         if (ns > 1) {  // publish this split; the pair's last split folds them all
             __syncwarp();
             int last = 0;
@@ -1646,10 +1637,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         HETIS_TS(0);
         HETIS_TS_SMID(6);
     }
-    // streaming combine: the dependent combine must not start before this kernel's wait for ITS
-    // predecessor (the previous step's combine, which returns the split counters to zero and writes the
-    // same O): the producer triggers after that wait; otherwise trigger at once
-    if (p.pair_done == nullptr) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     build_split_offsets(p, s_len, s_off);  // contains __syncthreads
     if (threadIdx.x == 0) {
         HETIS_TS(1);
@@ -1870,7 +1858,6 @@ Params make_params(const AttnArgs &a) {
     p.o_seq_stride = a.o_seq_stride;
     p.o_bf16 = a.o_dtype == HETIS_BF16;
     p.pair_cnt = a.pair_cnt;
-    p.pair_done = a.stream_combine ? a.pair_cnt : nullptr;
     if (a.peer != nullptr) {
         p.peer_mode = 1;
         p.peer = *a.peer;

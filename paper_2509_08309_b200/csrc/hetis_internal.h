@@ -57,12 +57,10 @@ struct AttnArgs {
     // kv rows per request; the kernel does the scatter's synchronisation (nullptr: ordinary launch)
     const struct PeerGroupDev *pull;
     int in_kv_stride;     // 0 = kv_heads (dense shards)
-    // streaming combine: count finished splits per pair in pair_cnt (launch_combine_stream folds them)
-    bool stream_combine;
 };
 
 struct WorkspaceLayout {
-    size_t split_off_offset, lse_offset, o_offset, counter_offset, pair_cnt_offset, rows_done_offset, total;
+    size_t split_off_offset, lse_offset, o_offset, counter_offset, pair_cnt_offset, total;
     int64_t max_items;
 };
 
@@ -122,13 +120,6 @@ struct PeerGroupDev {
 __host__ __device__ inline bool peer_is_target(const PeerGroupDev &g, int p) {
     return g.gather_root < 0 || p == g.gather_root;
 }
-// The streaming combine: launched right after the attention kernel that counts finished splits in
-// pair_done; folds each pair once its count reaches the pair's split count, then returns the counters
-// (pair_done, rows_done: [num_seqs * q_heads / r]) to zero.
-cudaError_t launch_combine_stream(int num_seqs, int q_heads, int r, int head_dim, const int32_t *seq_lens,
-                                  const float *part_lse, const float *part_o, void *o, int o_dtype,
-                                  int64_t o_seq_stride, int32_t *pair_done, int32_t *rows_done, cudaStream_t s,
-                                  int max_seq_len);
 cudaError_t launch_combine_peers(int num_seqs, int q_heads, int r, int head_dim, const int32_t *split_off,
                                  const float *part_lse, const float *part_o, int o_dtype, const PeerGroupDev &g,
                                  cudaStream_t s, int max_seq_len);

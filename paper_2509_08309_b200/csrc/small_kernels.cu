@@ -446,91 +446,6 @@ __global__ void __launch_bounds__(32 * kStagedWarps) combine_staged_kernel(
     if (lse != nullptr && d4 == 0) lse[flat] = lse2 * 0.69314718055994531f;  // log2 -> natural log
 }
 
-// Streaming combine: launched (PDL) once every CTA of the attention kernel has passed its own wait for
-// the previous step, it runs BESIDE the attention kernel: a row's group derives its request's split
-// range from seq_lens (the prefix the attention kernel uses; seq_lens is never written by it), waits
-// (acquire) until the attention kernel has counted all of the pair's splits in pair_done, folds them
-// (L2-only loads of rows other SMs just wrote; the combine's fold code and order: bit-identical), and
-// the pair's last row returns pair_done / rows_done to zero for the next step.  No griddepcontrol.wait:
-// a pair is merged as soon as its last split lands, not after the whole grid.
-__device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t *p) {
-    int32_t v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-template <int D, int OUT_BF16>
-__global__ void __launch_bounds__(kCombineThreads) combine_stream_kernel(int num_seqs, int q_heads, int r,
-                                                                         const int32_t *seq_lens,
-                                                                         const float *part_lse, const float *part_o,
-                                                                         void *o, int64_t o_seq_stride,
-                                                                         int32_t *pair_done, int32_t *rows_done) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    extern __shared__ int32_t s_off[];  // [num_seqs + 1] split offsets (exclusive prefix of ceil(L / C))
-    {
-        const int per = (num_seqs + blockDim.x - 1) / blockDim.x;
-        const int b0 = threadIdx.x * per, b1 = min(num_seqs, b0 + per);
-        int sum = 0;
-        for (int j = b0; j < b1; ++j) sum += (seq_lens[j] + kSplitTokens - 1) / kSplitTokens;
-        __shared__ int32_t s_part[kCombineThreads];
-        s_part[threadIdx.x] = sum;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int run = 0;
-            for (int t = 0; t < (int)blockDim.x; ++t) {
-                const int v = s_part[t];
-                s_part[t] = run;
-                run += v;
-            }
-            s_off[num_seqs] = run;
-        }
-        __syncthreads();
-        int run = s_part[threadIdx.x];
-        for (int j = b0; j < b1; ++j) {
-            s_off[j] = run;
-            run += (seq_lens[j] + kSplitTokens - 1) / kSplitTokens;
-        }
-        __syncthreads();
-    }
-    constexpr int TPH = D / 4, G = kCombineThreads / TPH;
-    const int grp = threadIdx.x / TPH, d4 = threadIdx.x % TPH;
-    const int64_t flat = (int64_t)blockIdx.x * G + grp;
-    if (flat >= (int64_t)num_seqs * q_heads) return;
-    const int j = (int)(flat / q_heads), h = (int)(flat - (int64_t)j * q_heads);
-    const int kv_heads = q_heads / r, g = h / r, rr = h - g * r, pair = j * kv_heads + g;
-    const int s0 = s_off[j], ns = s_off[j + 1] - s0;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    float lse2 = -INFINITY;
-    if (ns > 0) {
-        if (ld_acquire_gpu(pair_done + pair) < ns)
-            while (ld_acquire_gpu(pair_done + pair) < ns) __nanosleep(64);
-        acc = finish(fold_splits<D, true>(0, 1, ns, s0, kv_heads, g, r, rr, part_lse, part_o, d4), &lse2);
-    }
-    store_row4<OUT_BF16>(o, (size_t)j * o_seq_stride + (size_t)h * D + 4 * d4, acc);
-    const unsigned gmask = TPH == 32 ? 0xffffffffu : ((1u << TPH) - 1u) << ((threadIdx.x & 31) & ~(TPH - 1));
-    __syncwarp(gmask);  // the group's loads of the pair's partials are done
-    if (d4 == 0 && atomicAdd(rows_done + pair, 1) == r - 1) {  // the pair's last row: reset for the next step
-        pair_done[pair] = 0;
-        rows_done[pair] = 0;
-    }
-}
-
-cudaError_t launch_combine_stream(int num_seqs, int q_heads, int r, int head_dim, const int32_t *seq_lens,
-                                  const float *part_lse, const float *part_o, void *o, int o_dtype,
-                                  int64_t o_seq_stride, int32_t *pair_done, int32_t *rows_done, cudaStream_t s,
-                                  int max_seq_len) {
-    const int64_t pairs = (int64_t)num_seqs * q_heads;
-    if (pairs == 0) return cudaSuccess;
-    if ((max_seq_len + kSplitTokens - 1) / kSplitTokens > kNarrowSplits) return cudaErrorInvalidValue;
-    const int g = kCombineThreads / (head_dim / 4);
-    const int64_t blocks = (pairs + g - 1) / g;
-    const bool bf = o_dtype == HETIS_BF16;
-    decltype(&combine_stream_kernel<128, 0>) kern =
-        head_dim == 128 ? (bf ? combine_stream_kernel<128, 1> : combine_stream_kernel<128, 0>)
-                        : (bf ? combine_stream_kernel<64, 1> : combine_stream_kernel<64, 0>);
-    return launch_pdl(kern, dim3((unsigned)blocks), dim3(kCombineThreads), (size_t)(num_seqs + 1) * 4, s, num_seqs,
-                      q_heads, r, seq_lens, part_lse, part_o, o, o_seq_stride, pair_done, rows_done);
-}
-
 cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const int32_t *seq_lens,
                            const int32_t *split_off, const float *part_lse, const float *part_o, void *o,
                            int o_dtype, int64_t o_seq_stride, cudaStream_t s, float *lse, int max_seq_len,

@@ -101,7 +101,7 @@ def share_time(cfg, n: int, steps: int, warmup: int, device, split=None, rank: i
     t1.record()
     torch.cuda.synchronize()
     step_pipe_ms = t0.elapsed_time(t1) / steps
-    # the library's step call (hetis_attn_decode_append: the streaming combine beside the per-warp kernel)
+    # the library's one-call step (hetis_attn_decode_append: attention with the append fused, then the combine)
     g5 = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g5):
         for i in range(steps):

@@ -136,8 +136,7 @@ def test_workspace_formula(L):
     items = 64 * (4096 // C) * 40
     r256 = lambda b: (b + 255) // 256 * 256
     # split offsets + partial lse + partial o + work-claim counters + per-pair split counters (fused merge)
-    # (+ per-pair row counters of the streaming combine)
-    assert n == r256(65 * 4) + r256(items * 4) + r256(items * 128 * 4) + 256 + 2 * r256(64 * 40 * 4)
+    assert n == r256(65 * 4) + r256(items * 4) + r256(items * 128 * 4) + 256 + r256(64 * 40 * 4)
     with pytest.raises(hetis.HetisError) as e:
         hetis.attn_decode_workspace(SHAPE_70B, 64, 12, 4096)     # 12 heads = 1.5 kv groups
     assert e.value.name == "HETIS_E_GROUP_ALIGN"

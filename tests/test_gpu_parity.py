@@ -584,51 +584,6 @@ def test_merge_fused_into_attention_bit_identical_to_combine_kernel(H, Hkv, D, f
         assert_close(got, oracle_full(b), "fused merge")
 
 
-@pytest.mark.parametrize("H,Hkv,D,flags", [(64, 8, 128, 0), (16, 4, 64, 0), (16, 2, 128, hetis.ATTN_DEVICE_CLAIM),
-                                            (40, 40, 128, hetis.ATTN_MHA_TC)])
-def test_streaming_combine_bit_identical_and_graph_ordered(H, Hkv, D, flags):
-    """hetis_attn_decode(_append) with the per-warp kernel runs the streaming combine (launched beside the
-    attention kernel, folding each pair as its last split is counted): O bit-identical to hetis_attn_partial +
-    hetis_attn_combine, the append's pools identical, and K steps chained by programmatic dependent launch in
-    a CUDA graph on ONE workspace (the counters the combine returns to zero between steps) reproduce it."""
-    lens = EDGE_LENS + (4096, 2000)
-    a = gpu_batch(H, Hkv, D, "bf16", lens, seed=61)
-    b = gpu_batch(H, Hkv, D, "bf16", lens, seed=61)
-    s = hetis.make_shape(a.shape)
-    B, x, _ = a.q.shape
-    L = a.max_seq_len
-    hetis.kv_append(s, a.k_new, a.v_new, a.k_pool, a.v_pool, a.block_table, a.seq_lens)
-    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), "cuda")
-    ref = torch.full((B, x, D), float("nan"), device="cuda")
-    hetis.attn_partial(s, a.q, a.k_pool, a.v_pool, a.block_table, a.seq_lens, L, ws, flags=flags)
-    hetis.attn_combine(s, a.seq_lens, L, ref, ws)
-    o = torch.full_like(ref, float("nan"))
-    hetis.attn_decode_append(s, b.q, b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, o, ws,
-                             flags=flags)
-    torch.cuda.synchronize()
-    assert torch.equal(o, ref)
-    assert torch.equal(b.k_pool.view(torch.int16), a.k_pool.view(torch.int16))
-    assert torch.equal(b.v_pool.view(torch.int16), a.v_pool.view(torch.int16))
-    outs = [torch.full_like(ref, float("nan")) for _ in range(4)]
-    stream = torch.cuda.Stream()
-    stream.wait_stream(torch.cuda.current_stream())
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(stream):
-        with torch.cuda.graph(g, stream=stream):
-            for k in range(4):
-                hetis.attn_decode(s, a.q, a.k_pool, a.v_pool, a.block_table, a.seq_lens, L, outs[k], ws,
-                                  flags=flags)
-    torch.cuda.current_stream().wait_stream(stream)
-    for _ in range(3):
-        for t in outs:
-            t.fill_(float("nan"))
-        g.replay()
-        torch.cuda.synchronize()
-        for t in outs:
-            assert torch.equal(t, ref)
-    assert_close(ref, oracle_full(a), "streaming combine")
-
-
 def test_decode_step_fused_append_matches_separate_calls():
     from paper_2509_08309_b200.step import DecodeStep
     shape = workload.LLAMA2_70B
