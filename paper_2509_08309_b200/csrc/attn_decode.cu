@@ -66,7 +66,7 @@ constexpr int kQSlots = 2;
 //   8 heads 26.8 / 27.6 / 29.9.
 // The warp count never changes an item's arithmetic (bit-identical either way).  0 disables it.
 #ifndef HETIS_RESCALE_THRESHOLD
-#define HETIS_RESCALE_THRESHOLD 0
+#define HETIS_RESCALE_THRESHOLD 8
 #endif
 #ifndef HETIS_EARLY_RELEASE
 #define HETIS_EARLY_RELEASE 0
@@ -1335,6 +1335,7 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     RingPos pos{0, 0u};
     bool c_waited = false;  // this warp has executed griddepcontrol.wait (pipelined deferred pages)
     constexpr bool fused_out = FUSED;
+    const bool diag_stream = (p.flags & HETIS_ATTN_DIAG_STREAM_ONLY) != 0;  // hoisted out of the page loop
     const int64_t epoch = p.peer_mode ? current_epoch(p.peer) : 0;  // the previous step's peer_wait wrote it
     bool acked = false;
     for (int it = 0;; ++it) {
@@ -1428,7 +1429,7 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             if (w == 0 && lane == 0 && it == 0 && pg == 0) {
                 HETIS_TS(4);
             }
-            if (p.flags & HETIS_ATTN_DIAG_STREAM_ONLY) {
+            if (diag_stream) {
                 __syncwarp();
                 if (lane == 0) dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
                 pos.advance(1, SW);
@@ -1560,7 +1561,7 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
                     put_out<2>(p, obase + (size_t)grp * D + 8 * nt + 2 * tq, v);
                 }
             }
-        } else if (grp < R && !(p.flags & HETIS_ATTN_DIAG_STREAM_ONLY)) {
+        } else if (grp < R && !diag_stream) {
             const size_t row = (size_t)meta.item * R + grp;
             float *dst = p.part_o + row * D;
 #if HETIS_PARTIAL_EVICT_LAST
