@@ -357,10 +357,12 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
         o_full = step.buf.o_shard
     stream = torch.cuda.current_stream(device)
     # the local step (N = 1, and the NCCL exchange) through the library's one-call step,
-    # hetis_attn_decode_append: the attention kernel with the append fused, then the combine kernel (or,
-    # opt-in with --attn-flags 0x20, the merge fused into the attention kernel: one kernel, measured slower)
+    # hetis_attn_decode_append: the attention kernel with the append fused, then the combine kernel -- or ONE
+    # kernel with the merge fused: automatically in group mode (<= one (request, kv head) pair per SM, <= 8
+    # splits), opt-in elsewhere with --attn-flags 0x20 (measured slower there)
     fused = (not peer) and bool(args.fused_append)
-    merge_in_kernel = fused and hetis.attn_decode_launches(step.cshape, args.attn_flags) == 1
+    merge_in_kernel = fused and hetis.attn_decode_launches_for(step.cshape, B, q_count, max_len,
+                                                               args.attn_flags) == 1
 
     fused_peer = peer and bool(args.fused_append) and bool(args.attn_flags & hetis.ATTN_FUSED_MERGE) and \
         step.merge_fused(args.attn_flags)

@@ -150,6 +150,14 @@ typedef struct {
  * L2 round trips under a saturated memory system stall the merging warp), so
  * opt-in. */
 #define HETIS_ATTN_FUSED_MERGE 0x20u
+/* Merge-fused launches (above) run in GROUP MODE when they have at most one
+ * (request, kv head) pair per SM and at most 8 splits per pair (max_seq_len <=
+ * 2048), e.g. the LLaMA-70B GQA share of one of 8 GPUs: CTA c runs pair c,
+ * consumer warp w its split w, the warps stage their partials in shared memory
+ * and fold them there after one CTA barrier (the combine's arithmetic, same
+ * order: bit-identical).  This flag turns group mode off (the last-arriver
+ * merge through L2 instead). */
+#define HETIS_ATTN_NO_GROUP_MODE 0x40u
 /* Diagnostic only: stream every K/V page through the shared-memory ring but
  * skip the math (partials are left unwritten).  Measures the memory-system
  * ceiling of the pipeline; the CUDA-core kernel honours it. */
@@ -292,8 +300,10 @@ HETIS_API hetis_status hetis_attn_combine_lse(const hetis_shape *shape, int32_t 
  * _TC_SHARED_RING / _PIPELINED / _DIAG_STREAM_ONLY) it is ONE kernel: the warp
  * that finishes the last split of a (request, kv head) pair folds the pair's
  * splits (the combine's arithmetic, same order) and stores its r rows; a
- * one-split pair stores its rows straight from registers.  Otherwise two
- * kernels.  o must be 16-byte aligned. */
+ * one-split pair stores its rows straight from registers.  Launches that
+ * qualify for group mode (see hetis_attn_decode_launches_for) are one kernel
+ * without the flag.  Otherwise two kernels.  o must be 16-byte aligned for
+ * the one-kernel form (8-byte for the two-kernel form). */
 HETIS_API hetis_status hetis_attn_decode_append(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
                                                 int32_t q_head_count, const void *q, const void *k_new,
                                                 const void *v_new, void *k_pool, void *v_pool, int64_t num_pages,
@@ -312,8 +322,21 @@ HETIS_API hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_s
 
 /* Kernels hetis_attn_decode / _decode_append / _decode_units launch for this
  * shape and these flags: 1 (merge fused into the attention kernel) or 2
- * (attention + combine); -1 for an invalid shape. */
+ * (attention + combine); -1 for an invalid shape.  Launches in group mode
+ * (HETIS_ATTN_NO_GROUP_MODE above) are always 1: use
+ * hetis_attn_decode_launches_for for the count of one concrete launch. */
 HETIS_API int32_t hetis_attn_decode_launches(const hetis_shape *shape, uint32_t flags);
+
+/* Kernels one hetis_attn_decode / _decode_append launch of num_seqs requests,
+ * q_head_count local query heads and seq_lens <= max_seq_len runs, for a
+ * 16-byte aligned o (for _decode_units pass num_seqs = num_units and
+ * q_head_count = r): 1 when the merge is fused -- HETIS_ATTN_FUSED_MERGE, or
+ * automatically in group mode (<= one (request, kv head) pair per SM and
+ * max_seq_len <= 2048 on the per-warp tensor-core kernel, where one kernel is
+ * measured faster: the LLaMA-70B GQA 8-GPU share 27.9 vs 29.0 us per step) --
+ * else 2; -1 for invalid arguments. */
+HETIS_API int32_t hetis_attn_decode_launches_for(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_count,
+                                                 int32_t max_seq_len, uint32_t flags);
 
 /* A per-request plan (f2: x_i^j varying with request j, the Eq. 7 dispatcher's
  * output) executed by ONE attention launch and ONE

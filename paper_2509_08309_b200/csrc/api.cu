@@ -433,6 +433,19 @@ static bool fused_merge_ok(const hetis_shape *shape, uint32_t flags) {
                       HETIS_ATTN_DIAG_STREAM_ONLY));
 }
 
+// The one-kernel (merge-fused) decode: opt-in with HETIS_ATTN_FUSED_MERGE, and automatic for launches
+// in group mode (<= one (request, kv head) pair per SM, <= 8 splits per pair: hetis::group_mode_qualifies)
+// with a 16-byte aligned o -- there it is measured faster than attention + combine.
+static bool fused_for(const hetis_shape *shape, int64_t pairs, int32_t max_seq_len, uint32_t flags, const void *o) {
+    if (fused_merge_ok(shape, flags)) return true;
+    return aligned(o, 16) && hetis::group_mode_qualifies(pairs, max_seq_len, flags) &&
+           fused_merge_ok(shape, flags | HETIS_ATTN_FUSED_MERGE);
+}
+static int64_t pairs_of(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_count) {
+    const int r = shape->num_q_heads / shape->num_kv_heads;
+    return (int64_t)num_seqs * (q_head_count / r);
+}
+
 static hetis_status attn_partial_impl(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
                                       int32_t q_head_count, const void *q, const void *k_new, const void *v_new,
                                       const void *k_pool, const void *v_pool, int64_t num_pages,
@@ -733,6 +746,15 @@ int32_t hetis_attn_decode_launches(const hetis_shape *shape, uint32_t flags) {
     return fused_merge_ok(shape, flags) ? 1 : 2;
 }
 
+int32_t hetis_attn_decode_launches_for(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_count,
+                                       int32_t max_seq_len, uint32_t flags) {
+    if (!shape || check_shape(shape) != HETIS_OK) return -1;
+    const int r = shape->num_q_heads / shape->num_kv_heads;
+    if (num_seqs < 1 || q_head_count < r || q_head_count % r || max_seq_len < 1) return -1;
+    static const int16_t aligned16[8] __attribute__((aligned(16))) = {};
+    return fused_for(shape, pairs_of(shape, num_seqs, q_head_count), max_seq_len, flags, aligned16) ? 1 : 2;
+}
+
 hetis_status hetis_attn_decode_append(const hetis_shape *shape, int32_t num_seqs, int32_t q_head_begin,
                                       int32_t q_head_count, const void *q, const void *k_new, const void *v_new,
                                       void *k_pool, void *v_pool, int64_t num_pages, const int32_t *block_table,
@@ -740,7 +762,8 @@ hetis_status hetis_attn_decode_append(const hetis_shape *shape, int32_t num_seqs
                                       void *workspace, size_t workspace_bytes, uint32_t flags,
                                       hetis_stream_t stream) {
     if (!o && num_seqs > 0) return fail(HETIS_E_INVALID, "o is NULL");
-    if (shape && check_shape(shape) == HETIS_OK && fused_merge_ok(shape, flags)) {
+    if (shape && check_shape(shape) == HETIS_OK &&
+        fused_for(shape, pairs_of(shape, num_seqs, q_head_count), max_seq_len, flags, o)) {
         if (num_seqs > 0 && (!k_new || !v_new)) return fail(HETIS_E_INVALID, "k_new / v_new is NULL");
         if (!aligned(k_new, 16) || !aligned(v_new, 16))
             return fail(HETIS_E_INVALID, "k_new / v_new must be 16-B aligned");
@@ -763,7 +786,8 @@ hetis_status hetis_attn_decode(const hetis_shape *shape, int32_t num_seqs, int32
                                int32_t max_seq_len, void *o, void *workspace, size_t workspace_bytes, uint32_t flags,
                                hetis_stream_t stream) {
     if (!o && num_seqs > 0) return fail(HETIS_E_INVALID, "o is NULL");
-    if (shape && check_shape(shape) == HETIS_OK && fused_merge_ok(shape, flags)) {
+    if (shape && check_shape(shape) == HETIS_OK &&
+        fused_for(shape, pairs_of(shape, num_seqs, q_head_count), max_seq_len, flags, o)) {
         if (!aligned(o, 16)) return fail(HETIS_E_INVALID, "o must be 16-byte aligned");
         return attn_partial_impl(shape, num_seqs, q_head_begin, q_head_count, q, nullptr, nullptr, k_pool, v_pool,
                                  num_pages, block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes,
@@ -812,7 +836,8 @@ hetis_status hetis_attn_decode_units(const hetis_shape *shape, int32_t num_seqs,
     a.v_new = v_new;
     a.units = units;
     a.row_kv_heads = Hkv;
-    const bool fused = fused_merge_ok(shape, flags) && aligned(o, 16) && (o_seq_stride * oe) % 16 == 0;
+    const bool fused = fused_for(shape, num_units, max_seq_len, flags, o) && aligned(o, 16) &&
+                       (o_seq_stride * oe) % 16 == 0;
     if (fused) {  // one launch: the merge runs in the per-warp kernel
         a.o_out = o;
         a.o_seq_stride = o_seq_stride;

@@ -105,6 +105,9 @@ constexpr int kQSlots = 2;
 #ifndef HETIS_PARTIAL_EVICT_LAST
 #define HETIS_PARTIAL_EVICT_LAST 1
 #endif
+#ifndef HETIS_GROUP_MODE
+#define HETIS_GROUP_MODE 1  // merge-fused launches use group mode when they qualify (Params::group_mode)
+#endif
 #ifndef HETIS_WARP_STAGES
 #define HETIS_WARP_STAGES 4
 #endif
@@ -187,6 +190,11 @@ struct Params {
     // before the first q copy -- what hetis_scatter_pull did, without its copy
     int pull_mode;
     int in_kv_stride;  // kv rows per request in the q / k_new / v_new layouts (kv_heads when dense)
+    // group mode (merge-fused launches with at most one (request, kv head) pair per CTA and at most NW
+    // splits per pair, e.g. the c3 8-GPU share): CTA c runs pair c, its worker w split w; each warp stages
+    // its partial in its own (drained) sub-ring, one named barrier, and warp w folds row w from shared
+    // memory -- the combine's arithmetic (fold_splits_with), no global round trip, no combine launch
+    int group_mode;
 };
 
 // Row of (launch row j, local kv head g) in the block-table layout.
@@ -1066,6 +1074,7 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
                                             : (int)(((long long)n_items * static_pct / 100) / gridDim.x);
     const int n_static = device_claim ? (int)gridDim.x * NW : per_cta * (int)gridDim.x;
     auto claim = [&]() -> int {
+        if (p.group_mode) return n_items;
         if (!device_claim) {
             const int k = atomicAdd(sm.claim, 1);
             if (k < per_cta) return (int)blockIdx.x + k * (int)gridDim.x;
@@ -1079,7 +1088,14 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     // The first claim is CTA-local only: a steal touches the device-wide counter, which needs a
     // griddepcontrol.wait, and that wait must be executed by the converged producer warp (below).
     int item = device_claim ? w * (int)gridDim.x + (int)blockIdx.x : -2;
-    if (!device_claim) {
+    if (p.group_mode) {  // CTA c: pair c; worker w: its split w (one item per worker, no claims)
+        item = n_items;
+        const int c = (int)blockIdx.x;
+        if (c < p.num_seqs * p.kv_heads) {
+            const int jj = c / p.kv_heads, gg = c - jj * p.kv_heads;
+            if (w < s_off[jj + 1] - s_off[jj]) item = (s_off[jj] + w) * p.kv_heads + gg;
+        }
+    } else if (!device_claim) {
         const int k = atomicAdd(sm.claim, 1);
         if (k < per_cta) item = (int)blockIdx.x + k * (int)gridDim.x;
     }
@@ -1296,6 +1312,40 @@ __device__ __forceinline__ void merge_pair_rows(const Params &p, int ns, int s0,
             const float v[4] = {acc.x, acc.y, acc.z, acc.w};
             put_out<4>(p, obase + (size_t)rr * D + 4 * d4, v);
         }
+    }
+}
+
+// Group mode (Params::group_mode): every consumer warp of the CTA has staged its split's partial
+// ([R][D] o_s rows, then R lse_s) at the start of its own sub-ring; after one named barrier over the
+// consumer warps, warp w folds rows w, w + NW, ... (D = 64: two rows per pass) of the CTA's pair from
+// shared memory -- fold_splits_with(0, 1, ns), exactly the combine's narrow fold (ns <= NW <= 16).
+template <int D, int R, int NW>
+__device__ __forceinline__ void group_merge(const Params &p, const WarpSmem &sm, int SW, const int32_t *s_off,
+                                         int64_t epoch, bool acked, int w, int lane) {
+    constexpr int kStageBytes = 2 * kP * D * 2;
+    constexpr int TPH = D / 4, RPP = 32 / TPH;
+    static_assert(NW <= kNarrowSplits, "group mode folds with the narrow fold");
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * NW) : "memory");  // every split's partial is staged
+    const int c = (int)blockIdx.x;
+    if (c >= p.num_seqs * p.kv_heads || w * RPP >= R) return;
+    const int j = c / p.kv_heads, gk = c - j * p.kv_heads;
+    const int s0 = s_off[j], ns = s_off[j + 1] - s0;
+    if (ns <= 1) return;  // one split: its warp stored O from registers
+    const int jr = p.units != nullptr ? __ldg(p.units + 2 * j) : j;
+    const int gr = p.units != nullptr ? __ldg(p.units + 2 * j + 1) : gk;
+    const size_t obase = (size_t)jr * p.o_seq_stride + ((size_t)p.o_head0 + (size_t)gr * R) * D;
+    await_peer_acks(p, epoch, acked, lane);
+    const int d4 = lane % TPH;
+    for (int rr = w * RPP + lane / TPH; rr < R; rr += NW * RPP) {
+        const FoldState f = fold_splits_with(0, 1, ns, [&](int sp, float &l, float4 &v) {
+            const float *st = reinterpret_cast<const float *>(sm.ring + (size_t)sp * SW * kStageBytes);
+            l = st[R * D + rr];
+            v = *reinterpret_cast<const float4 *>(st + rr * D + 4 * d4);
+        });
+        float lse2;
+        const float4 acc = finish(f, &lse2);
+        const float v[4] = {acc.x, acc.y, acc.z, acc.w};
+        put_out<4>(p, obase + (size_t)rr * D + 4 * d4, v);
     }
 }
 
@@ -1561,6 +1611,15 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
                     put_out<2>(p, obase + (size_t)grp * D + 8 * nt + 2 * tq, v);
                 }
             }
+        } else if (fused_out && p.group_mode) {  // stage the partial in this warp's drained sub-ring
+            float *stg = reinterpret_cast<float *>(sm.ring + (size_t)w * SW * kStageBytes);
+            if (grp < R) {
+#pragma unroll
+                for (int nt = 0; nt < NT_O; ++nt)
+                    *reinterpret_cast<float2 *>(stg + grp * D + 8 * nt + 2 * tq) =
+                        make_float2(__fdiv_rn(o[nt][0] + o[nt][2], l), __fdiv_rn(o[nt][1] + o[nt][3], l));
+                if (tq == 0) stg[R * D + grp] = m + __log2f(l);
+            }
         } else if (grp < R && !diag_stream) {
             const size_t row = (size_t)meta.item * R + grp;
             float *dst = p.part_o + row * D;
@@ -1579,7 +1638,7 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             if (tq == 0) p.part_lse[row] = m + __log2f(l);
 #endif
         }
-        if (ns > 1) {  // publish this split; the pair's last split folds them all
+        if (ns > 1 && !p.group_mode) {  // publish this split; the pair's last split folds them all
             __syncwarp();
             int last = 0;
             if (lane == 0) {
@@ -1597,6 +1656,9 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
 #endif
             }
         }
+    }
+    if constexpr (fused_out) {
+        if (p.group_mode) group_merge<D, R, NW>(p, sm, SW, s_off, epoch, acked, w, lane);
     }
 }
 
@@ -1700,12 +1762,21 @@ cudaError_t launch_gqa_warp_nw(const Params &p0, int num_seqs, cudaStream_t s, c
     return launch_pdl(kern, dim3(num_sms()), dim3(32 * (NW + 1)), smem, s, p, tk, tv);
 }
 
+// Group mode (see Params::group_mode): at most one (request, kv head) pair per CTA and at most NW
+// splits per pair (seq_lens <= max_seq_len is a device-data contract), non-pipelined
+inline bool group_mode_ok(const Params &p, int num_seqs, int max_seq_len) {
+    return group_mode_qualifies((int64_t)num_seqs * p.kv_heads, max_seq_len, p.flags);
+}
+
 // warp count of the per-warp kernel for this launch (see HETIS_TC_NW_LARGE)
 template <int D, int R>
 cudaError_t launch_gqa_warp(const Params &p, int num_seqs, int max_seq_len, cudaStream_t s, const CUtensorMap &tk,
                             const CUtensorMap &tv, std::string *err) {
-    if (p.o_out != nullptr || p.peer_mode)  // the opt-in fused merge: one configuration
-        return launch_gqa_warp_nw<D, R, HETIS_TC_NW, true>(p, num_seqs, s, tk, tv, err);
+    if (p.o_out != nullptr || p.peer_mode) {  // the fused merge: one configuration
+        Params q = p;
+        q.group_mode = group_mode_ok(p, num_seqs, max_seq_len) ? 1 : 0;
+        return launch_gqa_warp_nw<D, R, HETIS_TC_NW, true>(q, num_seqs, s, tk, tv, err);
+    }
 #if HETIS_TC_NW_LARGE > 0
     const int64_t est_items = (int64_t)num_seqs * p.kv_heads * ((max_seq_len + kC - 1) / kC);
     if (est_items >= (int64_t)HETIS_TC_LARGE_ITEMS_PER_WORKER * num_sms() * HETIS_TC_NW_LARGE)
@@ -1940,6 +2011,17 @@ cudaError_t launch_attn_simt(const AttnArgs &a, cudaStream_t s) {
         if (a.head_dim == 64) return dispatch_r<HETIS_F32, 64, false>(a, p, s, dummy, dummy, &err);
     }
     return cudaErrorInvalidValue;
+}
+
+bool group_mode_qualifies(int64_t pairs, int max_seq_len, uint32_t flags) {
+#if HETIS_GROUP_MODE
+    return !(flags & (HETIS_ATTN_PIPELINED | HETIS_ATTN_DEVICE_CLAIM | HETIS_ATTN_NO_GROUP_MODE |
+                      HETIS_ATTN_DIAG_STREAM_ONLY)) &&
+           pairs >= 1 && pairs <= num_sms() && max_seq_len >= 1 && (max_seq_len + kC - 1) / kC <= HETIS_TC_NW;
+#else
+    (void)pairs; (void)max_seq_len; (void)flags;
+    return false;
+#endif
 }
 
 cudaError_t launch_attn_tc(const AttnArgs &a, cudaStream_t s, std::string *err) {

@@ -69,6 +69,11 @@ WorkspaceLayout workspace_layout(int num_seqs, int kv_heads, int r, int head_dim
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_attn_simt(const AttnArgs &a, cudaStream_t s);
 cudaError_t launch_attn_tc(const AttnArgs &a, cudaStream_t s, std::string *err);
+// Group mode of the merge-fused per-warp kernel (attn_decode.cu, Params::group_mode): launches with
+// at most one (request, kv head) pair per SM and at most HETIS_TC_NW splits per pair, not pipelined,
+// not device-claimed, not HETIS_ATTN_NO_GROUP_MODE.  The decode calls fuse the merge for such launches
+// even without HETIS_ATTN_FUSED_MERGE (measured faster: c3 8-GPU share 27.9 vs 29.0 us per step).
+bool group_mode_qualifies(int64_t pairs, int max_seq_len, uint32_t flags);
 cudaError_t launch_combine(int num_seqs, int q_heads, int r, int head_dim, const int32_t *seq_lens,
                            const int32_t *split_off, const float *part_lse, const float *part_o, void *o,
                            int o_dtype, int64_t o_seq_stride, cudaStream_t s, float *lse, int max_seq_len,

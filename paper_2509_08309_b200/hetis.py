@@ -29,12 +29,13 @@ ATTN_DEVICE_CLAIM = 0x4
 ATTN_MHA_TC = 0x8
 ATTN_PIPELINED = 0x10
 ATTN_FUSED_MERGE = 0x20
+ATTN_NO_GROUP_MODE = 0x40
 ATTN_DIAG_STREAM_ONLY = 0x100
 
 EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_split_tokens",
             "hetis_plan_create", "hetis_plan_destroy", "hetis_plan_heads", "hetis_plan_num_devices", "hetis_plan_units",
             "hetis_plan_check_capacity", "hetis_kv_append", "hetis_attn_decode_workspace", "hetis_attn_partial",
-            "hetis_attn_combine", "hetis_attn_decode", "hetis_attn_combine_peers", "hetis_peer_wait",
+            "hetis_attn_combine", "hetis_attn_decode", "hetis_attn_decode_launches_for", "hetis_attn_combine_peers", "hetis_peer_wait",
             "hetis_comm_workspace", "hetis_scatter_q", "hetis_gather", "hetis_kv_migrate",
             "hetis_attn_combine_lse", "hetis_seq_split_lens", "hetis_seq_merge", "hetis_seq_broadcast_q",
             "hetis_seq_allgather_merge", "hetis_peer_state_bytes", "hetis_peer_group_create",
@@ -113,6 +114,7 @@ def lib() -> ctypes.CDLL:
                                                             i32, vp, vp, sz, u32, vp]),
                 "hetis_scatter_pull": (ctypes.c_int, [vp, i32, vp, vp, vp, vp]),
                 "hetis_attn_decode_launches": (i32, [sp, u32]),
+                "hetis_attn_decode_launches_for": (i32, [sp, i32, i32, i32, u32]),
                 "hetis_peer_access": (ctypes.c_int, [i32]),
                 "hetis_attn_partial_pull": (ctypes.c_int, [vp, i32, vp, vp, i64, vp, i32, vp, i32, vp, sz, u32, vp]),
                 "hetis_attn_decode_peers": (ctypes.c_int, [vp, i32, vp, vp, vp, vp, vp, i64, vp, i32, vp, i32, vp, sz,
@@ -407,6 +409,14 @@ def attn_decode_launches(shape: CShape, flags: int = 0) -> int:
     n = lib().hetis_attn_decode_launches(ctypes.byref(shape), flags)
     if n < 0:
         raise ValueError("invalid shape")
+    return n
+
+
+def attn_decode_launches_for(shape: CShape, num_seqs: int, q_head_count: int, max_seq_len: int, flags: int = 0) -> int:
+    """Kernels of one hetis_attn_decode(_append) launch (1: merge fused, opt-in or group mode; 2: + combine)."""
+    n = lib().hetis_attn_decode_launches_for(ctypes.byref(shape), num_seqs, q_head_count, max_seq_len, flags)
+    if n < 0:
+        raise ValueError("invalid arguments")
     return n
 
 

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--decode", action="store_true", help="also time hetis_attn_decode_append with each flag set")
     a = ap.parse_args()
     cfg = workload.CONFIGS[a.config]
     shape = cfg.shape
@@ -58,8 +59,15 @@ def main():
                 attn(i)
                 hetis.attn_combine(s, b.seq_lens, L, o, ws)
 
+            def decode(i):   # the library's one-call step (one kernel with HETIS_ATTN_FUSED_MERGE)
+                hetis.attn_decode_append(s, b.q, b.k_new, b.v_new, kp[i % n_layers], vp[i % n_layers],
+                                         b.block_table, b.seq_lens, L, o, ws, flags=fl)
+
             res = {}
-            for name, fn in (("attn", attn), ("step", step)):
+            fns = [("attn", attn), ("step", step)]
+            if a.decode and not fl & hetis.ATTN_DIAG_STREAM_ONLY:
+                fns.append(("decode", decode))
+            for name, fn in fns:
                 for i in range(5):
                     fn(i)
                 g = torch.cuda.CUDAGraph()

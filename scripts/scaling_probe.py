@@ -116,7 +116,7 @@ def share_time(cfg, n: int, steps: int, warmup: int, device, split=None, rank: i
     step_decode_ms = t0.elapsed_time(t1) / steps
     # the step in ONE kernel where the attention kernel also merges the splits (hetis_attn_decode_append)
     step_fused_ms = None
-    if hetis.attn_decode_launches(s, 0) == 1:
+    if hetis.attn_decode_launches_for(s, B, x, L, 0) == 1:   # group mode (or an opt-in fused build)
         g4 = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g4):
             for i in range(steps):
@@ -180,7 +180,9 @@ def main():
         r["compute_scaling_decode_call_vs_n1"] = rows[0]["step_decode_call_us"] / r["step_decode_call_us"]
         r["compute_scaling_best_vs_n1"] = t1n / min(best)
         if r["step_fused_us"]:
-            r["compute_scaling_fused_vs_n1"] = rows[0]["step_fused_us"] / r["step_fused_us"]
+            # vs N = 1's one-kernel step when it has one, else its library step (attention + combine)
+            r["compute_scaling_fused_vs_n1"] = (rows[0]["step_fused_us"] or rows[0]["step_decode_call_us"]) / \
+                r["step_fused_us"]
         r["compute_scaling_best_vs_best_n1"] = min(best1) / min(best)
         r["config"] = cfg.name
         print(json.dumps(r), flush=True)

@@ -584,6 +584,53 @@ def test_merge_fused_into_attention_bit_identical_to_combine_kernel(H, Hkv, D, f
         assert_close(got, oracle_full(b), "fused merge")
 
 
+GROUP_LENS = (1, 15, 16, 17, 255, 256, 257, 511, 1000, 1024, 1500, 1793, 2000, 2047, 2048, 700)
+
+
+@pytest.mark.parametrize("H,Hkv,D,odt,B", [(64, 8, 128, "f32", 16), (16, 2, 128, "bf16", 64), (16, 4, 64, "f32", 37),
+                                           (8, 1, 128, "f32", 148), (8, 1, 128, "bf16", 149), (64, 8, 128, "f32", 19)])
+def test_group_mode_bit_identical_to_combine_kernel(H, Hkv, D, odt, B):
+    """Merge-fused launches with at most one (request, kv head) pair per SM and <= 8 splits per pair run in
+    group mode (CTA c = pair c, warp w = split w, partials staged in shared memory and folded after one CTA
+    barrier; 148 pairs is the boundary, 149 and 152 fall back to the last-arriver merge).  Every form is
+    bit-identical to hetis_attn_partial + hetis_attn_combine, including ragged tails, one-split pairs
+    (L <= 256) and the full 8 splits (L = 2048), for f32 and bf16 O; the append-fused form too; the oracle
+    agrees within tolerance."""
+    lens = [GROUP_LENS[i % len(GROUP_LENS)] for i in range(B)]
+    fresh = gpu_batch(H, Hkv, D, "bf16", lens, seed=321)
+    b = gpu_batch(H, Hkv, D, "bf16", lens, seed=321)
+    s = hetis.make_shape(b.shape, odt)
+    x = b.q.shape[1]
+    L = 2048
+    hetis.kv_append(s, b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens)
+    odtype = torch.bfloat16 if odt == "bf16" else torch.float32
+    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), "cuda")
+    ref = torch.full((B, x, D), float("nan"), dtype=odtype, device="cuda")
+    hetis.attn_partial(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, ws)
+    hetis.attn_combine(s, b.seq_lens, L, ref, ws)
+    group = B * (x // (H // Hkv)) <= 148   # B200: one pair per SM
+    assert hetis.attn_decode_launches_for(s, B, x, L, 0) == (1 if group else 2)
+    assert hetis.attn_decode_launches_for(s, B, x, L, hetis.ATTN_NO_GROUP_MODE) == 2
+    for flags in (0, FM, FM | hetis.ATTN_NO_GROUP_MODE):
+        for rep in range(2):
+            got = torch.full_like(ref, float("nan"))
+            n0 = hetis.launch_count()
+            hetis.attn_decode(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, got, ws, flags=flags)
+            assert hetis.launch_count() - n0 == hetis.attn_decode_launches_for(s, B, x, L, flags)
+            torch.cuda.synchronize()
+            assert torch.equal(got.view(torch.int16), ref.view(torch.int16)), (flags, rep)
+    # the append fused as well (the bench's one-kernel step): same O, same pools
+    got = torch.full_like(ref, float("nan"))
+    hetis.attn_decode_append(s, fresh.q, fresh.k_new, fresh.v_new, fresh.k_pool, fresh.v_pool, fresh.block_table,
+                             fresh.seq_lens, L, got, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(got.view(torch.int16), ref.view(torch.int16))
+    assert torch.equal(fresh.k_pool.view(torch.int16), b.k_pool.view(torch.int16))
+    assert torch.equal(fresh.v_pool.view(torch.int16), b.v_pool.view(torch.int16))
+    if odt == "f32":
+        assert_close(got, oracle_full(b), "group mode")
+
+
 def test_decode_step_fused_append_matches_separate_calls():
     from paper_2509_08309_b200.step import DecodeStep
     shape = workload.LLAMA2_70B
