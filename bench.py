@@ -6,11 +6,15 @@
 
 One step = one layer's decode step for the whole batch on every rank:
     N = 1:  hetis_attn_partial_append (kv_append fused) -> hetis_attn_combine
-    N > 1 (default, --exchange peer): hetis_scatter_pull (the rank's q / new k, v
-            straight from the Primary's buffers over NVLink) -> hetis_attn_partial_append
-            -> hetis_attn_combine_peers (the combine storing every O row into every
-            rank's o_full) -> hetis_peer_wait;  --exchange nccl: hetis_scatter_q ->
-            ... -> hetis_attn_combine -> hetis_gather (NCCL over NVLink)
+    N > 1 (default, --exchange peer): hetis_attn_partial_pull (the attention kernel
+            reads the rank's q / new k, v straight from the Primary's buffers over
+            NVLink, append fused) -> hetis_attn_combine_peers (the combine storing
+            every O row into every rank's o_full) -> hetis_peer_wait; where the rank's
+            launch runs in group mode (<= one (request, kv head) pair per SM, L <= 2048:
+            c3 at 8 GPUs) the merge and the stores are in the attention kernel too
+            (hetis_attn_decode_peers, pull form) -> hetis_peer_wait.  --pull 0: a separate
+            hetis_scatter_pull kernel first.  --exchange nccl: hetis_scatter_q -> ... ->
+            hetis_attn_combine -> hetis_gather (NCCL over NVLink)
 Metric (BASELINE.json): decode attention tokens/s (= batch / step time, one
 layer, all heads, max over ranks) and achieved HBM GB/s of the dominant kernel
 (% of the measured copy peak).  Default workload: config c2 (LLaMA2-13B, 40
@@ -356,6 +360,10 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
         step.buf.v_new.copy_(batch.v_new)
         o_full = step.buf.o_shard
     stream = torch.cuda.current_stream(device)
+    if peer and q_count > 0:   # the roofline's attention-only launches read the dense shard: this rank's inputs
+        step.buf.q_shard.copy_(batch.q)
+        step.buf.k_new.copy_(batch.k_new)
+        step.buf.v_new.copy_(batch.v_new)
     # the local step (N = 1, and the NCCL exchange) through the library's one-call step,
     # hetis_attn_decode_append: the attention kernel with the append fused, then the combine kernel -- or ONE
     # kernel with the merge fused: automatically in group mode (<= one (request, kv head) pair per SM, <= 8
@@ -364,16 +372,19 @@ def measure(args, cfg_name: str, D: Dist, rank: int, world: int, comm_ptr, headl
     merge_in_kernel = fused and hetis.attn_decode_launches_for(step.cshape, B, q_count, max_len,
                                                                args.attn_flags) == 1
 
-    fused_peer = peer and bool(args.fused_append) and bool(args.attn_flags & hetis.ATTN_FUSED_MERGE) and \
-        step.merge_fused(args.attn_flags)
+    # over peer memory the merge (+ the stores into every rank's o_full) is fused into the attention kernel where
+    # this rank's launch runs in group mode (or with --attn-flags 0x20)
+    fused_peer = peer and bool(args.fused_append) and step.merge_fused_default(args.attn_flags)
     # the scatter folded into the attention kernel (it reads q / new k, v from the Primary): the default
-    pull = peer and not fused_peer and bool(args.fused_append) and bool(args.pull) and \
-        step.pull_supported(args.attn_flags)
+    pull = peer and bool(args.fused_append) and bool(args.pull) and step.pull_supported(args.attn_flags)
 
     def attention(li):
-        if pull:
+        if pull and fused_peer:   # pull + append + attention + split merge + the stores into every rank's o_full
+            hetis.attn_decode_peers_pull(step.group, B, k_pools[li], v_pools[li], batch.block_table,
+                                         batch.seq_lens, max_len, step.buf.workspace, flags=args.attn_flags)
+        elif pull:
             hetis.attn_partial_pull(step.group, B, k_pools[li], v_pools[li], batch.block_table, batch.seq_lens,
-                                    max_len, step.buf.workspace, flags=args.attn_flags)
+                                    max_len, step.buf.workspace, flags=args.attn_flags & ~hetis.ATTN_FUSED_MERGE)
         elif fused_peer:          # append + attention + split merge + the stores into every rank's o_full
             hetis.attn_decode_peers(step.group, step.buf.q_shard, k_pools[li], v_pools[li], batch.block_table,
                                     batch.seq_lens, max_len, step.buf.workspace, k_new_shard=step.buf.k_new,

@@ -474,7 +474,15 @@ HETIS_API hetis_status hetis_attn_partial_pull(const hetis_peer_group *group, in
  * Only where hetis_attn_decode_launches(shape, flags | HETIS_ATTN_FUSED_MERGE)
  * == 1 (the per-warp tensor-core kernel; the flag is implied) and the rank
  * holds >= 1 head and >= 1 request; else HETIS_E_UNSUPPORTED (use the
- * two-kernel path).  o_full rows 16-B aligned. */
+ * two-kernel path).  o_full rows 16-B aligned.
+ * q_shard == NULL (then k_new_shard and v_new_shard NULL too): PULL form -- the
+ * kernel reads q and the new k, v rows from the Primary's buffers as
+ * hetis_attn_partial_pull does (its acknowledgement / epoch protocol, the
+ * append fused), so one step per rank is TWO kernels
+ *     hetis_attn_decode_peers(q_shard = NULL) -> hetis_peer_wait;
+ * the group needs the Primary's mappings.  Launches that qualify for group mode
+ * (hetis_attn_decode_launches_for) merge in shared memory (the default N > 1
+ * step for such shares, e.g. LLaMA-70B GQA on 8 GPUs). */
 HETIS_API hetis_status hetis_attn_decode_peers(const hetis_peer_group *group, int32_t num_seqs, const void *q_shard,
                                                const void *k_new_shard, const void *v_new_shard, void *k_pool,
                                                void *v_pool, int64_t num_pages, const int32_t *block_table,

@@ -692,21 +692,32 @@ hetis_status hetis_attn_decode_peers(const hetis_peer_group *g, int32_t num_seqs
     if (num_seqs < 1) return fail(HETIS_E_UNSUPPORTED, "no requests: use hetis_attn_combine_peers");
     if ((k_new_shard == nullptr) != (v_new_shard == nullptr))
         return fail(HETIS_E_INVALID, "pass both k_new_shard and v_new_shard, or neither");
+    const bool pull = q_shard == nullptr;  // the scatter folded in: q / new rows from the Primary's buffers
+    if (pull && k_new_shard) return fail(HETIS_E_INVALID, "the pull form takes the new rows from the Primary");
+    if (pull && (!g->dev.q_root || !g->dev.k_root || !g->dev.v_root))
+        return fail(HETIS_E_INVALID, "the group has no mapping of the Primary's inputs");
     if (k_new_shard && (!aligned(k_new_shard, 16) || !aligned(v_new_shard, 16)))
         return fail(HETIS_E_INVALID, "k_new / v_new must be 16-B aligned");
     if ((g->dev.o_seq_stride * esize(s.o_dtype)) % 16) return fail(HETIS_E_INVALID, "o_full rows must be 16-B aligned");
     for (int p = 0; p < g->dev.n; ++p)
         if (hetis::peer_is_target(g->dev, p) && !aligned(g->dev.o[p], 16))
             return fail(HETIS_E_INVALID, "o_full must be 16-byte aligned");
+    const int r = s.num_q_heads / s.num_kv_heads;
+    const size_t row = (size_t)s.head_dim * esize(s.kv_dtype);
+    const void *q = pull ? static_cast<const void *>(g->dev.q_root + (size_t)g->dev.head0 * row) : q_shard;
     hetis::AttnArgs a{};
-    hetis_status st = attn_args(&s, num_seqs, g->dev.head0, g->q_count, q_shard, k_pool, v_pool, num_pages,
+    hetis_status st = attn_args(&s, num_seqs, g->dev.head0, g->q_count, q, k_pool, v_pool, num_pages,
                                 block_table, max_pages, seq_lens, max_seq_len, workspace, workspace_bytes, &a);
     if (st != HETIS_OK) return st;
     a.flags = flags;
-    a.k_new = k_new_shard;
-    a.v_new = v_new_shard;
+    a.k_new = pull ? static_cast<const void *>(g->dev.k_root + (size_t)(g->dev.head0 / r) * row) : k_new_shard;
+    a.v_new = pull ? static_cast<const void *>(g->dev.v_root + (size_t)(g->dev.head0 / r) * row) : v_new_shard;
     a.o_dtype = s.o_dtype;
     a.peer = &g->dev;
+    if (pull) {
+        a.pull = &g->dev;
+        a.in_kv_stride = s.num_kv_heads;
+    }
     std::string err;
     cudaError_t e = hetis::launch_attn_tc(a, reinterpret_cast<cudaStream_t>(stream), &err);
     if (e != cudaSuccess)

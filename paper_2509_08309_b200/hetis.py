@@ -539,6 +539,17 @@ def attn_decode_peers(group: PeerGroup, q_shard, k_pool, v_pool, block_table, se
            "hetis_attn_decode_peers")
 
 
+def attn_decode_peers_pull(group: PeerGroup, num_seqs: int, k_pool, v_pool, block_table, seq_lens, max_seq_len: int,
+                           workspace, flags: int = 0, stream=None) -> None:
+    """The pull form of hetis_attn_decode_peers (q_shard = NULL): the scatter, the append, the attention, the
+    split merge and the stores into every receiving rank's o_full in ONE kernel (then hetis_peer_wait)."""
+    _check(lib().hetis_attn_decode_peers(group.handle, num_seqs, None, None, None, _dev(k_pool, "k_pool"),
+                                         _dev(v_pool, "v_pool"), k_pool.shape[0], _dev(block_table, "block_table"),
+                                         block_table.shape[2], _dev(seq_lens, "seq_lens"), max_seq_len,
+                                         _dev(workspace, "workspace"), workspace.numel() * workspace.element_size(),
+                                         flags, _stream(stream)), "hetis_attn_decode_peers")
+
+
 def peer_wait(group: PeerGroup, stream=None) -> None:
     """The step's last kernel: wait for every rank's rows of this step (receiving ranks), record the step."""
     _check(lib().hetis_peer_wait(group.handle, _stream(stream)), "hetis_peer_wait")

@@ -154,13 +154,20 @@ class DecodeStep:
         return self.q_count > 0 and self.num_seqs > 0 and hetis.attn_decode_launches(
             self.cshape, flags | hetis.ATTN_FUSED_MERGE) == 1
 
+    def merge_fused_default(self, flags: int = 0) -> bool:
+        """The default choice: the merge fused into the attention kernel where the caller opts in
+        (HETIS_ATTN_FUSED_MERGE) or where this rank's launch runs in group mode (<= one (request, kv head) pair
+        per SM, <= 8 splits: the merge then runs in shared memory and is measured faster than the combine)."""
+        return self.merge_fused(flags) and (bool(flags & hetis.ATTN_FUSED_MERGE) or hetis.attn_decode_launches_for(
+            self.cshape, self.num_seqs, self.q_count, self.max_seq_len, flags) == 1)
+
     def attention_gather_peers(self, k_pool, v_pool, block_table, seq_lens, stream=None, flags: int = 0,
                                fused_append: bool = True, merge_fused: bool | None = None):
         """Attention (kv_append fused by default) whose split merge stores every row into every receiving
         rank's o_full -- ONE kernel (hetis_attn_decode_peers) where the per-warp kernel runs, else the partial
         kernel + hetis_attn_combine_peers -- then the step's closing wait.  Returns o_full."""
-        if merge_fused is None:                 # opt-in: measured slower than the separate combine (DESIGN §6)
-            merge_fused = bool(flags & hetis.ATTN_FUSED_MERGE) and self.merge_fused(flags)
+        if merge_fused is None:                 # opt-in, or group mode (DESIGN §6)
+            merge_fused = self.merge_fused_default(flags)
         if merge_fused:
             hetis.attn_decode_peers(self.group, self.buf.q_shard, k_pool, v_pool, block_table, seq_lens,
                                     self.max_seq_len, self.buf.workspace,
@@ -183,19 +190,29 @@ class DecodeStep:
     def pull_supported(self, flags: int = 0) -> bool:
         """hetis_attn_partial_pull applies: this rank holds heads and requests, an ordinary launch."""
         return self.q_count > 0 and self.num_seqs > 0 and not (
-            flags & (hetis.ATTN_PIPELINED | hetis.ATTN_DIAG_STREAM_ONLY | hetis.ATTN_FUSED_MERGE))
+            flags & (hetis.ATTN_PIPELINED | hetis.ATTN_DIAG_STREAM_ONLY))
 
     def step_peers(self, k_pool, v_pool, block_table, seq_lens, stream=None, flags: int = 0,
                    merge_fused: bool | None = None, pull: bool | None = None):
         """The whole N > 1 step over peer memory, no NCCL and no per-step host argument (graph-capturable):
         by default the attention kernel itself pulls q and the new k, v rows from the Primary
         (hetis_attn_partial_pull), then combine + gather into every rank's o_full, then the closing wait --
-        three kernels; pull=False: the separate pull scatter kernel first (four)."""
+        three kernels; where the merge is fused (group mode, or opt-in) the pull, the attention, the merge and
+        the stores into every o_full are ONE kernel (hetis_attn_decode_peers with q_shard = NULL) + the wait;
+        pull=False: the separate pull scatter kernel first."""
+        if merge_fused is None:
+            merge_fused = self.merge_fused_default(flags)
         if pull is None:
-            pull = self.pull_supported(flags) and not merge_fused
+            pull = self.pull_supported(flags)
+        if pull and merge_fused:
+            hetis.attn_decode_peers_pull(self.group, self.num_seqs, k_pool, v_pool, block_table, seq_lens,
+                                         self.max_seq_len, self.buf.workspace, flags=flags, stream=stream)
+            hetis.peer_wait(self.group, stream=stream)
+            return self.o_full
         if pull:
             hetis.attn_partial_pull(self.group, self.num_seqs, k_pool, v_pool, block_table, seq_lens,
-                                    self.max_seq_len, self.buf.workspace, flags=flags, stream=stream)
+                                    self.max_seq_len, self.buf.workspace, flags=flags & ~hetis.ATTN_FUSED_MERGE,
+                                    stream=stream)
             hetis.attn_combine_peers(self.group, seq_lens, self.max_seq_len, self.buf.workspace, stream=stream)
             hetis.peer_wait(self.group, stream=stream)
             return self.o_full

@@ -73,16 +73,20 @@ def test_bench_default_line_with_sub_record():
     assert cpu["cores"] >= 1 and cpu["value"] > 0 and cpu["value_1thread"] > 0 and cpu["cpu_model"]
 
 
-@pytest.mark.parametrize("n,config,extra", [(2, "c1", []), (4, "c3", []), (5, "c4", ["--gather-root", "0"])])
+@pytest.mark.parametrize("n,config,extra", [(2, "c1", []), (4, "c3", []), (5, "c4", ["--gather-root", "0"]),
+                                             (8, "c3", [])])
 def test_bench_multirank_peer_exchange_sharing_one_gpu(n, config, extra):
     """torchrun with n ranks on cuda:0 (--share-gpu, gloo bootstrap): the default N > 1 step (pull scatter,
     attention, combine storing into every rank's o_full, closing wait) replayed as a CUDA graph, then the
     gathered O checked in bench.py against the unsplit result (bit for bit) and the oracle; c4 runs its
-    uneven 16/8/8/4/4 split with the gather to the Primary."""
+    uneven 16/8/8/4/4 split with the gather to the Primary; c3 over 8 ranks (128 (request, kv head) pairs
+    per rank) runs the group-mode step: pull, attention, merge and stores in ONE kernel, then the wait."""
     d = _torchrun(n, "--share-gpu", *extra, config=config)
     _check(d, n)
     assert d["launch_mode"].startswith("cuda_graph")
     assert d["config"]["exchange"] == "peer"
+    assert d["config"]["scatter_in_attention"]
+    assert d["config"]["merge_fused"] == (n == 8 and config == "c3")
 
 
 @pytest.mark.parametrize("exchange", ["peer", "nccl"])

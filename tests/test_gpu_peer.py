@@ -30,7 +30,7 @@ LENS = (300, 17, 1029, 2048, 5, 256, 1)
 EAGER_STEPS, GRAPH_STEPS, GRAPH_REPLAYS = 3, 2, 2
 
 
-def _rank(rank, world, rendezvous, shape_args, split, gather_root, merge_fused, pull, res):
+def _rank(rank, world, rendezvous, shape_args, split, gather_root, merge_fused, pull, flags, res):
     import torch
     import torch.distributed as dist
     from paper_2509_08309_b200 import hetis, workload
@@ -59,7 +59,7 @@ def _rank(rank, world, rendezvous, shape_args, split, gather_root, merge_fused, 
             if rank == 0:
                 q_full.neg_()                   # the step's new inputs, written before the root's pull
             step.step_peers(mine.k_pool, mine.v_pool, mine.block_table, mine.seq_lens, merge_fused=merge_fused,
-                            pull=pull)
+                            pull=pull, flags=flags)
 
         for _ in range(EAGER_STEPS):
             one_step()
@@ -103,24 +103,31 @@ def _rank(rank, world, rendezvous, shape_args, split, gather_root, merge_fused, 
 
 
 # merge_fused: True = hetis_attn_decode_peers (attention, split merge and the stores into every rank's
-# o_full in ONE kernel), None = partial kernel + hetis_attn_combine_peers (the default).
-# pull: None = the attention kernel reads q / new k, v from the Primary (hetis_attn_partial_pull, the
-# default), False = the separate hetis_scatter_pull kernel first
+# o_full in ONE kernel), False = partial kernel + hetis_attn_combine_peers, None = the default (fused where
+# the launch runs in group mode -- every GQA case below: 7 requests, L <= 2048 -- else the combine).
+# pull: None = the attention kernel reads q / new k, v from the Primary (the default), False = the
+# separate hetis_scatter_pull kernel first.  NG = HETIS_ATTN_NO_GROUP_MODE (the last-arriver merge)
+NG = 0x40
 CASES = [
-    ((64, 8, 128, 16, "bf16"), (32, 32), -1, None, None),           # even GQA, all-gather, pull in the kernel
-    ((64, 8, 128, 16, "bf16"), (32, 32), -1, None, False),          # ... with the separate pull kernel
-    ((64, 8, 128, 16, "bf16"), (32, 32), -1, True, False),          # the merge + gather fused
-    ((40, 40, 128, 16, "bf16"), (16, 8, 8, 4, 4), -1, None, None),  # c4's uneven split (CUDA-core MHA)
-    ((40, 40, 128, 16, "bf16"), (16, 8, 8, 4, 4), -1, None, False),
-    ((64, 8, 128, 16, "bf16"), (16, 16, 24, 8), 0, None, None),     # uneven GQA, gather to the Primary (paper)
-    ((64, 8, 128, 16, "bf16"), (16, 16, 24, 8), 0, True, False),    # ... fused
-    ((16, 2, 64, 16, "bf16"), (8, 8), -1, True, False),             # GQA d = 64, fused
-    ((8, 8, 64, 16, "f32"), (4, 4), -1, None, None),                # c1 shape, fp32, pull in the kernel
+    ((64, 8, 128, 16, "bf16"), (32, 32), -1, None, None, 0),        # default: pull + group merge, ONE kernel
+    ((64, 8, 128, 16, "bf16"), (32, 32), -1, False, None, 0),       # pull in the kernel, separate combine
+    ((64, 8, 128, 16, "bf16"), (32, 32), -1, False, False, 0),      # ... and the separate pull kernel
+    ((64, 8, 128, 16, "bf16"), (32, 32), -1, True, False, 0),       # separate pull, group merge + gather fused
+    ((64, 8, 128, 16, "bf16"), (32, 32), -1, True, False, NG),      # ... last-arriver merge through L2
+    ((64, 8, 128, 16, "bf16"), (32, 32), -1, True, None, NG),       # pull + last-arriver merge, one kernel
+    ((40, 40, 128, 16, "bf16"), (16, 8, 8, 4, 4), -1, None, None, 0),  # c4's uneven split (CUDA-core MHA)
+    ((40, 40, 128, 16, "bf16"), (16, 8, 8, 4, 4), -1, None, False, 0),
+    ((64, 8, 128, 16, "bf16"), (16, 16, 24, 8), 0, None, None, 0),  # uneven GQA, gather to the Primary (paper)
+    ((64, 8, 128, 16, "bf16"), (16, 16, 24, 8), 0, False, None, 0),
+    ((64, 8, 128, 16, "bf16"), (16, 16, 24, 8), 0, True, False, 0),
+    ((16, 2, 64, 16, "bf16"), (8, 8), -1, None, None, 0),           # GQA d = 64, pull + group merge
+    ((16, 2, 64, 16, "bf16"), (8, 8), -1, True, False, NG),         # GQA d = 64, last-arriver
+    ((8, 8, 64, 16, "f32"), (4, 4), -1, None, None, 0),             # c1 shape, fp32, pull in the kernel
 ]
 
 
-@pytest.mark.parametrize("shape_args,split,gather_root,merge_fused,pull", CASES)
-def test_peer_step_n_ranks_one_gpu(shape_args, split, gather_root, merge_fused, pull):
+@pytest.mark.parametrize("shape_args,split,gather_root,merge_fused,pull,flags", CASES)
+def test_peer_step_n_ranks_one_gpu(shape_args, split, gather_root, merge_fused, pull, flags):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     world = len(split)
@@ -128,7 +135,7 @@ def test_peer_step_n_ranks_one_gpu(shape_args, split, gather_root, merge_fused, 
     ctx = mp.get_context("spawn")
     res = ctx.Queue()
     ps = [ctx.Process(target=_rank, args=(r, world, rendezvous, shape_args, split, gather_root, merge_fused, pull,
-                                          res))
+                                          flags, res))
           for r in range(world)]
     for p in ps:
         p.start()
