@@ -122,23 +122,36 @@ class DecodeStep:
         mine = (reduce_tensor(self.peer_state), None if o_full is None else reduce_tensor(o_full), root_bufs)
         everyone = [None] * self.world
         dist.all_gather_object(everyone, mine)
+        peer_devices = set()
+
+        def open_here(red):
+            # torch's rebuild opens the IPC handle (cudaIpcOpenMemHandle, cudaIpcMemLazyEnablePeerAccess) under the
+            # device it is told; opening it under THIS rank's device maps the peer's memory into the context our
+            # kernels run in (NVLink peer memory when the exporter is another GPU) -- the documented pattern, rather
+            # than a mapping in the exporter device's context of this process.  The tensor is only used for its
+            # pointer.  Rebuild args: (type, size, stride, offset, storage type, dtype, device, handle, ...).
+            fn, args = red
+            args = list(args)
+            peer_devices.add(int(args[6]))
+            args[6] = self.device.index
+            return fn(*args)
+
         states, outs = [], []
         for i, (rs, ro, _) in enumerate(everyone):
             if i == self.rank:
                 states.append(self.peer_state)
                 outs.append(o_full)
             else:
-                states.append(rs[0](*rs[1]))
-                outs.append(None if ro is None else ro[0](*ro[1]))
+                states.append(open_here(rs))
+                outs.append(None if ro is None else open_here(ro))
         if self.rank == self.root:
             root = (q_full, k_new_full, v_new_full)
         else:
-            root = tuple(f(*a) for f, a in everyone[self.root][2])
+            root = tuple(open_here(red) for red in everyone[self.root][2])
         # the peers' buffers live on their own GPUs: this device's kernels load / store them over NVLink
         with torch.cuda.device(self.device):
-            for t in [*states, *outs, *root]:
-                if t is not None and t.device.index != torch.cuda.current_device():
-                    hetis.peer_access(t.device.index)
+            for d in sorted(peer_devices - {self.device.index}):
+                hetis.peer_access(d)
         stride = (o_full.stride(0) if o_full is not None
                   else self.shape.num_q_heads * self.shape.head_dim)
         self.group = hetis.PeerGroup(self.plan, self.rank, self.root, gather_root, states, outs, stride, *root)
