@@ -9,6 +9,7 @@ TAG=${1:-r2f}
 mkdir -p gpurun_out
 bash scripts/gpu_final.sh $TAG
 timeout -s KILL 600 python scripts/scaling_probe.py --config c3 > gpurun_out/scaling_${TAG}_c3.jsonl 2>&1
+timeout -s KILL 600 python scripts/attn_probe.py --heads 8,16 --flags 0,0x20,0x60 --decode --steps 100 > gpurun_out/group_mode_${TAG}.jsonl 2>&1
 timeout -s KILL 900 python scripts/scaling_probe.py --config c2 > gpurun_out/scaling_${TAG}_c2.jsonl 2>&1
 timeout -s KILL 900 python scripts/scaling_probe.py --config c4 --shares > gpurun_out/c4_shares_${TAG}.jsonl 2>&1
 timeout -s KILL 600 python scripts/seq_vs_head_probe.py --config c5 > gpurun_out/seq_vs_head_${TAG}_c5.jsonl 2>&1
