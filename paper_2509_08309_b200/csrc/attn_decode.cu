@@ -108,6 +108,13 @@ constexpr int kQSlots = 2;
 #ifndef HETIS_GROUP_MODE
 #define HETIS_GROUP_MODE 1  // merge-fused launches use group mode when they qualify (Params::group_mode)
 #endif
+#ifndef HETIS_CONSUMER_REFILL
+// Launches with at most one item per worker (small shares, group mode): the producer issues the first SW
+// pages of a worker's item and the consumer warp refills each stage it releases with the page SW ahead
+// itself -- no round trip through the producer's polling loop on the stage's turnaround, which bounds a
+// latency-bound stream (Little's law).  0 = the producer issues every page.
+#define HETIS_CONSUMER_REFILL 1
+#endif
 #ifndef HETIS_WARP_STAGES
 #define HETIS_WARP_STAGES 4
 #endif
@@ -243,7 +250,9 @@ struct ItemMeta {
     int new_slot;
     int defer_from;     // per-warp kernel, HETIS_ATTN_PIPELINED: pages >= defer_from are copied by the consumer
     int defer_page[2];  // their page ids (the producer may overwrite its page-id buffer before they are copied)
-    int pad[2];
+    int refill_from;    // per-warp kernel: pages >= refill_from are issued by the consumer warp itself (the
+                        // stage it just released, HETIS_CONSUMER_REFILL); npages = none
+    int pad;
 };
 
 __device__ __forceinline__ int upper_bound_smem(const int32_t *a, int n, int key) {
@@ -1069,12 +1078,15 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     const int static_pct =
         ((pipelined_launch && !pipe_steal) || n_items < HETIS_STATIC_ALL_BELOW * (int)gridDim.x * NW) ? 100
                                                                                                        : HETIS_STATIC_PCT;
+    // one item per worker at most: the consumer refills its own stages (HETIS_CONSUMER_REFILL)
+    const bool cr_mode = HETIS_CONSUMER_REFILL && !pipelined_launch && !device_claim &&
+                         (p.group_mode || n_items <= (int)gridDim.x * NW);
     const int per_cta = device_claim       ? 0
                         : static_pct == 100 ? (n_items + (int)gridDim.x - 1) / (int)gridDim.x
                                             : (int)(((long long)n_items * static_pct / 100) / gridDim.x);
     const int n_static = device_claim ? (int)gridDim.x * NW : per_cta * (int)gridDim.x;
     auto claim = [&]() -> int {
-        if (p.group_mode) return n_items;
+        if (p.group_mode || cr_mode) return n_items;  // one item per worker
         if (!device_claim) {
             const int k = atomicAdd(sm.claim, 1);
             if (k < per_cta) return (int)blockIdx.x + k * (int)gridDim.x;
@@ -1172,6 +1184,7 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         if (!q_done && dev::mbar_test(&sm.qempty[w], (it & 1) ^ 1)) {
             const int irow = in_row(p, j, g);
             ItemMeta m{item, ntok, np, -1, irow, 0, 0, np};
+            m.refill_from = cr_mode ? min(np, SW) : np;
             if (pipelined) {  // the pages holding the request's last two positions: the consumer waits + copies
                 while (m.defer_from > 0 && holds_recent_tokens(t0, m.defer_from - 1, s_len[j])) --m.defer_from;
                 for (int d = 0; d < 2 && m.defer_from + d < np; ++d)
@@ -1188,8 +1201,9 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             dev::bulk_g2s(sm.qbuf + (size_t)w * kQStride, src, kQBytes, &sm.qfull[w], pol);
             q_done = true;
         }
-        // issue as many pages as the worker's sub-ring has free stages
-        while (q_done && pg < np && dev::mbar_test(&sm.empty[w * SW + pos.stage], pos.phase ^ 1u)) {
+        // issue as many pages as the worker's sub-ring has free stages (consumer-refill mode: the first SW)
+        const int np_issue = cr_mode ? min(np, SW) : np;
+        while (q_done && pg < np_issue && dev::mbar_test(&sm.empty[w * SW + pos.stage], pos.phase ^ 1u)) {
             const int32_t page = sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + pg];
             // pipelined: a page an in-flight kernel may still write is COPIED by the consumer warp after its
             // own griddepcontrol.wait, so this warp (which feeds every worker) never blocks.  The stage is
@@ -1213,7 +1227,8 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             next = claim();
             load_next(next);
         }
-        if (q_done && pg == np && next != kNeedSteal) {  // item fully issued: move to the claimed next item
+        if (cr_mode && q_done && pg == np_issue && next == -1) next = n_items;  // the consumer issues the rest
+        if (q_done && pg == np_issue && next != kNeedSteal) {  // item fully issued: move to the claimed next item
             item = next;
             next = -1;
             ++it;
@@ -1456,6 +1471,22 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             __syncwarp();
         };
         for (int d = meta.defer_from; d < meta.npages && d < SW; ++d) issue_deferred(d);  // stages already free
+        // release the stage of page pg: to the producer, or (consumer-refill mode) refill it with page pg + SW
+        auto release_stage = [&](int pg) {
+            if (lane == 0) {
+                if (pg + SW < meta.npages && pg + SW >= meta.refill_from) {
+                    dev::fence_proxy_async_shared();  // this warp's reads / patch of the stage before the TMA write
+                    uint64_t *bar = &sm.full[w * SW + pos.stage];
+                    uint8_t *dst = sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes;
+                    const int row = sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + pg + SW] * kP;
+                    dev::mbar_arrive_expect_tx(bar, kStageBytes);
+                    dev::tma_load_3d(dst, tmap_k, 0, row, 0, bar, dev::policy_evict_first());
+                    dev::tma_load_3d(dst + kPageBytes, tmap_v, 0, row, 0, bar, dev::policy_evict_first());
+                } else {
+                    dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
+                }
+            }
+        };
         for (int pg = 0; pg < meta.npages; ++pg) {
 #ifdef HETIS_DEBUG_HANG
             {
@@ -1481,7 +1512,7 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             }
             if (diag_stream) {
                 __syncwarp();
-                if (lane == 0) dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
+                release_stage(pg);
                 pos.advance(1, SW);
                 if (pg + SW >= meta.defer_from && pg + SW < meta.npages) issue_deferred(pg + SW);
                 continue;
@@ -1511,7 +1542,7 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             }
 #if HETIS_EARLY_RELEASE
             __syncwarp();
-            if (lane == 0) dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
+            release_stage(pg);
             pos.advance(1, SW);
             if (pg + SW >= meta.defer_from && pg + SW < meta.npages) issue_deferred(pg + SW);  // its stage is free
 #endif
@@ -1580,7 +1611,7 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             }
 #if !HETIS_EARLY_RELEASE
             __syncwarp();
-            if (lane == 0) dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
+            release_stage(pg);
             pos.advance(1, SW);
             if (pg + SW >= meta.defer_from && pg + SW < meta.npages) issue_deferred(pg + SW);  // its stage is free
 #endif

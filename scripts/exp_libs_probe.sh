@@ -3,5 +3,5 @@
 #   bash scripts/exp_libs_probe.sh "<lib1> <lib2> ..." <heads> <out> [reps] [flags]
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
 for rep in $(seq 1 ${4:-2}); do for L in $1; do
-HETIS_LIB=$PWD/$L timeout -s KILL 300 python scripts/attn_probe.py --heads $2 --flags ${5:-0} --steps 100 2>&1 | grep '^{'
+HETIS_LIB=$PWD/$L timeout -s KILL 300 python scripts/attn_probe.py --heads $2 --flags ${5:-0} --decode --steps 100 2>&1 | grep '^{'
 done; done > gpurun_out/$3
