@@ -109,11 +109,12 @@ constexpr int kQSlots = 2;
 #define HETIS_GROUP_MODE 1  // merge-fused launches use group mode when they qualify (Params::group_mode)
 #endif
 #ifndef HETIS_CONSUMER_REFILL
-// Launches with at most one item per worker (small shares, group mode): the producer issues the first SW
-// pages of a worker's item and the consumer warp refills each stage it releases with the page SW ahead
-// itself -- no round trip through the producer's polling loop on the stage's turnaround, which bounds a
-// latency-bound stream (Little's law).  0 = the producer issues every page.
-#define HETIS_CONSUMER_REFILL 1
+// The producer issues the first SW pages of each item and the consumer warp refills each stage it releases
+// with the page SW ahead in the same item itself -- no round trip through the producer's polling loop on
+// the stage's turnaround, which bounds the per-warp stream (Little's law).  2 = every non-pipelined launch
+// (the producer claims the next item once sm.progress shows the consumer half-way through the current
+// one), 1 = launches with at most one item per worker only, 0 = the producer issues every page.
+#define HETIS_CONSUMER_REFILL 2
 #endif
 #ifndef HETIS_WARP_STAGES
 #define HETIS_WARP_STAGES 4
@@ -1016,6 +1017,7 @@ struct WarpSmem {
     uint64_t *qfull;    // [NW]
     uint64_t *qempty;   // [NW]
     int *claim;         // next CTA-local item index to hand out
+    int *progress;      // [NW] pages consumed so far by each worker (consumer refill in every launch)
 };
 
 template <int ROW_BYTES, int R, int NW>
@@ -1081,6 +1083,11 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     // one item per worker at most: the consumer refills its own stages (HETIS_CONSUMER_REFILL)
     const bool cr_mode = HETIS_CONSUMER_REFILL && !pipelined_launch && !device_claim &&
                          (p.group_mode || n_items <= (int)gridDim.x * NW);
+    // HETIS_CONSUMER_REFILL == 2: every (non-pipelined) launch -- the producer issues the first SW pages of each
+    // item and claims the next item once the consumer (sm.progress) is half-way through the current one
+    const bool cr_all = HETIS_CONSUMER_REFILL == 2 && !pipelined_launch && !cr_mode;
+    const bool cr = cr_mode || cr_all;
+    int base_seq = 0;  // page sequence number (this worker's ring) of the current item's first page
     const int per_cta = device_claim       ? 0
                         : static_pct == 100 ? (n_items + (int)gridDim.x - 1) / (int)gridDim.x
                                             : (int)(((long long)n_items * static_pct / 100) / gridDim.x);
@@ -1184,7 +1191,7 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         if (!q_done && dev::mbar_test(&sm.qempty[w], (it & 1) ^ 1)) {
             const int irow = in_row(p, j, g);
             ItemMeta m{item, ntok, np, -1, irow, 0, 0, np};
-            m.refill_from = cr_mode ? min(np, SW) : np;
+            m.refill_from = cr ? min(np, SW) : np;
             if (pipelined) {  // the pages holding the request's last two positions: the consumer waits + copies
                 while (m.defer_from > 0 && holds_recent_tokens(t0, m.defer_from - 1, s_len[j])) --m.defer_from;
                 for (int d = 0; d < 2 && m.defer_from + d < np; ++d)
@@ -1202,8 +1209,15 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
             q_done = true;
         }
         // issue as many pages as the worker's sub-ring has free stages (consumer-refill mode: the first SW)
-        const int np_issue = cr_mode ? min(np, SW) : np;
-        while (q_done && pg < np_issue && dev::mbar_test(&sm.empty[w * SW + pos.stage], pos.phase ^ 1u)) {
+        const int np_issue = cr ? min(np, SW) : np;
+        // cr_all: the producer skips the empty-barrier phases of the consumer-issued pages, so a parity test alone
+        // could see a phase two behind as complete -- first require the exact release count (sm.progress): page
+        // seq n needs the release of seq n - SW; the barrier is then exactly at that phase (acquire through it)
+        auto stage_free = [&]() -> bool {
+            if (cr_all && *reinterpret_cast<volatile int *>(sm.progress + w) < base_seq + pg - SW + 1) return false;
+            return dev::mbar_test(&sm.empty[w * SW + pos.stage], pos.phase ^ 1u);
+        };
+        while (q_done && pg < np_issue && stage_free()) {
             const int32_t page = sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + pg];
             // pipelined: a page an in-flight kernel may still write is COPIED by the consumer warp after its
             // own griddepcontrol.wait, so this warp (which feeds every worker) never blocks.  The stage is
@@ -1223,12 +1237,17 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
                 HETIS_TS(3);
             }
         }
-        if (next == -1 && kPagesPerItem * pg >= HETIS_CLAIM_AT * np) {
+        if (next == -1 && (cr_all ? q_done && pg == np_issue &&
+                                        kPagesPerItem * (*reinterpret_cast<volatile int *>(sm.progress + w) - base_seq +
+                                                         SW) >= HETIS_CLAIM_AT * np
+                                  : kPagesPerItem * pg >= HETIS_CLAIM_AT * np)) {
             next = claim();
             load_next(next);
         }
         if (cr_mode && q_done && pg == np_issue && next == -1) next = n_items;  // the consumer issues the rest
-        if (q_done && pg == np_issue && next != kNeedSteal) {  // item fully issued: move to the claimed next item
+        if (q_done && pg == np_issue && next != kNeedSteal && next != -1) {  // item issued: move to the next item
+            if (cr) pos.advance(np - np_issue, SW);  // the consumer issues (issued) the item's other pages
+            base_seq += np;
             item = next;
             next = -1;
             ++it;
@@ -1398,6 +1417,7 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         v_off[c2] = swz((mi & 1) * 8 + (lane & 7), 2 * c2 + (mi >> 1));
     }
     RingPos pos{0, 0u};
+    int pages_done = 0;     // pages this worker has consumed (sm.progress, read by the producer)
     bool c_waited = false;  // this warp has executed griddepcontrol.wait (pipelined deferred pages)
     constexpr bool fused_out = FUSED;
     const bool diag_stream = (p.flags & HETIS_ATTN_DIAG_STREAM_ONLY) != 0;  // hoisted out of the page loop
@@ -1472,6 +1492,7 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
         };
         for (int d = meta.defer_from; d < meta.npages && d < SW; ++d) issue_deferred(d);  // stages already free
         // release the stage of page pg: to the producer, or (consumer-refill mode) refill it with page pg + SW
+        // (the empty barrier completes once per page either way: the producer's phase count stays in step)
         auto release_stage = [&](int pg) {
             if (lane == 0) {
                 if (pg + SW < meta.npages && pg + SW >= meta.refill_from) {
@@ -1482,9 +1503,9 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
                     dev::mbar_arrive_expect_tx(bar, kStageBytes);
                     dev::tma_load_3d(dst, tmap_k, 0, row, 0, bar, dev::policy_evict_first());
                     dev::tma_load_3d(dst + kPageBytes, tmap_v, 0, row, 0, bar, dev::policy_evict_first());
-                } else {
-                    dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
                 }
+                dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
+                *reinterpret_cast<volatile int *>(sm.progress + w) = ++pages_done;
             }
         };
         for (int pg = 0; pg < meta.npages; ++pg) {
@@ -1713,7 +1734,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     sm.qfull = sm.empty + NW * SW;
     sm.qempty = sm.qfull + NW;
     sm.claim = reinterpret_cast<int *>(sm.qempty + NW);
-    int32_t *s_len = sm.claim + 2;
+    sm.progress = sm.claim + 2;
+    int32_t *s_len = sm.progress + NW;
     int32_t *s_off = s_len + p.num_seqs;
     if (threadIdx.x == 0) {
         for (int i = 0; i < NW * SW; ++i) {
@@ -1725,6 +1747,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
             dev::mbar_init(&sm.qempty[i], 1);
         }
         *sm.claim = 0;
+        for (int i = 0; i < NW; ++i) sm.progress[i] = 0;
         dev::fence_barrier_init();
     }
     if (threadIdx.x == 0) {
@@ -1765,7 +1788,7 @@ cudaError_t launch_gqa_warp_nw(const Params &p0, int num_seqs, cudaStream_t s, c
     Params p = p0;
     auto fixed = [&](int sw) {
         return (size_t)NW * kQStride + (size_t)NW * sizeof(ItemMeta) + (size_t)NW * 2 * kPagesPerItem * 4 +
-               (size_t)(2 * NW * sw + 2 * NW) * 8 + 8 + (size_t)(2 * num_seqs + 1) * 4 + 1024;
+               (size_t)(2 * NW * sw + 2 * NW) * 8 + 8 + (size_t)NW * 4 + (size_t)(2 * num_seqs + 1) * 4 + 1024;
     };
     int sw = HETIS_WARP_STAGES;
     while (sw > 2 && (size_t)NW * sw * kStageBytes + fixed(sw) > (size_t)kMaxSmem) --sw;
