@@ -1503,7 +1503,9 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
                     dev::mbar_arrive_expect_tx(bar, kStageBytes);
                     dev::tma_load_3d(dst, tmap_k, 0, row, 0, bar, dev::policy_evict_first());
                     dev::tma_load_3d(dst + kPageBytes, tmap_v, 0, row, 0, bar, dev::policy_evict_first());
-                }
+                } else if (meta.new_page >= 0 && pg == meta.new_pg) {
+                    dev::fence_proxy_async_shared();  // the appended row was patched in (generic stores) before
+                }                                     // the producer's next TMA write into this stage
                 dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
                 *reinterpret_cast<volatile int *>(sm.progress + w) = ++pages_done;
             }
