@@ -1713,6 +1713,20 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     }
     if constexpr (fused_out) {
         if (p.group_mode) group_merge<D, R, NW>(p, sm, SW, s_off, epoch, acked, w, lane);
+        // pairs without tokens (L_j = 0, a sequence split's empty local range) have no item: o = 0, as the
+        // combine kernel writes; warp w of CTA c takes pairs c * NW + w, + grid * NW, ...
+        const int n_pairs = p.num_seqs * p.kv_heads;
+        constexpr int TPH = D / 4, RPP = 32 / TPH;
+        for (int pr = (int)blockIdx.x * NW + w; pr < n_pairs; pr += (int)gridDim.x * NW) {
+            const int j = pr / p.kv_heads, gk = pr - j * p.kv_heads;
+            if (s_off[j + 1] != s_off[j]) continue;
+            const int jr = p.units != nullptr ? __ldg(p.units + 2 * j) : j;
+            const int gr = p.units != nullptr ? __ldg(p.units + 2 * j + 1) : gk;
+            const size_t obase = (size_t)jr * p.o_seq_stride + ((size_t)p.o_head0 + (size_t)gr * R) * D;
+            await_peer_acks(p, epoch, acked, lane);
+            const float z[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int rr = lane / TPH; rr < R; rr += RPP) put_out<4>(p, obase + (size_t)rr * D + 4 * (lane % TPH), z);
+        }
     }
 }
 

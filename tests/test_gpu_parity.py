@@ -631,6 +631,31 @@ def test_group_mode_bit_identical_to_combine_kernel(H, Hkv, D, odt, B):
         assert_close(got, oracle_full(b), "group mode")
 
 
+@pytest.mark.parametrize("H,Hkv,D,B", [(64, 8, 128, 9), (16, 4, 64, 40), (64, 8, 128, 40)])
+def test_fused_merge_empty_requests_write_zeros(H, Hkv, D, B):
+    """L_j = 0 (a device holding none of request j's tokens under a sequence split): the combine kernel writes
+    o = 0; the one-kernel forms must too -- group mode (9 x 8 = 72 pairs) and the last-arriver merge (flag
+    NO_GROUP_MODE, and 40 x 8 = 320 pairs where group mode does not apply) -- bit-identical to the two-kernel
+    path on a batch mixing empty and non-empty requests."""
+    lens = [(1 if i % 3 == 1 else GROUP_LENS[i % len(GROUP_LENS)]) for i in range(B)]
+    b = gpu_batch(H, Hkv, D, "bf16", lens, seed=77)
+    b.seq_lens[1::3] = 0      # the generator needs L >= 1 (the new token); these requests now hold no token
+    s = hetis.make_shape(b.shape, "f32")
+    x = b.q.shape[1]
+    L = max(lens)
+    ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), "cuda")
+    ref = torch.full((B, x, D), float("nan"), device="cuda")
+    hetis.attn_partial(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, ws)
+    hetis.attn_combine(s, b.seq_lens, L, ref, ws)
+    torch.cuda.synchronize()
+    assert torch.all(ref[1::3] == 0)
+    for flags in (0, FM, FM | hetis.ATTN_NO_GROUP_MODE):
+        got = torch.full_like(ref, float("nan"))
+        hetis.attn_decode(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, got, ws, flags=flags)
+        torch.cuda.synchronize()
+        assert torch.equal(got.view(torch.int32), ref.view(torch.int32)), flags
+
+
 def test_decode_step_fused_append_matches_separate_calls():
     from paper_2509_08309_b200.step import DecodeStep
     shape = workload.LLAMA2_70B
