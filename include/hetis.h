@@ -118,12 +118,19 @@ typedef struct {
 /* bf16 GQA tensor-core kernel with the shared page ring and per-item CTA merge
  * (the default gives every consumer warp whole items and its own sub-ring). */
 #define HETIS_ATTN_TC_SHARED_RING 0x2u
-/* bf16 GQA tensor-core kernel: claim work items device-wide instead of dealing
- * them to SMs round-robin.  For decode that shares the SMs with another kernel
- * (e.g. hetis_kv_migrate on a low-priority stream, the Hauler): slowed SMs take
- * fewer items (c3 beside a 16-CTA migration: 1.17x instead of 1.42x step time).
+/* bf16 GQA tensor-core kernel: claim work items device-wide (the first round
+ * dealt round-robin, every later claim from a device-wide counter).  The
+ * DEFAULT of that kernel for every launch that is neither pipelined nor in
+ * group mode (with the consumer refill it measured faster: c3 attention
+ * 171 -> 163 us); it also keeps decode fast beside another kernel (e.g.
+ * hetis_kv_migrate on a low-priority stream, the Hauler: slowed SMs take
+ * fewer items).  Passing the flag forces it and turns group mode off.
  * Ignored with HETIS_ATTN_PIPELINED. */
 #define HETIS_ATTN_DEVICE_CLAIM 0x4u
+/* The CTA-local deal instead of the default device-wide claiming (95% of the
+ * items dealt to CTAs round-robin, the rest stolen at the end; the default
+ * before round 2's consumer refill).  For A/B measurements. */
+#define HETIS_ATTN_STATIC_DEAL 0x80u
 /* bf16 MHA (r = 1) on the per-warp tensor-core kernel (one valid MMA row)
  * instead of the CUDA-core kernel (faster for large per-device problems, c5
  * -4%; slower at small ones, the c2 8-GPU share +5%). */

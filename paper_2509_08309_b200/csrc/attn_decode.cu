@@ -108,6 +108,12 @@ constexpr int kQSlots = 2;
 #ifndef HETIS_GROUP_MODE
 #define HETIS_GROUP_MODE 1  // merge-fused launches use group mode when they qualify (Params::group_mode)
 #endif
+#ifndef HETIS_DEFAULT_DEVICE_CLAIM
+// With the consumer refill, claiming items device-wide (the first round dealt statically and interleaved over
+// the CTAs, every later claim from a device-wide counter) beats the CTA-local deal with end-of-launch
+// stealing: c3 attention at N = 1 171 -> 163 us, 32 heads 83.6 -> 80.4 us (16: even; 8: 25.9 -> 24.6).
+#define HETIS_DEFAULT_DEVICE_CLAIM 1
+#endif
 #ifndef HETIS_CONSUMER_REFILL
 // The producer issues the first SW pages of each item and the consumer warp refills each stage it releases
 // with the page SW ahead in the same item itself -- no round trip through the producer's polling loop on
@@ -1071,7 +1077,11 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     // deal is one balanced wave and a wait in the middle of it would stall every worker of the CTA.
     constexpr int kNeedSteal = -3;
     const bool pipelined_launch = (p.flags & HETIS_ATTN_PIPELINED) != 0;
-    const bool device_claim = (p.flags & HETIS_ATTN_DEVICE_CLAIM) != 0 && !pipelined_launch;
+    // device-wide claiming: forced by the flag, and the default of every launch that is neither pipelined nor
+    // in group mode (HETIS_DEFAULT_DEVICE_CLAIM; HETIS_ATTN_STATIC_DEAL restores the CTA-local deal)
+    const bool device_claim =
+        !pipelined_launch && ((p.flags & HETIS_ATTN_DEVICE_CLAIM) != 0 ||
+                              (HETIS_DEFAULT_DEVICE_CLAIM && !p.group_mode && !(p.flags & HETIS_ATTN_STATIC_DEAL)));
     const bool pipe_steal = pipelined_launch && n_items >= 2 * (int)gridDim.x * NW;
     // Below two items per worker every item is dealt statically (no stealing): a steal is claimed once
     // the thief is half-way through its current item, i.e. at the start of the launch for such small

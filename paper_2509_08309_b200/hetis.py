@@ -30,6 +30,7 @@ ATTN_MHA_TC = 0x8
 ATTN_PIPELINED = 0x10
 ATTN_FUSED_MERGE = 0x20
 ATTN_NO_GROUP_MODE = 0x40
+ATTN_STATIC_DEAL = 0x80
 ATTN_DIAG_STREAM_ONLY = 0x100
 
 EXPORTED = ("hetis_status_str", "hetis_last_error", "hetis_abi_version", "hetis_split_tokens",

@@ -81,6 +81,7 @@ def main():
              ("GQA r=8 pipelined", workload.Shape(64, 8, 128, 16, "bf16"), hetis.ATTN_PIPELINED),
              ("GQA r=8 pipelined large", workload.Shape(64, 8, 128, 16, "bf16"), hetis.ATTN_PIPELINED | 0x10000),
              ("GQA r=8 device claim", workload.Shape(64, 8, 128, 16, "bf16"), hetis.ATTN_DEVICE_CLAIM),
+             ("GQA r=8 static deal", workload.Shape(64, 8, 128, 16, "bf16"), hetis.ATTN_STATIC_DEAL),
              ("MHA CUDA cores", workload.Shape(40, 40, 128, 16, "bf16"), 0),
              ("MHA CUDA cores pipelined", workload.Shape(40, 40, 128, 16, "bf16"), hetis.ATTN_PIPELINED),
              ("MHA tensor cores", workload.Shape(40, 40, 128, 16, "bf16"), hetis.ATTN_MHA_TC),

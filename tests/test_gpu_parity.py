@@ -422,9 +422,10 @@ def test_head_partition_bit_identical_at_config_size(name):
 # ------------------------------------------------------------------ work distribution does not change bits
 @pytest.mark.parametrize("lens", [(1, 255, 256, 257, 3000, 17), tuple([2048] * 96), (5,)])
 def test_device_claim_flag_is_bit_identical(lens):
-    """HETIS_ATTN_DEVICE_CLAIM (device-wide item claiming) and the default (CTA-local items + stealing of the
-    last 5%) hand items to different warps; an item's arithmetic depends on L_j only, so O is identical --
-    also over back-to-back launches, which exercises the self-resetting device-wide counter."""
+    """Device-wide item claiming (the default; HETIS_ATTN_DEVICE_CLAIM forces it and turns group mode off),
+    the CTA-local deal with stealing of the last 5% (HETIS_ATTN_STATIC_DEAL) and group mode hand items to
+    different warps; an item's arithmetic depends on L_j only, so O is identical -- also over back-to-back
+    launches, which exercises the self-resetting device-wide counter."""
     b = gpu_batch(64, 8, 128, "bf16", lens, 71)
     s = hetis.make_shape(b.shape)
     hetis.kv_append(s, b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens)
@@ -432,7 +433,8 @@ def test_device_claim_flag_is_bit_identical(lens):
     L = b.max_seq_len
     ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), "cuda")
     outs = []
-    for flags in (0, hetis.ATTN_DEVICE_CLAIM, hetis.ATTN_DEVICE_CLAIM, 0, hetis.ATTN_DEVICE_CLAIM):
+    SD, DC = hetis.ATTN_STATIC_DEAL, hetis.ATTN_DEVICE_CLAIM
+    for flags in (0, DC, SD, DC, 0, SD, SD, 0):
         o = torch.full((B, x, D), float("nan"), device="cuda")
         hetis.attn_decode(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, o, ws, flags=flags)
         outs.append(o)
