@@ -115,10 +115,16 @@ typedef struct {
 /* Flags for hetis_attn_partial(_append) / hetis_attn_decode(_append).  None of
  * them changes a result bit: an item's arithmetic depends on L_j only. */
 #define HETIS_ATTN_FORCE_SIMT 0x1u /* bf16 GQA on CUDA cores instead of tensor cores */
-/* bf16 GQA tensor-core kernel with the shared page ring and per-item CTA merge
- * (the default gives every consumer warp whole items and its own sub-ring). */
+/* The shared page ring with a per-item CTA merge instead of the per-warp
+ * kernel (whose default gives every consumer warp whole items and its own
+ * sub-ring): for bf16 GQA on tensor cores, and for bf16 MHA on CUDA cores
+ * (bf16 MHA defaults to the per-warp kernel with a CUDA-core consumer; its
+ * pipelined launches always run the shared-ring kernel, so they are
+ * bit-identical to serial launches WITH this flag, and within tolerance of
+ * the default). */
 #define HETIS_ATTN_TC_SHARED_RING 0x2u
-/* bf16 GQA tensor-core kernel: claim work items device-wide (the first round
+/* Per-warp kernel (bf16 GQA; bf16 MHA on its CUDA-core consumer): claim work
+ * items device-wide (the first round
  * dealt round-robin, every later claim from a device-wide counter).  The
  * DEFAULT of that kernel for every launch that is neither pipelined nor in
  * group mode (with the consumer refill it measured faster: c3 attention
@@ -131,9 +137,9 @@ typedef struct {
  * items dealt to CTAs round-robin, the rest stolen at the end; the default
  * before round 2's consumer refill).  For A/B measurements. */
 #define HETIS_ATTN_STATIC_DEAL 0x80u
-/* bf16 MHA (r = 1) on the per-warp tensor-core kernel (one valid MMA row)
- * instead of the CUDA-core kernel (faster for large per-device problems, c5
- * -4%; slower at small ones, the c2 8-GPU share +5%). */
+/* bf16 MHA (r = 1) with the per-warp kernel's tensor-core consumer (one valid
+ * MMA row) instead of its CUDA-core consumer (the default; c2 attention 751 vs
+ * 746 us: no gain -- decode MHA is HBM-bound, not a dense contraction). */
 #define HETIS_ATTN_MHA_TC 0x8u
 /* Pipelined steps: the caller passes two workspaces alternately to consecutive
  * steps on the stream (at most one kv_append -- fused or not -- per step).
@@ -167,7 +173,7 @@ typedef struct {
 #define HETIS_ATTN_NO_GROUP_MODE 0x40u
 /* Diagnostic only: stream every K/V page through the shared-memory ring but
  * skip the math (partials are left unwritten).  Measures the memory-system
- * ceiling of the pipeline; the CUDA-core kernel honours it. */
+ * ceiling of the pipeline; every kernel honours it. */
 #define HETIS_ATTN_DIAG_STREAM_ONLY 0x100u
 
 /* ---- status ------------------------------------------------------------ */

@@ -108,6 +108,12 @@ constexpr int kQSlots = 2;
 #ifndef HETIS_GROUP_MODE
 #define HETIS_GROUP_MODE 1  // merge-fused launches use group mode when they qualify (Params::group_mode)
 #endif
+#ifndef HETIS_MHA_WARP
+// bf16 MHA runs on the per-warp kernel with a CUDA-core consumer (consumer_warp_items_simt): the per-warp
+// workers with consumer refill and device-wide claiming outrun the shared-ring kernel's pipeline (whose
+// stream-only ceiling is below the per-warp kernel's).  0 = the shared-ring CUDA-core kernel.
+#define HETIS_MHA_WARP 1
+#endif
 #ifndef HETIS_DEFAULT_DEVICE_CLAIM
 // With the consumer refill, claiming items device-wide (the first round dealt statically and interleaved over
 // the CTAs, every later claim from a device-wide counter) beats the CTA-local deal with end-of-launch
@@ -1740,7 +1746,144 @@ __device__ void consumer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     }
 }
 
-template <int D, int R, int NW, bool FUSED>
+// bf16 MHA (r = 1) on CUDA cores in the per-warp kernel (the default for bf16 MHA launches that are
+// neither pipelined nor merge-fused): the same workers, sub-rings, consumer refill and device-wide claiming
+// as the tensor-core consumer above, with consumer_simt's per-page arithmetic (fma.rn.f32.bf16 dot products,
+// the transposing butterfly, FFMA2 p . v) reading the pages in their 128-B-swizzled TMA layout, and the
+// online softmax carried through the whole item by one warp (no cross-warp merge).
+template <int D, int NW>
+__device__ void consumer_warp_items_simt(const Params &p, const WarpSmem &sm, int SW, const void *tmap_k,
+                                         const void *tmap_v) {
+    constexpr int ROW_BYTES = D * 2;
+    constexpr int kPageBytes = kP * ROW_BYTES;
+    constexpr int kHalfBytes = kPageBytes / (D / 64);
+    constexpr int kStageBytes = 2 * kPageBytes;
+    constexpr int kQStride = (ROW_BYTES + 127) / 128 * 128;
+    constexpr int LPT = ROW_BYTES / 16;  // lanes per token row
+    constexpr int TPS = 32 / LPT;        // tokens per step
+    constexpr int STEPS = kP / TPS;      // steps per page
+    static_assert(TPS * LPT == 32 && STEPS * 2 == LPT, "d = 64 or 128");
+    const int lane = threadIdx.x & 31;
+    const int w = (threadIdx.x >> 5) - 1;
+    const int ltok = lane / LPT, lchk = lane % LPT;
+    const int my_step = lchk >> 1;         // after the butterfly: this lane's token is my_step * TPS + ltok
+    const bool l_owner = (lchk & 1) == 0;  // counts its token once in l
+    auto swz = [](int t, int c) -> uint32_t {
+        const int half = c >> 3, cc = c & 7;
+        return (uint32_t)(half * kHalfBytes + t * 128 + ((cc ^ (t & 7)) << 4));
+    };
+    const bool diag_stream = (p.flags & HETIS_ATTN_DIAG_STREAM_ONLY) != 0;
+    RingPos pos{0, 0u};
+    int pages_done = 0;
+    for (int it = 0;; ++it) {
+        dev::mbar_wait(&sm.qfull[w], it & 1);
+        const ItemMeta meta = sm.meta[w];
+        if (meta.item < 0) break;
+        const uint4 qv = *reinterpret_cast<const uint4 *>(sm.qbuf + (size_t)w * kQStride + lchk * 16);
+        __syncwarp();
+        if (lane == 0) dev::mbar_arrive(&sm.qempty[w]);
+        NewRow<ROW_BYTES> nr;
+        if (meta.new_page >= 0) nr.load(p, meta.jg, lane);
+        auto release_stage = [&](int pg) {  // as in consumer_warp_items (consumer refill)
+            if (lane == 0) {
+                if (pg + SW < meta.npages && pg + SW >= meta.refill_from) {
+                    dev::fence_proxy_async_shared();
+                    uint64_t *bar = &sm.full[w * SW + pos.stage];
+                    uint8_t *dst = sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes;
+                    const int row = sm.pids[(w * 2 + (it & 1)) * kPagesPerItem + pg + SW] * kP;
+                    dev::mbar_arrive_expect_tx(bar, kStageBytes);
+                    dev::tma_load_3d(dst, tmap_k, 0, row, 0, bar, dev::policy_evict_first());
+                    dev::tma_load_3d(dst + kPageBytes, tmap_v, 0, row, 0, bar, dev::policy_evict_first());
+                } else if (meta.new_page >= 0 && pg == meta.new_pg) {
+                    dev::fence_proxy_async_shared();
+                }
+                dev::mbar_arrive(&sm.empty[w * SW + pos.stage]);
+                *reinterpret_cast<volatile int *>(sm.progress + w) = ++pages_done;
+            }
+        };
+        float m = -INFINITY, l = 0.f, acc[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+        for (int pg = 0; pg < meta.npages; ++pg) {
+            dev::mbar_wait(&sm.full[w * SW + pos.stage], pos.phase);
+            uint8_t *kbp = sm.ring + ((size_t)w * SW + pos.stage) * kStageBytes;
+            if (meta.new_page >= 0 && pg == meta.new_pg)
+                nr.patch(p, kbp, kbp + kPageBytes, meta.new_page, meta.new_slot, lane, swz);
+            if (!diag_stream) {
+                const uint8_t *kb = kbp, *vb = kbp + kPageBytes;
+                const int valid = min(kP, meta.ntok - pg * kP);
+                uint4 kr[STEPS];
+#pragma unroll
+                for (int i = 0; i < STEPS; ++i) kr[i] = *reinterpret_cast<const uint4 *>(kb + swz(i * TPS + ltok, lchk));
+                float sv[STEPS];
+#pragma unroll
+                for (int i = 0; i < STEPS; ++i) {
+                    float a = 0.f;
+                    a = dev::fma_bf16x2(qv.x, kr[i].x, a);
+                    a = dev::fma_bf16x2(qv.y, kr[i].y, a);
+                    a = dev::fma_bf16x2(qv.z, kr[i].z, a);
+                    a = dev::fma_bf16x2(qv.w, kr[i].w, a);
+                    sv[i] = a;
+                }
+                float sc = butterfly_reduce<STEPS>(sv, lane, LPT) * p.scale_log2;
+                if (valid < kP && my_step * TPS + ltok >= valid) sc = -INFINITY;
+                float mx = sc;
+#pragma unroll
+                for (int o = 16; o >= 2; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                const float m_new = fmaxf(m, mx);
+                if (m_new != m) {  // warp-uniform
+                    const float alpha = dev::ex2(m - m_new);  // m = -inf -> 0
+                    l *= alpha;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc[e] *= alpha;
+                    m = m_new;
+                }
+                const float pr = dev::ex2(sc - m_new);
+                if (l_owner) l += pr;
+#pragma unroll
+                for (int i = 0; i < STEPS; ++i) {  // lane (ltok, lchk) accumulates tokens i * TPS + ltok on its chunk
+                    const int t = i * TPS + ltok;
+                    const float pt = __shfl_sync(0xffffffffu, pr, ltok * LPT + 2 * i);
+                    if (valid == kP || t < valid) {  // rows past the sequence end may hold anything (NaN)
+                        const uint4 vr = *reinterpret_cast<const uint4 *>(vb + swz(t, lchk));
+                        ffma2(acc[0], acc[1], dev::bf16lo(vr.x), dev::bf16hi(vr.x), pt);
+                        ffma2(acc[2], acc[3], dev::bf16lo(vr.y), dev::bf16hi(vr.y), pt);
+                        ffma2(acc[4], acc[5], dev::bf16lo(vr.z), dev::bf16hi(vr.z), pt);
+                        ffma2(acc[6], acc[7], dev::bf16lo(vr.w), dev::bf16hi(vr.w), pt);
+                    }
+                }
+            }
+            __syncwarp();
+            release_stage(pg);
+            pos.advance(1, SW);
+        }
+        // the item's partial: o_s = acc / l, lse_s = m + log2(l)
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+#pragma unroll
+        for (int o = 16; o >= LPT; o >>= 1) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+        }
+        if (ltok == 0 && !diag_stream) {
+            const size_t row = (size_t)meta.item;
+            float *dst = p.part_o + row * D + lchk * 8;
+#if HETIS_PARTIAL_EVICT_LAST
+            const uint64_t keep = dev::policy_evict_last();
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) dev::st_hint_f32x2(dst + e, __fdiv_rn(acc[e], l), __fdiv_rn(acc[e + 1], l), keep);
+            if (lchk == 0) dev::st_hint_f32(p.part_lse + row, m + __log2f(l), keep);
+#else
+#pragma unroll
+            for (int e = 0; e < 8; e += 2)
+                *reinterpret_cast<float2 *>(dst + e) = make_float2(__fdiv_rn(acc[e], l), __fdiv_rn(acc[e + 1], l));
+            if (lchk == 0) p.part_lse[row] = m + __log2f(l);
+#endif
+        }
+    }
+}
+
+template <int D, int R, int NW, bool FUSED, bool SIMT = false>
 __global__ void __launch_bounds__(32 * (NW + 1), 1)
     attn_gqa_warp_kernel(const Params p, const __grid_constant__ CUtensorMap tmap_k,
                          const __grid_constant__ CUtensorMap tmap_v) {
@@ -1788,6 +1931,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     const int n_items = s_off[p.num_seqs] * p.kv_heads;
     if (threadIdx.x < 32) {
         if (threadIdx.x < NW) producer_warp_items<ROW_BYTES, R, NW>(p, sm, SW, s_len, s_off, &tmap_k, &tmap_v);
+    } else if constexpr (SIMT) {
+        static_assert(R == 1 && !FUSED, "the CUDA-core per-warp consumer is for unfused MHA");
+        consumer_warp_items_simt<D, NW>(p, sm, SW, &tmap_k, &tmap_v);
     } else {
         consumer_warp_items<D, R, NW, FUSED>(p, sm, SW, n_items, &tmap_k, &tmap_v, s_off);
     }
@@ -1805,7 +1951,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
 
 }
 
-template <int D, int R, int NW, bool FUSED>
+template <int D, int R, int NW, bool FUSED, bool SIMT = false>
 cudaError_t launch_gqa_warp_nw(const Params &p0, int num_seqs, cudaStream_t s, const CUtensorMap &tk,
                             const CUtensorMap &tv, std::string *err) {
     constexpr int ROW_BYTES = D * 2;
@@ -1825,7 +1971,7 @@ cudaError_t launch_gqa_warp_nw(const Params &p0, int num_seqs, cudaStream_t s, c
         return cudaErrorInvalidValue;
     }
     p.stages = sw;
-    auto kern = attn_gqa_warp_kernel<D, R, NW, FUSED>;
+    auto kern = attn_gqa_warp_kernel<D, R, NW, FUSED, SIMT>;
     static std::atomic<int> configured[64];
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -1863,6 +2009,18 @@ cudaError_t launch_gqa_warp(const Params &p, int num_seqs, int max_seq_len, cuda
         return launch_gqa_warp_nw<D, R, HETIS_TC_NW_LARGE, false>(p, num_seqs, s, tk, tv, err);
 #endif
     return launch_gqa_warp_nw<D, R, HETIS_TC_NW, false>(p, num_seqs, s, tk, tv, err);
+}
+
+// bf16 MHA on CUDA cores in the per-warp kernel (consumer_warp_items_simt); warp count as above
+template <int D>
+cudaError_t launch_mha_warp_simt(const Params &p, int num_seqs, int max_seq_len, cudaStream_t s, const CUtensorMap &tk,
+                                 const CUtensorMap &tv, std::string *err) {
+#if HETIS_TC_NW_LARGE > 0
+    const int64_t est_items = (int64_t)num_seqs * p.kv_heads * ((max_seq_len + kC - 1) / kC);
+    if (est_items >= (int64_t)HETIS_TC_LARGE_ITEMS_PER_WORKER * num_sms() * HETIS_TC_NW_LARGE)
+        return launch_gqa_warp_nw<D, 1, HETIS_TC_NW_LARGE, false, true>(p, num_seqs, s, tk, tv, err);
+#endif
+    return launch_gqa_warp_nw<D, 1, HETIS_TC_NW, false, true>(p, num_seqs, s, tk, tv, err);
 }
 
 // ---------------------------------------------------------------- kernels
@@ -2083,6 +2241,16 @@ cudaError_t launch_attn_simt(const AttnArgs &a, cudaStream_t s) {
     CUtensorMap dummy;
     std::memset(&dummy, 0, sizeof dummy);
     std::string err;
+    // bf16 MHA: the per-warp kernel with the CUDA-core consumer (HETIS_MHA_WARP), except pipelined launches
+    // and HETIS_ATTN_TC_SHARED_RING, which keep the shared-ring kernel below
+    if (HETIS_MHA_WARP && a.dtype == HETIS_BF16 && a.r == 1 && a.o_out == nullptr && a.peer == nullptr &&
+        !(a.flags & (HETIS_ATTN_PIPELINED | HETIS_ATTN_TC_SHARED_RING)) && (a.head_dim == 128 || a.head_dim == 64)) {
+        CUtensorMap tk, tv;
+        if (!make_pool_map(&tk, a.k_pool, a.num_pages, a.head_dim, &err)) return cudaErrorInvalidValue;
+        if (!make_pool_map(&tv, a.v_pool, a.num_pages, a.head_dim, &err)) return cudaErrorInvalidValue;
+        return a.head_dim == 128 ? launch_mha_warp_simt<128>(p, a.num_seqs, a.max_seq_len, s, tk, tv, &err)
+                                 : launch_mha_warp_simt<64>(p, a.num_seqs, a.max_seq_len, s, tk, tv, &err);
+    }
     if (a.dtype == HETIS_BF16) {
         if (a.head_dim == 128) return dispatch_r<HETIS_BF16, 128, false>(a, p, s, dummy, dummy, &err);
         if (a.head_dim == 64) return dispatch_r<HETIS_BF16, 64, false>(a, p, s, dummy, dummy, &err);

@@ -83,6 +83,7 @@ def main():
              ("GQA r=8 device claim", workload.Shape(64, 8, 128, 16, "bf16"), hetis.ATTN_DEVICE_CLAIM),
              ("GQA r=8 static deal", workload.Shape(64, 8, 128, 16, "bf16"), hetis.ATTN_STATIC_DEAL),
              ("MHA CUDA cores", workload.Shape(40, 40, 128, 16, "bf16"), 0),
+             ("MHA CUDA cores shared ring", workload.Shape(40, 40, 128, 16, "bf16"), hetis.ATTN_TC_SHARED_RING),
              ("MHA CUDA cores pipelined", workload.Shape(40, 40, 128, 16, "bf16"), hetis.ATTN_PIPELINED),
              ("MHA tensor cores", workload.Shape(40, 40, 128, 16, "bf16"), hetis.ATTN_MHA_TC),
              ("fp32 d=64", workload.Shape(8, 8, 64, 16, "f32"), 0)]

@@ -712,6 +712,8 @@ def test_pipelined_steps_match_serial_steps(H, Hkv, D, dtype, extra, large):
         sl = [(lens0 + i + 1).to("cuda") for i in range(n_steps)]
         o = [torch.empty((B, x, D), device="cuda") for _ in range(n_steps)]
         flags = (hetis.ATTN_PIPELINED if mode == "pipelined" else 0) | extra
+        if mode == "serial" and H == Hkv and dtype == "bf16" and not extra & hetis.ATTN_MHA_TC:
+            flags |= hetis.ATTN_TC_SHARED_RING   # pipelined bf16 MHA runs the shared-ring kernel: same arithmetic
 
         def run():
             for i in range(n_steps):
