@@ -2012,13 +2012,16 @@ cudaError_t launch_gqa_warp(const Params &p, int num_seqs, int max_seq_len, cuda
 }
 
 // bf16 MHA on CUDA cores in the per-warp kernel (consumer_warp_items_simt); warp count as above
+#ifndef HETIS_MHA_NW_LARGE
+#define HETIS_MHA_NW_LARGE HETIS_TC_NW_LARGE
+#endif
 template <int D>
 cudaError_t launch_mha_warp_simt(const Params &p, int num_seqs, int max_seq_len, cudaStream_t s, const CUtensorMap &tk,
                                  const CUtensorMap &tv, std::string *err) {
-#if HETIS_TC_NW_LARGE > 0
+#if HETIS_MHA_NW_LARGE > 0
     const int64_t est_items = (int64_t)num_seqs * p.kv_heads * ((max_seq_len + kC - 1) / kC);
-    if (est_items >= (int64_t)HETIS_TC_LARGE_ITEMS_PER_WORKER * num_sms() * HETIS_TC_NW_LARGE)
-        return launch_gqa_warp_nw<D, 1, HETIS_TC_NW_LARGE, false, true>(p, num_seqs, s, tk, tv, err);
+    if (est_items >= (int64_t)HETIS_TC_LARGE_ITEMS_PER_WORKER * num_sms() * HETIS_MHA_NW_LARGE)
+        return launch_gqa_warp_nw<D, 1, HETIS_MHA_NW_LARGE, false, true>(p, num_seqs, s, tk, tv, err);
 #endif
     return launch_gqa_warp_nw<D, 1, HETIS_TC_NW, false, true>(p, num_seqs, s, tk, tv, err);
 }
