@@ -1994,6 +1994,15 @@ inline bool group_mode_ok(const Params &p, int num_seqs, int max_seq_len) {
     return group_mode_qualifies((int64_t)num_seqs * p.kv_heads, max_seq_len, p.flags);
 }
 
+// The larger warp count when it needs fewer rounds of items over the workers (e.g. 1280 items: 2 rounds of
+// 148 x 8 workers but 1 of 148 x 10), else from HETIS_TC_LARGE_ITEMS_PER_WORKER items per worker on.
+inline bool use_large_nw(int64_t est_items, int nw_large) {
+    if (nw_large <= 0) return false;
+    const int64_t w_small = (int64_t)num_sms() * HETIS_TC_NW, w_large = (int64_t)num_sms() * nw_large;
+    if ((est_items + w_large - 1) / w_large < (est_items + w_small - 1) / w_small) return true;
+    return est_items >= (int64_t)HETIS_TC_LARGE_ITEMS_PER_WORKER * w_large;
+}
+
 // warp count of the per-warp kernel for this launch (see HETIS_TC_NW_LARGE)
 template <int D, int R>
 cudaError_t launch_gqa_warp(const Params &p, int num_seqs, int max_seq_len, cudaStream_t s, const CUtensorMap &tk,
@@ -2005,7 +2014,7 @@ cudaError_t launch_gqa_warp(const Params &p, int num_seqs, int max_seq_len, cuda
     }
 #if HETIS_TC_NW_LARGE > 0
     const int64_t est_items = (int64_t)num_seqs * p.kv_heads * ((max_seq_len + kC - 1) / kC);
-    if (est_items >= (int64_t)HETIS_TC_LARGE_ITEMS_PER_WORKER * num_sms() * HETIS_TC_NW_LARGE)
+    if (use_large_nw(est_items, HETIS_TC_NW_LARGE))
         return launch_gqa_warp_nw<D, R, HETIS_TC_NW_LARGE, false>(p, num_seqs, s, tk, tv, err);
 #endif
     return launch_gqa_warp_nw<D, R, HETIS_TC_NW, false>(p, num_seqs, s, tk, tv, err);
@@ -2020,7 +2029,7 @@ cudaError_t launch_mha_warp_simt(const Params &p, int num_seqs, int max_seq_len,
                                  const CUtensorMap &tv, std::string *err) {
 #if HETIS_MHA_NW_LARGE > 0
     const int64_t est_items = (int64_t)num_seqs * p.kv_heads * ((max_seq_len + kC - 1) / kC);
-    if (est_items >= (int64_t)HETIS_TC_LARGE_ITEMS_PER_WORKER * num_sms() * HETIS_MHA_NW_LARGE)
+    if (use_large_nw(est_items, HETIS_MHA_NW_LARGE))
         return launch_gqa_warp_nw<D, 1, HETIS_MHA_NW_LARGE, false, true>(p, num_seqs, s, tk, tv, err);
 #endif
     return launch_gqa_warp_nw<D, 1, HETIS_TC_NW, false, true>(p, num_seqs, s, tk, tv, err);

@@ -7,8 +7,10 @@ paper's observation that attention time does not depend on the number of
 requests at fixed heads and cache (fig:execution_time_modeling (a)).
 
 h = query heads resident on the device (sum over requests), g = cached K/V
-head-vectors (2 * tokens * kv heads, Eq. 8's unit).  tau = one decode step's
-hetis_attn_partial + hetis_attn_combine, CUDA-graph replayed, KV larger than L2.
+head-vectors (2 * tokens * kv heads, Eq. 8's unit).  tau = one decode step of the
+library's one-call step hetis_attn_decode (attention + combine, or ONE kernel where
+the launch runs in group mode), CUDA-graph replayed, KV larger than L2;
+--two-kernel: hetis_attn_partial + hetis_attn_combine always.
 Negative fitted terms are clamped to 0 and refitted.  Accuracy
 is reported over the grid, over its small-share half (the steps of a device in
 an 8-way split, where the fixed cost c dominates -- reported with its minimum,
@@ -34,6 +36,9 @@ from paper_2509_08309_b200 import dispatch, hetis, workload  # noqa: E402
 L2 = 126 * 2 ** 20
 
 
+TWO_KERNEL = False
+
+
 def time_attention(shape, B: int, x: int, L: int, steps: int = 30) -> float:
     dev = torch.device("cuda", 0)
     lens = torch.full((B,), L, dtype=torch.int32)
@@ -48,8 +53,11 @@ def time_attention(shape, B: int, x: int, L: int, steps: int = 30) -> float:
     o = torch.empty((B, x, shape.head_dim), device=dev)
 
     def step(i):
-        hetis.attn_partial(s, b.q, kp[i % n_layers], vp[i % n_layers], b.block_table, b.seq_lens, L, ws)
-        hetis.attn_combine(s, b.seq_lens, L, o, ws)
+        if TWO_KERNEL:
+            hetis.attn_partial(s, b.q, kp[i % n_layers], vp[i % n_layers], b.block_table, b.seq_lens, L, ws)
+            hetis.attn_combine(s, b.seq_lens, L, o, ws)
+        else:
+            hetis.attn_decode(s, b.q, kp[i % n_layers], vp[i % n_layers], b.block_table, b.seq_lens, L, o, ws)
 
     for i in range(3):
         step(i)
@@ -72,7 +80,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shape", default="13b", choices=["13b", "70b"])
     ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--two-kernel", action="store_true", help="time attn_partial + attn_combine, not hetis_attn_decode")
     a = ap.parse_args()
+    global TWO_KERNEL
+    TWO_KERNEL = a.two_kernel
     shape = workload.LLAMA2_13B if a.shape == "13b" else workload.LLAMA2_70B
     r = shape.r
     xs = [shape.num_q_heads * k // 8 for k in range(1, 9)]            # 8 head counts (multiples of r)
@@ -111,6 +122,7 @@ def main():
     bt = np.array([q["tau_s"] for q in batch_rows])
     out = {
         "shape": a.shape, "r": r, "grid": rows,
+        "step": "hetis_attn_partial + hetis_attn_combine" if a.two_kernel else "hetis_attn_decode (library step)",
         "fit": {"a_s_per_head": m.a, "b_s_per_headvector": m.b, "c_s": m.c,
                 "implied_GBps_from_b": shape.head_dim * shape.elem_bytes / m.b / 1e9},
         "accuracy": {"mean": float(acc.mean()), "min": float(acc.min()), "max": float(acc.max())},
