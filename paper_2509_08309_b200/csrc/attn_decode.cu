@@ -606,7 +606,6 @@ __device__ __forceinline__ void merge_warp(const Params &p, const float *mbuf, i
         }
         const size_t row = (size_t)item * R + rr;
         float *dst = p.part_o + row * D + lane * DPL;
-#pragma unroll
 #if HETIS_PARTIAL_EVICT_LAST
         const uint64_t keep = dev::policy_evict_last();
 #pragma unroll
@@ -679,7 +678,6 @@ __device__ void consumer_simt(const Params &p, const uint8_t *ring, const uint8_
 
     const int lane = threadIdx.x & 31;
     const int cw = (threadIdx.x >> 5) - 1;  // consumer warp index
-    const int ctid = threadIdx.x - 32;
     const int ltok = lane / LPT, lchk = lane % LPT;
     const int my_step = lchk >> 1;          // after the butterfly: this lane's token is my_step * TPS + ltok
     const bool l_owner = (lchk & 1) == 0;   // counts its token once in l
@@ -844,7 +842,6 @@ __device__ void consumer_tc(const Params &p, const uint8_t *ring, const uint8_t 
 
     const int lane = threadIdx.x & 31;
     const int cw = (threadIdx.x >> 5) - 1;
-    const int ctid = threadIdx.x - 32;
     const int grp = lane >> 2;  // head row 0..7
     const int tq = lane & 3;
 
@@ -1042,7 +1039,6 @@ __device__ void producer_warp_items(const Params &p, const WarpSmem &sm, int SW,
     const int w = threadIdx.x & 31;  // worker served by this lane
     const unsigned mask = (1u << NW) - 1u;
     const int n_items = s_off[p.num_seqs] * p.kv_heads;
-    const int V = gridDim.x * NW;
     const uint64_t pol = dev::policy_evict_first();
     if (w == 0) {
         dev::prefetch_tmap(tmap_k);
