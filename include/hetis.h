@@ -161,7 +161,8 @@ typedef struct {
  * SLOWER than the separate combine on B200 (c3: 200 vs 188 us at N = 1, 33.1
  * vs 30.7 us for the 8-GPU share; without the fold 182 / 27.7 us -- the fold's
  * L2 round trips under a saturated memory system stall the merging warp), so
- * opt-in. */
+ * opt-in -- except for launches in group mode (below), where the
+ * merge runs in shared memory, is faster, and is the default. */
 #define HETIS_ATTN_FUSED_MERGE 0x20u
 /* Merge-fused launches (above) run in GROUP MODE when they have at most one
  * (request, kv head) pair per SM and at most 8 splits per pair (max_seq_len <=
