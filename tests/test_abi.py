@@ -290,3 +290,30 @@ def test_peer_group_validation(L):
     with pytest.raises(hetis.HetisError) as ei:
         _group(pr)
     assert ei.value.name == "HETIS_E_UNSUPPORTED"
+
+
+def test_decode_launches_for_group_mode_selection(L):
+    """hetis_attn_decode_launches_for (host logic, no launch): the one-kernel form where the launch qualifies for
+    group mode -- bf16 GQA, <= one (request, kv head) pair per SM (148 on B200; also the CPU box's fallback), <= 8
+    splits of 256 tokens -- or with HETIS_ATTN_FUSED_MERGE; two kernels otherwise; -1 on invalid arguments."""
+    from paper_2509_08309_b200 import hetis, workload
+    gqa = hetis.make_shape(workload.Shape(64, 8, 128, 16, "bf16"))
+    mha = hetis.make_shape(workload.Shape(40, 40, 128, 16, "bf16"))
+    f32 = hetis.make_shape(workload.Shape(8, 2, 64, 16, "f32"))
+    n = hetis.attn_decode_launches_for
+    assert n(gqa, 128, 8, 2048) == 1             # c3's 8-GPU share: 128 pairs, 8 splits
+    assert n(gqa, 148, 8, 2048) == 1             # the boundary
+    assert n(gqa, 149, 8, 2048) == 2
+    assert n(gqa, 128, 8, 2049) == 2             # 9 splits
+    assert n(gqa, 128, 16, 1024) == 2            # 256 pairs
+    assert n(gqa, 128, 64, 2048) == 2            # c3 at N = 1
+    assert n(gqa, 128, 64, 2048, hetis.ATTN_FUSED_MERGE) == 1
+    assert n(gqa, 128, 8, 2048, hetis.ATTN_NO_GROUP_MODE) == 2
+    assert n(gqa, 128, 8, 2048, hetis.ATTN_DEVICE_CLAIM) == 2
+    assert n(gqa, 128, 8, 2048, hetis.ATTN_PIPELINED) == 2
+    assert n(mha, 2, 40, 512) == 2               # MHA stays off the tensor cores: no fused merge
+    assert n(f32, 4, 8, 512) == 2
+    with pytest.raises(ValueError):
+        n(gqa, 0, 8, 2048)
+    with pytest.raises(ValueError):
+        n(gqa, 4, 6, 2048)                       # not whole kv groups
