@@ -118,7 +118,7 @@ def test_c1_two_virtual_devices_match_oracle_and_unsplit():
 # ------------------------------------------------------------------ edge lengths, all kernels
 @pytest.mark.parametrize("H,Hkv,D,dtype", [(8, 8, 128, "bf16"), (16, 2, 128, "bf16"), (8, 8, 64, "f32"),
                                            (16, 4, 64, "bf16"), (8, 1, 128, "bf16"), (4, 2, 128, "f32"),
-                                           (8, 4, 128, "bf16")])
+                                           (8, 4, 128, "bf16"), (8, 8, 64, "bf16")])
 def test_edge_lengths_ragged(H, Hkv, D, dtype):
     b = gpu_batch(H, Hkv, D, dtype, EDGE_LENS, seed=H * 7 + D + Hkv)
     o = run_gpu(b)
@@ -500,6 +500,43 @@ def test_mha_on_tensor_cores_matches_oracle(D, peaked):
     # L = 1 returns the V row bit for bit on the tensor-core path too
     v_row = b.v_new[0].float()
     assert torch.equal(o_tc[0], v_row)
+
+
+@pytest.mark.parametrize("D", [128, 64])
+@pytest.mark.parametrize("peaked", [False, True])
+def test_mha_per_warp_cuda_cores_matches_oracle(D, peaked):
+    """bf16 MHA's default: the per-warp kernel with the CUDA-core consumer (swizzled TMA pages, one warp per
+    16-page item, consumer refill, device-wide claiming), d = 128 and 64: within the north-star tolerance of
+    the oracle (peaked keys too) and of the shared-ring CUDA-core kernel; L = 1 returns the V row bit for bit;
+    the launch is bit-identical whatever claims the items (default, forced device claim, static deal)."""
+    lens = (1, 15, 16, 17, 255, 256, 257, 1029, 4096, 700)
+    b = gpu_batch(8, 8, D, "bf16", lens, seed=93)
+    if peaked:
+        b.k_pool.mul_(4)
+        b.k_new.mul_(4)
+    o_pw = run_gpu(b)
+    o_ring = run_gpu(b, append=False, flags=hetis.ATTN_TC_SHARED_RING)
+    ref = oracle_full(b)
+    assert_close(o_pw, ref, "mha per-warp cuda cores")
+    assert (o_pw - o_ring).abs().max().item() < 1e-3
+    assert torch.equal(o_pw[0], b.v_new[0].float())
+    for flags in (hetis.ATTN_DEVICE_CLAIM, hetis.ATTN_STATIC_DEAL):
+        assert torch.equal(run_gpu(b, append=False, flags=flags), o_pw), flags
+
+
+def test_mha_per_warp_head_partition_bit_identical():
+    """Head partition (c4's uneven 16/8/8/4/4) reproduces the unsplit result bit for bit on the default MHA
+    kernel (an item's arithmetic depends on L_j only)."""
+    shape = workload.Shape(40, 40, 128, 16, "bf16")
+    lens = torch.tensor([600, 5, 1300, 256, 3000], dtype=torch.int32)
+    full = workload.make_decode_batch(shape, lens, 29, "cuda")
+    o_full = run_gpu(full)
+    begin, outs = 0, []
+    for i, x in enumerate((16, 8, 8, 4, 4)):
+        part = workload.make_decode_batch(shape, lens, 29, "cuda", q_begin=begin, q_count=x, rank_salt=i + 1)
+        outs.append(run_gpu(part))
+        begin += x
+    assert torch.equal(torch.cat(outs, 1), o_full)
 
 
 def test_mha_tc_head_partition_bit_identical():
