@@ -146,8 +146,12 @@ typedef struct {
  * The attention kernel then streams cache pages while the previous step's
  * combine and attention tail still run: it waits for them only before a page
  * holding one of the last two positions of a request, and before it ends.
- * Pays when a device has about one work item per warp (c3 8-GPU share -12%);
- * costs a few % on large problems.  No work stealing in this mode.
+ * Measured before round 2's consumer refill: it paid when a device had about
+ * one work item per warp (c3 8-GPU share -12%).  With the final kernels the
+ * plain launches are faster everywhere (c3: 170.7 vs 195.8 us at N = 1, the
+ * 8-GPU share 26.6 us in group mode vs 30.1 pipelined), because pipelined
+ * launches keep the producer-issued pages and the CTA-local deal; kept as an
+ * option.  No work stealing in this mode.
  * Safety rests on at most ONE attention CTA per SM (step t + 1 reaches an SM
  * only after step t's CTA there, which waits for combine t - 1, has left):
  * pipelined launches reserve > 114 KiB of shared memory per CTA and the
