@@ -670,6 +670,37 @@ def test_group_mode_bit_identical_to_combine_kernel(H, Hkv, D, odt, B):
         assert_close(got, oracle_full(b), "group mode")
 
 
+def test_group_mode_randomized_shapes_bit_identical():
+    """30 seeded random launches around the group-mode boundary (r in {2, 4, 8}, d in {64, 128}, 1..160
+    pairs, ragged lengths up to 2048 with 1-split and 8-split pairs, f32 / bf16 O): the default one-call
+    decode (group mode where it qualifies, else attention + combine), the last-arriver merge and the
+    two-kernel path give the same bits."""
+    import random
+    rnd = random.Random(2509)
+    for case in range(30):
+        r = rnd.choice([2, 4, 8])
+        D = rnd.choice([64, 128])
+        Hkv = rnd.choice([1, 2, 4])
+        B = rnd.randint(1, max(1, 160 // Hkv))
+        lens = [rnd.choice([1, rnd.randint(1, 256), rnd.randint(1, 2048), 2048]) for _ in range(B)]
+        odt = rnd.choice(["f32", "bf16"])
+        b = gpu_batch(Hkv * r, Hkv, D, "bf16", lens, seed=1000 + case)
+        s = hetis.make_shape(b.shape, odt)
+        x = b.q.shape[1]
+        L = max(lens)
+        hetis.kv_append(s, b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens)
+        ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), "cuda")
+        odtype = torch.bfloat16 if odt == "bf16" else torch.float32
+        ref = torch.full((B, x, D), float("nan"), dtype=odtype, device="cuda")
+        hetis.attn_partial(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, ws)
+        hetis.attn_combine(s, b.seq_lens, L, ref, ws)
+        for flags in (0, FM | hetis.ATTN_NO_GROUP_MODE):
+            got = torch.full_like(ref, float("nan"))
+            hetis.attn_decode(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, got, ws, flags=flags)
+            torch.cuda.synchronize()
+            assert torch.equal(got.view(torch.int16), ref.view(torch.int16)), (case, r, D, Hkv, B, odt, flags)
+
+
 @pytest.mark.parametrize("H,Hkv,D,B", [(64, 8, 128, 9), (16, 4, 64, 40), (64, 8, 128, 40)])
 def test_fused_merge_empty_requests_write_zeros(H, Hkv, D, B):
     """L_j = 0 (a device holding none of request j's tokens under a sequence split): the combine kernel writes
