@@ -701,6 +701,37 @@ def test_group_mode_randomized_shapes_bit_identical():
             assert torch.equal(got.view(torch.int16), ref.view(torch.int16)), (case, r, D, Hkv, B, odt, flags)
 
 
+def test_claim_modes_randomized_launches_bit_identical():
+    """24 seeded random launches from one item per worker to several (r in {1, 2, 4, 8}: bf16 MHA on the
+    per-warp CUDA-core consumer and GQA on the tensor-core one; d in {64, 128}; up to ~6000 items): the
+    default (consumer refill + device-wide claiming), HETIS_ATTN_STATIC_DEAL and HETIS_ATTN_DEVICE_CLAIM hand
+    items to different warps and CTAs and give the same bits, twice in a row on one workspace."""
+    import random
+    rnd = random.Random(830)
+    for case in range(24):
+        r = rnd.choice([1, 2, 4, 8])
+        D = rnd.choice([64, 128])
+        Hkv = rnd.choice([2, 4, 8])
+        B = rnd.randint(1, 96)
+        lens = [rnd.randint(1, 4096) for _ in range(B)]
+        b = gpu_batch(Hkv * r, Hkv, D, "bf16", lens, seed=2000 + case)
+        s = hetis.make_shape(b.shape)
+        x = b.q.shape[1]
+        L = max(lens)
+        hetis.kv_append(s, b.k_new, b.v_new, b.k_pool, b.v_pool, b.block_table, b.seq_lens)
+        ws = hetis.alloc_workspace(hetis.attn_decode_workspace(s, B, x, L), "cuda")
+        outs = []
+        for flags in (0, hetis.ATTN_STATIC_DEAL, hetis.ATTN_DEVICE_CLAIM, 0):
+            o = torch.full((B, x, D), float("nan"), device="cuda")
+            hetis.attn_partial(s, b.q, b.k_pool, b.v_pool, b.block_table, b.seq_lens, L, ws, flags=flags)
+            hetis.attn_combine(s, b.seq_lens, L, o, ws)
+            outs.append(o)
+        torch.cuda.synchronize()
+        for k, o in enumerate(outs[1:]):
+            assert torch.equal(o, outs[0]), (case, r, D, Hkv, B, k)
+        assert torch.isfinite(outs[0]).all()
+
+
 @pytest.mark.parametrize("H,Hkv,D,B", [(64, 8, 128, 9), (16, 4, 64, 40), (64, 8, 128, 40)])
 def test_fused_merge_empty_requests_write_zeros(H, Hkv, D, B):
     """L_j = 0 (a device holding none of request j's tokens under a sequence split): the combine kernel writes
