@@ -72,7 +72,7 @@ constexpr int kQSlots = 2;
 #define HETIS_EARLY_RELEASE 0
 #endif
 #ifndef HETIS_PROLOGUE_PREFETCH
-#define HETIS_PROLOGUE_PREFETCH 2
+#define HETIS_PROLOGUE_PREFETCH 3
 #endif
 #ifndef HETIS_TC_NW_LARGE
 #define HETIS_TC_NW_LARGE 10
