@@ -73,7 +73,9 @@
 extern "C" {
 #endif
 
-#define HETIS_ABI_VERSION 3
+/* 4: hetis_attn_decode_launches_for; hetis_attn_decode(_append) / _units fuse the merge automatically in
+ * group mode; hetis_attn_decode_peers' pull form (q_shard NULL); flags NO_GROUP_MODE, STATIC_DEAL. */
+#define HETIS_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define HETIS_API __attribute__((visibility("default")))

@@ -45,7 +45,7 @@ def test_exported_symbols_match_nm():
 def test_status_strings_and_constants(L):
     for code, name in hetis.STATUS.items():
         assert hetis.status_str(code) == name
-    assert hetis.abi_version() == 3
+    assert hetis.abi_version() == 4
     assert hetis.split_tokens() % 16 == 0
 
 
